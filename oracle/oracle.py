@@ -1,0 +1,139 @@
+"""ctypes front-end of the CPU oracle (tsds_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's reference / cpu_baseline arm, never by the product package.
+The oracle restates the reference `thinseries` path (scalar semantics,
+SURVEY.md Appendix A); its parity with the real reference is pinned by
+tests/test_oracle_golden.py against tests/golden/*.npz, which
+tests/golden/make_golden.py produced by importing the reference itself.
+"""
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
+
+DTYPE_CODES = {
+    np.dtype(np.float16): 0,
+    np.dtype(np.float32): 1,
+    np.dtype(np.float64): 2,
+    np.dtype(np.int8): 3,
+    np.dtype(np.int16): 4,
+    np.dtype(np.int32): 5,
+    np.dtype(np.int64): 6,
+    np.dtype(np.uint8): 7,
+    np.dtype(np.uint16): 8,
+    np.dtype(np.uint32): 9,
+    np.dtype(np.uint64): 10,
+}
+
+ALGO_CODES = {"minmax": 1, "m4": 2, "lttb": 3, "minmaxlttb": 4}
+
+_lib = None
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        L = ctypes.CDLL(_LIB_PATH)
+        vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        L.or_argminmax.argtypes = [vp, i32, i64, i32, vp]
+        L.or_equal_count.argtypes = [i64, i64, vp]
+        L.or_is_uniform.argtypes = [vp, i32, i64]
+        L.or_equal_width.argtypes = [vp, i32, i64, i64, vp]
+        L.or_downsample.argtypes = [i32, vp, i32, vp, i32, i64, i64, i64, i32, i32, vp]
+        L.or_downsample.restype = i64
+        L.or_minmax_batched.argtypes = [vp, i32, i64, i64, i64, i32, i32, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _x_view(x):
+    if x is None:
+        return None
+    x = np.ascontiguousarray(x)
+    if np.issubdtype(x.dtype, np.datetime64):
+        x = x.view(np.int64)
+    return x
+
+
+def argminmax(y, nan=False):
+    y = np.ascontiguousarray(y)
+    out = np.zeros(2, np.int64)
+    lib().or_argminmax(_ptr(y), DTYPE_CODES[y.dtype], y.shape[0], int(nan), _ptr(out))
+    return int(out[0]), int(out[1])
+
+
+def equal_count(length, n_bins):
+    out = np.zeros(n_bins + 1, np.int64)
+    lib().or_equal_count(length, n_bins, _ptr(out))
+    return out.astype(np.uint64)
+
+
+def is_uniform(x):
+    x = _x_view(x)
+    return bool(lib().or_is_uniform(_ptr(x), DTYPE_CODES[x.dtype], x.shape[0]))
+
+
+def equal_width(x, n_bins):
+    x = _x_view(x)
+    out = np.zeros(n_bins + 1, np.int64)
+    rc = lib().or_equal_width(_ptr(x), DTYPE_CODES[x.dtype], x.shape[0], n_bins, _ptr(out))
+    if rc != 0:
+        raise ValueError("invalid index span")
+    return out.astype(np.uint64)
+
+
+def downsample(algo, *args, n_out, minmax_ratio=4, nan=False, threads=1):
+    """Indices of the reference algorithm on valid inputs (uint64)."""
+    if len(args) == 1:
+        x, y = None, args[0]
+    else:
+        x, y = args
+    y = np.ascontiguousarray(y)
+    x = _x_view(x)
+    out = np.zeros(max(int(n_out), 1), np.int64)  # every algorithm returns <= n_out
+    m = lib().or_downsample(
+        ALGO_CODES[algo],
+        _ptr(x),
+        0 if x is None else DTYPE_CODES[x.dtype],
+        _ptr(y),
+        DTYPE_CODES[y.dtype],
+        y.shape[0],
+        int(n_out),
+        int(minmax_ratio),
+        int(nan),
+        int(threads),
+        _ptr(out),
+    )
+    if m == -2:
+        raise ValueError("invalid index span")
+    if m < 0:
+        raise RuntimeError(f"oracle error {m}")
+    return out[:m].astype(np.uint64)
+
+
+def minmax_batched(Y, n_out, nan=False, threads=1):
+    """Row s == downsample('minmax', Y[s], n_out); returns (idx[S, n_out], counts)."""
+    Y = np.ascontiguousarray(Y)
+    S, L = Y.shape
+    out = np.zeros((S, n_out), np.int64)
+    counts = np.zeros(S, np.int64)
+    lib().or_minmax_batched(
+        _ptr(Y), DTYPE_CODES[Y.dtype], S, L, int(n_out), int(nan), int(threads), _ptr(out), _ptr(counts)
+    )
+    return out.astype(np.uint64), counts
