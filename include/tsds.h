@@ -1,0 +1,144 @@
+/*
+ * tsds.h -- C ABI of the B200 downsampling library (libtsds.so).
+ *
+ * Drop-in boundary for the data-parallel hot path of the reference
+ * `thinseries` package.  The reference has no FFI: its
+ * "operator API" is the set of numba kernels with caller-allocated outputs
+ * that algorithms.py / binning.py call.  Every entry point below replaces
+ * one of those kernels (operator layer) or one whole algorithm call
+ * (composed layer); the reference file:line each one replaces is cited.
+ *
+ * Conventions (mirroring the reference kernels, _kernels.py:300-306):
+ *   - outputs are caller-allocated; nothing is returned by ownership;
+ *   - kernels never raise: arguments are validated by the caller (the
+ *     Python layer reproduces the reference error strings) and only the
+ *     data-dependent "invalid index span" condition is reported here;
+ *   - every call returns an int status (TSDS_OK or a negative code) and
+ *     tsds_last_error() holds a per-thread message; no C++ exception
+ *     crosses the ABI;
+ *   - a tsds_ctx owns a CUDA stream and device workspace; one context per
+ *     host thread (calls on one context are serialised by an internal lock).
+ *
+ * dtype codes (thinseries.dtypes.VALUE_DTYPES order, dtypes.py:11-23):
+ *   0 f16, 1 f32, 2 f64, 3 i8, 4 i16, 5 i32, 6 i64, 7 u8, 8 u16, 9 u32, 10 u64
+ * Indices are int64 (the reference returns their uint64 view, same values).
+ */
+#ifndef TSDS_H
+#define TSDS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSDS_OK 0
+#define TSDS_ERR_ARG (-1)   /* invalid argument (caller bug)            */
+#define TSDS_ERR_SPAN (-2)  /* "invalid index span" (binning.py:51-52)  */
+#define TSDS_ERR_CUDA (-3)  /* CUDA runtime / launch failure            */
+#define TSDS_ERR_NOMEM (-4) /* device or pinned allocation failed       */
+
+/* algorithm codes, api.py:15 (_ALGORITHMS) minus "everynth" */
+#define TSDS_MINMAX 1
+#define TSDS_M4 2
+#define TSDS_LTTB 3
+#define TSDS_MINMAXLTTB 4
+
+/* nan_mode: 0 = reference semantics (scalar path),
+ *           1 = NaN-propagating (NaN* classes: first NaN wins both)      */
+
+/* mem: where x / y live.  TSDS_MEM_HOST: host memory (pageable or pinned),
+ * copied by the library; TSDS_MEM_DEVICE: device pointers on ctx's device. */
+#define TSDS_MEM_HOST 0
+#define TSDS_MEM_DEVICE 1
+
+typedef struct tsds_ctx tsds_ctx;
+
+int tsds_version(void);
+const char *tsds_last_error(void);
+int tsds_device_count(int *count);
+
+int tsds_ctx_create(int device, tsds_ctx **out);
+void tsds_ctx_destroy(tsds_ctx *ctx);
+/* use an external cudaStream_t (e.g. torch.cuda.current_stream()); NULL -> own */
+int tsds_ctx_set_stream(tsds_ctx *ctx, void *cuda_stream);
+void *tsds_ctx_stream(tsds_ctx *ctx);
+int tsds_ctx_synchronize(tsds_ctx *ctx);
+/* number of this library's kernels launched on ctx so far */
+int64_t tsds_ctx_launches(tsds_ctx *ctx);
+
+/* ---------------------------------------------------------------------------
+ * Composed layer: one whole algorithm call.
+ *
+ * tsds_downsample replaces algorithms.minmax / m4 / lttb / minmaxlttb
+ * (algorithms.py:118-255) as dispatched by api.downsample after validation
+ * (api.py:60-83, including the uniform-x normalisation of api.py:19-28).
+ * x may be NULL.  out: host int64[n_out]; *out_len receives the count.
+ * ------------------------------------------------------------------------ */
+int tsds_downsample(tsds_ctx *ctx, int algo, const void *x, int x_dtype, const void *y, int y_dtype,
+                    int64_t n, int64_t n_out, int64_t minmax_ratio, int nan_mode, int mem, int64_t *out,
+                    int64_t *out_len);
+
+/* Asynchronous device-resident variant for MinMax / M4 (no host sync, no
+ * copies): x, y, out_dev (int64[n_out]) and count_dev (int64) are device
+ * pointers; *status_dev (int32) receives TSDS_ERR_SPAN if the x span is
+ * invalid.  Enqueued on ctx's stream. */
+int tsds_downsample_async(tsds_ctx *ctx, int algo, const void *x, int x_dtype, const void *y, int y_dtype,
+                          int64_t n, int64_t n_out, int nan_mode, int64_t *out_dev, int64_t *count_dev,
+                          int32_t *status_dev);
+
+/* Batched MinMax (extension; the reference has no batch API):
+ * row s of y[n_series][len] gives out[s*n_out ...] and counts[s]; row s
+ * equals tsds_downsample(MINMAX, y[s]).  out/counts are host pointers
+ * (mem=HOST|DEVICE refers to y). */
+int tsds_minmax_batched(tsds_ctx *ctx, const void *y, int y_dtype, int64_t n_series, int64_t len,
+                        int64_t n_out, int nan_mode, int mem, int64_t *out, int64_t *counts);
+/* device-resident asynchronous variant (out_dev int64[n_series*n_out], counts_dev int64[n_series]) */
+int tsds_minmax_batched_async(tsds_ctx *ctx, const void *y, int y_dtype, int64_t n_series, int64_t len,
+                              int64_t n_out, int nan_mode, int64_t *out_dev, int64_t *counts_dev);
+
+/* Public whole-series argminmax (extrema.py:142-155). out2: host int64[2]. */
+int tsds_argminmax(tsds_ctx *ctx, const void *y, int y_dtype, int64_t n, int nan_mode, int mem, int64_t *out2);
+
+/* ---------------------------------------------------------------------------
+ * Operator layer: device pointers, enqueued on ctx's stream.
+ * ------------------------------------------------------------------------ */
+
+/* is_uniform_spaced (_kernels.py:506-518); *flag_dev (int32) = 1 if uniform */
+int tsds_op_is_uniform_spaced(tsds_ctx *ctx, const void *x, int x_dtype, int64_t n, int32_t *flag_dev);
+
+/* equal_count_boundaries (binning.py:32-40): off_dev int64[n_bins+1] */
+int tsds_op_equal_count_offsets(tsds_ctx *ctx, int64_t len, int64_t n_bins, int64_t *off_dev);
+
+/* equal_width_boundaries (binning.py:61-82 + fill_width_offsets
+ * _kernels.py:521-535), including the uniform-x shortcut.  Synchronises
+ * to report TSDS_ERR_SPAN. */
+int tsds_op_equal_width_offsets(tsds_ctx *ctx, const void *x, int x_dtype, int64_t n, int64_t n_bins,
+                                int64_t *off_dev);
+
+/* minmax_bins / m4_bins (_kernels.py:308-354): bins [b0, b1) of off_dev,
+ * writing idx_dev[width*(b-b0) + t] and cnt_dev[b-b0] (width 2 / 4). */
+int tsds_op_minmax_bins(tsds_ctx *ctx, const void *y, int y_dtype, const int64_t *off_dev, int64_t b0,
+                        int64_t b1, int nan_mode, int64_t *idx_dev, int64_t *cnt_dev);
+int tsds_op_m4_bins(tsds_ctx *ctx, const void *y, int y_dtype, const int64_t *off_dev, int64_t b0, int64_t b1,
+                    int nan_mode, int64_t *idx_dev, int64_t *cnt_dev);
+
+/* lttb_implicit / lttb_explicit (_kernels.py:375-480): x_f64 NULL for the
+ * implicit kernel; off_dev int64[n_bins+1]; out_dev int64[n_bins+2];
+ * *m_host receives the count (synchronises). */
+int tsds_op_lttb(tsds_ctx *ctx, const double *x_f64, const void *y, int y_dtype, int64_t n,
+                 const int64_t *off_dev, int64_t n_bins, int64_t *out_dev, int64_t *m_host);
+
+/* ---------------------------------------------------------------------------
+ * Host-side binning for host-resident x (exact reference semantics; the
+ * device only ever needs y when x stays on the host).
+ * ------------------------------------------------------------------------ */
+int tsds_host_is_uniform_spaced(const void *x, int x_dtype, int64_t n);
+/* returns TSDS_OK or TSDS_ERR_SPAN; off int64[n_bins+1] (host) */
+int tsds_host_equal_width_offsets(const void *x, int x_dtype, int64_t n, int64_t n_bins, int64_t *off);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TSDS_H */

@@ -1,0 +1,873 @@
+// tsds_api.cu -- C ABI (include/tsds.h): contexts, workspace, orchestration.
+//
+// The composed entry points reproduce algorithms.py (minmax/m4/lttb/
+// minmaxlttb, algorithms.py:118-255) as device pipelines:
+//   [x on device]  uniform_kernel -> width_offsets_kernel -> check_monotone
+//   [x on host]    tsds_host_* binning (only y crosses PCIe)
+//   scan_kernel (fused argminmax + segmented merge + compaction)
+//   LTTB: lttb_centroid_kernel -> lttb_walk_kernel (single CTA)
+// Everything is enqueued on the context's stream; host syncs happen only to
+// return variable-length results (and once between MinMaxLTTB's stages).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tsds.h"
+#include "tsds_bin.cuh"
+#include "tsds_lttb.cuh"
+#include "tsds_scan.cuh"
+
+using namespace tsds;
+
+#ifndef TSDS_UNROLL
+#define TSDS_UNROLL 8
+#endif
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct Misc {
+  int mis_api;      // uniform check of the full x (0 = uniform)
+  int mis_slice;    // uniform check of an x slice
+  int status;       // TSDS_ERR_SPAN from binning
+  unsigned blocks_done;
+  int nonmono;      // offsets decrease somewhere
+  int mis2;         // stage-2 uniform check
+  int pad[10];
+  int64_t count;    // @64
+  int64_t m2;
+  int64_t pair[2];
+};
+constexpr size_t MISC_RESET = 32;  // bytes of Misc zeroed per call
+
+}  // namespace
+
+struct tsds_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = true;
+  int sms = 148;
+  std::mutex mu;
+  DevBuf y, x, xf64, part, bincnt, res, off, out, misc, cent, scratch, y2, x2, x2f64, full, out2;
+  void* h_pin = nullptr;
+  size_t h_cap = 0;
+  bool dirty = false;
+  int64_t launches = 0;
+};
+
+#define CUDA_TRY(call)                                                                              \
+  do {                                                                                              \
+    cudaError_t e_ = (call);                                                                        \
+    if (e_ != cudaSuccess) {                                                                        \
+      ctx->dirty = true;                                                                            \
+      return set_err(e_ == cudaErrorMemoryAllocation ? TSDS_ERR_NOMEM : TSDS_ERR_CUDA,               \
+                     std::string(#call) + ": " + cudaGetErrorString(e_));                           \
+    }                                                                                               \
+  } while (0)
+
+#define LAUNCH_CHECK()                                                                              \
+  do {                                                                                              \
+    ctx->launches++;                                                                                \
+    cudaError_t e_ = cudaPeekAtLastError();                                                         \
+    if (e_ != cudaSuccess) {                                                                        \
+      cudaGetLastError();                                                                           \
+      ctx->dirty = true;                                                                            \
+      return set_err(TSDS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_));       \
+    }                                                                                               \
+  } while (0)
+
+#define RC_TRY(expr)             \
+  do {                           \
+    int rc_ = (expr);            \
+    if (rc_ != TSDS_OK) return rc_; \
+  } while (0)
+
+namespace {
+
+int ensure(tsds_ctx* ctx, DevBuf& b, size_t bytes, bool zero = false) {
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return TSDS_OK;
+  if (b.p) {
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(cudaFree(b.p));
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  size_t cap = std::max(bytes, b.cap + b.cap / 2);
+  cap = (cap + 255) & ~(size_t)255;
+  CUDA_TRY(cudaMalloc(&b.p, cap));
+  b.cap = cap;
+  if (zero) CUDA_TRY(cudaMemsetAsync(b.p, 0, cap, ctx->stream));
+  return TSDS_OK;
+}
+
+int ensure_host(tsds_ctx* ctx, size_t bytes) {
+  if (ctx->h_cap >= bytes) return TSDS_OK;
+  if (ctx->h_pin) {
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    cudaFreeHost(ctx->h_pin);
+    ctx->h_pin = nullptr;
+  }
+  size_t cap = std::max<size_t>(bytes, 1 << 16);
+  CUDA_TRY(cudaMallocHost(&ctx->h_pin, cap));
+  ctx->h_cap = cap;
+  return TSDS_OK;
+}
+
+Misc* misc(tsds_ctx* ctx) { return (Misc*)ctx->misc.p; }
+
+int begin_call(tsds_ctx* ctx) {
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  RC_TRY(ensure(ctx, ctx->misc, sizeof(Misc), true));
+  if (ctx->dirty) {
+    // a failed call may have left arrival counters set: re-zero them
+    if (ctx->bincnt.p) CUDA_TRY(cudaMemsetAsync(ctx->bincnt.p, 0, ctx->bincnt.cap, ctx->stream));
+    ctx->dirty = false;
+  }
+  CUDA_TRY(cudaMemsetAsync(ctx->misc.p, 0, MISC_RESET, ctx->stream));
+  return TSDS_OK;
+}
+
+int dtype_ok(int dt) { return dt >= 0 && dt < DT_COUNT; }
+int xdtype_ok(int dt) { return dt >= 1 && dt < DT_COUNT; }
+
+// ---------------------------------------------------------------- scan launch
+template <int DT, bool PROP>
+int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
+  using O = Ops<DT>;
+  constexpr int VEC = O::VEC;
+  constexpr int ES = 16 / VEC;
+  auto kern = scan_kernel<DT, PROP, TSDS_UNROLL>;
+  static int occ = 0;
+  if (occ == 0) {
+    int o = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, SCAN_WARPS * 32, 0));
+    occ = std::max(1, o);
+  }
+  if ((uintptr_t)A.y % ES) return set_err(TSDS_ERR_ARG, "y is not aligned to its element size");
+  A.shift = (int64_t)(((uintptr_t)A.y % 16) / ES);
+  const int64_t align = 32 * VEC;
+  A.vstart = ((A.E0 + A.shift) / align) * align;
+  int64_t vend = std::max(A.E1 + A.shift, A.vstart + 1);
+  int64_t tv = vend - A.vstart;
+  int64_t maxw = (int64_t)ctx->sms * occ * SCAN_WARPS;
+  const int64_t min_chunk_elems = 4096 / ES;
+  int64_t want = (tv + min_chunk_elems - 1) / min_chunk_elems;
+  int64_t nch = std::max<int64_t>(1, std::min(maxw, want));
+  int64_t che = (tv + nch - 1) / nch;
+  che = ((che + align - 1) / align) * align;
+  nch = (tv + che - 1) / che;
+  A.che = che;
+  A.nchunks = nch;
+  int64_t nbins = A.g1 - A.g0;
+  RC_TRY(ensure(ctx, ctx->part, (size_t)nch * 2 * sizeof(MinMaxCand)));
+  RC_TRY(ensure(ctx, ctx->bincnt, (size_t)nbins * sizeof(unsigned), true));
+  RC_TRY(ensure(ctx, ctx->res, (size_t)nbins * 2 * sizeof(int64_t)));
+  A.part = (MinMaxCand*)ctx->part.p;
+  A.bin_cnt = (unsigned*)ctx->bincnt.p;
+  A.res = (int64_t*)ctx->res.p;
+  A.blocks_done = &misc(ctx)->blocks_done;
+  int64_t grid = (nch + SCAN_WARPS - 1) / SCAN_WARPS;
+  if (A.independent || A.nonmono_flag) grid = std::max<int64_t>(grid, std::min<int64_t>(maxw / SCAN_WARPS, (nbins + SCAN_WARPS - 1) / SCAN_WARPS));
+  kern<<<(unsigned)grid, SCAN_WARPS * 32, 0, ctx->stream>>>(A);
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
+template <bool PROP>
+int launch_scan_p(tsds_ctx* ctx, int dt, ScanArgs& A) {
+  switch (dt) {
+    case DT_F16: return launch_scan_t<DT_F16, PROP>(ctx, A);
+    case DT_F32: return launch_scan_t<DT_F32, PROP>(ctx, A);
+    case DT_F64: return launch_scan_t<DT_F64, PROP>(ctx, A);
+    case DT_I8: return launch_scan_t<DT_I8, PROP>(ctx, A);
+    case DT_I16: return launch_scan_t<DT_I16, PROP>(ctx, A);
+    case DT_I32: return launch_scan_t<DT_I32, PROP>(ctx, A);
+    case DT_I64: return launch_scan_t<DT_I64, PROP>(ctx, A);
+    case DT_U8: return launch_scan_t<DT_U8, PROP>(ctx, A);
+    case DT_U16: return launch_scan_t<DT_U16, PROP>(ctx, A);
+    case DT_U32: return launch_scan_t<DT_U32, PROP>(ctx, A);
+    case DT_U64: return launch_scan_t<DT_U64, PROP>(ctx, A);
+    default: return set_err(TSDS_ERR_ARG, "unsupported dtype");
+  }
+}
+
+int launch_scan(tsds_ctx* ctx, int dt, int nan_mode, ScanArgs& A) {
+  return nan_mode ? launch_scan_p<true>(ctx, dt, A) : launch_scan_p<false>(ctx, dt, A);
+}
+
+ScanArgs scan_args(const void* y, BinSpec bins, int64_t g0, int64_t g1, int64_t E0, int64_t E1) {
+  ScanArgs A;
+  memset(&A, 0, sizeof(A));
+  A.y = y;
+  A.bins = bins;
+  A.g0 = g0;
+  A.g1 = g1;
+  A.E0 = E0;
+  A.E1 = E1;
+  return A;
+}
+
+// ------------------------------------------------------------- binning launch
+#define XDT_SWITCH(dt, CALL)                                   \
+  switch (dt) {                                                \
+    case DT_F32: { constexpr int XD = DT_F32; CALL; } break;   \
+    case DT_F64: { constexpr int XD = DT_F64; CALL; } break;   \
+    case DT_I8: { constexpr int XD = DT_I8; CALL; } break;     \
+    case DT_I16: { constexpr int XD = DT_I16; CALL; } break;   \
+    case DT_I32: { constexpr int XD = DT_I32; CALL; } break;   \
+    case DT_I64: { constexpr int XD = DT_I64; CALL; } break;   \
+    case DT_U8: { constexpr int XD = DT_U8; CALL; } break;     \
+    case DT_U16: { constexpr int XD = DT_U16; CALL; } break;   \
+    case DT_U32: { constexpr int XD = DT_U32; CALL; } break;   \
+    case DT_U64: { constexpr int XD = DT_U64; CALL; } break;   \
+    default: return set_err(TSDS_ERR_ARG, "unsupported x dtype"); \
+  }
+
+#define YDT_SWITCH(dt, CALL)                                   \
+  switch (dt) {                                                \
+    case DT_F16: { constexpr int YD = DT_F16; CALL; } break;   \
+    case DT_F32: { constexpr int YD = DT_F32; CALL; } break;   \
+    case DT_F64: { constexpr int YD = DT_F64; CALL; } break;   \
+    case DT_I8: { constexpr int YD = DT_I8; CALL; } break;     \
+    case DT_I16: { constexpr int YD = DT_I16; CALL; } break;   \
+    case DT_I32: { constexpr int YD = DT_I32; CALL; } break;   \
+    case DT_I64: { constexpr int YD = DT_I64; CALL; } break;   \
+    case DT_U8: { constexpr int YD = DT_U8; CALL; } break;     \
+    case DT_U16: { constexpr int YD = DT_U16; CALL; } break;   \
+    case DT_U32: { constexpr int YD = DT_U32; CALL; } break;   \
+    case DT_U64: { constexpr int YD = DT_U64; CALL; } break;   \
+    default: return set_err(TSDS_ERR_ARG, "unsupported dtype"); \
+  }
+
+int launch_uniform(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int* mis) {
+  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 4, (n + 511) / 512));
+  XDT_SWITCH(xdt, (uniform_kernel<XD><<<grid, 256, 0, ctx->stream>>>(x, n, mis)));
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
+// device equal-width offsets (+add) for x[0..n) into off; writes misc->status on span error
+int launch_width(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int64_t nb, int64_t add, int* mis,
+                 int uniform_first, const int* api_mis, int64_t* off) {
+  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (nb + 1 + 7) / 8));
+  int* status = &misc(ctx)->status;
+  XDT_SWITCH(xdt, (width_offsets_kernel<XD><<<grid, 256, 0, ctx->stream>>>(x, n, nb, add, mis, uniform_first,
+                                                                            api_mis, off, status)));
+  LAUNCH_CHECK();
+  check_monotone_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ctx->sms, (nb + 255) / 256)), 256, 0,
+                          ctx->stream>>>(off, nb, status, &misc(ctx)->nonmono);
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
+int launch_count_offsets(tsds_ctx* ctx, int64_t len, int64_t nb, int64_t add, int64_t* off) {
+  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 4, (nb + 256) / 256));
+  count_offsets_kernel<<<grid, 256, 0, ctx->stream>>>(len, nb, add, off);
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
+// host binning of host-resident x into a host vector, monotone flag out
+bool host_monotone(const std::vector<int64_t>& off) {
+  for (size_t k = 0; k + 1 < off.size(); k++)
+    if (off[k + 1] < off[k]) return false;
+  return true;
+}
+
+int upload(tsds_ctx* ctx, DevBuf& b, const void* h, size_t bytes) {
+  RC_TRY(ensure(ctx, b, bytes));
+  CUDA_TRY(cudaMemcpyAsync(b.p, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return TSDS_OK;
+}
+
+int stage_input(tsds_ctx* ctx, DevBuf& b, const void* p, size_t bytes, int mem, const void** dev) {
+  if (mem == TSDS_MEM_DEVICE) {
+    *dev = p;
+    return TSDS_OK;
+  }
+  RC_TRY(upload(ctx, b, p, bytes));
+  *dev = b.p;
+  return TSDS_OK;
+}
+
+int finish_status(tsds_ctx* ctx, const int* h_status) {
+  if (*h_status == TSDS_ERR_SPAN) return set_err(TSDS_ERR_SPAN, "invalid index span");
+  if (*h_status != 0) return set_err(TSDS_ERR_CUDA, "device status " + std::to_string(*h_status));
+  return TSDS_OK;
+}
+
+// copy count (at dev[0]) + up to cap entries, plus the status word; sync.
+int fetch_result(tsds_ctx* ctx, const int64_t* dev, int64_t cap, int64_t* out, int64_t* out_len) {
+  RC_TRY(ensure_host(ctx, (size_t)(cap + 1) * 8 + 64));
+  int64_t* h = (int64_t*)ctx->h_pin;
+  int* hs = (int*)(h + cap + 1);
+  CUDA_TRY(cudaMemcpyAsync(h, dev, (size_t)(cap + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(hs, &misc(ctx)->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  RC_TRY(finish_status(ctx, hs));
+  int64_t m = h[0];
+  if (m < 0 || m > cap) return set_err(TSDS_ERR_CUDA, "corrupt result count");
+  memcpy(out, h + 1, (size_t)m * 8);
+  *out_len = m;
+  return TSDS_OK;
+}
+
+// ----------------------------------------------------------------- MinMax / M4
+int run_minmax_m4(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y, int ydt, int64_t n, int64_t n_out,
+                  int nan_mode, int mem, int64_t* out_dev, int64_t* count_dev) {
+  const int width = algo == TSDS_MINMAX ? 2 : 4;
+  const int64_t nb = n_out / width;
+  BinSpec bins{0, nullptr, n, nb, 0};
+  ScanArgs A = scan_args(nullptr, bins, 0, nb, 0, n);
+  if (x) {
+    if (mem == TSDS_MEM_HOST) {
+      if (!tsds_host_is_uniform_spaced(x, xdt, n)) {
+        std::vector<int64_t> off(nb + 1);
+        int rc = tsds_host_equal_width_offsets(x, xdt, n, nb, off.data());
+        if (rc == TSDS_ERR_SPAN) return set_err(rc, "invalid index span");
+        RC_TRY(upload(ctx, ctx->off, off.data(), off.size() * 8));
+        A.bins.mode = 1;
+        A.bins.off = (const int64_t*)ctx->off.p;
+        A.independent = !host_monotone(off);
+      }
+    } else {
+      RC_TRY(ensure(ctx, ctx->off, (size_t)(nb + 1) * 8));
+      int64_t* off = (int64_t*)ctx->off.p;
+      RC_TRY(launch_uniform(ctx, x, xdt, n, &misc(ctx)->mis_api));
+      RC_TRY(launch_width(ctx, x, xdt, n, nb, 0, &misc(ctx)->mis_api, 1, nullptr, off));
+      A.bins.mode = 1;
+      A.bins.off = off;
+      A.abort_flag = &misc(ctx)->status;
+      A.nonmono_flag = &misc(ctx)->nonmono;
+    }
+  }
+  const void* dy;
+  RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
+  A.y = dy;
+  A.epi = algo == TSDS_MINMAX ? EPI_MINMAX : EPI_M4;
+  A.out = out_dev;
+  A.out_count = count_dev;
+  return launch_scan(ctx, ydt, nan_mode, A);
+}
+
+__global__ void iota_kernel(int64_t* out, int64_t n, int64_t* count) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) out[i] = i;
+  if (count && blockIdx.x == 0 && threadIdx.x == 0) *count = n;
+}
+
+__global__ void map_kernel(const int64_t* idx, const int64_t* map, int64_t m, int64_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = map[idx[i]];
+}
+
+// ------------------------------------------------------------------------ LTTB
+// Runs the walk over (x_f64 or implicit, y) with offsets off[nb+1]; out_dev
+// receives [count, idx...]; map (nullable) translates node ids.
+int run_lttb_walk(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
+                  const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev) {
+  RC_TRY(ensure(ctx, ctx->cent, (size_t)std::max<int64_t>(nb, 1) * sizeof(double2)));
+  double2* cent = (double2*)ctx->cent.p;
+  unsigned gc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 16, (nb + 7) / 8));
+  YDT_SWITCH(ydt, (lttb_centroid_kernel<YD><<<gc, 256, 0, ctx->stream>>>(xf, drop, y, off, nb, cent)));
+  LAUNCH_CHECK();
+  // scratch for the small-bucket (jump) strategy when buckets are small on average
+  LttbScratch S{nullptr, nullptr, nullptr};
+  int levels = 1;
+  while (((int64_t)1 << levels) <= nb + 1) levels++;
+  int64_t nodes_cap = 0;
+  const int64_t avg = (n - 2) / std::max<int64_t>(nb, 1);
+  if (avg <= SMALL_MAX / 2 && n <= ((int64_t)1 << 24)) {
+    size_t bytes = (size_t)(nb + 1) * 4 + (size_t)n * 4 + (size_t)levels * n * 4 + 64;
+    RC_TRY(ensure(ctx, ctx->scratch, bytes));
+    char* p = (char*)ctx->scratch.p;
+    S.firstne = (int32_t*)p;
+    p += ((nb + 1) * 4 + 15) & ~15;
+    S.bk = (int32_t*)p;
+    p += (n * 4 + 15) & ~15;
+    S.jump = (int32_t*)p;
+    nodes_cap = n;
+  }
+  YDT_SWITCH(ydt, (lttb_walk_kernel<YD><<<1, LTTB_THREADS, 0, ctx->stream>>>(
+                      xf, drop, y, n, off, nb, cent, map, out_dev + 1, out_dev, S, nodes_cap, levels)));
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
+int to_f64(tsds_ctx* ctx, const void* x, int xdt, int64_t n, DevBuf& buf, const double** xf) {
+  if (xdt == DT_F64) {
+    *xf = (const double*)x;
+    return TSDS_OK;
+  }
+  RC_TRY(ensure(ctx, buf, (size_t)n * 8));
+  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (n + 255) / 256));
+  XDT_SWITCH(xdt, (to_f64_kernel<XD><<<grid, 256, 0, ctx->stream>>>(x, n, (double*)buf.p)));
+  LAUNCH_CHECK();
+  *xf = (const double*)buf.p;
+  return TSDS_OK;
+}
+
+int gather(tsds_ctx* ctx, const void* src, int dt, const int64_t* idx, int64_t m, DevBuf& dst) {
+  int es = dtype_size(dt);
+  RC_TRY(ensure(ctx, dst, (size_t)m * es));
+  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (m + 255) / 256));
+  switch (es) {
+    case 1: gather_kernel<1><<<grid, 256, 0, ctx->stream>>>(src, idx, m, dst.p); break;
+    case 2: gather_kernel<2><<<grid, 256, 0, ctx->stream>>>(src, idx, m, dst.p); break;
+    case 4: gather_kernel<4><<<grid, 256, 0, ctx->stream>>>(src, idx, m, dst.p); break;
+    default: gather_kernel<8><<<grid, 256, 0, ctx->stream>>>(src, idx, m, dst.p); break;
+  }
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
+// interior offsets (algorithms.py:66-79): bins over 1..n-2 (+1).  Fills
+// either a formula BinSpec or ctx->off.  x_eff is NULL when x was dropped.
+int interior_bins(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int64_t nb, int mem, BinSpec* bins,
+                  ScanArgs* guards, const void** x_keep) {
+  *bins = BinSpec{0, nullptr, n - 2, nb, 1};
+  *x_keep = nullptr;
+  if (!x) return TSDS_OK;
+  const int es = dtype_size(xdt);
+  if (mem == TSDS_MEM_HOST) {
+    if (tsds_host_is_uniform_spaced(x, xdt, n)) return TSDS_OK;  // api.py:26-28
+    std::vector<int64_t> off(nb + 1);
+    int rc = tsds_host_equal_width_offsets((const char*)x + es, xdt, n - 2, nb, off.data());
+    if (rc == TSDS_ERR_SPAN) return set_err(rc, "invalid index span");
+    for (auto& v : off) v += 1;
+    RC_TRY(upload(ctx, ctx->off, off.data(), off.size() * 8));
+    *bins = BinSpec{1, (const int64_t*)ctx->off.p, 0, 0, 0};
+    guards->independent = !host_monotone(off);
+    *x_keep = x;
+    return TSDS_OK;
+  }
+  RC_TRY(ensure(ctx, ctx->off, (size_t)(nb + 1) * 8));
+  int64_t* off = (int64_t*)ctx->off.p;
+  RC_TRY(launch_uniform(ctx, x, xdt, n, &misc(ctx)->mis_api));
+  RC_TRY(launch_uniform(ctx, (const char*)x + es, xdt, n - 2, &misc(ctx)->mis_slice));
+  RC_TRY(launch_width(ctx, (const char*)x + es, xdt, n - 2, nb, 1, &misc(ctx)->mis_slice, 0, &misc(ctx)->mis_api,
+                      off));
+  *bins = BinSpec{1, off, 0, 0, 0};
+  guards->abort_flag = &misc(ctx)->status;
+  guards->nonmono_flag = &misc(ctx)->nonmono;
+  *x_keep = x;
+  return TSDS_OK;
+}
+
+int run_lttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, int64_t n, int64_t n_out, int mem,
+             int64_t* out, int64_t* out_len) {
+  const int64_t nb = n_out - 2;
+  BinSpec bins;
+  ScanArgs guards = scan_args(nullptr, BinSpec{}, 0, 0, 0, 0);
+  const void* xk;
+  RC_TRY(interior_bins(ctx, x, xdt, n, nb, mem, &bins, &guards, &xk));
+  const int64_t* off;
+  if (bins.mode == 0) {
+    RC_TRY(ensure(ctx, ctx->off, (size_t)(nb + 1) * 8));
+    RC_TRY(launch_count_offsets(ctx, n - 2, nb, 1, (int64_t*)ctx->off.p));
+  }
+  off = (const int64_t*)ctx->off.p;
+  const void* dy;
+  RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
+  const double* xf = nullptr;
+  const int* drop = nullptr;
+  if (xk) {
+    const void* dx;
+    RC_TRY(stage_input(ctx, ctx->x, xk, (size_t)n * dtype_size(xdt), mem, &dx));
+    RC_TRY(to_f64(ctx, dx, xdt, n, ctx->xf64, &xf));
+    if (mem == TSDS_MEM_DEVICE) drop = &misc(ctx)->mis_api;
+  }
+  RC_TRY(ensure(ctx, ctx->out, (size_t)(n_out + 2) * 8));
+  int64_t* dout = (int64_t*)ctx->out.p;
+  // the walk never runs on a failed binning: status is checked at fetch;
+  // guard by skipping the walk when the host already knows (host path), and
+  // on the device path the walk reads offsets that the width kernel wrote
+  // (on error they are stale but in-bounds only if monotone) -> sync first.
+  if (mem == TSDS_MEM_DEVICE && x) {
+    int hs = 0;
+    CUDA_TRY(cudaMemcpyAsync(&hs, &misc(ctx)->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    RC_TRY(finish_status(ctx, &hs));
+  }
+  RC_TRY(run_lttb_walk(ctx, xf, drop, dy, ydt, n, off, nb, nullptr, dout));
+  return fetch_result(ctx, dout, n_out, out, out_len);
+}
+
+int run_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, int64_t n, int64_t n_out,
+                   int64_t ratio, int nan_mode, int mem, int64_t* out, int64_t* out_len) {
+  const int64_t nsub = (n_out - 2) * ((ratio + 1) / 2);
+  ScanArgs A = scan_args(nullptr, BinSpec{}, 0, nsub, 1, n - 1);
+  const void* xk;
+  RC_TRY(interior_bins(ctx, x, xdt, n, nsub, mem, &A.bins, &A, &xk));
+  const void* dy;
+  RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
+  const int64_t fcap = 2 * nsub + 2;
+  RC_TRY(ensure(ctx, ctx->full, (size_t)(fcap + 1) * 8));
+  int64_t* dfull = (int64_t*)ctx->full.p;
+  A.y = dy;
+  A.epi = EPI_MINMAX;
+  A.out = dfull + 1;
+  A.out_count = dfull;
+  A.lttb_frame = 1;
+  A.n_frame = n;
+  RC_TRY(launch_scan(ctx, ydt, nan_mode, A));
+  // stage boundary: the candidate count decides stage 2
+  RC_TRY(ensure_host(ctx, (size_t)(fcap + 2) * 8 + 64));
+  int64_t* h = (int64_t*)ctx->h_pin;
+  int* hs = (int*)(h + fcap + 1);
+  CUDA_TRY(cudaMemcpyAsync(h, dfull, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(hs, &misc(ctx)->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  RC_TRY(finish_status(ctx, hs));
+  const int64_t m = h[0];
+  if (m <= n_out) return fetch_result(ctx, dfull, m, out, out_len);
+  const int64_t* full = dfull + 1;
+  const int64_t nb2 = n_out - 2;
+  RC_TRY(gather(ctx, dy, ydt, full, m, ctx->y2));
+  const double* x2f = nullptr;
+  int64_t* off2;
+  RC_TRY(ensure(ctx, ctx->off, (size_t)(nb2 + 1) * 8));
+  off2 = (int64_t*)ctx->off.p;
+  if (!xk) {
+    // candidate positions stand in for x (algorithms.py:244-250)
+    RC_TRY(to_f64(ctx, full, DT_I64, m, ctx->x2f64, &x2f));
+    RC_TRY(launch_count_offsets(ctx, m - 2, nb2, 1, off2));
+  } else if (mem == TSDS_MEM_HOST) {
+    // gather x[full] on the host (m ~ 2*nsub values), bin on the host
+    std::vector<int64_t> hfull(m);
+    CUDA_TRY(cudaMemcpyAsync(hfull.data(), full, (size_t)m * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    const int es = dtype_size(xdt);
+    std::vector<char> x2((size_t)m * es);
+    for (int64_t i = 0; i < m; i++) memcpy(&x2[(size_t)i * es], (const char*)xk + (size_t)hfull[i] * es, es);
+    std::vector<int64_t> o2(nb2 + 1);
+    int rc = tsds_host_equal_width_offsets(x2.data() + es, xdt, m - 2, nb2, o2.data());
+    if (rc == TSDS_ERR_SPAN) return set_err(rc, "invalid index span");
+    for (auto& v : o2) v += 1;
+    RC_TRY(upload(ctx, ctx->off, o2.data(), o2.size() * 8));
+    RC_TRY(upload(ctx, ctx->x2, x2.data(), x2.size()));
+    RC_TRY(to_f64(ctx, ctx->x2.p, xdt, m, ctx->x2f64, &x2f));
+  } else {
+    RC_TRY(gather(ctx, xk, xdt, full, m, ctx->x2));
+    const int es = dtype_size(xdt);
+    RC_TRY(launch_uniform(ctx, (const char*)ctx->x2.p + es, xdt, m - 2, &misc(ctx)->mis2));
+    RC_TRY(launch_width(ctx, (const char*)ctx->x2.p + es, xdt, m - 2, nb2, 1, &misc(ctx)->mis2, 0, nullptr, off2));
+    RC_TRY(to_f64(ctx, ctx->x2.p, xdt, m, ctx->x2f64, &x2f));
+    int hs2 = 0;
+    CUDA_TRY(cudaMemcpyAsync(&hs2, &misc(ctx)->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    RC_TRY(finish_status(ctx, &hs2));
+  }
+  RC_TRY(ensure(ctx, ctx->out, (size_t)(n_out + 2) * 8));
+  int64_t* dout = (int64_t*)ctx->out.p;
+  RC_TRY(run_lttb_walk(ctx, x2f, nullptr, ctx->y2.p, ydt, m, off2, nb2, full, dout));
+  return fetch_result(ctx, dout, n_out, out, out_len);
+}
+
+__global__ void iota_rows_kernel(int64_t* out, int64_t S, int64_t L, int64_t n_out, int64_t* counts) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < S * L; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = t / L, i = t - s * L;
+    out[s * n_out + i] = i;
+    if (i == 0) counts[s] = L;
+  }
+}
+
+int identity(tsds_ctx* ctx, int64_t n, int64_t* out, int64_t* out_len) {
+  for (int64_t i = 0; i < n; i++) out[i] = i;
+  *out_len = n;
+  return TSDS_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+
+extern "C" {
+
+int tsds_version(void) { return 100; }
+
+const char* tsds_last_error(void) { return g_err.c_str(); }
+
+int tsds_device_count(int* count) {
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return set_err(TSDS_ERR_CUDA, cudaGetErrorString(e));
+  }
+  return TSDS_OK;
+}
+
+int tsds_ctx_create(int device, tsds_ctx** out) {
+  *out = nullptr;
+  tsds_ctx* ctx = new tsds_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return set_err(TSDS_ERR_CUDA, std::string("tsds_ctx_create: ") + cudaGetErrorString(e));
+  }
+  *out = ctx;
+  return TSDS_OK;
+}
+
+void tsds_ctx_destroy(tsds_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (DevBuf* b : {&ctx->y, &ctx->x, &ctx->xf64, &ctx->part, &ctx->bincnt, &ctx->res, &ctx->off, &ctx->out,
+                    &ctx->misc, &ctx->cent, &ctx->scratch, &ctx->y2, &ctx->x2, &ctx->x2f64, &ctx->full, &ctx->out2})
+    if (b->p) cudaFree(b->p);
+  if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int tsds_ctx_set_stream(tsds_ctx* ctx, void* s) {
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (s) {
+    ctx->stream = (cudaStream_t)s;
+    ctx->own_stream = false;
+  } else {
+    cudaSetDevice(ctx->device);
+    cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    ctx->own_stream = true;
+  }
+  return TSDS_OK;
+}
+
+void* tsds_ctx_stream(tsds_ctx* ctx) { return (void*)ctx->stream; }
+
+int tsds_ctx_synchronize(tsds_ctx* ctx) {
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return TSDS_OK;
+}
+
+int64_t tsds_ctx_launches(tsds_ctx* ctx) { return ctx->launches; }
+
+int tsds_downsample(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y, int ydt, int64_t n, int64_t n_out,
+                    int64_t ratio, int nan_mode, int mem, int64_t* out, int64_t* out_len) {
+  if (!ctx || !y || !out || !out_len || n < 1 || !dtype_ok(ydt) || (x && !xdtype_ok(xdt)))
+    return set_err(TSDS_ERR_ARG, "tsds_downsample: invalid argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  RC_TRY(begin_call(ctx));
+  switch (algo) {
+    case TSDS_MINMAX:
+    case TSDS_M4: {
+      const int width = algo == TSDS_MINMAX ? 2 : 4;
+      if (n_out < width || n_out % width) return set_err(TSDS_ERR_ARG, "invalid n_out");
+      if (n <= n_out) return identity(ctx, n, out, out_len);
+      RC_TRY(ensure(ctx, ctx->out, (size_t)(n_out + 1) * 8));
+      int64_t* d = (int64_t*)ctx->out.p;
+      RC_TRY(run_minmax_m4(ctx, algo, x, xdt, y, ydt, n, n_out, nan_mode, mem, d + 1, d));
+      return fetch_result(ctx, d, n_out, out, out_len);
+    }
+    case TSDS_LTTB:
+      if (n_out < 3) return set_err(TSDS_ERR_ARG, "n_out too small for LTTB");
+      if (n <= n_out) return identity(ctx, n, out, out_len);
+      return run_lttb(ctx, x, xdt, y, ydt, n, n_out, mem, out, out_len);
+    case TSDS_MINMAXLTTB:
+      if (n_out < 3) return set_err(TSDS_ERR_ARG, "n_out too small for LTTB");
+      if (ratio < 1) return set_err(TSDS_ERR_ARG, "invalid ratio");
+      if (n <= n_out * ratio) {
+        if (n <= n_out) return identity(ctx, n, out, out_len);
+        return run_lttb(ctx, x, xdt, y, ydt, n, n_out, mem, out, out_len);
+      }
+      return run_minmaxlttb(ctx, x, xdt, y, ydt, n, n_out, ratio, nan_mode, mem, out, out_len);
+    default:
+      return set_err(TSDS_ERR_ARG, "unknown algorithm");
+  }
+}
+
+int tsds_downsample_async(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y, int ydt, int64_t n,
+                          int64_t n_out, int nan_mode, int64_t* out_dev, int64_t* count_dev, int32_t* status_dev) {
+  if (!ctx || !y || !out_dev || !count_dev || n < 1 || !dtype_ok(ydt) || (x && !xdtype_ok(xdt)) ||
+      (algo != TSDS_MINMAX && algo != TSDS_M4))
+    return set_err(TSDS_ERR_ARG, "tsds_downsample_async: invalid argument");
+  const int width = algo == TSDS_MINMAX ? 2 : 4;
+  if (n_out < width || n_out % width) return set_err(TSDS_ERR_ARG, "invalid n_out");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  RC_TRY(begin_call(ctx));
+  if (n <= n_out) {
+    iota_kernel<<<(unsigned)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, ctx->stream>>>(out_dev, n, count_dev);
+    LAUNCH_CHECK();
+  } else {
+    RC_TRY(run_minmax_m4(ctx, algo, x, xdt, y, ydt, n, n_out, nan_mode, TSDS_MEM_DEVICE, out_dev, count_dev));
+  }
+  if (status_dev)
+    CUDA_TRY(cudaMemcpyAsync(status_dev, &misc(ctx)->status, sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
+  return TSDS_OK;
+}
+
+static int batched_enqueue(tsds_ctx* ctx, const void* dy, int ydt, int64_t S, int64_t L, int64_t n_out, int nan_mode,
+                           int64_t* out_dev, int64_t* counts_dev) {
+  const int64_t nb = n_out / 2;
+  ScanArgs A = scan_args(dy, BinSpec{0, nullptr, L, nb, 0}, 0, S * nb, 0, S * L);
+  A.epi = EPI_PAIR;
+  A.out = nullptr;
+  RC_TRY(launch_scan(ctx, ydt, nan_mode, A));
+  A.epi = EPI_MINMAX;
+  A.out = out_dev;
+  compact_series_kernel<<<(unsigned)S, 256, 0, ctx->stream>>>(A, nb, n_out, L, counts_dev);
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
+int tsds_minmax_batched_async(tsds_ctx* ctx, const void* y, int ydt, int64_t S, int64_t L, int64_t n_out,
+                              int nan_mode, int64_t* out_dev, int64_t* counts_dev) {
+  if (!ctx || !y || S < 1 || L < 1 || !dtype_ok(ydt) || n_out < 2 || n_out % 2)
+    return set_err(TSDS_ERR_ARG, "tsds_minmax_batched_async: invalid argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  RC_TRY(begin_call(ctx));
+  if (L <= n_out) {
+    iota_rows_kernel<<<(unsigned)std::min<int64_t>(4096, (S * L + 255) / 256), 256, 0, ctx->stream>>>(out_dev, S, L,
+                                                                                                     n_out, counts_dev);
+    LAUNCH_CHECK();
+    return TSDS_OK;
+  }
+  return batched_enqueue(ctx, y, ydt, S, L, n_out, nan_mode, out_dev, counts_dev);
+}
+
+int tsds_minmax_batched(tsds_ctx* ctx, const void* y, int ydt, int64_t S, int64_t L, int64_t n_out, int nan_mode,
+                        int mem, int64_t* out, int64_t* counts) {
+  if (!ctx || !y || !out || !counts || S < 1 || L < 1 || !dtype_ok(ydt) || n_out < 2 || n_out % 2)
+    return set_err(TSDS_ERR_ARG, "tsds_minmax_batched: invalid argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  RC_TRY(begin_call(ctx));
+  if (L <= n_out) {
+    for (int64_t s = 0; s < S; s++) {
+      for (int64_t i = 0; i < L; i++) out[s * n_out + i] = i;
+      counts[s] = L;
+    }
+    return TSDS_OK;
+  }
+  const void* dy;
+  RC_TRY(stage_input(ctx, ctx->y, y, (size_t)S * L * dtype_size(ydt), mem, &dy));
+  RC_TRY(ensure(ctx, ctx->out, (size_t)(S * n_out + S) * 8));
+  int64_t* dout = (int64_t*)ctx->out.p;
+  int64_t* dcnt = dout + S * n_out;
+  RC_TRY(batched_enqueue(ctx, dy, ydt, S, L, n_out, nan_mode, dout, dcnt));
+  CUDA_TRY(cudaMemcpyAsync(out, dout, (size_t)S * n_out * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(counts, dcnt, (size_t)S * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return TSDS_OK;
+}
+
+int tsds_argminmax(tsds_ctx* ctx, const void* y, int ydt, int64_t n, int nan_mode, int mem, int64_t* out2) {
+  if (!ctx || !y || !out2 || n < 1 || !dtype_ok(ydt)) return set_err(TSDS_ERR_ARG, "tsds_argminmax: invalid argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  RC_TRY(begin_call(ctx));
+  const void* dy;
+  RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
+  ScanArgs A = scan_args(dy, BinSpec{0, nullptr, n, 1, 0}, 0, 1, 0, n);
+  A.epi = EPI_PAIR;
+  A.out = &misc(ctx)->pair[0];
+  RC_TRY(launch_scan(ctx, ydt, nan_mode, A));
+  RC_TRY(ensure_host(ctx, 64));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_pin, &misc(ctx)->pair[0], 16, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  memcpy(out2, ctx->h_pin, 16);
+  return TSDS_OK;
+}
+
+// ------------------------------------------------------------------ operators
+
+int tsds_op_is_uniform_spaced(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int32_t* flag_dev) {
+  if (!ctx || !x || !flag_dev || !xdtype_ok(xdt)) return set_err(TSDS_ERR_ARG, "invalid argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  RC_TRY(begin_call(ctx));
+  RC_TRY(launch_uniform(ctx, x, xdt, n, &misc(ctx)->mis_slice));
+  // flag = 1 - mismatch
+  int h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h, &misc(ctx)->mis_slice, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  int32_t v = h ? 0 : 1;
+  CUDA_TRY(cudaMemcpyAsync(flag_dev, &v, sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return TSDS_OK;
+}
+
+int tsds_op_equal_count_offsets(tsds_ctx* ctx, int64_t len, int64_t nb, int64_t* off_dev) {
+  if (!ctx || !off_dev || nb < 1 || len < 0) return set_err(TSDS_ERR_ARG, "invalid bin count");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  return launch_count_offsets(ctx, len, nb, 0, off_dev);
+}
+
+int tsds_op_equal_width_offsets(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int64_t nb, int64_t* off_dev) {
+  if (!ctx || !off_dev || nb < 1 || !xdtype_ok(xdt) || (n > 0 && !x)) return set_err(TSDS_ERR_ARG, "invalid argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  RC_TRY(begin_call(ctx));
+  if (n >= 1) RC_TRY(launch_uniform(ctx, x, xdt, n, &misc(ctx)->mis_slice));
+  else CUDA_TRY(cudaMemsetAsync(&misc(ctx)->mis_slice, 0xff, sizeof(int), ctx->stream));
+  RC_TRY(launch_width(ctx, x, xdt, n, nb, 0, &misc(ctx)->mis_slice, 0, nullptr, off_dev));
+  int hs = 0;
+  CUDA_TRY(cudaMemcpyAsync(&hs, &misc(ctx)->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return finish_status(ctx, &hs);
+}
+
+static int op_bins(tsds_ctx* ctx, int epi, const void* y, int ydt, const int64_t* off, int64_t b0, int64_t b1,
+                   int nan_mode, int64_t* idx, int64_t* cnt) {
+  if (!ctx || !y || !off || !idx || !cnt || b1 < b0 || !dtype_ok(ydt)) return set_err(TSDS_ERR_ARG, "invalid argument");
+  if (b1 == b0) return TSDS_OK;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  RC_TRY(begin_call(ctx));
+  // offsets may be non-monotone for arbitrary callers: E0/E1 from the host
+  std::vector<int64_t> h(b1 - b0 + 1);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), off + b0, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  ScanArgs A = scan_args(y, BinSpec{1, off, 0, 0, 0}, b0, b1, h.front(), h.back());
+  A.independent = !host_monotone(h) || h.front() > h.back();
+  A.epi = epi;
+  A.out = idx;
+  A.out_count = cnt;
+  return launch_scan(ctx, ydt, nan_mode, A);
+}
+
+int tsds_op_minmax_bins(tsds_ctx* ctx, const void* y, int ydt, const int64_t* off, int64_t b0, int64_t b1,
+                        int nan_mode, int64_t* idx, int64_t* cnt) {
+  return op_bins(ctx, EPI_SLOTS_MINMAX, y, ydt, off, b0, b1, nan_mode, idx, cnt);
+}
+
+int tsds_op_m4_bins(tsds_ctx* ctx, const void* y, int ydt, const int64_t* off, int64_t b0, int64_t b1, int nan_mode,
+                    int64_t* idx, int64_t* cnt) {
+  return op_bins(ctx, EPI_SLOTS_M4, y, ydt, off, b0, b1, nan_mode, idx, cnt);
+}
+
+int tsds_op_lttb(tsds_ctx* ctx, const double* xf, const void* y, int ydt, int64_t n, const int64_t* off, int64_t nb,
+                 int64_t* out_dev, int64_t* m_host) {
+  if (!ctx || !y || !off || !out_dev || !m_host || n < 2 || nb < 1 || !dtype_ok(ydt))
+    return set_err(TSDS_ERR_ARG, "invalid argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  RC_TRY(begin_call(ctx));
+  RC_TRY(ensure(ctx, ctx->out2, (size_t)(nb + 3) * 8));
+  int64_t* d = (int64_t*)ctx->out2.p;
+  RC_TRY(run_lttb_walk(ctx, xf, nullptr, y, ydt, n, off, nb, nullptr, d));
+  int64_t m = 0;
+  CUDA_TRY(cudaMemcpyAsync(&m, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(out_dev, d + 1, (size_t)m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  *m_host = m;
+  return TSDS_OK;
+}
+
+}  // extern "C"

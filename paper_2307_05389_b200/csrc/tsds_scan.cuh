@@ -1,0 +1,406 @@
+// tsds_scan.cuh -- fused binning-aware argmin/argmax streaming kernel.
+//
+// Replaces the reference's per-bin writers (_kernels.py:300-356) driven by
+// `_run_bins` (algorithms.py:82-100), and their compaction
+// (_kernels.py:359-369), with ONE persistent launch:
+//
+//   * the bins' element span [off(g0), off(g1)) is cut into equal,
+//     16-byte-aligned chunks, one per resident warp (load balance is by
+//     bytes, independent of the bin layout);
+//   * a warp walks its chunk bin segment by bin segment: 128-bit streaming
+//     loads (ld.global.nc.L1::no_allocate, U vectors in flight per lane),
+//     per-lane running extrema, shuffle reduction of (key, index);
+//   * a bin fully inside one chunk is finalised by that warp; a bin spread
+//     over several chunks leaves one partial per chunk and the LAST warp to
+//     arrive (per-bin atomic counter) merges them -- the segmented second
+//     pass, without a second launch;
+//   * the last CTA of the grid compacts the per-bin picks into the dense,
+//     ascending index array (MinMax: sorted unique {lo, hi}; M4: sorted
+//     unique {s, lo, hi, e-1}).
+#pragma once
+
+#include "tsds_ops.cuh"
+
+namespace tsds {
+
+constexpr int SCAN_WARPS = 8;  // 256 threads per CTA
+
+enum Epilogue : int { EPI_MINMAX = 0, EPI_M4 = 1, EPI_PAIR = 2, EPI_SLOTS_MINMAX = 3, EPI_SLOTS_M4 = 4 };
+
+struct BinSpec {
+  int mode;            // 0: equal-count formula, 1: explicit offsets array
+  const int64_t* off;  // mode 1: offsets[0..nbins]
+  int64_t len;         // mode 0: series length L
+  int64_t nb;          // mode 0: bins per series
+  int64_t base;        // mode 0: offset added to every boundary
+};
+
+__device__ __forceinline__ int64_t bin_off(const BinSpec& b, int64_t g) {
+  if (b.mode == 1) return __ldg(b.off + g);
+  int64_t s = g / b.nb;
+  int64_t k = g - s * b.nb;
+  unsigned __int128 p = (unsigned __int128)(uint64_t)k * (uint64_t)b.len;
+  return s * b.len + b.base + (int64_t)(p / (uint64_t)b.nb);
+}
+
+// largest g in [g0, g1-1] with off(g) <= i   (warp-uniform result)
+__device__ __forceinline__ int64_t bin_of(const BinSpec& b, int64_t i, int64_t g0, int64_t g1) {
+  if (b.mode == 0) {
+    int64_t ip = i - b.base;
+    int64_t s = ip / b.len;
+    int64_t r = ip - s * b.len;
+    unsigned __int128 p = (unsigned __int128)(uint64_t)(r + 1) * (uint64_t)b.nb;
+    int64_t k = (int64_t)((p - 1) / (uint64_t)b.len);
+    if (k > b.nb - 1) k = b.nb - 1;
+    int64_t g = s * b.nb + k;
+    return g < g0 ? g0 : (g > g1 - 1 ? g1 - 1 : g);
+  }
+  // 32-ary search over the offsets array: invariant off(lo) <= i, answer in [lo, hi)
+  const int lane = threadIdx.x & 31;
+  int64_t lo = g0, hi = g1;
+  while (hi - lo > 1) {
+    int64_t step = (hi - lo + 31) / 32;
+    int64_t p = lo + (int64_t)lane * step;
+    bool ok = (p < hi) && (__ldg(b.off + p) <= i);
+    unsigned m = __ballot_sync(0xffffffffu, ok);
+    int last = 31 - __clz((int)m);  // lane 0 is always ok
+    lo = lo + (int64_t)last * step;
+    int64_t nhi = lo + step;
+    hi = nhi < hi ? nhi : hi;
+  }
+  return lo;
+}
+
+struct ScanArgs {
+  const void* y;       // element 0 of the indexed series
+  int64_t shift;       // (address of y mod 16) / sizeof(element)
+  BinSpec bins;
+  int64_t g0, g1;      // bins to process
+  int64_t E0, E1;      // element span off(g0) .. off(g1)
+  int64_t vstart;      // virtual (shifted) aligned start
+  int64_t che;         // chunk length in elements (multiple of VEC)
+  int64_t nchunks;
+  MinMaxCand* part;    // [nchunks][2] partials (0: head, 1: tail)
+  unsigned* bin_cnt;   // [g1-g0] arrival counters, zero between launches
+  int64_t* res;        // [g1-g0][2] picks (lo, hi)
+  unsigned* blocks_done;
+  // epilogue
+  int epi;
+  int64_t* out;        // compacted output (or idx slots)
+  int64_t* out_count;  // device scalar (or cnt array for slot epilogues)
+  int64_t idx_sub;     // subtracted from every output index
+  int lttb_frame;      // 1: out[0]=0 and out[total+1]=n_frame-1 (MinMaxLTTB `full`)
+  int64_t n_frame;
+  // guards
+  const int* abort_flag;    // non-zero -> binning failed ("invalid index span"): emit nothing
+  int independent;          // host-known non-monotone offsets
+  const int* nonmono_flag;  // device-known non-monotone offsets
+};
+
+// ------------------------------------------------------------------------
+// one bin segment [a, c) reduced by a warp
+
+template <int DT, bool PROP, int U>
+__device__ MinMaxCand seg_reduce(const ScanArgs& A, int64_t a, int64_t c) {
+  using O = Ops<DT>;
+  using E = typename O::E;
+  using R = typename O::R;
+  constexpr int VEC = O::VEC;
+  const int lane = threadIdx.x & 31;
+  const E* y = static_cast<const E*>(A.y);
+  const uint4* yv = reinterpret_cast<const uint4*>(y - A.shift);
+  MinMaxCand res{cand_none_min(), cand_none_max()};
+
+  auto scalar = [&](int64_t i) {
+    if constexpr (O::IEEE || (PROP && O::NANABLE)) {
+      if (elem_is_nan<DT>(y, i)) {
+        if constexpr (PROP) {
+          merge_min(res.mn, Cand{0ull, i});
+          merge_max(res.mx, Cand{KEY_MAX, i});
+        }
+        if constexpr (O::IEEE) return;  // plain IEEE: NaN is never picked here
+      }
+    }
+    uint64_t k = O::key(O::load(y, i));
+    merge_min(res.mn, Cand{k, i});
+    merge_max(res.mx, Cand{k, i});
+  };
+
+  const int64_t jb = (a + A.shift + VEC - 1) / VEC;
+  const int64_t je = (c + A.shift) / VEC;
+  if (jb >= je) {
+    for (int64_t i = a + lane; i < c; i += 32) scalar(i);
+  } else {
+    const int64_t hend = jb * VEC - A.shift;
+    if (a + lane < hend) scalar(a + lane);
+    const int64_t tbeg = je * VEC - A.shift;
+    if (tbeg + lane < c) scalar(tbeg + lane);
+
+    R rmn = O::min_init(), rmx = O::max_init();
+    int64_t jmn = -1, jmx = -1, jnan = -1;
+    auto step = [&](const uint4& v, int64_t jj) {
+      R vmn, vmx;
+      O::vminmax(v, vmn, vmx);
+      if (O::upd_min(vmn, rmn)) jmn = jj;
+      if (O::upd_max(vmx, rmx)) jmx = jj;
+      if constexpr (PROP && O::NANABLE) {
+        if (jnan < 0 && O::vec_hasnan(v)) jnan = jj;
+      }
+    };
+    int64_t j = jb + lane;
+    for (; j + 32 * (U - 1) < je; j += 32 * U) {
+      uint4 buf[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) buf[u] = ldg_stream(yv + j + 32 * u);
+#pragma unroll
+      for (int u = 0; u < U; u++) step(buf[u], j + 32 * u);
+    }
+    for (; j < je; j += 32) step(ldg_stream(yv + j), j);
+
+    if constexpr (O::FALLBACK) {
+      if (jb + lane < je) {
+        if (jmn < 0) jmn = jb + lane;
+        if (jmx < 0) jmx = jb + lane;
+      }
+    }
+    if (jmn >= 0 && O::valid(rmn)) {
+      uint4 v = __ldg(yv + jmn);
+      int p = 0;
+#pragma unroll
+      for (int q = VEC - 1; q >= 0; q--)
+        if (O::elem(v, q) == rmn) p = q;
+      merge_min(res.mn, Cand{O::key(rmn), jmn * VEC + p - A.shift});
+    }
+    if (jmx >= 0 && O::valid(rmx)) {
+      uint4 v = __ldg(yv + jmx);
+      int p = 0;
+#pragma unroll
+      for (int q = VEC - 1; q >= 0; q--)
+        if (O::elem(v, q) == rmx) p = q;
+      merge_max(res.mx, Cand{O::key(rmx), jmx * VEC + p - A.shift});
+    }
+    if constexpr (PROP && O::NANABLE) {
+      if (jnan >= 0) {
+        uint4 v = __ldg(yv + jnan);
+        int p = 0;
+#pragma unroll
+        for (int q = VEC - 1; q >= 0; q--)
+          if (O::elem_nan(v, q)) p = q;
+        int64_t idx = jnan * VEC + p - A.shift;
+        merge_min(res.mn, Cand{0ull, idx});
+        merge_max(res.mx, Cand{KEY_MAX, idx});
+      }
+    }
+  }
+  warp_reduce(res);
+  return res;
+}
+
+// ------------------------------------------------------------------------
+// finalisation of one bin's picks (reference NaN-first-slot rule, A.3)
+
+template <int DT, bool PROP>
+__device__ __forceinline__ void finalize(const ScanArgs& A, int64_t g, const MinMaxCand& r) {
+  int64_t lo = r.mn.idx, hi = r.mx.idx;
+  if constexpr (!PROP && Ops<DT>::IEEE) {
+    int64_t s = bin_off(A.bins, g);
+    if (elem_is_nan<DT>(A.y, s)) { lo = s; hi = s; }
+  }
+  int64_t* o = A.res + 2 * (g - A.g0);
+  o[0] = lo;
+  o[1] = hi;
+}
+
+// values emitted for bin g, sorted ascending; returns count
+__device__ __forceinline__ int bin_emit(const ScanArgs& A, int64_t g, int64_t v[4]) {
+  int64_t s = bin_off(A.bins, g), e = bin_off(A.bins, g + 1);
+  if (e <= s) return 0;
+  int64_t lo = ld_cg_i64(A.res + 2 * (g - A.g0));
+  int64_t hi = ld_cg_i64(A.res + 2 * (g - A.g0) + 1);
+  int64_t p = lo < hi ? lo : hi, q = lo < hi ? hi : lo;
+  if (A.epi == EPI_MINMAX || A.epi == EPI_SLOTS_MINMAX) {
+    v[0] = p;
+    if (p == q) return 1;
+    v[1] = q;
+    return 2;
+  }
+  int m = 1;
+  v[0] = s;
+  if (p > s) v[m++] = p;
+  if (q > v[m - 1]) v[m++] = q;
+  if (e - 1 > v[m - 1]) v[m++] = e - 1;
+  return m;
+}
+
+// One CTA compacts bins [ga, gb) into out[pos0 ...]; returns the count.
+__device__ int64_t cta_compact(const ScanArgs& A, int64_t ga, int64_t gb, int64_t* out, int64_t sub) {
+  __shared__ int64_t warp_tot[32];
+  __shared__ int64_t running;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) running = 0;
+  __syncthreads();
+  for (int64_t base = ga; base < gb; base += blockDim.x) {
+    int64_t g = base + tid;
+    int64_t v[4];
+    int c = g < gb ? bin_emit(A, g, v) : 0;
+    // block exclusive scan of c
+    int incl = c;
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, incl, m);
+      if (lane >= m) incl += t;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    int64_t before = running;
+    for (int w = 0; w < wid; w++) before += warp_tot[w];
+    int64_t pos = before + incl - c;
+    for (int t = 0; t < c; t++) out[pos + t] = v[t] - sub;
+    __syncthreads();
+    if (tid == 0) {
+      int64_t tot = 0;
+      for (int w = 0; w < nw; w++) tot += warp_tot[w];
+      running += tot;
+    }
+    __syncthreads();
+  }
+  return running;
+}
+
+// slot epilogue (reference writer layout idx[w*b + t], cnt[b])
+__device__ void cta_slots(const ScanArgs& A) {
+  const int width = A.epi == EPI_SLOTS_MINMAX ? 2 : 4;
+  for (int64_t g = A.g0 + threadIdx.x; g < A.g1; g += blockDim.x) {
+    int64_t v[4];
+    int c = bin_emit(A, g, v);
+    for (int t = 0; t < c; t++) A.out[width * (g - A.g0) + t] = v[t] - A.idx_sub;
+    A.out_count[g - A.g0] = c;
+  }
+}
+
+template <int DT, bool PROP, int U>
+__global__ void __launch_bounds__(SCAN_WARPS * 32)
+scan_kernel(const ScanArgs A) {
+  using O = Ops<DT>;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps_grid = (int64_t)gridDim.x * SCAN_WARPS;
+  const int64_t first = A.vstart - A.shift;  // element index of chunk 0 start (may be < E0)
+
+  const bool aborted = A.abort_flag && *(volatile const int*)A.abort_flag;
+  const bool indep = A.independent || (A.nonmono_flag && *(volatile const int*)A.nonmono_flag);
+  if (!aborted && indep) {
+    // non-monotone offsets (x violated its documented precondition): bins
+    // may overlap, so every bin is reduced on its own, like the reference.
+    for (int64_t g = A.g0 + (int64_t)blockIdx.x * SCAN_WARPS + (threadIdx.x >> 5); g < A.g1; g += nwarps_grid) {
+      int64_t s = bin_off(A.bins, g), e = bin_off(A.bins, g + 1);
+      if (e <= s) continue;
+      MinMaxCand r = seg_reduce<DT, PROP, U>(A, s, e);
+      if (lane == 0) finalize<DT, PROP>(A, g, r);
+    }
+  }
+  for (int64_t w = (int64_t)blockIdx.x * SCAN_WARPS + (threadIdx.x >> 5); !aborted && !indep && w < A.nchunks;
+       w += nwarps_grid) {
+    int64_t cs = first + w * A.che, ce = cs + A.che;
+    if (cs < A.E0) cs = A.E0;
+    if (ce > A.E1) ce = A.E1;
+    if (cs >= ce) continue;
+    int64_t g = bin_of(A.bins, cs, A.g0, A.g1);
+    int64_t pos = cs;
+    while (pos < ce && g < A.g1) {
+      int64_t s = bin_off(A.bins, g), e = bin_off(A.bins, g + 1);
+      if (e <= pos) { g++; continue; }
+      int64_t se = e < ce ? e : ce;
+      MinMaxCand r = seg_reduce<DT, PROP, U>(A, pos, se);
+      bool before = s < cs, after = e > ce;
+      if (!before && !after) {
+        if (lane == 0) finalize<DT, PROP>(A, g, r);
+      } else {
+        unsigned old = 0;
+        if (lane == 0) {
+          MinMaxCand* slot = A.part + 2 * w + (before ? 0 : 1);
+          slot->mn = r.mn;
+          slot->mx = r.mx;
+          __threadfence();
+          old = atomicAdd(A.bin_cnt + (g - A.g0), 1u);
+        }
+        old = __shfl_sync(0xffffffffu, old, 0);
+        int64_t wa = (s + A.shift - A.vstart) / A.che;
+        int64_t wb = (e - 1 + A.shift - A.vstart) / A.che;
+        if ((int64_t)old == wb - wa) {  // last arriver merges the partials
+          __threadfence();
+          MinMaxCand acc{cand_none_min(), cand_none_max()};
+          for (int64_t ww = wa + lane; ww <= wb; ww += 32) {
+            const MinMaxCand* sl = A.part + 2 * ww + (ww == wa ? 1 : 0);
+            Cand a{ld_cg_u64(&sl->mn.key), ld_cg_i64(&sl->mn.idx)};
+            Cand b{ld_cg_u64(&sl->mx.key), ld_cg_i64(&sl->mx.idx)};
+            merge_min(acc.mn, a);
+            merge_max(acc.mx, b);
+          }
+          warp_reduce(acc);
+          if (lane == 0) {
+            A.bin_cnt[g - A.g0] = 0u;
+            finalize<DT, PROP>(A, g, acc);
+          }
+        }
+      }
+      pos = se;
+      g++;
+    }
+  }
+
+  if (A.epi == EPI_PAIR && A.out == nullptr) return;
+  // ---- last CTA: compaction epilogue
+  __shared__ int is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned t = atomicAdd(A.blocks_done, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (aborted) {
+    if (threadIdx.x == 0) {
+      if (A.epi == EPI_SLOTS_MINMAX || A.epi == EPI_SLOTS_M4) {
+        for (int64_t g = A.g0; g < A.g1; g++) A.out_count[g - A.g0] = 0;
+      } else if (A.epi != EPI_PAIR) {
+        *A.out_count = 0;
+      }
+      *A.blocks_done = 0u;
+    }
+    return;
+  }
+  if (A.epi == EPI_SLOTS_MINMAX || A.epi == EPI_SLOTS_M4) {
+    cta_slots(A);
+  } else if (A.epi == EPI_PAIR) {
+    if (threadIdx.x == 0) {
+      A.out[0] = ld_cg_i64(A.res);
+      A.out[1] = ld_cg_i64(A.res + 1);
+    }
+  } else {
+    int64_t* out = A.out + (A.lttb_frame ? 1 : 0);
+    int64_t tot = cta_compact(A, A.g0, A.g1, out, A.idx_sub);
+    if (threadIdx.x == 0) {
+      if (A.lttb_frame) {
+        A.out[0] = 0;
+        A.out[tot + 1] = A.n_frame - 1;
+        tot += 2;
+      }
+      *A.out_count = tot;
+    }
+  }
+  if (threadIdx.x == 0) *A.blocks_done = 0u;
+}
+
+// batched compaction: one CTA per series (bins [s*nb, (s+1)*nb))
+__global__ void compact_series_kernel(const ScanArgs A, int64_t nb_per_series, int64_t n_out_stride,
+                                      int64_t series_len, int64_t* counts) {
+  int64_t s = blockIdx.x;
+  int64_t ga = A.g0 + s * nb_per_series, gb = ga + nb_per_series;
+  int64_t tot = cta_compact(A, ga, gb, A.out + s * n_out_stride, (ga / nb_per_series) * series_len);
+  if (threadIdx.x == 0) counts[s] = tot;
+}
+
+}  // namespace tsds

@@ -1,0 +1,187 @@
+"""GPU parity: the CUDA path (through libtsds.so) against the reference.
+
+Expected values come from the golden fixtures made by importing the real
+reference (tests/golden/make_golden.py), or from the pinned CPU oracle at
+sizes where no fixture exists.  Index work is bit-exact: every comparison
+is array equality.
+"""
+
+import numpy as np
+import pytest
+
+import golden_io as G
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ts():
+    import paper_2307_05389_b200 as m
+
+    return m
+
+
+def _args(x, y):
+    return (y,) if x is None else (x, y)
+
+
+@pytest.mark.parametrize("algo", ["minmax", "m4", "lttb", "minmaxlttb"])
+def test_sweep_matches_reference(ts, algo):
+    n = 0
+    for rec, x, y, want, _ in G.sweep(algo):
+        kw = {"minmax_ratio": rec["ratio"]} if algo == "minmaxlttb" else {}
+        got = ts.downsample(algo, *_args(x, y), n_out=rec["n_out"], **kw)
+        assert got.dtype == np.uint64
+        assert got.tolist() == want.tolist(), rec
+        n += 1
+    assert n >= 80
+
+
+def test_argminmax_cases(ts):
+    c, A = G.cases()
+    for case in c["argminmax"]:
+        assert list(ts.argminmax(A[case["y"]])) == case["want"], case["note"]
+
+
+def test_downsample_cases(ts):
+    c, A = G.cases()
+    for case in c["downsample"]:
+        y = A[case["y"]]
+        args = (y,) if case["x"] is None else (A[case["x"]], y)
+        got = ts.downsample(case["algo"], *args, n_out=case["n_out"], **case["kw"])
+        assert got.tolist() == case["want"], (case["algo"], case["note"])
+
+
+def test_equal_width_cases_host_and_device(ts):
+    import torch
+
+    c, A = G.cases()
+    for case in c["equal_width"]:
+        x = A[case["x"]]
+        if case["error"]:
+            with pytest.raises(ValueError, match=case["error"]):
+                ts.equal_width_boundaries(x, case["n_bins"])
+            continue
+        assert ts.equal_width_boundaries(x, case["n_bins"]).tolist() == case["want"], case["note"]
+        if x.shape[0] and x.dtype != np.uint32 and x.dtype != np.uint64:
+            xd = torch.from_numpy(x).cuda()
+            assert ts.equal_width_boundaries(xd, case["n_bins"]).tolist() == case["want"], case["note"]
+
+
+@pytest.mark.parametrize("algo", ["minmax", "m4", "minmaxlttb"])
+def test_nan_propagating_vs_oracle(ts, oracle, algo):
+    for i, tag in enumerate(["f16", "f32", "f64"] * 4):
+        n = [777, 5000, 20_000, 100_003][i // 3]
+        y = W.nan_series(tag, n, 40 + i, frac=0.002, at_starts=[0, n // 3])
+        n_out = 64 if algo != "minmaxlttb" else 50
+        got = ts.downsample("nan" + algo, y, n_out=n_out)
+        want = oracle.downsample(algo, y, n_out=n_out, nan=True)
+        assert got.tolist() == want.tolist(), (algo, tag, n)
+        plain = ts.downsample(algo, y, n_out=n_out)
+        assert plain.tolist() == oracle.downsample(algo, y, n_out=n_out).tolist(), (algo, tag, n)
+
+
+def test_device_inputs_equal_host(ts):
+    import torch
+
+    for rec, x, y, want, _ in list(G.sweep("m4"))[:30]:
+        if y.dtype in (np.uint16, np.uint32, np.uint64) or (x is not None and x.dtype in (np.uint32, np.uint64)):
+            continue
+        yd = torch.from_numpy(y).cuda()
+        xd = None if x is None else torch.from_numpy(x).cuda()
+        got = ts.downsample("m4", *_args(xd, yd), n_out=rec["n_out"])
+        assert got.tolist() == want.tolist(), rec
+    for rec, x, y, want, _ in list(G.sweep("minmaxlttb"))[:30]:
+        if y.dtype in (np.uint16, np.uint32, np.uint64) or (x is not None and x.dtype in (np.uint32, np.uint64)):
+            continue
+        yd = torch.from_numpy(y).cuda()
+        xd = None if x is None else torch.from_numpy(x).cuda()
+        got = ts.downsample("minmaxlttb", *_args(xd, yd), n_out=rec["n_out"], minmax_ratio=rec["ratio"])
+        assert got.tolist() == want.tolist(), rec
+
+
+def test_misaligned_and_tiny_bins(ts, oracle):
+    # slices that start at every offset within a 16-byte vector, bins of 1..70 elements
+    base = W.random_series("f32", 50_000, 3, ties=True)
+    for off in range(0, 5):
+        y = base[off:]
+        for n_out in (2, 4, 10, 1000, 20_000, 49_990):
+            got = ts.downsample("minmax", y, n_out=n_out)
+            assert got.tolist() == oracle.downsample("minmax", y, n_out=n_out).tolist(), (off, n_out)
+    for tag in W.ALL_TAGS:
+        y = W.random_series(tag, 30_001, 9, ties=True)[1:]
+        for n_out in (4, 8, 400, 7_500):
+            got = ts.downsample("m4", y, n_out=n_out)
+            assert got.tolist() == oracle.downsample("m4", y, n_out=n_out).tolist(), (tag, n_out)
+
+
+def test_all_equal_and_extreme_values(ts, oracle):
+    for tag in W.ALL_TAGS:
+        dt = W.DTYPES[tag]
+        for fill in ("zero", "max", "min"):
+            if fill == "zero":
+                y = np.zeros(70_001, dt)
+            elif dt in (np.float16, np.float32, np.float64):
+                y = np.full(70_001, np.inf if fill == "max" else -np.inf, dt)
+            else:
+                info = np.iinfo(dt)
+                y = np.full(70_001, info.max if fill == "max" else info.min, dt)
+            for algo, n_out in (("minmax", 40), ("m4", 40), ("minmaxlttb", 30)):
+                got = ts.downsample(algo, y, n_out=n_out)
+                assert got.tolist() == oracle.downsample(algo, y, n_out=n_out).tolist(), (tag, fill, algo)
+
+
+def test_whole_array_argminmax_large(ts, oracle):
+    for tag in ("f32", "u8", "i64", "f16"):
+        y = W.random_series(tag, 5_000_017, 5, ties=True)
+        assert ts.argminmax(y) == oracle.argminmax(y), tag
+
+
+def test_batched_rows_equal_single(ts, oracle):
+    for tag in ("i16", "u8", "f16"):
+        Y = W.config5(tag, S=24, L=200_000)
+        idx, cnt = ts.minmax_batched(Y, n_out=1000)
+        want, wcnt = oracle.minmax_batched(Y, n_out=1000)
+        assert np.array_equal(cnt, wcnt)
+        for s in range(Y.shape[0]):
+            assert idx[s, : cnt[s]].tolist() == want[s, : wcnt[s]].tolist(), (tag, s)
+
+
+def test_c1_config(ts):
+    g = G.configs()
+    y = W.config1()
+    assert ts.downsample("minmax", y, n_out=2000).tolist() == g["c1_minmax"].tolist()
+
+
+def test_c2_config_m4_and_nanm4(ts, oracle):
+    import torch
+
+    g = G.configs()
+    x, y = W.config2()
+    assert ts.downsample("m4", x, y, n_out=4000).tolist() == g["c2_m4"].tolist()
+    assert ts.downsample("minmax", x, y, n_out=4000).tolist() == g["c2_minmax"].tolist()
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    assert ts.downsample("m4", xd, yd, n_out=4000).tolist() == g["c2_m4"].tolist()
+    want_nan = oracle.downsample("m4", x, y, n_out=4000, nan=True, threads=8)
+    assert ts.downsample("nanm4", xd, yd, n_out=4000).tolist() == want_nan.tolist()
+
+
+def test_c3_config_lttb(ts):
+    g = G.configs()
+    y = W.config3()
+    assert ts.downsample("lttb", y, n_out=1000).tolist() == g["c3_lttb_1000"].tolist()
+    assert ts.downsample("lttb", y, n_out=10000).tolist() == g["c3_lttb_10000"].tolist()
+
+
+def test_c5_first_series_hashes(ts):
+    import hashlib
+
+    g = G.configs()
+    for tag in ("i16", "f16", "u8"):
+        Y = W.config5(tag, S=16)
+        idx, cnt = ts.minmax_batched(Y, n_out=1000)
+        for s in range(16):
+            row = idx[s, : cnt[s]]
+            h = int.from_bytes(hashlib.blake2b(row.astype("<u8").tobytes(), digest_size=8).digest(), "little")
+            assert h == int(g[f"c5_{tag}_hash"][s]), (tag, s)
