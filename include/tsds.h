@@ -66,6 +66,11 @@ void *tsds_ctx_stream(tsds_ctx *ctx);
 int tsds_ctx_synchronize(tsds_ctx *ctx);
 /* number of this library's kernels launched on ctx so far */
 int64_t tsds_ctx_launches(tsds_ctx *ctx);
+/* measurement hooks: record CUDA events around every argmin/argmax scan
+ * launch; _read synchronises, returns their summed duration and count, and
+ * clears the record */
+int tsds_ctx_profile(tsds_ctx *ctx, int enable);
+int tsds_ctx_profile_read(tsds_ctx *ctx, double *total_ms, int64_t *count);
 
 /* ---------------------------------------------------------------------------
  * Composed layer: one whole algorithm call.

@@ -34,6 +34,8 @@ EXPORTED = (
     "tsds_ctx_stream",
     "tsds_ctx_synchronize",
     "tsds_ctx_launches",
+    "tsds_ctx_profile",
+    "tsds_ctx_profile_read",
     "tsds_downsample",
     "tsds_downsample_async",
     "tsds_minmax_batched",
@@ -86,6 +88,8 @@ def load():
         L.tsds_ctx_synchronize.argtypes = [vp]
         L.tsds_ctx_launches.argtypes = [vp]
         L.tsds_ctx_launches.restype = i64
+        L.tsds_ctx_profile.argtypes = [vp, i32]
+        L.tsds_ctx_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), p64]
         L.tsds_downsample.argtypes = [vp, i32, vp, i32, vp, i32, i64, i64, i64, i32, i32, vp, p64]
         L.tsds_downsample_async.argtypes = [vp, i32, vp, i32, vp, i32, i64, i64, i32, vp, vp, vp]
         L.tsds_minmax_batched.argtypes = [vp, vp, i32, i64, i64, i64, i32, i32, vp, vp]

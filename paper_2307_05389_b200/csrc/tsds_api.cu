@@ -2,7 +2,7 @@
 //
 // The composed entry points reproduce algorithms.py (minmax/m4/lttb/
 // minmaxlttb, algorithms.py:118-255) as device pipelines:
-//   [x on device]  uniform_kernel -> width_offsets_kernel -> check_monotone
+//   [x on device]  binning_kernel (uniform checks + exact edge searches) -PDL-> scan
 //   [x on host]    tsds_host_* binning (only y crosses PCIe)
 //   scan_kernel (fused argminmax + segmented merge + compaction)
 //   LTTB: lttb_centroid_kernel -> lttb_walk_kernel (single CTA)
@@ -42,18 +42,13 @@ struct DevBuf {
 };
 
 struct Misc {
-  int mis_api;      // uniform check of the full x (0 = uniform)
-  int mis_slice;    // uniform check of an x slice
-  int status;       // TSDS_ERR_SPAN from binning
-  unsigned blocks_done;
-  int nonmono;      // offsets decrease somewhere
-  int mis2;         // stage-2 uniform check
-  int pad[10];
-  int64_t count;    // @64
+  PipeFlags F;         // binning/scan flags (zero between pipelines)
+  int status_copy;     // status exported by the resetting scan
+  int pad[15];
+  int64_t count;
   int64_t m2;
   int64_t pair[2];
 };
-constexpr size_t MISC_RESET = 32;  // bytes of Misc zeroed per call
 
 }  // namespace
 
@@ -67,7 +62,11 @@ struct tsds_ctx {
   void* h_pin = nullptr;
   size_t h_cap = 0;
   bool dirty = false;
+  bool flags_clean = false;  // Misc flags known to be zero on the device
   int64_t launches = 0;
+  // profiling: CUDA events around every scan-kernel launch (bench roofline)
+  bool profile = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
 };
 
 #define CUDA_TRY(call)                                                                              \
@@ -138,8 +137,12 @@ int begin_call(tsds_ctx* ctx) {
     // a failed call may have left arrival counters set: re-zero them
     if (ctx->bincnt.p) CUDA_TRY(cudaMemsetAsync(ctx->bincnt.p, 0, ctx->bincnt.cap, ctx->stream));
     ctx->dirty = false;
+    ctx->flags_clean = false;
   }
-  CUDA_TRY(cudaMemsetAsync(ctx->misc.p, 0, MISC_RESET, ctx->stream));
+  if (!ctx->flags_clean) {
+    CUDA_TRY(cudaMemsetAsync(ctx->misc.p, 0, sizeof(Misc), ctx->stream));
+    ctx->flags_clean = true;
+  }
   return TSDS_OK;
 }
 
@@ -161,31 +164,69 @@ int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
   }
   if ((uintptr_t)A.y % ES) return set_err(TSDS_ERR_ARG, "y is not aligned to its element size");
   A.shift = (int64_t)(((uintptr_t)A.y % 16) / ES);
-  const int64_t align = 32 * VEC;
+  const int64_t align = 32 * VEC;  // one 512-byte warp load
   A.vstart = ((A.E0 + A.shift) / align) * align;
-  int64_t vend = std::max(A.E1 + A.shift, A.vstart + 1);
-  int64_t tv = vend - A.vstart;
-  int64_t maxw = (int64_t)ctx->sms * occ * SCAN_WARPS;
-  const int64_t min_chunk_elems = 4096 / ES;
-  int64_t want = (tv + min_chunk_elems - 1) / min_chunk_elems;
-  int64_t nch = std::max<int64_t>(1, std::min(maxw, want));
-  int64_t che = (tv + nch - 1) / nch;
-  che = ((che + align - 1) / align) * align;
-  nch = (tv + che - 1) / che;
-  A.che = che;
-  A.nchunks = nch;
-  int64_t nbins = A.g1 - A.g0;
-  RC_TRY(ensure(ctx, ctx->part, (size_t)nch * 2 * sizeof(MinMaxCand)));
+  const int64_t vend = std::max(A.E1 + A.shift, A.vstart + 1);
+  const int64_t tv = vend - A.vstart;
+  const int64_t W = (int64_t)ctx->sms * occ * SCAN_WARPS;
+  // ~80% of the bytes in one static contiguous chunk per resident warp, the
+  // rest in 8 KB units handed out dynamically (absorbs SM-to-SM imbalance)
+  const int64_t unit = std::max<int64_t>(align, ((8192 / ES) / align) * align);
+  int64_t che = ((tv * 4 / 5) / W / align) * align;
+  if (che < 4 * unit) {
+    // small input: all static, >= 4 KB per chunk
+    const int64_t minc = std::max<int64_t>(align, ((4096 / ES + align - 1) / align) * align);
+    int64_t nch = std::max<int64_t>(1, std::min<int64_t>(W, (tv + minc - 1) / minc));
+    che = (((tv + nch - 1) / nch + align - 1) / align) * align;
+    A.che = che;
+    A.n_static = (tv + che - 1) / che;
+    A.dse = che;
+    A.n_dyn = 0;
+  } else {
+    A.che = che;
+    A.n_static = W;
+    A.dse = unit;
+    A.n_dyn = (tv - W * che + unit - 1) / unit;
+  }
+  const int64_t nchunks = A.n_static + A.n_dyn;
+  const int64_t nbins = A.g1 - A.g0;
+  RC_TRY(ensure(ctx, ctx->part, (size_t)nchunks * 2 * sizeof(MinMaxCand)));
   RC_TRY(ensure(ctx, ctx->bincnt, (size_t)nbins * sizeof(unsigned), true));
   RC_TRY(ensure(ctx, ctx->res, (size_t)nbins * 2 * sizeof(int64_t)));
   A.part = (MinMaxCand*)ctx->part.p;
   A.bin_cnt = (unsigned*)ctx->bincnt.p;
   A.res = (int64_t*)ctx->res.p;
-  A.blocks_done = &misc(ctx)->blocks_done;
-  int64_t grid = (nch + SCAN_WARPS - 1) / SCAN_WARPS;
-  if (A.independent || A.nonmono_flag) grid = std::max<int64_t>(grid, std::min<int64_t>(maxw / SCAN_WARPS, (nbins + SCAN_WARPS - 1) / SCAN_WARPS));
-  kern<<<(unsigned)grid, SCAN_WARPS * 32, 0, ctx->stream>>>(A);
+  A.flags = &misc(ctx)->F;
+  int64_t grid = std::min<int64_t>(W / SCAN_WARPS, (nchunks + SCAN_WARPS - 1) / SCAN_WARPS);
+  if (A.independent || A.check_flags)
+    grid = std::max<int64_t>(grid, std::min<int64_t>(W / SCAN_WARPS, (nbins + SCAN_WARPS - 1) / SCAN_WARPS));
+  grid = std::max<int64_t>(grid, 1);
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (ctx->profile) {
+    if (ctx->ev_free.empty()) {
+      CUDA_TRY(cudaEventCreate(&ev.first));
+      CUDA_TRY(cudaEventCreate(&ev.second));
+    } else {
+      ev = ctx->ev_free.back();
+      ctx->ev_free.pop_back();
+    }
+    CUDA_TRY(cudaEventRecord(ev.first, ctx->stream));
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(SCAN_WARPS * 32);
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ctx->profile ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
   LAUNCH_CHECK();
+  if (ctx->profile) {
+    CUDA_TRY(cudaEventRecord(ev.second, ctx->stream));
+    ctx->ev_used.push_back(ev);
+  }
   return TSDS_OK;
 }
 
@@ -255,24 +296,16 @@ ScanArgs scan_args(const void* y, BinSpec bins, int64_t g0, int64_t g1, int64_t 
     default: return set_err(TSDS_ERR_ARG, "unsupported dtype"); \
   }
 
-int launch_uniform(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int* mis) {
-  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 4, (n + 511) / 512));
-  XDT_SWITCH(xdt, (uniform_kernel<XD><<<grid, 256, 0, ctx->stream>>>(x, n, mis)));
+// one fused binning launch (uniform checks + edges + verdict); flags land in Misc.F
+int launch_binning(tsds_ctx* ctx, int xdt, const void* x, int64_t n, int64_t nb, int64_t add, const void* xapi,
+                   int64_t napi, int uniform_first, int materialize, int64_t* off) {
+  BinJob J{x, n, nb, add, xapi, napi, uniform_first, materialize, off, &misc(ctx)->F};
+  const int64_t edge_blocks = (nb + 7) / 8;
+  const int64_t piece_blocks = (std::max(n, napi) + 511) / 512;
+  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 4, std::max(edge_blocks, piece_blocks)));
+  XDT_SWITCH(xdt, (binning_kernel<XD><<<grid, 256, 0, ctx->stream>>>(J)));
   LAUNCH_CHECK();
-  return TSDS_OK;
-}
-
-// device equal-width offsets (+add) for x[0..n) into off; writes misc->status on span error
-int launch_width(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int64_t nb, int64_t add, int* mis,
-                 int uniform_first, const int* api_mis, int64_t* off) {
-  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (nb + 1 + 7) / 8));
-  int* status = &misc(ctx)->status;
-  XDT_SWITCH(xdt, (width_offsets_kernel<XD><<<grid, 256, 0, ctx->stream>>>(x, n, nb, add, mis, uniform_first,
-                                                                            api_mis, off, status)));
-  LAUNCH_CHECK();
-  check_monotone_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ctx->sms, (nb + 255) / 256)), 256, 0,
-                          ctx->stream>>>(off, nb, status, &misc(ctx)->nonmono);
-  LAUNCH_CHECK();
+  ctx->flags_clean = false;
   return TSDS_OK;
 }
 
@@ -318,8 +351,11 @@ int fetch_result(tsds_ctx* ctx, const int64_t* dev, int64_t cap, int64_t* out, i
   int64_t* h = (int64_t*)ctx->h_pin;
   int* hs = (int*)(h + cap + 1);
   CUDA_TRY(cudaMemcpyAsync(h, dev, (size_t)(cap + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(cudaMemcpyAsync(hs, &misc(ctx)->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(hs, &misc(ctx)->F.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(hs + 1, &misc(ctx)->status_copy, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (hs[0] == 0) hs[0] = hs[1];
+  if (hs[0] != 0) ctx->flags_clean = false;
   RC_TRY(finish_status(ctx, hs));
   int64_t m = h[0];
   if (m < 0 || m > cap) return set_err(TSDS_ERR_CUDA, "corrupt result count");
@@ -349,12 +385,12 @@ int run_minmax_m4(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y
     } else {
       RC_TRY(ensure(ctx, ctx->off, (size_t)(nb + 1) * 8));
       int64_t* off = (int64_t*)ctx->off.p;
-      RC_TRY(launch_uniform(ctx, x, xdt, n, &misc(ctx)->mis_api));
-      RC_TRY(launch_width(ctx, x, xdt, n, nb, 0, &misc(ctx)->mis_api, 1, nullptr, off));
-      A.bins.mode = 1;
+      RC_TRY(launch_binning(ctx, xdt, x, n, nb, 0, nullptr, 0, 1, 0, off));
       A.bins.off = off;
-      A.abort_flag = &misc(ctx)->status;
-      A.nonmono_flag = &misc(ctx)->nonmono;
+      A.use_dyn_mode = 1;
+      A.check_flags = 1;
+      A.reset_flags = 1;
+      A.status_out = &misc(ctx)->status_copy;
     }
   }
   const void* dy;
@@ -363,7 +399,9 @@ int run_minmax_m4(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y
   A.epi = algo == TSDS_MINMAX ? EPI_MINMAX : EPI_M4;
   A.out = out_dev;
   A.out_count = count_dev;
-  return launch_scan(ctx, ydt, nan_mode, A);
+  RC_TRY(launch_scan(ctx, ydt, nan_mode, A));
+  if (A.reset_flags) ctx->flags_clean = true;
+  return TSDS_OK;
 }
 
 __global__ void iota_kernel(int64_t* out, int64_t n, int64_t* count) {
@@ -439,7 +477,7 @@ int gather(tsds_ctx* ctx, const void* src, int dt, const int64_t* idx, int64_t m
 // interior offsets (algorithms.py:66-79): bins over 1..n-2 (+1).  Fills
 // either a formula BinSpec or ctx->off.  x_eff is NULL when x was dropped.
 int interior_bins(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int64_t nb, int mem, BinSpec* bins,
-                  ScanArgs* guards, const void** x_keep) {
+                  ScanArgs* guards, const void** x_keep, int materialize) {
   *bins = BinSpec{0, nullptr, n - 2, nb, 1};
   *x_keep = nullptr;
   if (!x) return TSDS_OK;
@@ -458,13 +496,10 @@ int interior_bins(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int64_t nb, 
   }
   RC_TRY(ensure(ctx, ctx->off, (size_t)(nb + 1) * 8));
   int64_t* off = (int64_t*)ctx->off.p;
-  RC_TRY(launch_uniform(ctx, x, xdt, n, &misc(ctx)->mis_api));
-  RC_TRY(launch_uniform(ctx, (const char*)x + es, xdt, n - 2, &misc(ctx)->mis_slice));
-  RC_TRY(launch_width(ctx, (const char*)x + es, xdt, n - 2, nb, 1, &misc(ctx)->mis_slice, 0, &misc(ctx)->mis_api,
-                      off));
-  *bins = BinSpec{1, off, 0, 0, 0};
-  guards->abort_flag = &misc(ctx)->status;
-  guards->nonmono_flag = &misc(ctx)->nonmono;
+  RC_TRY(launch_binning(ctx, xdt, (const char*)x + es, n - 2, nb, 1, x, n, 0, materialize, off));
+  bins->off = off;  // formula fields stay valid for the equal-count verdict
+  guards->use_dyn_mode = 1;
+  guards->check_flags = 1;
   *x_keep = x;
   return TSDS_OK;
 }
@@ -475,9 +510,9 @@ int run_lttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, int6
   BinSpec bins;
   ScanArgs guards = scan_args(nullptr, BinSpec{}, 0, 0, 0, 0);
   const void* xk;
-  RC_TRY(interior_bins(ctx, x, xdt, n, nb, mem, &bins, &guards, &xk));
+  RC_TRY(interior_bins(ctx, x, xdt, n, nb, mem, &bins, &guards, &xk, 1));
   const int64_t* off;
-  if (bins.mode == 0) {
+  if (bins.mode == 0 && !guards.use_dyn_mode) {
     RC_TRY(ensure(ctx, ctx->off, (size_t)(nb + 1) * 8));
     RC_TRY(launch_count_offsets(ctx, n - 2, nb, 1, (int64_t*)ctx->off.p));
   }
@@ -490,7 +525,7 @@ int run_lttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, int6
     const void* dx;
     RC_TRY(stage_input(ctx, ctx->x, xk, (size_t)n * dtype_size(xdt), mem, &dx));
     RC_TRY(to_f64(ctx, dx, xdt, n, ctx->xf64, &xf));
-    if (mem == TSDS_MEM_DEVICE) drop = &misc(ctx)->mis_api;
+    if (mem == TSDS_MEM_DEVICE) drop = &misc(ctx)->F.mis_api;
   }
   RC_TRY(ensure(ctx, ctx->out, (size_t)(n_out + 2) * 8));
   int64_t* dout = (int64_t*)ctx->out.p;
@@ -500,8 +535,9 @@ int run_lttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, int6
   // (on error they are stale but in-bounds only if monotone) -> sync first.
   if (mem == TSDS_MEM_DEVICE && x) {
     int hs = 0;
-    CUDA_TRY(cudaMemcpyAsync(&hs, &misc(ctx)->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(&hs, &misc(ctx)->F.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (hs) ctx->flags_clean = false;
     RC_TRY(finish_status(ctx, &hs));
   }
   RC_TRY(run_lttb_walk(ctx, xf, drop, dy, ydt, n, off, nb, nullptr, dout));
@@ -513,7 +549,7 @@ int run_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt
   const int64_t nsub = (n_out - 2) * ((ratio + 1) / 2);
   ScanArgs A = scan_args(nullptr, BinSpec{}, 0, nsub, 1, n - 1);
   const void* xk;
-  RC_TRY(interior_bins(ctx, x, xdt, n, nsub, mem, &A.bins, &A, &xk));
+  RC_TRY(interior_bins(ctx, x, xdt, n, nsub, mem, &A.bins, &A, &xk, 0));
   const void* dy;
   RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
   const int64_t fcap = 2 * nsub + 2;
@@ -525,14 +561,19 @@ int run_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt
   A.out_count = dfull;
   A.lttb_frame = 1;
   A.n_frame = n;
+  if (A.check_flags) {
+    A.reset_flags = 1;
+    A.status_out = &misc(ctx)->status_copy;
+  }
   RC_TRY(launch_scan(ctx, ydt, nan_mode, A));
   // stage boundary: the candidate count decides stage 2
   RC_TRY(ensure_host(ctx, (size_t)(fcap + 2) * 8 + 64));
   int64_t* h = (int64_t*)ctx->h_pin;
   int* hs = (int*)(h + fcap + 1);
   CUDA_TRY(cudaMemcpyAsync(h, dfull, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(cudaMemcpyAsync(hs, &misc(ctx)->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(hs, &misc(ctx)->status_copy, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (*hs) ctx->flags_clean = false;
   RC_TRY(finish_status(ctx, hs));
   const int64_t m = h[0];
   if (m <= n_out) return fetch_result(ctx, dfull, m, out, out_len);
@@ -565,11 +606,10 @@ int run_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt
   } else {
     RC_TRY(gather(ctx, xk, xdt, full, m, ctx->x2));
     const int es = dtype_size(xdt);
-    RC_TRY(launch_uniform(ctx, (const char*)ctx->x2.p + es, xdt, m - 2, &misc(ctx)->mis2));
-    RC_TRY(launch_width(ctx, (const char*)ctx->x2.p + es, xdt, m - 2, nb2, 1, &misc(ctx)->mis2, 0, nullptr, off2));
+    RC_TRY(launch_binning(ctx, xdt, (const char*)ctx->x2.p + es, m - 2, nb2, 1, nullptr, 0, 0, 1, off2));
     RC_TRY(to_f64(ctx, ctx->x2.p, xdt, m, ctx->x2f64, &x2f));
     int hs2 = 0;
-    CUDA_TRY(cudaMemcpyAsync(&hs2, &misc(ctx)->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(&hs2, &misc(ctx)->F.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     RC_TRY(finish_status(ctx, &hs2));
   }
@@ -662,6 +702,28 @@ int tsds_ctx_synchronize(tsds_ctx* ctx) {
 
 int64_t tsds_ctx_launches(tsds_ctx* ctx) { return ctx->launches; }
 
+int tsds_ctx_profile(tsds_ctx* ctx, int enable) {
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  ctx->profile = enable != 0;
+  return TSDS_OK;
+}
+
+int tsds_ctx_profile_read(tsds_ctx* ctx, double* total_ms, int64_t* count) {
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  double t = 0.0;
+  for (auto& ev : ctx->ev_used) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, ev.first, ev.second));
+    t += ms;
+    ctx->ev_free.push_back(ev);
+  }
+  *count = (int64_t)ctx->ev_used.size();
+  *total_ms = t;
+  ctx->ev_used.clear();
+  return TSDS_OK;
+}
+
 int tsds_downsample(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y, int ydt, int64_t n, int64_t n_out,
                     int64_t ratio, int nan_mode, int mem, int64_t* out, int64_t* out_len) {
   if (!ctx || !y || !out || !out_len || n < 1 || !dtype_ok(ydt) || (x && !xdtype_ok(xdt)))
@@ -712,7 +774,7 @@ int tsds_downsample_async(tsds_ctx* ctx, int algo, const void* x, int xdt, const
     RC_TRY(run_minmax_m4(ctx, algo, x, xdt, y, ydt, n, n_out, nan_mode, TSDS_MEM_DEVICE, out_dev, count_dev));
   }
   if (status_dev)
-    CUDA_TRY(cudaMemcpyAsync(status_dev, &misc(ctx)->status, sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(status_dev, &misc(ctx)->status_copy, sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
   return TSDS_OK;
 }
 
@@ -793,10 +855,10 @@ int tsds_op_is_uniform_spaced(tsds_ctx* ctx, const void* x, int xdt, int64_t n, 
   if (!ctx || !x || !flag_dev || !xdtype_ok(xdt)) return set_err(TSDS_ERR_ARG, "invalid argument");
   std::lock_guard<std::mutex> lk(ctx->mu);
   RC_TRY(begin_call(ctx));
-  RC_TRY(launch_uniform(ctx, x, xdt, n, &misc(ctx)->mis_slice));
-  // flag = 1 - mismatch
+  RC_TRY(ensure(ctx, ctx->off, 16));
+  RC_TRY(launch_binning(ctx, xdt, x, n, 1, 0, nullptr, 0, 0, 0, (int64_t*)ctx->off.p));
   int h = 0;
-  CUDA_TRY(cudaMemcpyAsync(&h, &misc(ctx)->mis_slice, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(&h, &misc(ctx)->F.mis_slice, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   int32_t v = h ? 0 : 1;
   CUDA_TRY(cudaMemcpyAsync(flag_dev, &v, sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
@@ -815,11 +877,9 @@ int tsds_op_equal_width_offsets(tsds_ctx* ctx, const void* x, int xdt, int64_t n
   if (!ctx || !off_dev || nb < 1 || !xdtype_ok(xdt) || (n > 0 && !x)) return set_err(TSDS_ERR_ARG, "invalid argument");
   std::lock_guard<std::mutex> lk(ctx->mu);
   RC_TRY(begin_call(ctx));
-  if (n >= 1) RC_TRY(launch_uniform(ctx, x, xdt, n, &misc(ctx)->mis_slice));
-  else CUDA_TRY(cudaMemsetAsync(&misc(ctx)->mis_slice, 0xff, sizeof(int), ctx->stream));
-  RC_TRY(launch_width(ctx, x, xdt, n, nb, 0, &misc(ctx)->mis_slice, 0, nullptr, off_dev));
+  RC_TRY(launch_binning(ctx, xdt, x, n, nb, 0, nullptr, 0, 0, 1, off_dev));
   int hs = 0;
-  CUDA_TRY(cudaMemcpyAsync(&hs, &misc(ctx)->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(&hs, &misc(ctx)->F.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return finish_status(ctx, &hs);
 }

@@ -46,11 +46,11 @@ __device__ __forceinline__ double xf64(const void* x, int64_t i) {
   return (double)__ldg((const typename XT<XDT>::T*)x + i);
 }
 
-// Sets *mismatch = 1 unless x[0..n) is uniformly spaced.  *mismatch must be
-// 0 on entry.  Blocks walk pieces in increasing order and stop as soon as
-// any block has seen a mismatch (the reference exits at the first one).
+// Block-level uniform-spacing check of x[0..n): sets *mismatch = 1 unless x
+// is uniformly spaced.  Blocks walk pieces in increasing order and stop as
+// soon as any block has seen a mismatch (the reference exits at the first).
 template <int XDT>
-__global__ void uniform_kernel(const void* xv, int64_t n, int* mismatch) {
+__device__ void uniform_pieces(const void* xv, int64_t n, int* mismatch) {
   using T = typename XT<XDT>::T;
   using D = typename XT<XDT>::D;
   const T* x = (const T*)xv;
@@ -67,6 +67,7 @@ __global__ void uniform_kernel(const void* xv, int64_t n, int* mismatch) {
   const int64_t ngaps = n - 2;  // gaps i = 1 .. n-2
   __shared__ int stop;
   for (int64_t p0 = (int64_t)blockIdx.x * piece; p0 < ngaps; p0 += (int64_t)gridDim.x * piece) {
+    __syncthreads();
     if (threadIdx.x == 0) stop = *(volatile int*)mismatch;
     __syncthreads();
     if (stop) return;
@@ -115,65 +116,103 @@ __device__ int64_t lower_bound_exact(const void* x, int64_t n, double edge) {
   return lo;
 }
 
-// Equal-width offsets for x[0..n), written as off[k] + add.
-//   api_mismatch (nullable): result of the api-level uniform check on the
-//     FULL x; 0 means x was dropped, so bins are equal-count;
-//   uniform_first = 1: api-level normalization order (api.py:19-28): a
-//     uniform x becomes equal-count bins before any span check;
-//   uniform_first = 0: equal_width_boundaries order (binning.py:61-82):
-//     empty / span checks first, then the uniform shortcut.
-// *mismatch is the result of uniform_kernel on the same x (0 = uniform).
+// One launch computes the bins of x[0..n) (binning.py:43-82 semantics):
+//   * uniform-spacing checks of the binned slice and (optionally) of the
+//     whole x for the api-level normalisation (api.py:19-28);
+//   * speculative equal-width edge searches (one warp per edge, exact
+//     reference probe sequence) running concurrently with the checks;
+//   * the last CTA applies the reference's decision order and publishes the
+//     verdict: flags->mode = 0 (equal-count formula; written into `off` when
+//     `materialize`), 1 (offsets array), flags->status = -2 for a
+//     non-finite span, flags->nonmono when the offsets decrease.
+// The scan kernel is launched as its programmatic dependent.
+struct BinJob {
+  const void* x;      // binned slice
+  int64_t n;
+  int64_t nb;
+  int64_t add;        // added to every offset (interior bins: +1)
+  const void* xapi;   // nullable: whole x for the api-level uniform check
+  int64_t napi;
+  int uniform_first;  // 1: a uniform slice short-circuits before span checks
+  int materialize;    // write equal-count offsets into `off` too
+  int64_t* off;       // [nb+1]
+  PipeFlags* F;
+};
+
 template <int XDT>
-__global__ void width_offsets_kernel(const void* x, int64_t n, int64_t nb, int64_t add,
-                                     const int* mismatch, int uniform_first, const int* api_mismatch,
-                                     int64_t* off, int* status) {
+__global__ void binning_kernel(const BinJob J) {
+  pdl_launch_dependents();
+  PipeFlags* F = J.F;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const bool uniform = (*mismatch) == 0;
-  int mode;  // 0 zeros, 1 zero-span, 2 equal-count, 3 edges, 4 error
-  double x0 = 0.0, span = 0.0;
-  if (api_mismatch && *api_mismatch == 0) {
-    mode = 2;  // the whole x was uniform: api.py:19-28 dropped it -> equal-count bins
-  } else if (uniform_first && uniform) {
-    mode = 2;
-  } else if (n == 0) {
-    mode = 0;
-  } else {
-    x0 = xf64<XDT>(x, 0);
-    double xn = xf64<XDT>(x, n - 1);
-    span = __dsub_rn(xn, x0);
-    if (!isfinite(span)) mode = 4;
-    else if (span == 0.0) mode = 1;
-    else if (uniform) mode = 2;
-    else mode = 3;
-  }
-  if (mode == 4) {
-    if (gw == 0 && lane == 0) *status = -2;
-    return;
-  }
-  for (int64_t k = gw; k <= nb; k += nwarps) {
-    int64_t v;
-    if (mode == 0) v = 0;
-    else if (mode == 1) v = (k == nb) ? n : 0;
-    else if (mode == 2) {
-      unsigned __int128 p = (unsigned __int128)(uint64_t)k * (uint64_t)n;
-      v = (int64_t)(p / (uint64_t)nb);
-    } else if (k == 0) v = 0;
-    else if (k == nb) v = n;
-    else {
-      double e = __dadd_rn(x0, __ddiv_rn(__dmul_rn((double)k, span), (double)nb));
-      v = lower_bound_exact<XDT>(x, n, e);
-    }
-    if (lane == 0) off[k] = v + add;
-  }
-}
+  const int64_t n = J.n, nb = J.nb;
 
-// flags offsets that decrease somewhere (non-monotone x)
-__global__ inline void check_monotone_kernel(const int64_t* off, int64_t nb, const int* abort_flag, int* flag) {
-  if (abort_flag && *abort_flag) return;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nb; k += (int64_t)gridDim.x * blockDim.x)
-    if (off[k + 1] < off[k]) atomicExch(flag, 1);
+  // speculative edges (valid whenever the verdict turns out to be "edges")
+  if (n > 0) {
+    const double x0 = xf64<XDT>(J.x, 0);
+    const double span = __dsub_rn(xf64<XDT>(J.x, n - 1), x0);
+    if (isfinite(span) && span != 0.0) {
+      for (int64_t k = 1 + gw; k < nb; k += nwarps) {
+        double e = __dadd_rn(x0, __ddiv_rn(__dmul_rn((double)k, span), (double)nb));
+        int64_t v = lower_bound_exact<XDT>(J.x, n, e);
+        if (lane == 0) J.off[k] = v + J.add;
+      }
+    }
+  }
+  uniform_pieces<XDT>(J.x, n, &F->mis_slice);
+  if (J.xapi) uniform_pieces<XDT>(J.xapi, J.napi, &F->mis_api);
+
+  __shared__ int s_last, s_mode;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = atomicAdd(&F->bin_blocks_done, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    const bool api_uniform = J.xapi && *(volatile int*)&F->mis_api == 0;
+    const bool sl_uniform = *(volatile int*)&F->mis_slice == 0;
+    int mode;  // 0 formula, 1 zeros, 2 zero span, 3 edges, 4 error
+    if (api_uniform || (J.uniform_first && sl_uniform)) {
+      mode = 0;
+    } else if (n == 0) {
+      mode = 1;
+    } else {
+      double x0 = xf64<XDT>(J.x, 0);
+      double span = __dsub_rn(xf64<XDT>(J.x, n - 1), x0);
+      mode = !isfinite(span) ? 4 : span == 0.0 ? 2 : sl_uniform ? 0 : 3;
+    }
+    s_mode = mode;
+    if (mode == 4) F->status = -2;
+    F->mode = mode == 0 ? 0 : 1;
+    F->bin_blocks_done = 0u;
+  }
+  __syncthreads();
+  const int mode = s_mode;
+  if (mode == 0) {
+    if (J.materialize)
+      for (int64_t k = threadIdx.x; k <= nb; k += blockDim.x) {
+        unsigned __int128 p = (unsigned __int128)(uint64_t)k * (uint64_t)n;
+        J.off[k] = (int64_t)(p / (uint64_t)nb) + J.add;
+      }
+  } else if (mode == 1 || mode == 2) {
+    for (int64_t k = threadIdx.x; k <= nb; k += blockDim.x)
+      J.off[k] = (mode == 2 && k == nb ? n : 0) + J.add;
+  } else if (mode == 3) {
+    if (threadIdx.x == 0) {
+      J.off[0] = J.add;
+      J.off[nb] = n + J.add;
+    }
+    __syncthreads();
+    bool bad = false;
+    for (int64_t k = threadIdx.x; k < nb; k += blockDim.x)
+      bad |= ld_cg_i64(J.off + k + 1) < ld_cg_i64(J.off + k);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) F->nonmono = 1;
+  }
 }
 
 // equal-count offsets (materialised; used by the operator-level C-ABI)

@@ -30,6 +30,29 @@ __host__ __device__ inline int dtype_size(int dt) {
 }
 
 constexpr int64_t IDX_NONE = INT64_MAX;
+
+// Device-resident flags shared by the binning and scan kernels of one
+// pipeline.  Zero between pipelines: the scan's last CTA clears what the
+// binning kernel set (after exporting the status word).
+struct PipeFlags {
+  int mis_api;     // api-level uniform check of the whole x: 1 = not uniform
+  int mis_slice;   // uniform check of the binned slice
+  int status;      // -2: "invalid index span"
+  int nonmono;     // offsets decrease somewhere (x not monotone)
+  int mode;        // binning verdict: 0 equal-count formula, 1 offsets array
+  unsigned bin_blocks_done;
+  unsigned scan_blocks_done;
+  int pad0;
+  unsigned long long work_ctr;  // dynamic work units handed out by the scan
+  unsigned long long pad1[3];
+};
+
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 constexpr uint64_t KEY_MAX = ~0ull;
 
 struct Cand {

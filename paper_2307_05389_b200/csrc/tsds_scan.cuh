@@ -74,16 +74,25 @@ __device__ __forceinline__ int64_t bin_of(const BinSpec& b, int64_t i, int64_t g
 struct ScanArgs {
   const void* y;       // element 0 of the indexed series
   int64_t shift;       // (address of y mod 16) / sizeof(element)
-  BinSpec bins;
+  BinSpec bins;        // static bin description (mode may be overridden at run time)
   int64_t g0, g1;      // bins to process
   int64_t E0, E1;      // element span off(g0) .. off(g1)
-  int64_t vstart;      // virtual (shifted) aligned start
-  int64_t che;         // chunk length in elements (multiple of VEC)
-  int64_t nchunks;
-  MinMaxCand* part;    // [nchunks][2] partials (0: head, 1: tail)
+  // work decomposition (virtual, 16-byte aligned element space):
+  // chunks [0, n_static) of `che` elements are owned by warp w (static),
+  // chunks [n_static, n_static + n_dyn) of `dse` elements are handed out
+  // dynamically, so SMs that stream faster absorb the tail.
+  int64_t vstart;
+  int64_t che, n_static;
+  int64_t dse, n_dyn;
+  MinMaxCand* part;    // [n_static + n_dyn][2] partials (0: head, 1: tail)
   unsigned* bin_cnt;   // [g1-g0] arrival counters, zero between launches
   int64_t* res;        // [g1-g0][2] picks (lo, hi)
-  unsigned* blocks_done;
+  PipeFlags* flags;
+  int use_dyn_mode;    // take the bin mode from flags->mode (set by binning_kernel)
+  int check_flags;     // honour flags->status (abort) and flags->nonmono
+  int reset_flags;     // clear the binning flags at the end (pipeline consumer)
+  int* status_out;     // nullable: receives flags->status before the reset
+  int independent;     // host-known non-monotone offsets
   // epilogue
   int epi;
   int64_t* out;        // compacted output (or idx slots)
@@ -91,11 +100,28 @@ struct ScanArgs {
   int64_t idx_sub;     // subtracted from every output index
   int lttb_frame;      // 1: out[0]=0 and out[total+1]=n_frame-1 (MinMaxLTTB `full`)
   int64_t n_frame;
-  // guards
-  const int* abort_flag;    // non-zero -> binning failed ("invalid index span"): emit nothing
-  int independent;          // host-known non-monotone offsets
-  const int* nonmono_flag;  // device-known non-monotone offsets
 };
+
+__device__ __forceinline__ int64_t chunk_of(const ScanArgs& A, int64_t i) {
+  int64_t v = i + A.shift - A.vstart;
+  int64_t st = A.n_static * A.che;
+  return v < st ? v / A.che : A.n_static + (v - st) / A.dse;
+}
+
+__device__ __forceinline__ void chunk_range(const ScanArgs& A, int64_t w, int64_t& cs, int64_t& ce) {
+  int64_t v0, len;
+  if (w < A.n_static) {
+    v0 = A.vstart + w * A.che;
+    len = A.che;
+  } else {
+    v0 = A.vstart + A.n_static * A.che + (w - A.n_static) * A.dse;
+    len = A.dse;
+  }
+  cs = v0 - A.shift;
+  ce = cs + len;
+  if (cs < A.E0) cs = A.E0;
+  if (ce > A.E1) ce = A.E1;
+}
 
 // ------------------------------------------------------------------------
 // one bin segment [a, c) reduced by a warp
@@ -200,10 +226,10 @@ __device__ MinMaxCand seg_reduce(const ScanArgs& A, int64_t a, int64_t c) {
 // finalisation of one bin's picks (reference NaN-first-slot rule, A.3)
 
 template <int DT, bool PROP>
-__device__ __forceinline__ void finalize(const ScanArgs& A, int64_t g, const MinMaxCand& r) {
+__device__ __forceinline__ void finalize(const ScanArgs& A, const BinSpec& B, int64_t g, const MinMaxCand& r) {
   int64_t lo = r.mn.idx, hi = r.mx.idx;
   if constexpr (!PROP && Ops<DT>::IEEE) {
-    int64_t s = bin_off(A.bins, g);
+    int64_t s = bin_off(B, g);
     if (elem_is_nan<DT>(A.y, s)) { lo = s; hi = s; }
   }
   int64_t* o = A.res + 2 * (g - A.g0);
@@ -212,8 +238,8 @@ __device__ __forceinline__ void finalize(const ScanArgs& A, int64_t g, const Min
 }
 
 // values emitted for bin g, sorted ascending; returns count
-__device__ __forceinline__ int bin_emit(const ScanArgs& A, int64_t g, int64_t v[4]) {
-  int64_t s = bin_off(A.bins, g), e = bin_off(A.bins, g + 1);
+__device__ __forceinline__ int bin_emit(const ScanArgs& A, const BinSpec& B, int64_t g, int64_t v[4]) {
+  int64_t s = bin_off(B, g), e = bin_off(B, g + 1);
   if (e <= s) return 0;
   int64_t lo = ld_cg_i64(A.res + 2 * (g - A.g0));
   int64_t hi = ld_cg_i64(A.res + 2 * (g - A.g0) + 1);
@@ -232,8 +258,9 @@ __device__ __forceinline__ int bin_emit(const ScanArgs& A, int64_t g, int64_t v[
   return m;
 }
 
-// One CTA compacts bins [ga, gb) into out[pos0 ...]; returns the count.
-__device__ int64_t cta_compact(const ScanArgs& A, int64_t ga, int64_t gb, int64_t* out, int64_t sub) {
+// One CTA compacts bins [ga, gb) into out[...]; returns the count.
+__device__ int64_t cta_compact(const ScanArgs& A, const BinSpec& B, int64_t ga, int64_t gb, int64_t* out,
+                               int64_t sub) {
   __shared__ int64_t warp_tot[32];
   __shared__ int64_t running;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
@@ -242,8 +269,7 @@ __device__ int64_t cta_compact(const ScanArgs& A, int64_t ga, int64_t gb, int64_
   for (int64_t base = ga; base < gb; base += blockDim.x) {
     int64_t g = base + tid;
     int64_t v[4];
-    int c = g < gb ? bin_emit(A, g, v) : 0;
-    // block exclusive scan of c
+    int c = g < gb ? bin_emit(A, B, g, v) : 0;
     int incl = c;
 #pragma unroll
     for (int m = 1; m < 32; m <<= 1) {
@@ -268,94 +294,107 @@ __device__ int64_t cta_compact(const ScanArgs& A, int64_t ga, int64_t gb, int64_
 }
 
 // slot epilogue (reference writer layout idx[w*b + t], cnt[b])
-__device__ void cta_slots(const ScanArgs& A) {
+__device__ void cta_slots(const ScanArgs& A, const BinSpec& B) {
   const int width = A.epi == EPI_SLOTS_MINMAX ? 2 : 4;
   for (int64_t g = A.g0 + threadIdx.x; g < A.g1; g += blockDim.x) {
     int64_t v[4];
-    int c = bin_emit(A, g, v);
+    int c = bin_emit(A, B, g, v);
     for (int t = 0; t < c; t++) A.out[width * (g - A.g0) + t] = v[t] - A.idx_sub;
     A.out_count[g - A.g0] = c;
+  }
+}
+
+// one chunk [cs, ce) walked bin segment by bin segment by a warp
+template <int DT, bool PROP, int U>
+__device__ __forceinline__ void process_chunk(const ScanArgs& A, const BinSpec& B, int64_t w) {
+  const int lane = threadIdx.x & 31;
+  int64_t cs, ce;
+  chunk_range(A, w, cs, ce);
+  if (cs >= ce) return;
+  int64_t g = bin_of(B, cs, A.g0, A.g1);
+  int64_t pos = cs;
+  while (pos < ce && g < A.g1) {
+    int64_t s = bin_off(B, g), e = bin_off(B, g + 1);
+    if (e <= pos) { g++; continue; }
+    int64_t se = e < ce ? e : ce;
+    MinMaxCand r = seg_reduce<DT, PROP, U>(A, pos, se);
+    bool before = s < cs, after = e > ce;
+    if (!before && !after) {
+      if (lane == 0) finalize<DT, PROP>(A, B, g, r);
+    } else {
+      unsigned old = 0;
+      if (lane == 0) {
+        MinMaxCand* slot = A.part + 2 * w + (before ? 0 : 1);
+        slot->mn = r.mn;
+        slot->mx = r.mx;
+        __threadfence();
+        old = atomicAdd(A.bin_cnt + (g - A.g0), 1u);
+      }
+      old = __shfl_sync(0xffffffffu, old, 0);
+      int64_t wa = chunk_of(A, s), wb = chunk_of(A, e - 1);
+      if ((int64_t)old == wb - wa) {  // last arriver merges the partials
+        __threadfence();
+        MinMaxCand acc{cand_none_min(), cand_none_max()};
+        for (int64_t ww = wa + lane; ww <= wb; ww += 32) {
+          const MinMaxCand* sl = A.part + 2 * ww + (ww == wa ? 1 : 0);
+          Cand a{ld_cg_u64(&sl->mn.key), ld_cg_i64(&sl->mn.idx)};
+          Cand b{ld_cg_u64(&sl->mx.key), ld_cg_i64(&sl->mx.idx)};
+          merge_min(acc.mn, a);
+          merge_max(acc.mx, b);
+        }
+        warp_reduce(acc);
+        if (lane == 0) {
+          A.bin_cnt[g - A.g0] = 0u;
+          finalize<DT, PROP>(A, B, g, acc);
+        }
+      }
+    }
+    pos = se;
+    g++;
   }
 }
 
 template <int DT, bool PROP, int U>
 __global__ void __launch_bounds__(SCAN_WARPS * 32)
 scan_kernel(const ScanArgs A) {
-  using O = Ops<DT>;
+  // programmatic dependent launch: everything below may read what the
+  // binning kernel (the primary grid) wrote
+  pdl_wait();
   const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * SCAN_WARPS + (threadIdx.x >> 5);
   const int64_t nwarps_grid = (int64_t)gridDim.x * SCAN_WARPS;
-  const int64_t first = A.vstart - A.shift;  // element index of chunk 0 start (may be < E0)
+  PipeFlags* F = A.flags;
+  BinSpec B = A.bins;
+  if (A.use_dyn_mode) B.mode = *(volatile int*)&F->mode;
+  const bool aborted = A.check_flags && *(volatile int*)&F->status;
+  const bool indep = A.independent || (A.check_flags && *(volatile int*)&F->nonmono);
 
-  const bool aborted = A.abort_flag && *(volatile const int*)A.abort_flag;
-  const bool indep = A.independent || (A.nonmono_flag && *(volatile const int*)A.nonmono_flag);
   if (!aborted && indep) {
     // non-monotone offsets (x violated its documented precondition): bins
     // may overlap, so every bin is reduced on its own, like the reference.
-    for (int64_t g = A.g0 + (int64_t)blockIdx.x * SCAN_WARPS + (threadIdx.x >> 5); g < A.g1; g += nwarps_grid) {
-      int64_t s = bin_off(A.bins, g), e = bin_off(A.bins, g + 1);
+    for (int64_t g = A.g0 + gw; g < A.g1; g += nwarps_grid) {
+      int64_t s = bin_off(B, g), e = bin_off(B, g + 1);
       if (e <= s) continue;
       MinMaxCand r = seg_reduce<DT, PROP, U>(A, s, e);
-      if (lane == 0) finalize<DT, PROP>(A, g, r);
+      if (lane == 0) finalize<DT, PROP>(A, B, g, r);
     }
-  }
-  for (int64_t w = (int64_t)blockIdx.x * SCAN_WARPS + (threadIdx.x >> 5); !aborted && !indep && w < A.nchunks;
-       w += nwarps_grid) {
-    int64_t cs = first + w * A.che, ce = cs + A.che;
-    if (cs < A.E0) cs = A.E0;
-    if (ce > A.E1) ce = A.E1;
-    if (cs >= ce) continue;
-    int64_t g = bin_of(A.bins, cs, A.g0, A.g1);
-    int64_t pos = cs;
-    while (pos < ce && g < A.g1) {
-      int64_t s = bin_off(A.bins, g), e = bin_off(A.bins, g + 1);
-      if (e <= pos) { g++; continue; }
-      int64_t se = e < ce ? e : ce;
-      MinMaxCand r = seg_reduce<DT, PROP, U>(A, pos, se);
-      bool before = s < cs, after = e > ce;
-      if (!before && !after) {
-        if (lane == 0) finalize<DT, PROP>(A, g, r);
-      } else {
-        unsigned old = 0;
-        if (lane == 0) {
-          MinMaxCand* slot = A.part + 2 * w + (before ? 0 : 1);
-          slot->mn = r.mn;
-          slot->mx = r.mx;
-          __threadfence();
-          old = atomicAdd(A.bin_cnt + (g - A.g0), 1u);
-        }
-        old = __shfl_sync(0xffffffffu, old, 0);
-        int64_t wa = (s + A.shift - A.vstart) / A.che;
-        int64_t wb = (e - 1 + A.shift - A.vstart) / A.che;
-        if ((int64_t)old == wb - wa) {  // last arriver merges the partials
-          __threadfence();
-          MinMaxCand acc{cand_none_min(), cand_none_max()};
-          for (int64_t ww = wa + lane; ww <= wb; ww += 32) {
-            const MinMaxCand* sl = A.part + 2 * ww + (ww == wa ? 1 : 0);
-            Cand a{ld_cg_u64(&sl->mn.key), ld_cg_i64(&sl->mn.idx)};
-            Cand b{ld_cg_u64(&sl->mx.key), ld_cg_i64(&sl->mx.idx)};
-            merge_min(acc.mn, a);
-            merge_max(acc.mx, b);
-          }
-          warp_reduce(acc);
-          if (lane == 0) {
-            A.bin_cnt[g - A.g0] = 0u;
-            finalize<DT, PROP>(A, g, acc);
-          }
-        }
-      }
-      pos = se;
-      g++;
+  } else if (!aborted) {
+    for (int64_t w = gw; w < A.n_static; w += nwarps_grid) process_chunk<DT, PROP, U>(A, B, w);
+    while (true) {
+      unsigned long long u = 0;
+      if (lane == 0) u = atomicAdd(&F->work_ctr, 1ull);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if ((int64_t)u >= A.n_dyn) break;
+      process_chunk<DT, PROP, U>(A, B, A.n_static + (int64_t)u);
     }
   }
 
-  if (A.epi == EPI_PAIR && A.out == nullptr) return;
-  // ---- last CTA: compaction epilogue
+  // ---- last CTA: compaction epilogue, counter and flag reset
   __shared__ int is_last;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    unsigned t = atomicAdd(A.blocks_done, 1u);
+    unsigned t = atomicAdd(&F->scan_blocks_done, 1u);
     is_last = (t == gridDim.x - 1);
   }
   __syncthreads();
@@ -365,23 +404,20 @@ scan_kernel(const ScanArgs A) {
     if (threadIdx.x == 0) {
       if (A.epi == EPI_SLOTS_MINMAX || A.epi == EPI_SLOTS_M4) {
         for (int64_t g = A.g0; g < A.g1; g++) A.out_count[g - A.g0] = 0;
-      } else if (A.epi != EPI_PAIR) {
+      } else if (A.epi != EPI_PAIR && A.out_count) {
         *A.out_count = 0;
       }
-      *A.blocks_done = 0u;
     }
-    return;
-  }
-  if (A.epi == EPI_SLOTS_MINMAX || A.epi == EPI_SLOTS_M4) {
-    cta_slots(A);
+  } else if (A.epi == EPI_SLOTS_MINMAX || A.epi == EPI_SLOTS_M4) {
+    cta_slots(A, B);
   } else if (A.epi == EPI_PAIR) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && A.out) {
       A.out[0] = ld_cg_i64(A.res);
       A.out[1] = ld_cg_i64(A.res + 1);
     }
-  } else {
+  } else if (A.out) {
     int64_t* out = A.out + (A.lttb_frame ? 1 : 0);
-    int64_t tot = cta_compact(A, A.g0, A.g1, out, A.idx_sub);
+    int64_t tot = cta_compact(A, B, A.g0, A.g1, out, A.idx_sub);
     if (threadIdx.x == 0) {
       if (A.lttb_frame) {
         A.out[0] = 0;
@@ -391,7 +427,18 @@ scan_kernel(const ScanArgs A) {
       *A.out_count = tot;
     }
   }
-  if (threadIdx.x == 0) *A.blocks_done = 0u;
+  if (threadIdx.x == 0) {
+    if (A.status_out) *A.status_out = *(volatile int*)&F->status;
+    if (A.reset_flags) {
+      F->mis_api = 0;
+      F->mis_slice = 0;
+      F->status = 0;
+      F->nonmono = 0;
+      F->mode = 0;
+    }
+    F->work_ctr = 0ull;
+    F->scan_blocks_done = 0u;
+  }
 }
 
 // batched compaction: one CTA per series (bins [s*nb, (s+1)*nb))
@@ -399,7 +446,7 @@ __global__ void compact_series_kernel(const ScanArgs A, int64_t nb_per_series, i
                                       int64_t series_len, int64_t* counts) {
   int64_t s = blockIdx.x;
   int64_t ga = A.g0 + s * nb_per_series, gb = ga + nb_per_series;
-  int64_t tot = cta_compact(A, ga, gb, A.out + s * n_out_stride, (ga / nb_per_series) * series_len);
+  int64_t tot = cta_compact(A, A.bins, ga, gb, A.out + s * n_out_stride, (ga / nb_per_series) * series_len);
   if (threadIdx.x == 0) counts[s] = tot;
 }
 
