@@ -20,6 +20,7 @@
 #include "tsds_bin.cuh"
 #include "tsds_lttb.cuh"
 #include "tsds_scan.cuh"
+#include "tsds_tma.cuh"
 
 using namespace tsds;
 
@@ -58,7 +59,7 @@ struct tsds_ctx {
   bool own_stream = true;
   int sms = 148;
   std::mutex mu;
-  DevBuf y, x, xf64, part, bincnt, res, off, out, misc, cent, scratch, y2, x2, x2f64, full, out2;
+  DevBuf y, x, xf64, part, bincnt, res, off, out, misc, cent, scratch, y2, x2, x2f64, full, out2, rctr;
   void* h_pin = nullptr;
   size_t h_cap = 0;
   bool dirty = false;
@@ -147,7 +148,103 @@ int begin_call(tsds_ctx* ctx) {
 }
 
 int dtype_ok(int dt) { return dt >= 0 && dt < DT_COUNT; }
+
+int64_t dyn_percent() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("TSDS_DYN_PERCENT");
+    v = e ? std::max(0, std::min(90, atoi(e))) : 0;
+  }
+  return v;
+}
 int xdtype_ok(int dt) { return dt >= 1 && dt < DT_COUNT; }
+
+// ------------------------------------------------------------ TMA scan launch
+int64_t tma_min_bytes() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("TSDS_TMA_MIN_BYTES");
+    v = e ? atoll(e) : (int64_t)16 << 20;
+  }
+  return v;
+}
+
+template <int DT, bool PROP>
+int launch_scan_tma_t(tsds_ctx* ctx, ScanArgs& A) {
+  using O = Ops<DT>;
+  constexpr int VEC = O::VEC;
+  constexpr int ES = 16 / VEC;
+  constexpr int64_t TE = TMA_TILE_BYTES / ES;
+  auto kern = tma_scan_kernel<DT, PROP>;
+  auto mkern = merge_kernel<DT, PROP>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM));
+    attr_set = true;
+  }
+  A.shift = (int64_t)(((uintptr_t)A.y % 16) / ES);
+  const int64_t align = 32 * VEC;
+  A.vstart = ((A.E0 + A.shift) / align) * align;
+  const int64_t vend = std::max(A.E1 + A.shift, A.vstart + 1);
+  const int64_t ntiles = (vend - A.vstart + TE - 1) / TE;
+  A.che = TE;
+  A.n_static = ntiles;
+  A.dse = TE;
+  A.n_dyn = 0;
+  const int64_t G = std::max<int64_t>(1, std::min<int64_t>(ctx->sms, ntiles));
+  A.n_ranges = G;
+  A.range_len = (ntiles + G - 1) / G;
+  const int64_t cv_lo = (A.E0 + A.shift + VEC - 1) / VEC;
+  const int64_t cv_hi = (A.E1 + A.shift) / VEC;
+  const int64_t nbins = A.g1 - A.g0;
+  RC_TRY(ensure(ctx, ctx->part, (size_t)ntiles * 2 * sizeof(MinMaxCand)));
+  RC_TRY(ensure(ctx, ctx->bincnt, (size_t)nbins * sizeof(unsigned), true));
+  RC_TRY(ensure(ctx, ctx->res, (size_t)nbins * 2 * sizeof(int64_t)));
+  RC_TRY(ensure(ctx, ctx->rctr, (size_t)G * 8, true));
+  A.part = (MinMaxCand*)ctx->part.p;
+  A.bin_cnt = (unsigned*)ctx->bincnt.p;
+  A.res = (int64_t*)ctx->res.p;
+  A.flags = &misc(ctx)->F;
+  A.range_ctr = (unsigned long long*)ctx->rctr.p;
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (ctx->profile) {
+    if (ctx->ev_free.empty()) {
+      CUDA_TRY(cudaEventCreate(&ev.first));
+      CUDA_TRY(cudaEventCreate(&ev.second));
+    } else {
+      ev = ctx->ev_free.back();
+      ctx->ev_free.pop_back();
+    }
+    CUDA_TRY(cudaEventRecord(ev.first, ctx->stream));
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ctx->profile ? 0 : 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)G);
+  cfg.blockDim = dim3(TMA_THREADS);
+  cfg.dynamicSmemBytes = TMA_SMEM;
+  cfg.stream = ctx->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A, cv_lo, cv_hi));
+  LAUNCH_CHECK();
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t mcfg = {};
+  const int64_t mgrid = std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 4, (nbins + SCAN_WARPS - 1) / SCAN_WARPS));
+  mcfg.gridDim = dim3((unsigned)mgrid);
+  mcfg.blockDim = dim3(SCAN_WARPS * 32);
+  mcfg.stream = ctx->stream;
+  mcfg.attrs = attr;
+  mcfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&mcfg, mkern, A));
+  LAUNCH_CHECK();
+  if (ctx->profile) {
+    CUDA_TRY(cudaEventRecord(ev.second, ctx->stream));
+    ctx->ev_used.push_back(ev);
+  }
+  return TSDS_OK;
+}
 
 // ---------------------------------------------------------------- scan launch
 template <int DT, bool PROP>
@@ -155,6 +252,8 @@ int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
   using O = Ops<DT>;
   constexpr int VEC = O::VEC;
   constexpr int ES = 16 / VEC;
+  if (!A.independent && (A.E1 - A.E0) * ES >= tma_min_bytes() && (uintptr_t)A.y % ES == 0)
+    return launch_scan_tma_t<DT, PROP>(ctx, A);
   auto kern = scan_kernel<DT, PROP, TSDS_UNROLL>;
   static int occ = 0;
   if (occ == 0) {
@@ -169,12 +268,13 @@ int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
   const int64_t vend = std::max(A.E1 + A.shift, A.vstart + 1);
   const int64_t tv = vend - A.vstart;
   const int64_t W = (int64_t)ctx->sms * occ * SCAN_WARPS;
-  // ~80% of the bytes in one static contiguous chunk per resident warp, the
-  // rest in 8 KB units handed out dynamically (absorbs SM-to-SM imbalance)
+  // one static contiguous chunk per resident warp (>= 4 KB each); optional
+  // dynamic tail units (TSDS_DYN_PERCENT of the bytes, handed out by an
+  // atomic counter) -- off by default: the single counter serialises.
   const int64_t unit = std::max<int64_t>(align, ((8192 / ES) / align) * align);
-  int64_t che = ((tv * 4 / 5) / W / align) * align;
-  if (che < 4 * unit) {
-    // small input: all static, >= 4 KB per chunk
+  const int64_t dyn_pct = dyn_percent();
+  int64_t che = ((tv * (100 - dyn_pct) / 100) / W / align) * align;
+  if (dyn_pct == 0 || che < 4 * unit) {
     const int64_t minc = std::max<int64_t>(align, ((4096 / ES + align - 1) / align) * align);
     int64_t nch = std::max<int64_t>(1, std::min<int64_t>(W, (tv + minc - 1) / minc));
     che = (((tv + nch - 1) / nch + align - 1) / align) * align;
@@ -299,11 +399,12 @@ ScanArgs scan_args(const void* y, BinSpec bins, int64_t g0, int64_t g1, int64_t 
 // one fused binning launch (uniform checks + edges + verdict); flags land in Misc.F
 int launch_binning(tsds_ctx* ctx, int xdt, const void* x, int64_t n, int64_t nb, int64_t add, const void* xapi,
                    int64_t napi, int uniform_first, int materialize, int64_t* off) {
-  BinJob J{x, n, nb, add, xapi, napi, uniform_first, materialize, off, &misc(ctx)->F};
-  const int64_t edge_blocks = (nb + 7) / 8;
-  const int64_t piece_blocks = (std::max(n, napi) + 511) / 512;
-  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 4, std::max(edge_blocks, piece_blocks)));
-  XDT_SWITCH(xdt, (binning_kernel<XD><<<grid, 256, 0, ctx->stream>>>(J)));
+  const int cta_edges = (nb - 1) * BIN_THREADS <= (int64_t)ctx->sms * 2048 ? 1 : 0;
+  BinJob J{x, n, nb, add, xapi, napi, uniform_first, materialize, cta_edges, off, &misc(ctx)->F};
+  const int64_t edge_blocks = cta_edges ? nb - 1 : (nb + BIN_THREADS / 32 - 1) / (BIN_THREADS / 32);
+  const int64_t piece_blocks = std::min<int64_t>((int64_t)ctx->sms * 8, (std::max(n, napi) + 511) / 512);
+  unsigned grid = (unsigned)std::max<int64_t>(1, std::max(std::min<int64_t>((int64_t)ctx->sms * 16, edge_blocks), piece_blocks));
+  XDT_SWITCH(xdt, (binning_kernel<XD><<<grid, BIN_THREADS, 0, ctx->stream>>>(J)));
   LAUNCH_CHECK();
   ctx->flags_clean = false;
   return TSDS_OK;
@@ -672,7 +773,8 @@ void tsds_ctx_destroy(tsds_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->y, &ctx->x, &ctx->xf64, &ctx->part, &ctx->bincnt, &ctx->res, &ctx->off, &ctx->out,
-                    &ctx->misc, &ctx->cent, &ctx->scratch, &ctx->y2, &ctx->x2, &ctx->x2f64, &ctx->full, &ctx->out2})
+                    &ctx->misc, &ctx->cent, &ctx->scratch, &ctx->y2, &ctx->x2, &ctx->x2f64, &ctx->full, &ctx->out2,
+                    &ctx->rctr})
     if (b->p) cudaFree(b->p);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);

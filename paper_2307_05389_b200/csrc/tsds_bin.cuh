@@ -63,7 +63,7 @@ __device__ void uniform_pieces(const void* xv, int64_t n, int* mismatch) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *mismatch = 1;
     return;
   }
-  const int64_t piece = 2 * (int64_t)blockDim.x;
+  const int64_t piece = 4 * (int64_t)blockDim.x;
   const int64_t ngaps = n - 2;  // gaps i = 1 .. n-2
   __shared__ int stop;
   for (int64_t p0 = (int64_t)blockIdx.x * piece; p0 < ngaps; p0 += (int64_t)gridDim.x * piece) {
@@ -116,6 +116,45 @@ __device__ int64_t lower_bound_exact(const void* x, int64_t n, double edge) {
   return lo;
 }
 
+// Same probe sequence with a whole CTA of BIN_THREADS (128) threads: 127
+// lanes probe the next 7 levels of the reference's binary-search tree per
+// round (27 levels for 1e8 points -> 4 dependent rounds instead of 6).  All
+// threads return lo.
+constexpr int BIN_THREADS = 128;
+constexpr int BIN_LEVELS = 7;
+
+template <int XDT>
+__device__ int64_t lower_bound_exact_cta(const void* x, int64_t n, double edge) {
+  __shared__ uint32_t s_bits[BIN_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int node = tid + 1;  // heap node 1..127 (last thread idle)
+    const int depth = 31 - __clz(node);
+    int64_t l = lo, h = hi;
+    bool active = node < BIN_THREADS;
+    for (int d = depth - 1; d >= 0 && active; d--) {
+      if (l >= h) { active = false; break; }
+      int64_t mid = (l + h) >> 1;
+      if ((node >> d) & 1) l = mid + 1; else h = mid;
+    }
+    bool pred = false;
+    if (active && l < h) pred = xf64<XDT>(x, (l + h) >> 1) < edge;
+    unsigned bal = __ballot_sync(0xffffffffu, pred);
+    if (lane == 0) s_bits[tid >> 5] = bal;
+    __syncthreads();
+    int cur = 1;
+    for (int lev = 0; lev < BIN_LEVELS && lo < hi; lev++) {
+      int64_t mid = (lo + hi) >> 1;
+      bool pr = (s_bits[(cur - 1) >> 5] >> ((cur - 1) & 31)) & 1u;
+      if (pr) lo = mid + 1; else hi = mid;
+      cur = 2 * cur + (pr ? 1 : 0);
+    }
+    __syncthreads();
+  }
+  return lo;
+}
+
 // One launch computes the bins of x[0..n) (binning.py:43-82 semantics):
 //   * uniform-spacing checks of the binned slice and (optionally) of the
 //     whole x for the api-level normalisation (api.py:19-28);
@@ -135,6 +174,7 @@ struct BinJob {
   int64_t napi;
   int uniform_first;  // 1: a uniform slice short-circuits before span checks
   int materialize;    // write equal-count offsets into `off` too
+  int cta_edges;      // 1: one CTA per edge (few edges), 0: one warp per edge
   int64_t* off;       // [nb+1]
   PipeFlags* F;
 };
@@ -153,10 +193,18 @@ __global__ void binning_kernel(const BinJob J) {
     const double x0 = xf64<XDT>(J.x, 0);
     const double span = __dsub_rn(xf64<XDT>(J.x, n - 1), x0);
     if (isfinite(span) && span != 0.0) {
-      for (int64_t k = 1 + gw; k < nb; k += nwarps) {
-        double e = __dadd_rn(x0, __ddiv_rn(__dmul_rn((double)k, span), (double)nb));
-        int64_t v = lower_bound_exact<XDT>(J.x, n, e);
-        if (lane == 0) J.off[k] = v + J.add;
+      if (J.cta_edges) {
+        for (int64_t k = 1 + blockIdx.x; k < nb; k += gridDim.x) {
+          double e = __dadd_rn(x0, __ddiv_rn(__dmul_rn((double)k, span), (double)nb));
+          int64_t v = lower_bound_exact_cta<XDT>(J.x, n, e);
+          if (threadIdx.x == 0) J.off[k] = v + J.add;
+        }
+      } else {
+        for (int64_t k = 1 + gw; k < nb; k += nwarps) {
+          double e = __dadd_rn(x0, __ddiv_rn(__dmul_rn((double)k, span), (double)nb));
+          int64_t v = lower_bound_exact<XDT>(J.x, n, e);
+          if (lane == 0) J.off[k] = v + J.add;
+        }
       }
     }
   }

@@ -100,6 +100,10 @@ struct ScanArgs {
   int64_t idx_sub;     // subtracted from every output index
   int lttb_frame;      // 1: out[0]=0 and out[total+1]=n_frame-1 (MinMaxLTTB `full`)
   int64_t n_frame;
+  // TMA path (tsds_tma.cuh): per-CTA tile ranges claimed through counters
+  unsigned long long* range_ctr;  // [n_ranges], zero between launches
+  int64_t n_ranges;
+  int64_t range_len;   // tiles per home range
 };
 
 __device__ __forceinline__ int64_t chunk_of(const ScanArgs& A, int64_t i) {
@@ -126,15 +130,27 @@ __device__ __forceinline__ void chunk_range(const ScanArgs& A, int64_t w, int64_
 // ------------------------------------------------------------------------
 // one bin segment [a, c) reduced by a warp
 
-template <int DT, bool PROP, int U>
-__device__ MinMaxCand seg_reduce(const ScanArgs& A, int64_t a, int64_t c) {
+// vector sources: global memory (streaming loads) or a shared-memory tile
+struct GlobalSrc {
+  const uint4* yv;  // virtual vector 0
+  __device__ __forceinline__ uint4 stream(int64_t j) const { return ldg_stream(yv + j); }
+  __device__ __forceinline__ uint4 again(int64_t j) const { return __ldg(yv + j); }
+};
+struct SmemSrc {
+  const uint4* sv;  // smem copy of the tile; sv[0] is virtual vector v0
+  int64_t v0;
+  __device__ __forceinline__ uint4 stream(int64_t j) const { return sv[j - v0]; }
+  __device__ __forceinline__ uint4 again(int64_t j) const { return sv[j - v0]; }
+};
+
+template <int DT, bool PROP, int U, class Src>
+__device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, const Src& src) {
   using O = Ops<DT>;
   using E = typename O::E;
   using R = typename O::R;
   constexpr int VEC = O::VEC;
   const int lane = threadIdx.x & 31;
   const E* y = static_cast<const E*>(A.y);
-  const uint4* yv = reinterpret_cast<const uint4*>(y - A.shift);
   MinMaxCand res{cand_none_min(), cand_none_max()};
 
   auto scalar = [&](int64_t i) {
@@ -177,11 +193,11 @@ __device__ MinMaxCand seg_reduce(const ScanArgs& A, int64_t a, int64_t c) {
     for (; j + 32 * (U - 1) < je; j += 32 * U) {
       uint4 buf[U];
 #pragma unroll
-      for (int u = 0; u < U; u++) buf[u] = ldg_stream(yv + j + 32 * u);
+      for (int u = 0; u < U; u++) buf[u] = src.stream(j + 32 * u);
 #pragma unroll
       for (int u = 0; u < U; u++) step(buf[u], j + 32 * u);
     }
-    for (; j < je; j += 32) step(ldg_stream(yv + j), j);
+    for (; j < je; j += 32) step(src.stream(j), j);
 
     if constexpr (O::FALLBACK) {
       if (jb + lane < je) {
@@ -190,7 +206,7 @@ __device__ MinMaxCand seg_reduce(const ScanArgs& A, int64_t a, int64_t c) {
       }
     }
     if (jmn >= 0 && O::valid(rmn)) {
-      uint4 v = __ldg(yv + jmn);
+      uint4 v = src.again(jmn);
       int p = 0;
 #pragma unroll
       for (int q = VEC - 1; q >= 0; q--)
@@ -198,7 +214,7 @@ __device__ MinMaxCand seg_reduce(const ScanArgs& A, int64_t a, int64_t c) {
       merge_min(res.mn, Cand{O::key(rmn), jmn * VEC + p - A.shift});
     }
     if (jmx >= 0 && O::valid(rmx)) {
-      uint4 v = __ldg(yv + jmx);
+      uint4 v = src.again(jmx);
       int p = 0;
 #pragma unroll
       for (int q = VEC - 1; q >= 0; q--)
@@ -207,7 +223,7 @@ __device__ MinMaxCand seg_reduce(const ScanArgs& A, int64_t a, int64_t c) {
     }
     if constexpr (PROP && O::NANABLE) {
       if (jnan >= 0) {
-        uint4 v = __ldg(yv + jnan);
+        uint4 v = src.again(jnan);
         int p = 0;
 #pragma unroll
         for (int q = VEC - 1; q >= 0; q--)
@@ -220,6 +236,13 @@ __device__ MinMaxCand seg_reduce(const ScanArgs& A, int64_t a, int64_t c) {
   }
   warp_reduce(res);
   return res;
+}
+
+template <int DT, bool PROP, int U>
+__device__ __forceinline__ MinMaxCand seg_reduce(const ScanArgs& A, int64_t a, int64_t c) {
+  using E = typename Ops<DT>::E;
+  GlobalSrc src{reinterpret_cast<const uint4*>(static_cast<const E*>(A.y) - A.shift)};
+  return seg_reduce_src<DT, PROP, U>(A, a, c, src);
 }
 
 // ------------------------------------------------------------------------
@@ -354,42 +377,10 @@ __device__ __forceinline__ void process_chunk(const ScanArgs& A, const BinSpec& 
   }
 }
 
-template <int DT, bool PROP, int U>
-__global__ void __launch_bounds__(SCAN_WARPS * 32)
-scan_kernel(const ScanArgs A) {
-  // programmatic dependent launch: everything below may read what the
-  // binning kernel (the primary grid) wrote
-  pdl_wait();
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t)blockIdx.x * SCAN_WARPS + (threadIdx.x >> 5);
-  const int64_t nwarps_grid = (int64_t)gridDim.x * SCAN_WARPS;
+// Last CTA of a launch: compaction epilogue, counter and flag reset.
+// Every CTA of the grid must call it exactly once.
+__device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted) {
   PipeFlags* F = A.flags;
-  BinSpec B = A.bins;
-  if (A.use_dyn_mode) B.mode = *(volatile int*)&F->mode;
-  const bool aborted = A.check_flags && *(volatile int*)&F->status;
-  const bool indep = A.independent || (A.check_flags && *(volatile int*)&F->nonmono);
-
-  if (!aborted && indep) {
-    // non-monotone offsets (x violated its documented precondition): bins
-    // may overlap, so every bin is reduced on its own, like the reference.
-    for (int64_t g = A.g0 + gw; g < A.g1; g += nwarps_grid) {
-      int64_t s = bin_off(B, g), e = bin_off(B, g + 1);
-      if (e <= s) continue;
-      MinMaxCand r = seg_reduce<DT, PROP, U>(A, s, e);
-      if (lane == 0) finalize<DT, PROP>(A, B, g, r);
-    }
-  } else if (!aborted) {
-    for (int64_t w = gw; w < A.n_static; w += nwarps_grid) process_chunk<DT, PROP, U>(A, B, w);
-    while (true) {
-      unsigned long long u = 0;
-      if (lane == 0) u = atomicAdd(&F->work_ctr, 1ull);
-      u = __shfl_sync(0xffffffffu, u, 0);
-      if ((int64_t)u >= A.n_dyn) break;
-      process_chunk<DT, PROP, U>(A, B, A.n_static + (int64_t)u);
-    }
-  }
-
-  // ---- last CTA: compaction epilogue, counter and flag reset
   __shared__ int is_last;
   __threadfence();
   __syncthreads();
@@ -439,6 +430,46 @@ scan_kernel(const ScanArgs A) {
     F->work_ctr = 0ull;
     F->scan_blocks_done = 0u;
   }
+  if (threadIdx.x == 0 && A.range_ctr)
+    for (int64_t c = 0; c < A.n_ranges; c++) A.range_ctr[c] = 0ull;
+}
+
+template <int DT, bool PROP, int U>
+__global__ void __launch_bounds__(SCAN_WARPS * 32)
+scan_kernel(const ScanArgs A) {
+  // programmatic dependent launch: everything below may read what the
+  // binning kernel (the primary grid) wrote
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * SCAN_WARPS + (threadIdx.x >> 5);
+  const int64_t nwarps_grid = (int64_t)gridDim.x * SCAN_WARPS;
+  PipeFlags* F = A.flags;
+  BinSpec B = A.bins;
+  if (A.use_dyn_mode) B.mode = *(volatile int*)&F->mode;
+  const bool aborted = A.check_flags && *(volatile int*)&F->status;
+  const bool indep = A.independent || (A.check_flags && *(volatile int*)&F->nonmono);
+
+  if (!aborted && indep) {
+    // non-monotone offsets (x violated its documented precondition): bins
+    // may overlap, so every bin is reduced on its own, like the reference.
+    for (int64_t g = A.g0 + gw; g < A.g1; g += nwarps_grid) {
+      int64_t s = bin_off(B, g), e = bin_off(B, g + 1);
+      if (e <= s) continue;
+      MinMaxCand r = seg_reduce<DT, PROP, U>(A, s, e);
+      if (lane == 0) finalize<DT, PROP>(A, B, g, r);
+    }
+  } else if (!aborted) {
+    for (int64_t w = gw; w < A.n_static; w += nwarps_grid) process_chunk<DT, PROP, U>(A, B, w);
+    while (A.n_dyn > 0) {
+      unsigned long long u = 0;
+      if (lane == 0) u = atomicAdd(&F->work_ctr, 1ull);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if ((int64_t)u >= A.n_dyn) break;
+      process_chunk<DT, PROP, U>(A, B, A.n_static + (int64_t)u);
+    }
+  }
+
+  scan_epilogue(A, B, aborted);
 }
 
 // batched compaction: one CTA per series (bins [s*nb, (s+1)*nb))
