@@ -26,6 +26,7 @@ MEM_DEVICE = 1
 
 EXPORTED = (
     "tsds_version",
+    "tsds_set_option",
     "tsds_last_error",
     "tsds_device_count",
     "tsds_ctx_create",
@@ -78,6 +79,7 @@ def load():
         p64 = ctypes.POINTER(ctypes.c_int64)
         L.tsds_version.restype = i32
         L.tsds_last_error.restype = ctypes.c_char_p
+        L.tsds_set_option.argtypes = [ctypes.c_char_p, i64]
         L.tsds_device_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
         L.tsds_ctx_create.argtypes = [i32, ctypes.POINTER(vp)]
         L.tsds_ctx_destroy.argtypes = [vp]

@@ -149,24 +149,25 @@ int begin_call(tsds_ctx* ctx) {
 
 int dtype_ok(int dt) { return dt >= 0 && dt < DT_COUNT; }
 
+// tuning knobs: environment defaults, overridable with tsds_set_option
+int64_t g_dyn_percent = -1, g_tma_min_bytes = -1;
+
 int64_t dyn_percent() {
-  static int64_t v = -1;
-  if (v < 0) {
+  if (g_dyn_percent < 0) {
     const char* e = getenv("TSDS_DYN_PERCENT");
-    v = e ? std::max(0, std::min(90, atoi(e))) : 0;
+    g_dyn_percent = e ? std::max(0, std::min(90, atoi(e))) : 0;
   }
-  return v;
+  return g_dyn_percent;
 }
 int xdtype_ok(int dt) { return dt >= 1 && dt < DT_COUNT; }
 
 // ------------------------------------------------------------ TMA scan launch
 int64_t tma_min_bytes() {
-  static int64_t v = -1;
-  if (v < 0) {
+  if (g_tma_min_bytes < 0) {
     const char* e = getenv("TSDS_TMA_MIN_BYTES");
-    v = e ? atoll(e) : (int64_t)16 << 20;
+    g_tma_min_bytes = e ? atoll(e) : (int64_t)16 << 20;
   }
-  return v;
+  return g_tma_min_bytes;
 }
 
 template <int DT, bool PROP>
@@ -741,6 +742,15 @@ int identity(tsds_ctx* ctx, int64_t n, int64_t* out, int64_t* out_len) {
 extern "C" {
 
 int tsds_version(void) { return 100; }
+
+int tsds_set_option(const char* name, int64_t value) {
+  if (!name) return set_err(TSDS_ERR_ARG, "option name is NULL");
+  std::string n(name);
+  if (n == "tma_min_bytes") g_tma_min_bytes = std::max<int64_t>(0, value);
+  else if (n == "dyn_percent") g_dyn_percent = std::max<int64_t>(0, std::min<int64_t>(90, value));
+  else return set_err(TSDS_ERR_ARG, "unknown option " + n);
+  return TSDS_OK;
+}
 
 const char* tsds_last_error(void) { return g_err.c_str(); }
 

@@ -23,7 +23,7 @@ constexpr int TMA_CONSUMERS = 8;
 constexpr int TMA_STAGES = 16;          // multiple of TMA_CONSUMERS
 constexpr int TMA_TILE_BYTES = 12288;   // 16 stages x 12 KB = 192 KB ring
 constexpr int TMA_THREADS = 32 * (TMA_CONSUMERS + 1);
-constexpr int TMA_CLAIM = 4;            // tiles per counter claim
+constexpr int TMA_CLAIM = 8;            // tiles per counter claim
 constexpr size_t TMA_SMEM = (size_t)TMA_STAGES * TMA_TILE_BYTES + TMA_STAGES * 24 + 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -147,19 +147,28 @@ tma_scan_kernel(const ScanArgs A, int64_t cv_lo, int64_t cv_hi) {
         }
         q++;
       };
+      // claims are prefetched one batch ahead so the atomic's latency hides
+      // behind issuing (and waiting for free stages of) the current batch
       const int64_t G = A.n_ranges;
       int64_t victim = blockIdx.x;
+      auto range_len = [&](int64_t v) {
+        const int64_t base = v * A.range_len;
+        return base >= A.n_static ? (int64_t)0 : (A.n_static - base < A.range_len ? A.n_static - base : A.range_len);
+      };
+      unsigned long long t = atomicAdd(&A.range_ctr[victim], (unsigned long long)TMA_CLAIM);
       for (int64_t tried = 0; tried < G;) {
-        const int64_t base = victim * A.range_len;
-        const int64_t len = base >= A.n_static ? 0 : (A.n_static - base < A.range_len ? A.n_static - base : A.range_len);
-        unsigned long long t = len > 0 ? atomicAdd(&A.range_ctr[victim], (unsigned long long)TMA_CLAIM) : (unsigned long long)len;
+        const int64_t len = range_len(victim);
         if ((int64_t)t >= len) {
           victim = victim + 1 == G ? 0 : victim + 1;
           tried++;
+          if (tried < G) t = atomicAdd(&A.range_ctr[victim], (unsigned long long)TMA_CLAIM);
           continue;
         }
+        const unsigned long long tn = atomicAdd(&A.range_ctr[victim], (unsigned long long)TMA_CLAIM);
+        const int64_t base = victim * A.range_len;
         const int64_t t1 = (int64_t)t + TMA_CLAIM < len ? (int64_t)t + TMA_CLAIM : len;
         for (int64_t j = (int64_t)t; j < t1; j++) issue(base + j);
+        t = tn;
       }
       for (int c = 0; c < TMA_CONSUMERS; c++) issue(-1);
     }
