@@ -161,6 +161,17 @@ int64_t dyn_percent() {
 }
 int xdtype_ok(int dt) { return dt >= 1 && dt < DT_COUNT; }
 
+// reciprocals for the division-free equal-count formula (BinSpec::fast)
+void prepare_bins(BinSpec& b, int64_t max_index) {
+  b.fast = 0;
+  if (b.len > 0 && b.nb > 0) {
+    b.rlen = 1.0 / (double)b.len;
+    b.rnb = 1.0 / (double)b.nb;
+    const double lim = 4503599627370496.0;  // 2^52
+    b.fast = ((double)b.len * (double)b.nb < lim && (double)max_index < lim) ? 1 : 0;
+  }
+}
+
 // ------------------------------------------------------------ TMA scan launch
 int64_t tma_min_bytes() {
   if (g_tma_min_bytes < 0) {
@@ -183,6 +194,7 @@ int launch_scan_tma_t(tsds_ctx* ctx, ScanArgs& A) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM));
     attr_set = true;
   }
+  prepare_bins(A.bins, A.E1 + (int64_t)(A.g1 - A.g0) * 4 + 64);
   A.shift = (int64_t)(((uintptr_t)A.y % 16) / ES);
   const int64_t align = 32 * VEC;
   A.vstart = ((A.E0 + A.shift) / align) * align;
@@ -263,6 +275,7 @@ int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
     occ = std::max(1, o);
   }
   if ((uintptr_t)A.y % ES) return set_err(TSDS_ERR_ARG, "y is not aligned to its element size");
+  prepare_bins(A.bins, A.E1 + (int64_t)(A.g1 - A.g0) * 4 + 64);
   A.shift = (int64_t)(((uintptr_t)A.y % 16) / ES);
   const int64_t align = 32 * VEC;  // one 512-byte warp load
   A.vstart = ((A.E0 + A.shift) / align) * align;

@@ -24,6 +24,9 @@
 namespace tsds {
 
 constexpr int SCAN_WARPS = 8;  // 256 threads per CTA
+#ifndef SCAN_MIN_BLOCKS
+#define SCAN_MIN_BLOCKS 4  // <= 64 registers: 32 resident warps per SM
+#endif
 
 enum Epilogue : int { EPI_MINMAX = 0, EPI_M4 = 1, EPI_PAIR = 2, EPI_SLOTS_MINMAX = 3, EPI_SLOTS_M4 = 4 };
 
@@ -33,10 +36,27 @@ struct BinSpec {
   int64_t len;         // mode 0: series length L
   int64_t nb;          // mode 0: bins per series
   int64_t base;        // mode 0: offset added to every boundary
+  double rlen, rnb;    // 1/len, 1/nb (set by the host, see prepare_bins)
+  int fast;            // every dividend of the formula is < 2^52
 };
+
+// floor(a / b) for 0 <= a < 2^52 from a double reciprocal and one exact
+// integer correction step (64-bit integer division is a long software
+// sequence on the GPU; this keeps the per-bin cost to a few instructions).
+__device__ __forceinline__ int64_t fdiv(int64_t a, int64_t b, double rb) {
+  int64_t q = (int64_t)((double)a * rb);
+  while (q * b > a) q--;
+  while ((q + 1) * b <= a) q++;
+  return q;
+}
 
 __device__ __forceinline__ int64_t bin_off(const BinSpec& b, int64_t g) {
   if (b.mode == 1) return __ldg(b.off + g);
+  if (b.fast) {
+    int64_t s = fdiv(g, b.nb, b.rnb);
+    int64_t k = g - s * b.nb;
+    return s * b.len + b.base + fdiv(k * b.len, b.nb, b.rnb);
+  }
   int64_t s = g / b.nb;
   int64_t k = g - s * b.nb;
   unsigned __int128 p = (unsigned __int128)(uint64_t)k * (uint64_t)b.len;
@@ -47,10 +67,17 @@ __device__ __forceinline__ int64_t bin_off(const BinSpec& b, int64_t g) {
 __device__ __forceinline__ int64_t bin_of(const BinSpec& b, int64_t i, int64_t g0, int64_t g1) {
   if (b.mode == 0) {
     int64_t ip = i - b.base;
-    int64_t s = ip / b.len;
-    int64_t r = ip - s * b.len;
-    unsigned __int128 p = (unsigned __int128)(uint64_t)(r + 1) * (uint64_t)b.nb;
-    int64_t k = (int64_t)((p - 1) / (uint64_t)b.len);
+    int64_t s, k;
+    if (b.fast) {
+      s = fdiv(ip, b.len, b.rlen);
+      int64_t r = ip - s * b.len;
+      k = fdiv((r + 1) * b.nb - 1, b.len, b.rlen);
+    } else {
+      s = ip / b.len;
+      int64_t r = ip - s * b.len;
+      unsigned __int128 p = (unsigned __int128)(uint64_t)(r + 1) * (uint64_t)b.nb;
+      k = (int64_t)((p - 1) / (uint64_t)b.len);
+    }
     if (k > b.nb - 1) k = b.nb - 1;
     int64_t g = s * b.nb + k;
     return g < g0 ? g0 : (g > g1 - 1 ? g1 - 1 : g);
@@ -133,16 +160,30 @@ __device__ __forceinline__ void chunk_range(const ScanArgs& A, int64_t w, int64_
 // vector sources: global memory (streaming loads) or a shared-memory tile
 struct GlobalSrc {
   const uint4* yv;  // virtual vector 0
-  __device__ __forceinline__ uint4 stream(int64_t j) const { return ldg_stream(yv + j); }
-  __device__ __forceinline__ uint4 again(int64_t j) const { return __ldg(yv + j); }
+  __device__ __forceinline__ const uint4* base(int64_t jb) const { return yv + jb; }
+  __device__ __forceinline__ uint4 stream(const uint4* p, int j) const { return ldg_stream(p + j); }
+  __device__ __forceinline__ uint4 again(const uint4* p, int j) const { return __ldg(p + j); }
 };
 struct SmemSrc {
-  const uint4* sv;  // smem copy of the tile; sv[0] is virtual vector v0
+  uint32_t sv;  // shared-memory address of the tile copy; it starts at virtual vector v0
   int64_t v0;
-  __device__ __forceinline__ uint4 stream(int64_t j) const { return sv[j - v0]; }
-  __device__ __forceinline__ uint4 again(int64_t j) const { return sv[j - v0]; }
+  __device__ __forceinline__ const uint4* base(int64_t jb) const {
+    return reinterpret_cast<const uint4*>((uintptr_t)(sv + (uint32_t)(jb - v0) * 16u));
+  }
+  __device__ __forceinline__ uint4 stream(const uint4* p, int j) const {
+    uint4 r;
+    uint32_t a = (uint32_t)(uintptr_t)p + (uint32_t)j * 16u;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+    return r;
+  }
+  __device__ __forceinline__ uint4 again(const uint4* p, int j) const { return stream(p, j); }
 };
 
+// One warp reduces elements [a, c) of the series: full 16-byte vectors
+// through `src`, the (< VEC) unaligned head/tail elements with scalar loads.
+// Vector indices inside the loop are 32-bit offsets from the first full
+// vector, and the scalar candidates are formed after the loop, to keep the
+// hot loop's register footprint small (64 registers -> 32 warps per SM).
 template <int DT, bool PROP, int U, class Src>
 __device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, const Src& src) {
   using O = Ops<DT>;
@@ -173,14 +214,11 @@ __device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, co
   if (jb >= je) {
     for (int64_t i = a + lane; i < c; i += 32) scalar(i);
   } else {
-    const int64_t hend = jb * VEC - A.shift;
-    if (a + lane < hend) scalar(a + lane);
-    const int64_t tbeg = je * VEC - A.shift;
-    if (tbeg + lane < c) scalar(tbeg + lane);
-
+    const int nv = (int)(je - jb);
+    const uint4* p = src.base(jb);
     R rmn = O::min_init(), rmx = O::max_init();
-    int64_t jmn = -1, jmx = -1, jnan = -1;
-    auto step = [&](const uint4& v, int64_t jj) {
+    int jmn = -1, jmx = -1, jnan = -1;
+    auto step = [&](const uint4& v, int jj) {
       R vmn, vmx;
       O::vminmax(v, vmn, vmx);
       if (O::upd_min(vmn, rmn)) jmn = jj;
@@ -189,50 +227,55 @@ __device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, co
         if (jnan < 0 && O::vec_hasnan(v)) jnan = jj;
       }
     };
-    int64_t j = jb + lane;
-    for (; j + 32 * (U - 1) < je; j += 32 * U) {
+    int j = lane;
+    for (; j + 32 * (U - 1) < nv; j += 32 * U) {
       uint4 buf[U];
 #pragma unroll
-      for (int u = 0; u < U; u++) buf[u] = src.stream(j + 32 * u);
+      for (int u = 0; u < U; u++) buf[u] = src.stream(p, j + 32 * u);
 #pragma unroll
       for (int u = 0; u < U; u++) step(buf[u], j + 32 * u);
     }
-    for (; j < je; j += 32) step(src.stream(j), j);
+    for (; j < nv; j += 32) step(src.stream(p, j), j);
 
     if constexpr (O::FALLBACK) {
-      if (jb + lane < je) {
-        if (jmn < 0) jmn = jb + lane;
-        if (jmx < 0) jmx = jb + lane;
+      if (lane < nv) {
+        if (jmn < 0) jmn = lane;
+        if (jmx < 0) jmx = lane;
       }
     }
+    const int64_t i0 = jb * VEC - A.shift;  // element index of vector jb
     if (jmn >= 0 && O::valid(rmn)) {
-      uint4 v = src.again(jmn);
-      int p = 0;
+      uint4 v = src.again(p, jmn);
+      int q0 = 0;
 #pragma unroll
       for (int q = VEC - 1; q >= 0; q--)
-        if (O::elem(v, q) == rmn) p = q;
-      merge_min(res.mn, Cand{O::key(rmn), jmn * VEC + p - A.shift});
+        if (O::elem(v, q) == rmn) q0 = q;
+      merge_min(res.mn, Cand{O::key(rmn), i0 + (int64_t)jmn * VEC + q0});
     }
     if (jmx >= 0 && O::valid(rmx)) {
-      uint4 v = src.again(jmx);
-      int p = 0;
+      uint4 v = src.again(p, jmx);
+      int q0 = 0;
 #pragma unroll
       for (int q = VEC - 1; q >= 0; q--)
-        if (O::elem(v, q) == rmx) p = q;
-      merge_max(res.mx, Cand{O::key(rmx), jmx * VEC + p - A.shift});
+        if (O::elem(v, q) == rmx) q0 = q;
+      merge_max(res.mx, Cand{O::key(rmx), i0 + (int64_t)jmx * VEC + q0});
     }
     if constexpr (PROP && O::NANABLE) {
       if (jnan >= 0) {
-        uint4 v = src.again(jnan);
-        int p = 0;
+        uint4 v = src.again(p, jnan);
+        int q0 = 0;
 #pragma unroll
         for (int q = VEC - 1; q >= 0; q--)
-          if (O::elem_nan(v, q)) p = q;
-        int64_t idx = jnan * VEC + p - A.shift;
+          if (O::elem_nan(v, q)) q0 = q;
+        int64_t idx = i0 + (int64_t)jnan * VEC + q0;
         merge_min(res.mn, Cand{0ull, idx});
         merge_max(res.mx, Cand{KEY_MAX, idx});
       }
     }
+    // unaligned head / tail elements
+    if (a + lane < i0) scalar(a + lane);
+    const int64_t tbeg = je * VEC - A.shift;
+    if (tbeg + lane < c) scalar(tbeg + lane);
   }
   warp_reduce(res);
   return res;
@@ -435,7 +478,7 @@ __device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted)
 }
 
 template <int DT, bool PROP, int U>
-__global__ void __launch_bounds__(SCAN_WARPS * 32)
+__global__ void __launch_bounds__(SCAN_WARPS * 32, SCAN_MIN_BLOCKS)
 scan_kernel(const ScanArgs A) {
   // programmatic dependent launch: everything below may read what the
   // binning kernel (the primary grid) wrote

@@ -23,7 +23,8 @@ constexpr int TMA_CONSUMERS = 8;
 constexpr int TMA_STAGES = 16;          // multiple of TMA_CONSUMERS
 constexpr int TMA_TILE_BYTES = 12288;   // 16 stages x 12 KB = 192 KB ring
 constexpr int TMA_THREADS = 32 * (TMA_CONSUMERS + 1);
-constexpr int TMA_CLAIM = 8;            // tiles per counter claim
+constexpr int TMA_CLAIM = 16;           // tiles per home-range claim
+constexpr int TMA_STEAL = 4;            // tiles per stolen claim
 constexpr size_t TMA_SMEM = (size_t)TMA_STAGES * TMA_TILE_BYTES + TMA_STAGES * 24 + 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -63,7 +64,7 @@ __device__ __forceinline__ void tma_tile(const ScanArgs& A, const BinSpec& B, in
   int64_t cs, ce;
   chunk_range(A, tile, cs, ce);
   if (cs >= ce) return;
-  const SmemSrc src{sv, (A.vstart + tile * A.che) / VEC};
+  const SmemSrc src{smem_u32(sv), (A.vstart + tile * A.che) / VEC};
   int64_t g = bin_of(B, cs, A.g0, A.g1);
   int64_t pos = cs;
   while (pos < ce && g < A.g1) {
@@ -128,9 +129,13 @@ tma_scan_kernel(const ScanArgs A, int64_t cv_lo, int64_t cv_hi) {
 
   if (warp == 0) {
     // ---------------------------------------------------------- producer
-    if (lane == 0) {
-      int64_t q = 0;
-      auto issue = [&](int64_t tile) {
+    // Lane 0 issues the bulk copies; the whole warp takes part in claiming.
+    // The CTA first drains its own home range in batches of TMA_CLAIM tiles,
+    // then steals: all 32 lanes read the other ranges' counters at once and
+    // the warp claims TMA_STEAL tiles from the range with the most left.
+    int64_t q = 0;
+    auto issue = [&](int64_t tile) {
+      if (lane == 0) {
         const int s = (int)(q % TMA_STAGES);
         const int64_t k = q / TMA_STAGES;
         if (k > 0) mbar_wait(&empty[s], (uint32_t)((k - 1) & 1));
@@ -145,33 +150,48 @@ tma_scan_kernel(const ScanArgs A, int64_t cv_lo, int64_t cv_hi) {
           mbar_arrive_expect_tx(&full[s], bytes);
           if (bytes) bulk_g2s(stages + (size_t)s * (TMA_TILE_BYTES / 16) + (a - v0), yv + a, bytes, &full[s]);
         }
-        q++;
-      };
-      // claims are prefetched one batch ahead so the atomic's latency hides
-      // behind issuing (and waiting for free stages of) the current batch
-      const int64_t G = A.n_ranges;
-      int64_t victim = blockIdx.x;
-      auto range_len = [&](int64_t v) {
-        const int64_t base = v * A.range_len;
-        return base >= A.n_static ? (int64_t)0 : (A.n_static - base < A.range_len ? A.n_static - base : A.range_len);
-      };
-      unsigned long long t = atomicAdd(&A.range_ctr[victim], (unsigned long long)TMA_CLAIM);
-      for (int64_t tried = 0; tried < G;) {
-        const int64_t len = range_len(victim);
-        if ((int64_t)t >= len) {
-          victim = victim + 1 == G ? 0 : victim + 1;
-          tried++;
-          if (tried < G) t = atomicAdd(&A.range_ctr[victim], (unsigned long long)TMA_CLAIM);
-          continue;
-        }
-        const unsigned long long tn = atomicAdd(&A.range_ctr[victim], (unsigned long long)TMA_CLAIM);
-        const int64_t base = victim * A.range_len;
-        const int64_t t1 = (int64_t)t + TMA_CLAIM < len ? (int64_t)t + TMA_CLAIM : len;
-        for (int64_t j = (int64_t)t; j < t1; j++) issue(base + j);
-        t = tn;
       }
-      for (int c = 0; c < TMA_CONSUMERS; c++) issue(-1);
+      q++;
+    };
+    const int64_t G = A.n_ranges;
+    auto range_len = [&](int64_t v) {
+      const int64_t base = v * A.range_len;
+      return base >= A.n_static ? (int64_t)0 : (A.n_static - base < A.range_len ? A.n_static - base : A.range_len);
+    };
+    auto claim = [&](int64_t v, int64_t want) -> unsigned long long {
+      unsigned long long t = 0;
+      if (lane == 0) t = atomicAdd(&A.range_ctr[v], (unsigned long long)want);
+      return __shfl_sync(0xffffffffu, t, 0);
+    };
+    {
+      const int64_t v = blockIdx.x, len = range_len(v), base = v * A.range_len;
+      while (true) {
+        const int64_t t = (int64_t)claim(v, TMA_CLAIM);
+        if (t >= len) break;
+        const int64_t t1 = t + TMA_CLAIM < len ? t + TMA_CLAIM : len;
+        for (int64_t j = t; j < t1; j++) issue(base + j);
+      }
     }
+    while (true) {
+      int64_t best = -1, left = 0;
+      for (int64_t v = lane; v < G; v += 32) {
+        const int64_t l = range_len(v) - (int64_t)*(volatile unsigned long long*)&A.range_ctr[v];
+        if (l > left) { left = l; best = v; }
+      }
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) {
+        const int64_t ol = __shfl_xor_sync(0xffffffffu, left, m);
+        const int64_t ob = __shfl_xor_sync(0xffffffffu, best, m);
+        if (ol > left || (ol == left && ob < best)) { left = ol; best = ob; }
+      }
+      if (left <= 0) break;
+      const int64_t len = range_len(best), base = best * A.range_len;
+      const int64_t t = (int64_t)claim(best, TMA_STEAL);
+      if (t >= len) continue;
+      const int64_t t1 = t + TMA_STEAL < len ? t + TMA_STEAL : len;
+      for (int64_t j = t; j < t1; j++) issue(base + j);
+    }
+    for (int c = 0; c < TMA_CONSUMERS; c++) issue(-1);
   } else {
     // ---------------------------------------------------------- consumers
     const int cw = warp - 1;
