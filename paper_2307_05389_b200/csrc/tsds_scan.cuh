@@ -227,15 +227,29 @@ __device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, co
         if (jnan < 0 && O::vec_hasnan(v)) jnan = jj;
       }
     };
-    int j = lane;
-    for (; j + 32 * (U - 1) < nv; j += 32 * U) {
+    // Every batch -- including the last, partial one -- issues all of its U
+    // loads before consuming any, so short segments keep U loads in flight.
+    // Indices past the end are clamped to the last vector: re-reading it
+    // (with its own index) can never change a strict-improvement extremum.
+    // The batch loop is warp-uniform (no divergent tail to serialise).
+    const int last = nv - 1;
+    int jb0 = 0;
+    for (; jb0 + 32 * U <= nv; jb0 += 32 * U) {
+      const int j = jb0 + lane;
       uint4 buf[U];
 #pragma unroll
       for (int u = 0; u < U; u++) buf[u] = src.stream(p, j + 32 * u);
 #pragma unroll
       for (int u = 0; u < U; u++) step(buf[u], j + 32 * u);
     }
-    for (; j < nv; j += 32) step(src.stream(p, j), j);
+    if (jb0 < nv) {
+      const int j = jb0 + lane;
+      uint4 buf[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) buf[u] = src.stream(p, min(j + 32 * u, last));
+#pragma unroll
+      for (int u = 0; u < U; u++) step(buf[u], min(j + 32 * u, last));
+    }
 
     if constexpr (O::FALLBACK) {
       if (lane < nv) {
