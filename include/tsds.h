@@ -57,7 +57,7 @@ typedef struct tsds_ctx tsds_ctx;
 int tsds_version(void);
 const char *tsds_last_error(void);
 /* process-wide tuning knobs (no effect on results): "tma_min_bytes" (inputs
- * at least this large use the TMA bulk-copy scan; default 16 MiB, env
+ * at least this large use the TMA bulk-copy scan; default: off (the LDG scan measured faster), env
  * TSDS_TMA_MIN_BYTES), "dyn_percent" (share of the LDG scan handed out
  * dynamically; default 0, env TSDS_DYN_PERCENT) */
 int tsds_set_option(const char *name, int64_t value);

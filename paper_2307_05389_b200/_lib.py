@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtsds.so")
+LIB_PATH = os.environ.get("TSDS_LIB") or os.path.join(HERE, "libtsds.so")
 
 TSDS_OK = 0
 TSDS_ERR_ARG = -1

@@ -176,7 +176,7 @@ void prepare_bins(BinSpec& b, int64_t max_index) {
 int64_t tma_min_bytes() {
   if (g_tma_min_bytes < 0) {
     const char* e = getenv("TSDS_TMA_MIN_BYTES");
-    g_tma_min_bytes = e ? atoll(e) : (int64_t)16 << 20;
+    g_tma_min_bytes = e ? atoll(e) : INT64_MAX;  // opt-in: the LDG scan measured faster
   }
   return g_tma_min_bytes;
 }

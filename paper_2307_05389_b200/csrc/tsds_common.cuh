@@ -121,13 +121,31 @@ __device__ __forceinline__ bool f16_bits_isnan(uint32_t u) {
 // ---------------------------------------------------------------------------
 // streaming loads
 
+// L1ALLOC: let the stream allocate in L1 so the locate re-reads of short
+// (narrow-dtype) segments hit it; wide dtypes stream past L1.
+template <bool L1ALLOC>
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+  if constexpr (L1ALLOC) {
+    asm volatile("ld.global.nc.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  } else {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  }
   return r;
 }
+
+// Per-dtype scan tuning (measured on B200, tools/variants.py): 1- and 2-byte
+// types run 32 warps/SM (64 registers) with L1-allocating streams; 4- and
+// 8-byte types 24 warps/SM (80 registers, all U loads hoisted) past L1.
+template <int ES>
+struct ScanCfg {
+  static constexpr int MIN_BLOCKS = ES <= 2 ? 4 : 3;
+  static constexpr bool L1ALLOC = ES <= 2;
+};
 
 template <class T>
 __device__ __forceinline__ T ldg_elem(const T* p) {

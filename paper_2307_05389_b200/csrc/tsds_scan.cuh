@@ -24,9 +24,6 @@
 namespace tsds {
 
 constexpr int SCAN_WARPS = 8;  // 256 threads per CTA
-#ifndef SCAN_MIN_BLOCKS
-#define SCAN_MIN_BLOCKS 4  // <= 64 registers: 32 resident warps per SM
-#endif
 
 enum Epilogue : int { EPI_MINMAX = 0, EPI_M4 = 1, EPI_PAIR = 2, EPI_SLOTS_MINMAX = 3, EPI_SLOTS_M4 = 4 };
 
@@ -158,10 +155,11 @@ __device__ __forceinline__ void chunk_range(const ScanArgs& A, int64_t w, int64_
 // one bin segment [a, c) reduced by a warp
 
 // vector sources: global memory (streaming loads) or a shared-memory tile
+template <bool L1ALLOC>
 struct GlobalSrc {
   const uint4* yv;  // virtual vector 0
   __device__ __forceinline__ const uint4* base(int64_t jb) const { return yv + jb; }
-  __device__ __forceinline__ uint4 stream(const uint4* p, int j) const { return ldg_stream(p + j); }
+  __device__ __forceinline__ uint4 stream(const uint4* p, int j) const { return ldg_stream<L1ALLOC>(p + j); }
   __device__ __forceinline__ uint4 again(const uint4* p, int j) const { return __ldg(p + j); }
 };
 struct SmemSrc {
@@ -258,29 +256,32 @@ __device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, co
       }
     }
     const int64_t i0 = jb * VEC - A.shift;  // element index of vector jb
+    // re-read the (at most three) vectors holding this lane's extrema; all
+    // loads are issued before any is used so they overlap
+    const uint4 vmn = src.again(p, jmn >= 0 ? jmn : 0);
+    const uint4 vmx = src.again(p, jmx >= 0 ? jmx : 0);
+    uint4 vnan = vmn;
+    if constexpr (PROP && O::NANABLE) vnan = src.again(p, jnan >= 0 ? jnan : 0);
     if (jmn >= 0 && O::valid(rmn)) {
-      uint4 v = src.again(p, jmn);
       int q0 = 0;
 #pragma unroll
       for (int q = VEC - 1; q >= 0; q--)
-        if (O::elem(v, q) == rmn) q0 = q;
+        if (O::elem(vmn, q) == rmn) q0 = q;
       merge_min(res.mn, Cand{O::key(rmn), i0 + (int64_t)jmn * VEC + q0});
     }
     if (jmx >= 0 && O::valid(rmx)) {
-      uint4 v = src.again(p, jmx);
       int q0 = 0;
 #pragma unroll
       for (int q = VEC - 1; q >= 0; q--)
-        if (O::elem(v, q) == rmx) q0 = q;
+        if (O::elem(vmx, q) == rmx) q0 = q;
       merge_max(res.mx, Cand{O::key(rmx), i0 + (int64_t)jmx * VEC + q0});
     }
     if constexpr (PROP && O::NANABLE) {
       if (jnan >= 0) {
-        uint4 v = src.again(p, jnan);
         int q0 = 0;
 #pragma unroll
         for (int q = VEC - 1; q >= 0; q--)
-          if (O::elem_nan(v, q)) q0 = q;
+          if (O::elem_nan(vnan, q)) q0 = q;
         int64_t idx = i0 + (int64_t)jnan * VEC + q0;
         merge_min(res.mn, Cand{0ull, idx});
         merge_max(res.mx, Cand{KEY_MAX, idx});
@@ -298,7 +299,7 @@ __device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, co
 template <int DT, bool PROP, int U>
 __device__ __forceinline__ MinMaxCand seg_reduce(const ScanArgs& A, int64_t a, int64_t c) {
   using E = typename Ops<DT>::E;
-  GlobalSrc src{reinterpret_cast<const uint4*>(static_cast<const E*>(A.y) - A.shift)};
+  GlobalSrc<ScanCfg<sizeof(E)>::L1ALLOC> src{reinterpret_cast<const uint4*>(static_cast<const E*>(A.y) - A.shift)};
   return seg_reduce_src<DT, PROP, U>(A, a, c, src);
 }
 
@@ -492,7 +493,7 @@ __device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted)
 }
 
 template <int DT, bool PROP, int U>
-__global__ void __launch_bounds__(SCAN_WARPS * 32, SCAN_MIN_BLOCKS)
+__global__ void __launch_bounds__(SCAN_WARPS * 32, ScanCfg<sizeof(typename Ops<DT>::E)>::MIN_BLOCKS)
 scan_kernel(const ScanArgs A) {
   // programmatic dependent launch: everything below may read what the
   // binning kernel (the primary grid) wrote
