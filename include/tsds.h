@@ -97,6 +97,24 @@ int tsds_downsample_async(tsds_ctx *ctx, int algo, const void *x, int x_dtype, c
                           int64_t n, int64_t n_out, int nan_mode, int64_t *out_dev, int64_t *count_dev,
                           int32_t *status_dev);
 
+/* One shard of a sharded MinMax / M4 (multi-GPU): the bins
+ * [b0, b1) of a larger series, i.e. _run_bins' per-thread bin chunk
+ * (algorithms.py:88-98) on one device.  y_dev holds the shard's elements;
+ * off_dev[0..n_bins] are the shard's bin offsets relative to y_dev;
+ * idx_base is added to every emitted index (the shard's global start).
+ * out_dev: int64[width*n_bins] (compacted, ascending), count_dev: int64. */
+int tsds_downsample_bins_async(tsds_ctx *ctx, int algo, const void *y_dev, int y_dtype, const int64_t *off_dev,
+                               int64_t n_bins, int64_t idx_base, int nan_mode, int64_t *out_dev,
+                               int64_t *count_dev);
+
+/* MinMaxLTTB stage 2 (algorithms.py:235-255) on gathered candidates, for
+ * the sharded path: full[0..m) are the candidate positions ([0] + per-bin
+ * picks + [n-1]), y2 = y[full] and x2 = x[full] (x2 NULL when the series
+ * has no x: positions stand in for x and the bins are equal-count).  Host
+ * pointers; out int64[n_out] receives original indices. */
+int tsds_lttb_stage2(tsds_ctx *ctx, const void *x2, int x_dtype, const void *y2, int y_dtype, const int64_t *full,
+                     int64_t m, int64_t n_out, int64_t *out, int64_t *out_len);
+
 /* Batched MinMax (extension; the reference has no batch API):
  * row s of y[n_series][len] gives out[s*n_out ...] and counts[s]; row s
  * equals tsds_downsample(MINMAX, y[s]).  out/counts are host pointers

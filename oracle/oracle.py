@@ -54,6 +54,8 @@ def lib():
         L.or_downsample.argtypes = [i32, vp, i32, vp, i32, i64, i64, i64, i32, i32, vp]
         L.or_downsample.restype = i64
         L.or_minmax_batched.argtypes = [vp, i32, i64, i64, i64, i32, i32, vp, vp]
+        L.or_lttb_walk.argtypes = [vp, i32, vp, i32, i64, vp, i64, vp]
+        L.or_lttb_walk.restype = i64
         _lib = L
     return _lib
 
@@ -137,3 +139,30 @@ def minmax_batched(Y, n_out, nan=False, threads=1):
         _ptr(Y), DTYPE_CODES[Y.dtype], S, L, int(n_out), int(nan), int(threads), _ptr(out), _ptr(counts)
     )
     return out.astype(np.uint64), counts
+
+
+def lttb_walk(x, y, off):
+    """The reference triangle walk with caller-supplied offsets (x None: implicit)."""
+    y = np.ascontiguousarray(y)
+    x = _x_view(x)
+    off = np.ascontiguousarray(off, dtype=np.int64)
+    out = np.zeros(off.shape[0] + 1, np.int64)
+    m = lib().or_lttb_walk(_ptr(x), 0 if x is None else DTYPE_CODES[x.dtype], _ptr(y), DTYPE_CODES[y.dtype],
+                           y.shape[0], _ptr(off), off.shape[0] - 1, _ptr(out))
+    return out[:m]
+
+
+def stage2(x, y, full, n_out):
+    """MinMaxLTTB stage 2 on candidates `full` (algorithms.py:243-255)."""
+    full = np.asarray(full, np.int64)
+    m = full.shape[0]
+    y2 = np.ascontiguousarray(y[full])
+    nb = n_out - 2
+    if x is None:
+        off2 = (np.arange(nb + 1, dtype=np.int64) * (m - 2)) // nb + 1
+        sel = lttb_walk(full, y2, off2)
+    else:
+        x2 = np.ascontiguousarray(np.asarray(x)[full])
+        off2 = equal_width(x2[1:-1], nb).astype(np.int64) + 1
+        sel = lttb_walk(x2, y2, off2)
+    return full[sel].astype(np.uint64)

@@ -341,6 +341,12 @@ static int64_t lttb_walk(const void *x, int xdt, const void *y, int ydt, int64_t
     return m + 1;
 }
 
+/* exported walk with caller offsets (for stage-2 checks of sharded runs) */
+int64_t or_lttb_walk(const void *x, int xdt, const void *y, int ydt, int64_t n,
+                     const int64_t *off, int64_t nb, int64_t *out) {
+    return lttb_walk(x, xdt, y, ydt, n, off, nb, out);
+}
+
 /* ------------------------------------------------------------------------ */
 /* algorithms (algorithms.py) -- validation happens in the Python wrapper,   */
 /* x is already normalized (api.py:19-28).  Return value: the number of      */

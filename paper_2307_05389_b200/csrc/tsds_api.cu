@@ -414,10 +414,11 @@ ScanArgs scan_args(const void* y, BinSpec bins, int64_t g0, int64_t g1, int64_t 
 int launch_binning(tsds_ctx* ctx, int xdt, const void* x, int64_t n, int64_t nb, int64_t add, const void* xapi,
                    int64_t napi, int uniform_first, int materialize, int64_t* off) {
   const int cta_edges = (nb - 1) * BIN_THREADS <= (int64_t)ctx->sms * 2048 ? 1 : 0;
-  BinJob J{x, n, nb, add, xapi, napi, uniform_first, materialize, cta_edges, off, &misc(ctx)->F};
-  const int64_t edge_blocks = cta_edges ? nb - 1 : (nb + BIN_THREADS / 32 - 1) / (BIN_THREADS / 32);
-  const int64_t piece_blocks = std::min<int64_t>((int64_t)ctx->sms * 8, (std::max(n, napi) + 511) / 512);
-  unsigned grid = (unsigned)std::max<int64_t>(1, std::max(std::min<int64_t>((int64_t)ctx->sms * 16, edge_blocks), piece_blocks));
+  const int64_t edge_blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 16,
+      cta_edges ? nb - 1 : (nb + BIN_THREADS / 32 - 1) / (BIN_THREADS / 32)));
+  const int64_t piece_blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms, (std::max(n, napi) + 511) / 512));
+  BinJob J{x, n, nb, add, xapi, napi, uniform_first, materialize, cta_edges, piece_blocks, off, &misc(ctx)->F};
+  unsigned grid = (unsigned)(piece_blocks + edge_blocks);
   XDT_SWITCH(xdt, (binning_kernel<XD><<<grid, BIN_THREADS, 0, ctx->stream>>>(J)));
   LAUNCH_CHECK();
   ctx->flags_clean = false;
@@ -901,6 +902,65 @@ int tsds_downsample_async(tsds_ctx* ctx, int algo, const void* x, int xdt, const
   if (status_dev)
     CUDA_TRY(cudaMemcpyAsync(status_dev, &misc(ctx)->status_copy, sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
   return TSDS_OK;
+}
+
+int tsds_lttb_stage2(tsds_ctx* ctx, const void* x2, int xdt, const void* y2, int ydt, const int64_t* full, int64_t m,
+                     int64_t n_out, int64_t* out, int64_t* out_len) {
+  if (!ctx || !y2 || !full || !out || !out_len || m < 2 || n_out < 3 || !dtype_ok(ydt) || (x2 && !xdtype_ok(xdt)))
+    return set_err(TSDS_ERR_ARG, "tsds_lttb_stage2: invalid argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (m <= n_out) {
+    memcpy(out, full, (size_t)m * 8);
+    *out_len = m;
+    return TSDS_OK;
+  }
+  RC_TRY(begin_call(ctx));
+  const int64_t nb2 = n_out - 2;
+  std::vector<int64_t> o2(nb2 + 1);
+  if (!x2) {
+    for (int64_t k = 0; k <= nb2; k++) o2[k] = (int64_t)((unsigned __int128)k * (uint64_t)(m - 2) / (uint64_t)nb2) + 1;
+  } else {
+    int rc = tsds_host_equal_width_offsets((const char*)x2 + dtype_size(xdt), xdt, m - 2, nb2, o2.data());
+    if (rc == TSDS_ERR_SPAN) return set_err(rc, "invalid index span");
+    for (auto& v : o2) v += 1;
+  }
+  RC_TRY(upload(ctx, ctx->off, o2.data(), o2.size() * 8));
+  RC_TRY(upload(ctx, ctx->full, full, (size_t)m * 8));
+  RC_TRY(upload(ctx, ctx->y2, y2, (size_t)m * dtype_size(ydt)));
+  const double* x2f = nullptr;
+  if (!x2) {
+    RC_TRY(to_f64(ctx, ctx->full.p, DT_I64, m, ctx->x2f64, &x2f));
+  } else {
+    RC_TRY(upload(ctx, ctx->x2, x2, (size_t)m * dtype_size(xdt)));
+    RC_TRY(to_f64(ctx, ctx->x2.p, xdt, m, ctx->x2f64, &x2f));
+  }
+  RC_TRY(ensure(ctx, ctx->out, (size_t)(n_out + 2) * 8));
+  int64_t* dout = (int64_t*)ctx->out.p;
+  RC_TRY(run_lttb_walk(ctx, x2f, nullptr, ctx->y2.p, ydt, m, (const int64_t*)ctx->off.p, nb2,
+                       (const int64_t*)ctx->full.p, dout));
+  return fetch_result(ctx, dout, n_out, out, out_len);
+}
+
+int tsds_downsample_bins_async(tsds_ctx* ctx, int algo, const void* y, int ydt, const int64_t* off, int64_t nb,
+                               int64_t idx_base, int nan_mode, int64_t* out_dev, int64_t* count_dev) {
+  if (!ctx || !y || !off || !out_dev || !count_dev || nb < 1 || !dtype_ok(ydt) ||
+      (algo != TSDS_MINMAX && algo != TSDS_M4))
+    return set_err(TSDS_ERR_ARG, "tsds_downsample_bins_async: invalid argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  RC_TRY(begin_call(ctx));
+  // the shard's span: offsets are relative to y; read the two ends
+  int64_t ends[2];
+  CUDA_TRY(cudaMemcpyAsync(&ends[0], off, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(&ends[1], off + nb, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  ScanArgs A = scan_args(y, BinSpec{1, off, 0, 0, 0}, 0, nb, ends[0], ends[1]);
+  A.independent = ends[1] < ends[0];
+  A.epi = algo == TSDS_MINMAX ? EPI_MINMAX : EPI_M4;
+  A.out = out_dev;
+  A.out_count = count_dev;
+  A.idx_sub = -idx_base;
+  if (ends[1] < ends[0]) return set_err(TSDS_ERR_ARG, "non-monotone shard offsets");
+  return launch_scan(ctx, ydt, nan_mode, A);
 }
 
 static int batched_enqueue(tsds_ctx* ctx, const void* dy, int ydt, int64_t S, int64_t L, int64_t n_out, int nan_mode,

@@ -50,23 +50,23 @@ __device__ __forceinline__ double xf64(const void* x, int64_t i) {
 // is uniformly spaced.  Blocks walk pieces in increasing order and stop as
 // soon as any block has seen a mismatch (the reference exits at the first).
 template <int XDT>
-__device__ void uniform_pieces(const void* xv, int64_t n, int* mismatch) {
+__device__ void uniform_pieces(const void* xv, int64_t n, int* mismatch, int64_t rb, int64_t rn) {
   using T = typename XT<XDT>::T;
   using D = typename XT<XDT>::D;
   const T* x = (const T*)xv;
   if (n < 2) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *mismatch = 1;
+    if (rb == 0 && threadIdx.x == 0) *mismatch = 1;
     return;
   }
   const D d = xgap<XDT>(x, 0);
   if (!gap_positive<XDT>(d)) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *mismatch = 1;
+    if (rb == 0 && threadIdx.x == 0) *mismatch = 1;
     return;
   }
   const int64_t piece = 4 * (int64_t)blockDim.x;
   const int64_t ngaps = n - 2;  // gaps i = 1 .. n-2
   __shared__ int stop;
-  for (int64_t p0 = (int64_t)blockIdx.x * piece; p0 < ngaps; p0 += (int64_t)gridDim.x * piece) {
+  for (int64_t p0 = rb * piece; p0 < ngaps; p0 += rn * piece) {
     __syncthreads();
     if (threadIdx.x == 0) stop = *(volatile int*)mismatch;
     __syncthreads();
@@ -155,6 +155,67 @@ __device__ int64_t lower_bound_exact_cta(const void* x, int64_t n, double edge) 
   return lo;
 }
 
+// Interpolation-guided lower bound with exact verification (CTA-wide).
+// 1) guess the boundary from (e - x0) / span and load a BIN_THREADS*8
+//    window around it; if the window brackets the boundary, r = window start
+//    + number of elements < e;  2) verify that the reference's binary search
+//    (mid = (lo+hi)>>1, x[mid] < e -> lo = mid+1) ends at r: walk the path
+//    that "mid < r" dictates and check x[mid] < e == (mid < r) at each of its
+//    <= 64 probes (all loaded at once).  If either step fails (x far from
+//    linear, or not monotone) fall back to the exact tree emulation.  Two
+//    dependent memory rounds instead of four for typical timestamps.
+template <int XDT>
+__device__ int64_t lower_bound_fast_cta(const void* x, int64_t n, double e, double x0, double span) {
+  constexpr int PER = 8;
+  constexpr int64_t W = (int64_t)BIN_THREADS * PER;
+  __shared__ int s_cnt, s_ok;
+  const int tid = threadIdx.x;
+  if (tid == 0) { s_cnt = 0; s_ok = 1; }
+  __syncthreads();
+  double t = __ddiv_rn(__dsub_rn(e, x0), span);
+  t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+  int64_t g = (int64_t)(t * (double)(n - 1));
+  int64_t ws = g - W / 2;
+  if (ws > n - W) ws = n - W;
+  if (ws < 0) ws = 0;
+  const int64_t we = ws + W < n ? ws + W : n;
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < PER; k++) {
+    const int64_t i = ws + (int64_t)tid * PER + k;
+    if (i < we) cnt += xf64<XDT>(x, i) < e ? 1 : 0;
+  }
+  // bracket: x[ws] < e (or ws == 0) and x[we-1] >= e (or we == n)
+  bool br = true;
+  if (tid == 0) br = ws == 0 || xf64<XDT>(x, ws) < e;
+  if (tid == 1) br = we == n || !(xf64<XDT>(x, we - 1) < e);
+  for (int m = 16; m >= 1; m >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
+  if ((tid & 31) == 0 && cnt) atomicAdd(&s_cnt, cnt);
+  if (!br) atomicExch(&s_ok, 0);
+  __syncthreads();
+  const int64_t r = ws + s_cnt;
+  bool ok = s_ok != 0;
+  if (ok) {
+    // verification: thread l checks level l of the path to r
+    if (tid < 64) {
+      int64_t lo = 0, hi = n, mid = -1;
+      for (int l = 0; l <= tid && lo < hi; l++) {
+        mid = (lo + hi) >> 1;
+        if (l == tid) break;
+        if (mid < r) lo = mid + 1; else hi = mid;
+      }
+      if (lo < hi && mid >= 0) {
+        if ((xf64<XDT>(x, mid) < e) != (mid < r)) atomicExch(&s_ok, 0);
+      }
+    }
+    __syncthreads();
+    ok = s_ok != 0;
+  }
+  __syncthreads();
+  if (ok) return r;
+  return lower_bound_exact_cta<XDT>(x, n, e);
+}
+
 // One launch computes the bins of x[0..n) (binning.py:43-82 semantics):
 //   * uniform-spacing checks of the binned slice and (optionally) of the
 //     whole x for the api-level normalisation (api.py:19-28);
@@ -175,6 +236,7 @@ struct BinJob {
   int uniform_first;  // 1: a uniform slice short-circuits before span checks
   int materialize;    // write equal-count offsets into `off` too
   int cta_edges;      // 1: one CTA per edge (few edges), 0: one warp per edge
+  int64_t n_uniform;  // blocks [0, n_uniform) check uniform spacing, the rest search edges
   int64_t* off;       // [nb+1]
   PipeFlags* F;
 };
@@ -188,19 +250,26 @@ __global__ void binning_kernel(const BinJob J) {
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n = J.n, nb = J.nb;
 
-  // speculative edges (valid whenever the verdict turns out to be "edges")
-  if (n > 0) {
+  // Blocks [0, n_uniform) run the uniform-spacing checks while the other
+  // blocks search the edges speculatively (valid whenever the verdict turns
+  // out to be "edges"); both roles proceed concurrently.
+  if ((int64_t)blockIdx.x < J.n_uniform) {
+    uniform_pieces<XDT>(J.x, n, &F->mis_slice, blockIdx.x, J.n_uniform);
+    if (J.xapi) uniform_pieces<XDT>(J.xapi, J.napi, &F->mis_api, blockIdx.x, J.n_uniform);
+  } else if (n > 0) {
+    const int64_t eb = blockIdx.x - J.n_uniform, neb = gridDim.x - J.n_uniform;
     const double x0 = xf64<XDT>(J.x, 0);
     const double span = __dsub_rn(xf64<XDT>(J.x, n - 1), x0);
     if (isfinite(span) && span != 0.0) {
       if (J.cta_edges) {
-        for (int64_t k = 1 + blockIdx.x; k < nb; k += gridDim.x) {
+        for (int64_t k = 1 + eb; k < nb; k += neb) {
           double e = __dadd_rn(x0, __ddiv_rn(__dmul_rn((double)k, span), (double)nb));
-          int64_t v = lower_bound_exact_cta<XDT>(J.x, n, e);
+          int64_t v = lower_bound_fast_cta<XDT>(J.x, n, e, x0, span);
           if (threadIdx.x == 0) J.off[k] = v + J.add;
         }
       } else {
-        for (int64_t k = 1 + gw; k < nb; k += nwarps) {
+        const int64_t w0 = eb * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        for (int64_t k = 1 + w0; k < nb; k += neb * (blockDim.x >> 5)) {
           double e = __dadd_rn(x0, __ddiv_rn(__dmul_rn((double)k, span), (double)nb));
           int64_t v = lower_bound_exact<XDT>(J.x, n, e);
           if (lane == 0) J.off[k] = v + J.add;
@@ -208,8 +277,8 @@ __global__ void binning_kernel(const BinJob J) {
       }
     }
   }
-  uniform_pieces<XDT>(J.x, n, &F->mis_slice);
-  if (J.xapi) uniform_pieces<XDT>(J.xapi, J.napi, &F->mis_api);
+  (void)gw;
+  (void)nwarps;
 
   __shared__ int s_last, s_mode;
   __threadfence();
