@@ -59,7 +59,10 @@ const char *tsds_last_error(void);
 /* process-wide tuning knobs (no effect on results): "tma_min_bytes" (inputs
  * at least this large use the TMA bulk-copy scan; default: off (the LDG scan measured faster), env
  * TSDS_TMA_MIN_BYTES), "dyn_percent" (share of the LDG scan handed out
- * dynamically; default 0, env TSDS_DYN_PERCENT) */
+ * dynamically; default 0, env TSDS_DYN_PERCENT), "lttb_exact" (centroid
+ * summation of large-bucket LTTB: 0 auto = the reference's sequential order
+ * for buckets <= 16384 points, a pairwise tree above; 1 always sequential;
+ * 2 always tree; env TSDS_LTTB_EXACT) */
 int tsds_set_option(const char *name, int64_t value);
 int tsds_device_count(int *count);
 
@@ -71,6 +74,9 @@ void *tsds_ctx_stream(tsds_ctx *ctx);
 int tsds_ctx_synchronize(tsds_ctx *ctx);
 /* number of this library's kernels launched on ctx so far */
 int64_t tsds_ctx_launches(tsds_ctx *ctx);
+/* counters: "launches", "lttb_rounds" (verification rounds of the last
+ * large-bucket LTTB); -1 for an unknown name */
+int64_t tsds_ctx_stat(tsds_ctx *ctx, const char *name);
 /* measurement hooks: record CUDA events around every argmin/argmax scan
  * launch; _read synchronises, returns their summed duration and count, and
  * clears the record */

@@ -35,6 +35,7 @@ EXPORTED = (
     "tsds_ctx_stream",
     "tsds_ctx_synchronize",
     "tsds_ctx_launches",
+    "tsds_ctx_stat",
     "tsds_ctx_profile",
     "tsds_ctx_profile_read",
     "tsds_downsample",
@@ -92,6 +93,8 @@ def load():
         L.tsds_ctx_synchronize.argtypes = [vp]
         L.tsds_ctx_launches.argtypes = [vp]
         L.tsds_ctx_launches.restype = i64
+        L.tsds_ctx_stat.argtypes = [vp, ctypes.c_char_p]
+        L.tsds_ctx_stat.restype = i64
         L.tsds_ctx_profile.argtypes = [vp, i32]
         L.tsds_ctx_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), p64]
         L.tsds_downsample.argtypes = [vp, i32, vp, i32, vp, i32, i64, i64, i64, i32, i32, vp, p64]

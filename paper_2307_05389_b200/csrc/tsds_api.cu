@@ -19,6 +19,7 @@
 #include "../../include/tsds.h"
 #include "tsds_bin.cuh"
 #include "tsds_lttb.cuh"
+#include "tsds_lttb_large.cuh"
 #include "tsds_scan.cuh"
 #include "tsds_tma.cuh"
 
@@ -59,7 +60,9 @@ struct tsds_ctx {
   bool own_stream = true;
   int sms = 148;
   std::mutex mu;
-  DevBuf y, x, xf64, part, bincnt, res, off, out, misc, cent, scratch, y2, x2, x2f64, full, out2, rctr;
+  DevBuf y, x, xf64, part, bincnt, res, off, out, misc, cent, scratch, y2, x2, x2f64, full, out2, rctr, lscr;
+  int64_t lttb_rounds = 0;  // verification rounds of the last large-bucket LTTB
+  int64_t lttb_dirty1 = 0;  // buckets whose guess was wrong in the first round
   void* h_pin = nullptr;
   size_t h_cap = 0;
   bool dirty = false;
@@ -533,13 +536,146 @@ __global__ void map_kernel(const int64_t* idx, const int64_t* map, int64_t m, in
 // ------------------------------------------------------------------------ LTTB
 // Runs the walk over (x_f64 or implicit, y) with offsets off[nb+1]; out_dev
 // receives [count, idx...]; map (nullable) translates node ids.
-int run_lttb_walk(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
-                  const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev) {
+int64_t g_lttb_exact = -1;  // 0 auto, 1 sequential centroids always, 2 tree sums always
+
+int lttb_exact_mode() {
+  if (g_lttb_exact < 0) {
+    const char* e = getenv("TSDS_LTTB_EXACT");
+    g_lttb_exact = e ? std::max(0, std::min(2, atoi(e))) : 0;
+  }
+  return (int)g_lttb_exact;
+}
+
+int run_lttb_walk_small(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
+                        const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev, bool have_cent = false);
+
+// Large buckets: prepass -> guess walk on the reduced problem -> verify/fix rounds.
+int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
+                   const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev) {
   RC_TRY(ensure(ctx, ctx->cent, (size_t)std::max<int64_t>(nb, 1) * sizeof(double2)));
   double2* cent = (double2*)ctx->cent.p;
-  unsigned gc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 16, (nb + 7) / 8));
-  YDT_SWITCH(ydt, (lttb_centroid_kernel<YD><<<gc, 256, 0, ctx->stream>>>(xf, drop, y, off, nb, cent)));
+  const int64_t NC = LTTB_NC;
+  const int64_t maxch = (n + LTTB_CH - 1) / LTTB_CH + nb + 1;
+  const int64_t maxseg = nb / LTTB_SEG + 2;
+  size_t need = 0;
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  need += al(8 * (nb + 1)) + al(4 * maxch) + al(4 * nb) + al(4 * nb) + al(64) + al(32 * nb) + al(16 * nb) +
+          al(sizeof(LttbChunkPart) * maxch) + al(8 * NC * nb) + al(NC * nb) + al(NC * maxseg) + al(maxseg) +
+          al(8 * (nb + 4)) + al(4 * nb) * 2 + al(64) + al(sizeof(LttbAreaPart) * maxch);
+  RC_TRY(ensure(ctx, ctx->lscr, need));
+  char* p = (char*)ctx->lscr.p;
+  auto take = [&](size_t bytes) { char* r = p; p += al(bytes); return r; };
+  int64_t* cstart = (int64_t*)take(8 * (nb + 1));
+  int32_t* cb = (int32_t*)take(4 * maxch);
+  int32_t* rank = (int32_t*)take(4 * nb);
+  int32_t* nonempty = (int32_t*)take(4 * nb);
+  int64_t* counts = (int64_t*)take(64);
+  double4* bbox = (double4*)take(32 * nb);
+  double2* slopes = (double2*)take(16 * nb);
+  LttbChunkPart* cpart = (LttbChunkPart*)take(sizeof(LttbChunkPart) * maxch);
+  int64_t* ext = (int64_t*)take(8 * NC * nb);
+  uint8_t* T = (uint8_t*)take(NC * nb);
+  uint8_t* C = (uint8_t*)take(NC * maxseg);
+  uint8_t* entry = (uint8_t*)take(maxseg);
+  int64_t* walkout = (int64_t*)take(8 * (nb + 4));
+  int32_t* dirty_a = (int32_t*)take(4 * nb);
+  int32_t* dirty_b = (int32_t*)take(4 * nb);
+  int32_t* ndirty = (int32_t*)take(64);
+  LttbAreaPart* apart = (LttbAreaPart*)take(sizeof(LttbAreaPart) * maxch);
+  int64_t* picks = walkout + 2;
+  const int mode = lttb_exact_mode();
+  const int64_t avg = (n - 2) / std::max<int64_t>(nb, 1);
+  const int exact = mode == 1 ? 1 : (mode == 2 ? 0 : (avg <= 1024 ? 1 : 0));
+  const unsigned gw8 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 16, (nb + 7) / 8));
+  // ---- layout, sampling, slopes
+  lttb_layout_kernel<<<1, 1024, 0, ctx->stream>>>(off, nb, cstart, cb, rank, nonempty, counts);
   LAUNCH_CHECK();
+  YDT_SWITCH(ydt, (lttb_sample_kernel<YD><<<gw8, 256, 0, ctx->stream>>>(y, off, nb, bbox)));
+  LAUNCH_CHECK();
+  YDT_SWITCH(ydt, (lttb_slopes_kernel<YD><<<(unsigned)std::max<int64_t>(1, (nb + 255) / 256), 256, 0, ctx->stream>>>(
+                      xf, drop, y, off, nb, n, bbox, slopes)));
+  LAUNCH_CHECK();
+  // ---- chunk prepass + per-bucket merge (centroids, candidates)
+  const unsigned gch = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (maxch + 7) / 8));
+  YDT_SWITCH(ydt, (lttb_chunk_prepass_kernel<YD><<<gch, 256, 0, ctx->stream>>>(xf, drop, y, off, cstart, cb, counts,
+                                                                             slopes, cpart)));
+  LAUNCH_CHECK();
+  YDT_SWITCH(ydt, (lttb_chunk_merge_kernel<YD><<<gw8, 256, 0, ctx->stream>>>(xf, drop, off, nb, cstart, cpart, cent,
+                                                                           ext)));
+  LAUNCH_CHECK();
+  if (exact) {
+    unsigned gc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 16, (nb + 7) / 8));
+    YDT_SWITCH(ydt, (lttb_centroid_kernel<YD><<<gc, 256, 0, ctx->stream>>>(xf, drop, y, off, nb, cent)));
+    LAUNCH_CHECK();
+  }
+  int64_t hc[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(hc, counts, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  const int64_t L = hc[0], NCH = hc[1];
+  if (L > 0) {
+    // ---- guess chain on the candidates (composed transition tables)
+    const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (L * NC + 255) / 256));
+    YDT_SWITCH(ydt, (lttb_cand_table_kernel<YD><<<gt, 256, 0, ctx->stream>>>(xf, drop, y, n, off, nb, cent, ext,
+                                                                           nonempty, counts, T)));
+    LAUNCH_CHECK();
+    const int64_t NS = (L + LTTB_SEG - 1) / LTTB_SEG;
+    const unsigned gs = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (NS + 7) / 8));
+    lttb_seg_compose_kernel<<<gs, 256, 0, ctx->stream>>>(T, counts, C);
+    LAUNCH_CHECK();
+    const int64_t cap = 40000;
+    lttb_seg_entry_kernel<<<1, 1024, (size_t)(std::min<int64_t>(NS * NC, cap) + 16), ctx->stream>>>(T, C, counts, entry,
+                                                                                                    cap);
+    LAUNCH_CHECK();
+    lttb_seg_expand_kernel<<<gs, 256, 0, ctx->stream>>>(T, entry, ext, nonempty, counts, picks);
+    LAUNCH_CHECK();
+    // ---- verify / fix rounds (double-buffered dirty flags)
+    CUDA_TRY(cudaMemsetAsync(dirty_b, 0, 4 * nb, ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(dirty_a, 0, 4 * nb, ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(dirty_a, 0xff, 4 * L, ctx->stream));
+    int32_t *cur = dirty_a, *nxt = dirty_b;
+    const unsigned gv = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (NCH + 7) / 8));
+    const unsigned gl = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (L + 7) / 8));
+    for (int round = 0;; round++) {
+      CUDA_TRY(cudaMemsetAsync(ndirty, 0, 4, ctx->stream));
+      YDT_SWITCH(ydt, (lttb_chunk_verify_kernel<YD><<<gv, 256, 0, ctx->stream>>>(
+                          xf, drop, y, n, off, nb, cent, cstart, cb, rank, counts, picks, cur, apart)));
+      LAUNCH_CHECK();
+      lttb_chunk_settle_kernel<<<gl, 256, 0, ctx->stream>>>(off, cstart, nonempty, counts, apart, picks, cur, nxt,
+                                                           ndirty);
+      LAUNCH_CHECK();
+      int32_t hd = 0;
+      CUDA_TRY(cudaMemcpyAsync(&hd, ndirty, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+      ctx->lttb_rounds = round + 1;
+      if (round == 0) ctx->lttb_dirty1 = hd;
+      if (hd == 0) break;
+      if (round > nb + 2) return set_err(TSDS_ERR_CUDA, "LTTB verification did not converge");
+      std::swap(cur, nxt);
+    }
+    (void)NCH;
+  }
+  lttb_emit_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, (L + 257) / 256)), 256, 0, ctx->stream>>>(
+      picks, counts, n, map, out_dev + 1, out_dev);
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
+int run_lttb_walk(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
+                  const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev) {
+  const int64_t avg = (n - 2) / std::max<int64_t>(nb, 1);
+  if (avg > SMALL_MAX / 2) return run_lttb_large(ctx, xf, drop, y, ydt, n, off, nb, map, out_dev);
+  return run_lttb_walk_small(ctx, xf, drop, y, ydt, n, off, nb, map, out_dev);
+}
+
+int run_lttb_walk_small(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
+                        const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev, bool have_cent) {
+  RC_TRY(ensure(ctx, ctx->cent, (size_t)std::max<int64_t>(nb, 1) * sizeof(double2)));
+  double2* cent = (double2*)ctx->cent.p;
+  if (!have_cent) {
+    unsigned gc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 16, (nb + 7) / 8));
+    YDT_SWITCH(ydt, (lttb_centroid_kernel<YD><<<gc, 256, 0, ctx->stream>>>(xf, drop, y, off, nb, cent)));
+    LAUNCH_CHECK();
+  }
   // scratch for the small-bucket (jump) strategy when buckets are small on average
   LttbScratch S{nullptr, nullptr, nullptr};
   int levels = 1;
@@ -762,6 +898,7 @@ int tsds_set_option(const char* name, int64_t value) {
   std::string n(name);
   if (n == "tma_min_bytes") g_tma_min_bytes = std::max<int64_t>(0, value);
   else if (n == "dyn_percent") g_dyn_percent = std::max<int64_t>(0, std::min<int64_t>(90, value));
+  else if (n == "lttb_exact") g_lttb_exact = std::max<int64_t>(0, std::min<int64_t>(2, value));
   else return set_err(TSDS_ERR_ARG, "unknown option " + n);
   return TSDS_OK;
 }
@@ -798,7 +935,7 @@ void tsds_ctx_destroy(tsds_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->y, &ctx->x, &ctx->xf64, &ctx->part, &ctx->bincnt, &ctx->res, &ctx->off, &ctx->out,
                     &ctx->misc, &ctx->cent, &ctx->scratch, &ctx->y2, &ctx->x2, &ctx->x2f64, &ctx->full, &ctx->out2,
-                    &ctx->rctr})
+                    &ctx->rctr, &ctx->lscr})
     if (b->p) cudaFree(b->p);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -827,6 +964,15 @@ int tsds_ctx_synchronize(tsds_ctx* ctx) {
 }
 
 int64_t tsds_ctx_launches(tsds_ctx* ctx) { return ctx->launches; }
+
+int64_t tsds_ctx_stat(tsds_ctx* ctx, const char* name) {
+  if (!ctx || !name) return -1;
+  std::string n(name);
+  if (n == "launches") return ctx->launches;
+  if (n == "lttb_rounds") return ctx->lttb_rounds;
+  if (n == "lttb_dirty1") return ctx->lttb_dirty1;
+  return -1;
+}
 
 int tsds_ctx_profile(tsds_ctx* ctx, int enable) {
   std::lock_guard<std::mutex> lk(ctx->mu);

@@ -185,3 +185,24 @@ def test_c5_first_series_hashes(ts):
             row = idx[s, : cnt[s]]
             h = int.from_bytes(hashlib.blake2b(row.astype("<u8").tobytes(), digest_size=8).digest(), "little")
             assert h == int(g[f"c5_{tag}_hash"][s]), (tag, s)
+
+
+def test_lttb_large_bucket_modes(ts, oracle):
+    """Guess/verify LTTB with the reference's sequential centroids (exact=1)
+    is bit-exact; tree-summed centroids (exact=2) match here too (SURVEY
+    probe 8 found no near-ties on such data)."""
+    from paper_2307_05389_b200 import _lib
+
+    L = _lib.load()
+    y = W.config3(2_000_000)
+    x = np.cumsum(np.random.default_rng(4).exponential(1.0, y.shape[0]))
+    try:
+        for mode in (1, 2, 0):
+            L.tsds_set_option(b"lttb_exact", mode)
+            for n_out in (50, 1000):
+                assert ts.downsample("lttb", y, n_out=n_out).tolist() == oracle.downsample("lttb", y, n_out=n_out).tolist()
+                assert ts.downsample("lttb", x, y, n_out=n_out).tolist() == oracle.downsample("lttb", x, y, n_out=n_out).tolist()
+            rounds = L.tsds_ctx_stat(_lib.context().handle, b"lttb_rounds")
+            assert 1 <= rounds <= 64
+    finally:
+        L.tsds_set_option(b"lttb_exact", 0)

@@ -28,11 +28,16 @@ def timeit(fn, reps=5):
 def main():
     which = sys.argv[1:] or ["c3", "c4"]
     if "c3" in which:
-        y = W.config3()
+        n = int(os.environ.get("C3_N", W.C3_N))
+        y = W.config3(n)
         yd = torch.from_numpy(y).cuda()
         for n_out in (1000, 10000):
             ms, r = timeit(lambda: ts.downsample("lttb", yd, n_out=n_out))
-            print(f"c3 lttb n_out={n_out}: {ms:.3f} ms  ({y.nbytes/ms/1e6:.0f} GB/s)  m={len(r)}")
+            from paper_2307_05389_b200 import _lib
+            st = {k: _lib.load().tsds_ctx_stat(_lib.context().handle, k.encode()) for k in ("lttb_rounds", "lttb_dirty1")}
+            g = np.load(os.path.join(ROOT, "tests", "golden", "configs.npz"))
+            ok = np.array_equal(r, g[f"c3_lttb_{n_out}"]) if n == W.C3_N else None
+            print(f"c3 lttb n_out={n_out}: {ms:.3f} ms  ({y.nbytes/ms/1e6:.0f} GB/s)  m={len(r)} {st} parity={ok}")
         del yd
     if "c4" in which:
         n = int(os.environ.get("C4_N", W.C4_N))
