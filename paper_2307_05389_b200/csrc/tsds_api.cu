@@ -608,8 +608,8 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
     YDT_SWITCH(ydt, (lttb_centroid_kernel<YD><<<gc, 256, 0, ctx->stream>>>(xf, drop, y, off, nb, cent)));
     LAUNCH_CHECK();
   }
-  int64_t hc[2] = {0, 0};
-  CUDA_TRY(cudaMemcpyAsync(hc, counts, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  int64_t hc[3] = {0, 0, 0};
+  CUDA_TRY(cudaMemcpyAsync(hc, counts, 24, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   const int64_t L = hc[0], NCH = hc[1];
   if (L > 0) {
@@ -628,28 +628,37 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
     LAUNCH_CHECK();
     lttb_seg_expand_kernel<<<gs, 256, 0, ctx->stream>>>(T, entry, ext, nonempty, counts, picks);
     LAUNCH_CHECK();
-    // ---- verify / fix rounds (double-buffered dirty flags)
-    CUDA_TRY(cudaMemsetAsync(dirty_b, 0, 4 * nb, ctx->stream));
-    CUDA_TRY(cudaMemsetAsync(dirty_a, 0, 4 * nb, ctx->stream));
+    // ---- verify every bucket once, then fix-up rounds on a work list of
+    //      buckets whose predecessor changed
     CUDA_TRY(cudaMemsetAsync(dirty_a, 0xff, 4 * L, ctx->stream));
-    int32_t *cur = dirty_a, *nxt = dirty_b;
-    const unsigned gv = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (NCH + 7) / 8));
+    CUDA_TRY(cudaMemsetAsync(ndirty, 0, 4, ctx->stream));
+    const unsigned gv = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, NCH));
     const unsigned gl = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (L + 7) / 8));
-    for (int round = 0;; round++) {
-      CUDA_TRY(cudaMemsetAsync(ndirty, 0, 4, ctx->stream));
-      YDT_SWITCH(ydt, (lttb_chunk_verify_kernel<YD><<<gv, 256, 0, ctx->stream>>>(
-                          xf, drop, y, n, off, nb, cent, cstart, cb, rank, counts, picks, cur, apart)));
-      LAUNCH_CHECK();
-      lttb_chunk_settle_kernel<<<gl, 256, 0, ctx->stream>>>(off, cstart, nonempty, counts, apart, picks, cur, nxt,
-                                                           ndirty);
-      LAUNCH_CHECK();
+    YDT_SWITCH(ydt, (lttb_chunk_verify_kernel<YD><<<gv, 256, 0, ctx->stream>>>(
+                        xf, drop, y, n, off, nb, cent, cstart, cb, rank, counts, picks, dirty_a, apart)));
+    LAUNCH_CHECK();
+    int32_t *cur = dirty_b, *nxt = dirty_a;  // work lists
+    lttb_chunk_settle_kernel<<<gl, 256, 0, ctx->stream>>>(off, cstart, nonempty, counts, apart, picks, dirty_a, cur,
+                                                         ndirty);
+    LAUNCH_CHECK();
+    for (int round = 1;; round++) {
       int32_t hd = 0;
       CUDA_TRY(cudaMemcpyAsync(&hd, ndirty, 4, cudaMemcpyDeviceToHost, ctx->stream));
       CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-      ctx->lttb_rounds = round + 1;
-      if (round == 0) ctx->lttb_dirty1 = hd;
+      ctx->lttb_rounds = round;
+      if (round == 1) ctx->lttb_dirty1 = hd;
       if (hd == 0) break;
       if (round > nb + 2) return set_err(TSDS_ERR_CUDA, "LTTB verification did not converge");
+      CUDA_TRY(cudaMemsetAsync(ndirty, 0, 4, ctx->stream));
+      const int64_t maxch = std::max<int64_t>(1, hc[2]);
+      const unsigned g1 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, hd * maxch));
+      YDT_SWITCH(ydt, (lttb_list_verify_kernel<YD><<<g1, 256, 0, ctx->stream>>>(
+                          xf, drop, y, n, off, nb, cent, cstart, nonempty, picks, cur, hd, maxch, apart)));
+      LAUNCH_CHECK();
+      const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (hd + 7) / 8));
+      lttb_list_settle_kernel<<<g2, 256, 0, ctx->stream>>>(off, cstart, nonempty, counts, apart, picks, cur, hd, nxt,
+                                                           ndirty);
+      LAUNCH_CHECK();
       std::swap(cur, nxt);
     }
     (void)NCH;

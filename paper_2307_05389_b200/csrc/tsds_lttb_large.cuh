@@ -48,8 +48,9 @@ lttb_layout_kernel(const int64_t* off, int64_t nb, int64_t* cstart, int32_t* cb,
                    int64_t* counts) {
   __shared__ int64_t wt[2][32];
   __shared__ int64_t run[2];
+  __shared__ unsigned long long smax;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  if (tid == 0) { run[0] = 0; run[1] = 0; }
+  if (tid == 0) { run[0] = 0; run[1] = 0; smax = 0ull; }
   __syncthreads();
   for (int64_t base = 0; base < nb; base += blockDim.x) {
     const int64_t k = base + tid;
@@ -57,6 +58,7 @@ lttb_layout_kernel(const int64_t* off, int64_t nb, int64_t* cstart, int32_t* cb,
     if (k < nb) len = __ldg(off + k + 1) - __ldg(off + k);
     const int64_t nch = len > 0 ? (len + LTTB_CH - 1) / LTTB_CH : 0;
     const int64_t ne = len > 0 ? 1 : 0;
+    if (nch) atomicMax(&smax, (unsigned long long)nch);
     int64_t a = nch, b = ne;
 #pragma unroll
     for (int m = 1; m < 32; m <<= 1) {
@@ -84,6 +86,7 @@ lttb_layout_kernel(const int64_t* off, int64_t nb, int64_t* cstart, int32_t* cb,
   if (tid == 0) {
     counts[0] = run[1];
     counts[1] = run[0];
+    counts[2] = (int64_t)smax;
   }
 }
 
@@ -167,7 +170,7 @@ __global__ void lttb_slopes_kernel(const double* xin, const int* drop, const voi
 // warp per chunk: candidate partials (fp32 projections relative to the
 // bucket's first point; they only steer the guess) and pairwise sums
 template <int YDT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 lttb_chunk_prepass_kernel(const double* xin, const int* drop, const void* y, const int64_t* off,
                           const int64_t* cstart, const int32_t* cb, const int64_t* counts, const double2* slopes,
                           LttbChunkPart* part) {
@@ -192,28 +195,37 @@ lttb_chunk_prepass_kernel(const double* xin, const int* drop, const void* y, con
 #pragma unroll
     for (int j = 0; j < LTTB_K; j++) { cmax[j] = -INFINITY; cmin[j] = INFINITY; imax[j] = -1; imin[j] = -1; }
     double px = 0.0, py = 0.0;
-    for (int64_t i0 = cs + lane; i0 < ce; i0 += 4 * 32) {
-      double vy[4], vx[4];
+    // 8 loads in flight per lane; the doubles are folded into the sums and
+    // narrowed to fp32 right away to keep the register footprint small
+    for (int64_t i0 = cs + lane; i0 < ce; i0 += 8 * 32) {
+      float vf[8], dxf[8];
+      {
+        double vy[8];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int64_t i = i0 + u * 32;
-        vy[u] = i < ce ? yd<YDT>(y, i) : __longlong_as_double(0x7ff8000000000000ll);
-        vx[u] = i < ce ? xd(x, i) : 0.0;
+        for (int u = 0; u < 8; u++) {
+          const int64_t i = i0 + u * 32;
+          vy[u] = i < ce ? yd<YDT>(y, i) : __longlong_as_double(0x7ff8000000000000ll);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int64_t i = i0 + u * 32;
+          double vx = 0.0;
+          if (i < ce) {
+            py = __dadd_rn(py, vy[u]);
+            vx = xd(x, i);
+            if (x) px = __dadd_rn(px, vx);
+          }
+          vf[u] = vy[u] == vy[u] ? (float)(vy[u] - yb) : __int_as_float(0x7fc00000);
+          dxf[u] = (float)(vx - xs);
+        }
       }
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int64_t i = i0 + u * 32;
-        const double v = vy[u];
-        if (i < ce) {
-          py = __dadd_rn(py, v);
-          if (x) px = __dadd_rn(px, vx[u]);
-        }
-        if (v == v) {
-          const float vf = (float)(v - yb), dxf = (float)(vx[u] - xs);
-          const int32_t ii = (int32_t)(i - s);
+      for (int u = 0; u < 8; u++) {
+        if (vf[u] == vf[u]) {
+          const int32_t ii = (int32_t)(i0 + u * 32 - s);
 #pragma unroll
           for (int j = 0; j < LTTB_K; j++) {
-            const float t = fmaf(-sl[j], dxf, vf);
+            const float t = fmaf(-sl[j], dxf[u], vf[u]);
             if (t > cmax[j]) { cmax[j] = t; imax[j] = ii; }
             if (t < cmin[j]) { cmin[j] = t; imin[j] = ii; }
           }
@@ -419,15 +431,16 @@ lttb_chunk_verify_kernel(const double* xin, const int* drop, const void* y, int6
                          int64_t nb, const double2* cent, const int64_t* cstart, const int32_t* cb,
                          const int32_t* rank, const int64_t* counts, const int64_t* picks, const int32_t* dirty,
                          LttbAreaPart* part) {
+  // one CTA (256 threads) per chunk: a dirty bucket's chunk costs ~4 dependent
+  // load batches, so fix-up rounds stay short
   const double* x = eff_x(xin, drop);
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  __shared__ AreaCand sc[8];
   const int64_t NCH = counts[1];
-  for (int64_t c = gw; c < NCH; c += nw) {
+  for (int64_t c = blockIdx.x; c < NCH; c += gridDim.x) {
     const int64_t k = cb[c];
     const int64_t j = rank[k];
-    if (!dirty[j]) continue;
+    if (!dirty[j]) continue;  // block-uniform
     const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
     const int64_t cs = s + (c - cstart[k]) * LTTB_CH;
     const int64_t ce = cs + LTTB_CH < e ? cs + LTTB_CH : e;
@@ -436,17 +449,17 @@ lttb_chunk_verify_kernel(const double* xin, const int* drop, const void* y, int6
     double cx, cy;
     centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
     AreaCand best{-1.0, IDX_NONE};
-    for (int64_t i0 = cs + lane; i0 < ce; i0 += 4 * 32) {
+    for (int64_t i0 = cs + tid; i0 < ce; i0 += 4 * 256) {
       double vy[4], vx[4];
 #pragma unroll
       for (int u = 0; u < 4; u++) {
-        const int64_t i = i0 + u * 32;
+        const int64_t i = i0 + u * 256;
         vy[u] = i < ce ? yd<YDT>(y, i) : 0.0;
         vx[u] = i < ce ? xd(x, i) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 4; u++) {
-        const int64_t i = i0 + u * 32;
+        const int64_t i = i0 + u * 256;
         if (i < ce) {
           AreaCand a{tri_area(ax, ay, cx, cy, vx[u], vy[u]), i};
           if (area_better(a, best)) best = a;
@@ -454,10 +467,16 @@ lttb_chunk_verify_kernel(const double* xin, const int* drop, const void* y, int6
       }
     }
     best = warp_area_max(best);
-    if (lane == 0) {
-      part[c].a = best.a;
-      part[c].i = best.i;
+    if (lane == 0) sc[wid] = best;
+    __syncthreads();
+    if (tid == 0) {
+      AreaCand b = sc[0];
+      for (int w = 1; w < 8; w++)
+        if (area_better(sc[w], b)) b = sc[w];
+      part[c].a = b.a;
+      part[c].i = b.i;
     }
+    __syncthreads();
   }
 }
 
@@ -485,10 +504,88 @@ __global__ void lttb_chunk_settle_kernel(const int64_t* off, const int64_t* csta
       const int64_t p = best.i == IDX_NONE ? s : best.i;
       if (p != picks[j]) {
         picks[j] = p;
-        if (j + 1 < L) {
-          next_dirty[j + 1] = 1;
-          atomicAdd(ndirty, 1);
+        if (j + 1 < L) next_dirty[atomicAdd(ndirty, 1)] = (int32_t)(j + 1);  // work list
+      }
+    }
+  }
+}
+
+// Fix-up rounds run on a work list of buckets whose predecessor changed:
+// one CTA per (listed bucket, chunk); then one warp per listed bucket.
+template <int YDT>
+__global__ void __launch_bounds__(256)
+lttb_list_verify_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off,
+                        int64_t nb, const double2* cent, const int64_t* cstart, const int32_t* nonempty,
+                        const int64_t* picks, const int32_t* list, int64_t count, int64_t maxch, LttbAreaPart* part) {
+  const double* x = eff_x(xin, drop);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  __shared__ AreaCand sc[8];
+  for (int64_t t = blockIdx.x; t < count * maxch; t += gridDim.x) {
+    const int64_t j = list[t / maxch], q = t % maxch;
+    const int64_t k = nonempty[j];
+    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+    const int64_t cs = s + q * LTTB_CH;
+    if (cs >= e) continue;  // block-uniform
+    const int64_t ce = cs + LTTB_CH < e ? cs + LTTB_CH : e;
+    const int64_t prev = j == 0 ? 0 : picks[j - 1];
+    const double ax = xd(x, prev), ay = yd<YDT>(y, prev);
+    double cx, cy;
+    centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
+    AreaCand best{-1.0, IDX_NONE};
+    for (int64_t i0 = cs + tid; i0 < ce; i0 += 4 * 256) {
+      double vy[4], vx[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t i = i0 + u * 256;
+        vy[u] = i < ce ? yd<YDT>(y, i) : 0.0;
+        vx[u] = i < ce ? xd(x, i) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t i = i0 + u * 256;
+        if (i < ce) {
+          AreaCand a{tri_area(ax, ay, cx, cy, vx[u], vy[u]), i};
+          if (area_better(a, best)) best = a;
         }
+      }
+    }
+    best = warp_area_max(best);
+    if (lane == 0) sc[wid] = best;
+    __syncthreads();
+    if (tid == 0) {
+      AreaCand b = sc[0];
+      for (int w = 1; w < 8; w++)
+        if (area_better(sc[w], b)) b = sc[w];
+      part[cstart[k] + q].a = b.a;
+      part[cstart[k] + q].i = b.i;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void lttb_list_settle_kernel(const int64_t* off, const int64_t* cstart, const int32_t* nonempty,
+                                        const int64_t* counts, const LttbAreaPart* part, int64_t* picks,
+                                        const int32_t* list, int64_t count, int32_t* next_list, int32_t* ndirty) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t L = counts[0];
+  for (int64_t t = gw; t < count; t += nw) {
+    const int64_t j = list[t];
+    const int64_t k = nonempty[j];
+    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+    const int64_t c0 = cstart[k], nch = (e - s + LTTB_CH - 1) / LTTB_CH;
+    AreaCand best{-1.0, IDX_NONE};
+    for (int64_t q = lane; q < nch; q += 32) {
+      AreaCand a{part[c0 + q].a, part[c0 + q].i};
+      if (area_better(a, best)) best = a;
+    }
+    best = warp_area_max(best);
+    if (lane == 0) {
+      const int64_t p = best.i == IDX_NONE ? s : best.i;
+      if (p != picks[j]) {
+        picks[j] = p;
+        if (j + 1 < L) next_list[atomicAdd(ndirty, 1)] = (int32_t)(j + 1);
       }
     }
   }
