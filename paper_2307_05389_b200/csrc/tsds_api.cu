@@ -63,6 +63,8 @@ struct tsds_ctx {
   DevBuf y, x, xf64, part, bincnt, res, off, out, misc, cent, scratch, y2, x2, x2f64, full, out2, rctr, lscr;
   int64_t lttb_rounds = 0;  // verification rounds of the last large-bucket LTTB
   int64_t lttb_dirty1 = 0;  // buckets whose guess was wrong in the first round
+  int32_t* h_lstat = nullptr;  // pinned {rounds, dirty1} of the last large-bucket LTTB
+  bool lstat_pending = false;
   void* h_pin = nullptr;
   size_t h_cap = 0;
   bool dirty = false;
@@ -549,6 +551,19 @@ int lttb_exact_mode() {
 int run_lttb_walk_small(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
                         const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev, bool have_cent = false);
 
+int ensure_lstat(tsds_ctx* ctx) {
+  if (!ctx->h_lstat) CUDA_TRY(cudaMallocHost(&ctx->h_lstat, 16));
+  return TSDS_OK;
+}
+
+// grid of exactly one resident wave of `kernel` (persistent kernels)
+template <typename K>
+unsigned one_wave(tsds_ctx* ctx, K kernel, int threads) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, 0) != cudaSuccess || b < 1) b = 1;
+  return (unsigned)(ctx->sms * b);
+}
+
 // Large buckets: prepass -> guess walk on the reduced problem -> verify/fix rounds.
 int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
                    const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev) {
@@ -578,9 +593,9 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   uint8_t* C = (uint8_t*)take(NC * maxseg);
   uint8_t* entry = (uint8_t*)take(maxseg);
   int64_t* walkout = (int64_t*)take(8 * (nb + 4));
-  int32_t* dirty_a = (int32_t*)take(4 * nb);
-  int32_t* dirty_b = (int32_t*)take(4 * nb);
-  int32_t* ndirty = (int32_t*)take(64);
+  int32_t* list_a = (int32_t*)take(4 * nb);
+  int32_t* list_b = (int32_t*)take(4 * nb);
+  int32_t* ctr = (int32_t*)take(64);
   LttbAreaPart* apart = (LttbAreaPart*)take(sizeof(LttbAreaPart) * maxch);
   int64_t* picks = walkout + 2;
   const int mode = lttb_exact_mode();
@@ -596,9 +611,10 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
                       xf, drop, y, off, nb, n, bbox, slopes)));
   LAUNCH_CHECK();
   // ---- chunk prepass + per-bucket merge (centroids, candidates)
-  const unsigned gch = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (maxch + 7) / 8));
-  YDT_SWITCH(ydt, (lttb_chunk_prepass_kernel<YD><<<gch, 256, 0, ctx->stream>>>(xf, drop, y, off, cstart, cb, counts,
-                                                                             slopes, cpart)));
+  const int vec_ok = ((uintptr_t)y & 15) == 0 ? 1 : 0;
+  YDT_SWITCH(ydt, (lttb_chunk_prepass_kernel<YD><<<one_wave(ctx, lttb_chunk_prepass_kernel<YD>, 256), 256, 0,
+                                                  ctx->stream>>>(xf, drop, y, off, cstart, cb, counts, slopes, cpart,
+                                                                 vec_ok)));
   LAUNCH_CHECK();
   YDT_SWITCH(ydt, (lttb_chunk_merge_kernel<YD><<<gw8, 256, 0, ctx->stream>>>(xf, drop, off, nb, cstart, cpart, cent,
                                                                            ext)));
@@ -608,17 +624,15 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
     YDT_SWITCH(ydt, (lttb_centroid_kernel<YD><<<gc, 256, 0, ctx->stream>>>(xf, drop, y, off, nb, cent)));
     LAUNCH_CHECK();
   }
-  int64_t hc[3] = {0, 0, 0};
-  CUDA_TRY(cudaMemcpyAsync(hc, counts, 24, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  const int64_t L = hc[0], NCH = hc[1];
-  if (L > 0) {
+  // No host round trip from here on: grids are sized from nb (the kernels
+  // read the actual counts L, NCH from the device).
+  {
     // ---- guess chain on the candidates (composed transition tables)
-    const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (L * NC + 255) / 256));
+    const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (nb * NC + 255) / 256));
     YDT_SWITCH(ydt, (lttb_cand_table_kernel<YD><<<gt, 256, 0, ctx->stream>>>(xf, drop, y, n, off, nb, cent, ext,
                                                                            nonempty, counts, T)));
     LAUNCH_CHECK();
-    const int64_t NS = (L + LTTB_SEG - 1) / LTTB_SEG;
+    const int64_t NS = (nb + LTTB_SEG - 1) / LTTB_SEG;
     const unsigned gs = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (NS + 7) / 8));
     lttb_seg_compose_kernel<<<gs, 256, 0, ctx->stream>>>(T, counts, C);
     LAUNCH_CHECK();
@@ -628,42 +642,31 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
     LAUNCH_CHECK();
     lttb_seg_expand_kernel<<<gs, 256, 0, ctx->stream>>>(T, entry, ext, nonempty, counts, picks);
     LAUNCH_CHECK();
-    // ---- verify every bucket once, then fix-up rounds on a work list of
-    //      buckets whose predecessor changed
-    CUDA_TRY(cudaMemsetAsync(dirty_a, 0xff, 4 * L, ctx->stream));
-    CUDA_TRY(cudaMemsetAsync(ndirty, 0, 4, ctx->stream));
-    const unsigned gv = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, NCH));
-    const unsigned gl = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (L + 7) / 8));
-    YDT_SWITCH(ydt, (lttb_chunk_verify_kernel<YD><<<gv, 256, 0, ctx->stream>>>(
-                        xf, drop, y, n, off, nb, cent, cstart, cb, rank, counts, picks, dirty_a, apart)));
+    // ---- verify every bucket once (round 1), then the fix-up rounds on a
+    //      work list of buckets whose predecessor changed
+    CUDA_TRY(cudaMemsetAsync(ctr, 0, 16, ctx->stream));
+    const unsigned gl = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (nb + 7) / 8));
+    YDT_SWITCH(ydt, (lttb_chunk_verify_kernel<YD><<<one_wave(ctx, lttb_chunk_verify_kernel<YD>, 256), 256, 0,
+                                                   ctx->stream>>>(xf, drop, y, n, off, nb, cent, cstart, cb, rank,
+                                                                  counts, picks, apart, vec_ok)));
     LAUNCH_CHECK();
-    int32_t *cur = dirty_b, *nxt = dirty_a;  // work lists
-    lttb_chunk_settle_kernel<<<gl, 256, 0, ctx->stream>>>(off, cstart, nonempty, counts, apart, picks, dirty_a, cur,
-                                                         ndirty);
+    lttb_chunk_settle_kernel<<<gl, 256, 0, ctx->stream>>>(off, cstart, nonempty, counts, apart, picks, list_a, ctr);
     LAUNCH_CHECK();
-    for (int round = 1;; round++) {
-      int32_t hd = 0;
-      CUDA_TRY(cudaMemcpyAsync(&hd, ndirty, 4, cudaMemcpyDeviceToHost, ctx->stream));
-      CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-      ctx->lttb_rounds = round;
-      if (round == 1) ctx->lttb_dirty1 = hd;
-      if (hd == 0) break;
-      if (round > nb + 2) return set_err(TSDS_ERR_CUDA, "LTTB verification did not converge");
-      CUDA_TRY(cudaMemsetAsync(ndirty, 0, 4, ctx->stream));
-      const int64_t maxch = std::max<int64_t>(1, hc[2]);
-      const unsigned g1 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, hd * maxch));
-      YDT_SWITCH(ydt, (lttb_list_verify_kernel<YD><<<g1, 256, 0, ctx->stream>>>(
-                          xf, drop, y, n, off, nb, cent, cstart, nonempty, picks, cur, hd, maxch, apart)));
-      LAUNCH_CHECK();
-      const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (hd + 7) / 8));
-      lttb_list_settle_kernel<<<g2, 256, 0, ctx->stream>>>(off, cstart, nonempty, counts, apart, picks, cur, hd, nxt,
-                                                           ndirty);
-      LAUNCH_CHECK();
-      std::swap(cur, nxt);
-    }
-    (void)NCH;
+    YDT_SWITCH(ydt, ({
+                 const void* fx = (const void*)lttb_fixup_kernel<YD>;
+                 const unsigned gf = one_wave(ctx, lttb_fixup_kernel<YD>, 256);
+                 void* args[] = {(void*)&xf,       (void*)&drop,     (void*)&y,    (void*)&n,      (void*)&off,
+                                 (void*)&nb,       (void*)&cent,     (void*)&cstart, (void*)&nonempty,
+                                 (void*)&counts,   (void*)&picks,    (void*)&list_a, (void*)&list_b, (void*)&ctr,
+                                 (void*)&apart};
+                 CUDA_TRY(cudaLaunchCooperativeKernel(fx, dim3(gf), dim3(256), args, 0, ctx->stream));
+               }));
+    LAUNCH_CHECK();
+    RC_TRY(ensure_lstat(ctx));
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_lstat, ctr + 2, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->lstat_pending = true;
   }
-  lttb_emit_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, (L + 257) / 256)), 256, 0, ctx->stream>>>(
+  lttb_emit_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, (nb + 257) / 256)), 256, 0, ctx->stream>>>(
       picks, counts, n, map, out_dev + 1, out_dev);
   LAUNCH_CHECK();
   return TSDS_OK;
@@ -947,6 +950,7 @@ void tsds_ctx_destroy(tsds_ctx* ctx) {
                     &ctx->rctr, &ctx->lscr})
     if (b->p) cudaFree(b->p);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+  if (ctx->h_lstat) cudaFreeHost(ctx->h_lstat);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -978,6 +982,15 @@ int64_t tsds_ctx_stat(tsds_ctx* ctx, const char* name) {
   if (!ctx || !name) return -1;
   std::string n(name);
   if (n == "launches") return ctx->launches;
+  if (ctx->lstat_pending && (n == "lttb_rounds" || n == "lttb_dirty1")) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    if (cudaStreamSynchronize(ctx->stream) == cudaSuccess) {
+      ctx->lttb_rounds = ctx->h_lstat[0];
+      ctx->lttb_dirty1 = ctx->h_lstat[1];
+    }
+    ctx->lstat_pending = false;
+  }
   if (n == "lttb_rounds") return ctx->lttb_rounds;
   if (n == "lttb_dirty1") return ctx->lttb_dirty1;
   return -1;

@@ -25,19 +25,55 @@ namespace tsds {
 constexpr int LTTB_THREADS = 1024;
 constexpr int64_t SMALL_MAX = 64;
 
+// storage type of each value dtype and its exact conversion to f64
+template <int YDT> struct YT;
+template <> struct YT<DT_F16> { using T = unsigned short; };
+template <> struct YT<DT_F32> { using T = float; };
+template <> struct YT<DT_F64> { using T = double; };
+template <> struct YT<DT_I8> { using T = int8_t; };
+template <> struct YT<DT_I16> { using T = int16_t; };
+template <> struct YT<DT_I32> { using T = int32_t; };
+template <> struct YT<DT_I64> { using T = long long; };
+template <> struct YT<DT_U8> { using T = uint8_t; };
+template <> struct YT<DT_U16> { using T = uint16_t; };
+template <> struct YT<DT_U32> { using T = uint32_t; };
+template <> struct YT<DT_U64> { using T = unsigned long long; };
+
+template <int YDT>
+__device__ __forceinline__ double ycv(typename YT<YDT>::T v) {
+  if constexpr (YDT == DT_F16) return (double)__half2float(__ushort_as_half(v));
+  else if constexpr (YDT == DT_I64) return __ll2double_rn(v);
+  else if constexpr (YDT == DT_U64) return __ull2double_rn(v);
+  else return (double)v;
+}
+
 template <int YDT>
 __device__ __forceinline__ double yd(const void* y, int64_t i) {
-  if constexpr (YDT == DT_F16) return (double)__half2float(__ushort_as_half(__ldg((const unsigned short*)y + i)));
-  else if constexpr (YDT == DT_F32) return (double)__ldg((const float*)y + i);
-  else if constexpr (YDT == DT_F64) return __ldg((const double*)y + i);
-  else if constexpr (YDT == DT_I8) return (double)__ldg((const int8_t*)y + i);
-  else if constexpr (YDT == DT_I16) return (double)__ldg((const int16_t*)y + i);
-  else if constexpr (YDT == DT_I32) return (double)__ldg((const int32_t*)y + i);
-  else if constexpr (YDT == DT_I64) return __ll2double_rn(__ldg((const long long*)y + i));
-  else if constexpr (YDT == DT_U8) return (double)__ldg((const uint8_t*)y + i);
-  else if constexpr (YDT == DT_U16) return (double)__ldg((const uint16_t*)y + i);
-  else if constexpr (YDT == DT_U32) return (double)__ldg((const uint32_t*)y + i);
-  else return __ull2double_rn(__ldg((const unsigned long long*)y + i));
+  return ycv<YDT>(__ldg((const typename YT<YDT>::T*)y + i));
+}
+
+// element e of a 128-bit vector of YDT values, as f64
+// (e is a compile-time constant after unrolling: pure register extraction)
+template <int YDT>
+__device__ __forceinline__ double vget(const uint4& q, int e) {
+  using T = typename YT<YDT>::T;
+  constexpr int ES = (int)sizeof(T);
+  if constexpr (ES == 8) {
+    const unsigned long long b = e == 0 ? ((unsigned long long)q.y << 32 | q.x) : ((unsigned long long)q.w << 32 | q.z);
+    T v;
+    memcpy(&v, &b, 8);
+    return ycv<YDT>(v);
+  } else {
+    const int wi = e * ES / 4;
+    const unsigned w = wi == 0 ? q.x : (wi == 1 ? q.y : (wi == 2 ? q.z : q.w));
+    const unsigned b = w >> (8 * ((e * ES) & 3));
+    if constexpr (ES == 4) {
+      T v;
+      memcpy(&v, &b, 4);
+      return ycv<YDT>(v);
+    } else if constexpr (ES == 2) return ycv<YDT>((T)(unsigned short)(b & 0xffffu));
+    else return ycv<YDT>((T)(uint8_t)(b & 0xffu));
+  }
 }
 
 __device__ __forceinline__ double xd(const double* x, int64_t i) {

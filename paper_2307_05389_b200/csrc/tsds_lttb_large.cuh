@@ -21,13 +21,29 @@
 #pragma once
 
 #include "tsds_lttb.cuh"
+#include <cooperative_groups.h>
 
 namespace tsds {
 
 constexpr int LTTB_K = 7;            // candidate slopes per bucket
 constexpr int LTTB_NC = 2 * LTTB_K;  // candidates per bucket (argmax + argmin per slope)
-constexpr int64_t LTTB_CH = 4096;    // points per chunk
+#ifndef LTTB_CH_N
+#define LTTB_CH_N 4096
+#endif
+constexpr int64_t LTTB_CH = LTTB_CH_N;  // points per chunk
 constexpr int LTTB_SEG = 64;         // buckets per composed segment
+
+// Pieces: the series is cut into globally aligned chunks of LTTB_CH points;
+// piece q of bucket [s, e) is its intersection with chunk s/LTTB_CH + q
+// (aligned starts let the scans use 128-bit loads).
+__device__ __forceinline__ int64_t lttb_npieces(int64_t s, int64_t e) {
+  return e > s ? (e - 1) / LTTB_CH - s / LTTB_CH + 1 : 0;
+}
+__device__ __forceinline__ void lttb_piece(int64_t s, int64_t e, int64_t q, int64_t& cs, int64_t& ce) {
+  const int64_t g = s / LTTB_CH + q;
+  cs = g * LTTB_CH > s ? g * LTTB_CH : s;
+  ce = (g + 1) * LTTB_CH < e ? (g + 1) * LTTB_CH : e;
+}
 
 struct LttbChunkPart {  // per-chunk partial of the prepass
   float v[LTTB_NC];
@@ -56,7 +72,7 @@ lttb_layout_kernel(const int64_t* off, int64_t nb, int64_t* cstart, int32_t* cb,
     const int64_t k = base + tid;
     int64_t len = 0;
     if (k < nb) len = __ldg(off + k + 1) - __ldg(off + k);
-    const int64_t nch = len > 0 ? (len + LTTB_CH - 1) / LTTB_CH : 0;
+    const int64_t nch = k < nb ? lttb_npieces(__ldg(off + k), __ldg(off + k + 1)) : 0;
     const int64_t ne = len > 0 ? 1 : 0;
     if (nch) atomicMax(&smax, (unsigned long long)nch);
     int64_t a = nch, b = ne;
@@ -167,14 +183,13 @@ __global__ void lttb_slopes_kernel(const double* xin, const int* drop, const voi
   }
 }
 
-// warp per chunk: candidate partials (fp32 projections relative to the
-// bucket's first point; they only steer the guess) and pairwise sums
+// warp per piece: candidate partials (fp32 projections relative to the
+// bucket's first point; they only steer the guess) and fixed-order sums.
+// Scalar form: explicit x or a y base that is not 16-byte aligned.
 template <int YDT>
-__global__ void __launch_bounds__(256, 3)
-lttb_chunk_prepass_kernel(const double* xin, const int* drop, const void* y, const int64_t* off,
-                          const int64_t* cstart, const int32_t* cb, const int64_t* counts, const double2* slopes,
-                          LttbChunkPart* part) {
-  const double* x = eff_x(xin, drop);
+__device__ __forceinline__ void lttb_prepass_scalar(const double* x, const void* y, const int64_t* off,
+                                                    const int64_t* cstart, const int32_t* cb, const int64_t* counts,
+                                                    const double2* slopes, LttbChunkPart* part) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -182,8 +197,8 @@ lttb_chunk_prepass_kernel(const double* xin, const int* drop, const void* y, con
   for (int64_t c = gw; c < NCH; c += nw) {
     const int64_t k = cb[c];
     const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-    const int64_t cs = s + (c - cstart[k]) * LTTB_CH;
-    const int64_t ce = cs + LTTB_CH < e ? cs + LTTB_CH : e;
+    int64_t cs, ce;
+    lttb_piece(s, e, c - cstart[k], cs, ce);
     const double2 sr = slopes[k];
     float sl[LTTB_K];
 #pragma unroll
@@ -263,6 +278,189 @@ lttb_chunk_prepass_kernel(const double* xin, const int* drop, const void* y, con
   }
 }
 
+#ifndef LTTB_PV_N
+#define LTTB_PV_N 8
+#endif
+#ifndef LTTB_PMINB
+#define LTTB_PMINB 2
+#endif
+#ifndef LTTB_VMINB
+#define LTTB_VMINB 2
+#endif
+constexpr int LTTB_PV = LTTB_PV_N;  // 128-bit vectors per lane in flight
+
+__device__ __forceinline__ unsigned f32_key(float f) {  // order-preserving (no NaN)
+  const unsigned b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// Steering projection of a piece element (vector form): re = element index
+// relative to the piece start, dxb = x offset of the vector's first element
+// from the bucket start.  The locate pass recomputes it bit-identically.
+__device__ __forceinline__ float lttb_vx(float base, int rv0) { return __fadd_rn(base, (float)rv0); }
+
+template <int YDT, bool CHECK>
+__device__ __forceinline__ void lttb_pv_fold(const uint4& q, int re0, int len, float dxb, double yb,
+                                             const float (&sl)[LTTB_K], float (&bm)[LTTB_K], float (&bn)[LTTB_K],
+                                             double& py) {
+  constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
+  float vf[EPV];
+#pragma unroll
+  for (int e = 0; e < EPV; e++) {
+    const double d = vget<YDT>(q, e);
+    const bool ok = !CHECK || (unsigned)(re0 + e) < (unsigned)len;
+    if (ok) py = __dadd_rn(py, d);
+    vf[e] = ok ? __double2float_rn(__dsub_rn(d, yb)) : __int_as_float(0x7fc00000);
+  }
+#pragma unroll
+  for (int j = 0; j < LTTB_K; j++) {
+    float m = bm[j], n = bn[j];
+#pragma unroll
+    for (int e = 0; e < EPV; e++) {
+      const float t = fmaf(-sl[j], __fadd_rn(dxb, (float)e), vf[e]);
+      m = fmaxf(m, t);
+      n = fminf(n, t);
+    }
+    bm[j] = m;
+    bn[j] = n;
+  }
+}
+
+// Vector form (implicit x, aligned y): each warp streams a contiguous range
+// of pieces with LTTB_PV 128-bit loads per lane in flight.  Per lane and
+// batch only the extremum VALUES are folded (3-input min/max); the batch that
+// first improved a lane's extremum is remembered (8-bit ids) and the winning element is located afterwards by
+// re-reading that one batch.
+template <int YDT>
+__global__ void __launch_bounds__(256, LTTB_PMINB)
+lttb_chunk_prepass_kernel(const double* xin, const int* drop, const void* y, const int64_t* off,
+                          const int64_t* cstart, const int32_t* cb, const int64_t* counts, const double2* slopes,
+                          LttbChunkPart* part, int vec_ok) {
+  const double* x = eff_x(xin, drop);
+  if (x || !vec_ok) {
+    lttb_prepass_scalar<YDT>(x, y, off, cstart, cb, counts, slopes, part);
+    return;
+  }
+  constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
+  constexpr int BV = 32 * LTTB_PV;  // vectors per warp batch
+  static_assert(LTTB_CH / (EPV * BV) <= 255, "batch ids must fit 8 bits");
+  const uint4* yv = (const uint4*)y;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t NCH = counts[1];
+  const int64_t p0 = NCH * gw / nw, p1 = NCH * (gw + 1) / nw;
+  int64_t kc = -1, s = 0, e = 0;
+  double yb = 0.0;
+  float sl[LTTB_K];
+#pragma unroll
+  for (int j = 0; j < LTTB_K; j++) sl[j] = 0.0f;
+  for (int64_t c = p0; c < p1; c++) {
+    const int64_t k = cb[c];
+    if (k != kc) {
+      kc = k;
+      s = __ldg(off + k);
+      e = __ldg(off + k + 1);
+      const double2 sr = slopes[k];
+#pragma unroll
+      for (int j = 0; j < LTTB_K; j++) sl[j] = (float)(sr.x + (sr.y - sr.x) * ((double)j / (double)(LTTB_K - 1)));
+      const double ys0 = yd<YDT>(y, s);
+      yb = ys0 == ys0 ? ys0 : 0.0;
+    }
+    int64_t cs, ce;
+    lttb_piece(s, e, c - cstart[k], cs, ce);
+    const int64_t v0 = cs / EPV;
+    const int nvec = (int)((ce + EPV - 1) / EPV - v0);
+    const int r0 = (int)(v0 * EPV - cs), len = (int)(ce - cs);  // r0 in (-EPV, 0]
+    const float base = (float)(cs - s);
+    const uint4* pv = yv + v0;
+    float cmax[LTTB_K], cmin[LTTB_K];
+    unsigned long long bmx = ~0ull, bmn = ~0ull;  // 8-bit batch id per slope, 0xff = none
+#pragma unroll
+    for (int j = 0; j < LTTB_K; j++) { cmax[j] = -INFINITY; cmin[j] = INFINITY; }
+    double py = 0.0;
+    const int nbat = (nvec + BV - 1) / BV;
+    for (int b = 0; b < nbat; b++) {
+      uint4 q[LTTB_PV];
+#pragma unroll
+      for (int u = 0; u < LTTB_PV; u++) {
+        const int rv = b * BV + u * 32 + lane;
+        q[u] = rv < nvec ? ldg_stream<false>(pv + rv) : make_uint4(0u, 0u, 0u, 0u);
+      }
+      float bm[LTTB_K], bn[LTTB_K];
+#pragma unroll
+      for (int j = 0; j < LTTB_K; j++) { bm[j] = -INFINITY; bn[j] = INFINITY; }
+#pragma unroll
+      for (int u = 0; u < LTTB_PV; u++) {
+        const int rv = b * BV + u * 32 + lane;
+        const int re0 = r0 + rv * EPV;
+        const float dxb = lttb_vx(base, re0);
+        if (re0 >= 0 && re0 + EPV <= len) lttb_pv_fold<YDT, false>(q[u], re0, len, dxb, yb, sl, bm, bn, py);
+        else if (rv < nvec) lttb_pv_fold<YDT, true>(q[u], re0, len, dxb, yb, sl, bm, bn, py);
+      }
+#pragma unroll
+      for (int j = 0; j < LTTB_K; j++) {
+        if (bm[j] > cmax[j]) { cmax[j] = bm[j]; bmx = (bmx & ~(0xffull << (8 * j))) | ((unsigned long long)b << (8 * j)); }
+        if (bn[j] < cmin[j]) { cmin[j] = bn[j]; bmn = (bmn & ~(0xffull << (8 * j))) | ((unsigned long long)b << (8 * j)); }
+      }
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) py = __dadd_rn(py, __shfl_xor_sync(0xffffffffu, py, m));
+    // winners: extreme value, then the lowest (batch, lane) holding it
+    float myW = 0.0f, mysl = 0.0f;
+    int myb = -1, mywl = 0;
+#pragma unroll
+    for (int t = 0; t < LTTB_NC; t++) {
+      const int j = t >> 1;
+      const bool mn = t & 1;
+      const float v = mn ? cmin[j] : cmax[j];
+      const unsigned bid = (unsigned)((mn ? bmn : bmx) >> (8 * j)) & 0xffu;
+      const unsigned key = f32_key(v);
+      const unsigned W = mn ? __reduce_min_sync(0xffffffffu, key) : __reduce_max_sync(0xffffffffu, key);
+      const unsigned tie = (key == W && bid != 0xffu) ? (bid * 32u + (unsigned)lane) : 0xffffffffu;
+      const unsigned win = __reduce_min_sync(0xffffffffu, tie);
+      const float wv = __shfl_sync(0xffffffffu, v, (int)(win & 31u));
+      if (lane == t) {
+        myW = wv;
+        mysl = sl[j];
+        myb = win == 0xffffffffu ? -1 : (int)(win >> 5);
+        mywl = (int)(win & 31u);
+      }
+    }
+    int64_t found = -1;
+    if (lane < LTTB_NC && myb >= 0) {
+      uint4 q[LTTB_PV];
+#pragma unroll
+      for (int u = 0; u < LTTB_PV; u++) {
+        const int rv = myb * BV + u * 32 + mywl;
+        q[u] = rv < nvec ? __ldg(pv + rv) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < LTTB_PV; u++) {
+        const int rv = myb * BV + u * 32 + mywl;
+        const int re0 = r0 + rv * EPV;
+        const float dxb = lttb_vx(base, re0);
+#pragma unroll
+        for (int ee = 0; ee < EPV; ee++) {
+          const double d = vget<YDT>(q[u], ee);
+          const bool ok = rv < nvec && (unsigned)(re0 + ee) < (unsigned)len;
+          const float vf = ok ? __double2float_rn(__dsub_rn(d, yb)) : __int_as_float(0x7fc00000);
+          const float t = fmaf(-mysl, __fadd_rn(dxb, (float)ee), vf);
+          if (found < 0 && t == myW) found = cs + re0 + ee;
+        }
+      }
+    }
+    if (lane < LTTB_NC) {
+      part[c].v[lane] = myW;
+      part[c].i[lane] = found;
+    }
+    if (lane == 0) {
+      part[c].sx = 0.0;  // implicit x: the merge uses the closed form
+      part[c].sy = py;
+    }
+  }
+}
+
 // warp per bucket: merge its chunk partials -> centroid (pairwise, chunk
 // order) and the LTTB_NC candidates in index order
 template <int YDT>
@@ -275,7 +473,7 @@ __global__ void lttb_chunk_merge_kernel(const double* xin, const int* drop, cons
   for (int64_t k = gw; k < nb; k += nw) {
     const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
     if (e <= s) continue;
-    const int64_t c0 = cstart[k], nch = (e - s + LTTB_CH - 1) / LTTB_CH;
+    const int64_t c0 = cstart[k], nch = lttb_npieces(s, e);
     // sums: lane-strided over chunks, then butterfly (fixed order)
     double sx = 0.0, sy = 0.0;
     for (int64_t q = lane; q < nch; q += 32) {
@@ -313,7 +511,8 @@ __global__ void lttb_chunk_merge_kernel(const double* xin, const int* drop, cons
     if (lane == 0) {
       if (!x) {
         const double cnt = (double)(e - s);
-        if ((double)(s + e - 1) * cnt < 9007199254740992.0) sx = (double)((s + e - 1) * (e - s) / 2);
+        sx = (double)(s + e - 1) * cnt < 9007199254740992.0 ? (double)((s + e - 1) * (e - s) / 2)
+                                                            : 0.5 * ((double)(s + e - 1) * cnt);
       }
       const double cw = (double)(e - s);
       cent[k] = make_double2(__ddiv_rn(sx, cw), __ddiv_rn(sy, cw));
@@ -423,158 +622,191 @@ __global__ void __launch_bounds__(256) lttb_seg_expand_kernel(const uint8_t* T, 
   }
 }
 
-// warp per chunk of a dirty bucket: exact first-max area with the current
-// predecessor; part[c] = (area, index) of the chunk
+// exact area partial of one piece, scalar form (explicit x / unaligned y):
+// the CTA's warps stride over the piece
 template <int YDT>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ AreaCand lttb_piece_area_scalar(const double* x, const void* y, int64_t cs, int64_t ce,
+                                                           double ax, double ay, double cx, double cy, int tid,
+                                                           int nthreads) {
+  AreaCand best{-1.0, IDX_NONE};
+  for (int64_t i0 = cs + tid; i0 < ce; i0 += 4 * nthreads) {
+    double vy[4], vx[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int64_t i = i0 + u * nthreads;
+      vy[u] = i < ce ? yd<YDT>(y, i) : 0.0;
+      vx[u] = i < ce ? xd(x, i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int64_t i = i0 + u * nthreads;
+      if (i < ce) {
+        AreaCand a{tri_area(ax, ay, cx, cy, vx[u], vy[u]), i};
+        if (area_better(a, best)) best = a;
+      }
+    }
+  }
+  return best;
+}
+
+// the reference area of element e of a vector (implicit x): dA = ax - x of
+// the vector's first element (an exact integer in f64)
+template <int YDT>
+__device__ __forceinline__ double lttb_varea(const uint4& q, int e, double dA, double ay, double K1, double K2) {
+  const double t1 = __dmul_rn(K1, __dsub_rn(vget<YDT>(q, e), ay));
+  const double t2 = __dmul_rn(__dsub_rn(dA, (double)e), K2);
+  return __dmul_rn(0.5, fabs(__dsub_rn(t1, t2)));
+}
+
+// Verification, round 1 (every bucket, predecessor = the guess): exact
+// first-max area per piece.  Vector form: persistent warps over contiguous
+// piece ranges, LTTB_PV 128-bit loads per lane in flight; per lane and
+// batch only the max AREA is folded, the first batch reaching a lane's max
+// is remembered, and the tying lanes re-read that batch to find their first
+// element (exact first-occurrence over the piece).  Scalar form: one CTA per
+// piece.  part[c] = (area, index) of piece c.
+template <int YDT>
+__global__ void __launch_bounds__(256, LTTB_VMINB)
 lttb_chunk_verify_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off,
                          int64_t nb, const double2* cent, const int64_t* cstart, const int32_t* cb,
-                         const int32_t* rank, const int64_t* counts, const int64_t* picks, const int32_t* dirty,
-                         LttbAreaPart* part) {
-  // one CTA (256 threads) per chunk: a dirty bucket's chunk costs ~4 dependent
-  // load batches, so fix-up rounds stay short
+                         const int32_t* rank, const int64_t* counts, const int64_t* picks, LttbAreaPart* part,
+                         int vec_ok) {
   const double* x = eff_x(xin, drop);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  __shared__ AreaCand sc[8];
   const int64_t NCH = counts[1];
-  for (int64_t c = blockIdx.x; c < NCH; c += gridDim.x) {
-    const int64_t k = cb[c];
-    const int64_t j = rank[k];
-    if (!dirty[j]) continue;  // block-uniform
-    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-    const int64_t cs = s + (c - cstart[k]) * LTTB_CH;
-    const int64_t ce = cs + LTTB_CH < e ? cs + LTTB_CH : e;
-    const int64_t prev = j == 0 ? 0 : picks[j - 1];
-    const double ax = xd(x, prev), ay = yd<YDT>(y, prev);
-    double cx, cy;
-    centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
-    AreaCand best{-1.0, IDX_NONE};
-    for (int64_t i0 = cs + tid; i0 < ce; i0 += 4 * 256) {
-      double vy[4], vx[4];
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int64_t i = i0 + u * 256;
-        vy[u] = i < ce ? yd<YDT>(y, i) : 0.0;
-        vx[u] = i < ce ? xd(x, i) : 0.0;
+  if (x || !vec_ok) {
+    __shared__ AreaCand sc[8];
+    for (int64_t c = blockIdx.x; c < NCH; c += gridDim.x) {
+      const int64_t k = cb[c];
+      const int64_t j = rank[k];
+      const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+      int64_t cs, ce;
+      lttb_piece(s, e, c - cstart[k], cs, ce);
+      const int64_t prev = j == 0 ? 0 : picks[j - 1];
+      double cx, cy;
+      centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
+      AreaCand best = lttb_piece_area_scalar<YDT>(x, y, cs, ce, xd(x, prev), yd<YDT>(y, prev), cx, cy, tid, 256);
+      best = warp_area_max(best);
+      if (lane == 0) sc[wid] = best;
+      __syncthreads();
+      if (tid == 0) {
+        AreaCand bb = sc[0];
+        for (int w = 1; w < 8; w++)
+          if (area_better(sc[w], bb)) bb = sc[w];
+        part[c].a = bb.a;
+        part[c].i = bb.i;
       }
+      __syncthreads();
+    }
+    return;
+  }
+  constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
+  constexpr int BV = 32 * LTTB_PV;
+  const uint4* yv = (const uint4*)y;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t p0 = NCH * gw / nw, p1 = NCH * (gw + 1) / nw;
+  int64_t kc = -1, s = 0, e = 0, prev = 0;
+  double ay = 0.0, K1 = 0.0, K2 = 0.0;
+  for (int64_t c = p0; c < p1; c++) {
+    const int64_t k = cb[c];
+    if (k != kc) {
+      kc = k;
+      s = __ldg(off + k);
+      e = __ldg(off + k + 1);
+      const int64_t j = rank[k];
+      prev = j == 0 ? 0 : picks[j - 1];
+      ay = yd<YDT>(y, prev);
+      double cx, cy;
+      centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
+      K1 = __dsub_rn((double)prev, cx);
+      K2 = __dsub_rn(cy, ay);
+    }
+    int64_t cs, ce;
+    lttb_piece(s, e, c - cstart[k], cs, ce);
+    const int64_t v0 = cs / EPV;
+    const int nvec = (int)((ce + EPV - 1) / EPV - v0);
+    const int r0 = (int)(v0 * EPV - cs), len = (int)(ce - cs);
+    const double dA0 = (double)(prev - cs);  // ax - x at the piece start
+    const uint4* pv = yv + v0;
+    double best = -1.0;
+    int bid = -1;
+    const int nbat = (nvec + BV - 1) / BV;
+    for (int b = 0; b < nbat; b++) {
+      uint4 q[LTTB_PV];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int64_t i = i0 + u * 256;
-        if (i < ce) {
-          AreaCand a{tri_area(ax, ay, cx, cy, vx[u], vy[u]), i};
-          if (area_better(a, best)) best = a;
+      for (int u = 0; u < LTTB_PV; u++) {
+        const int rv = b * BV + u * 32 + lane;
+        q[u] = rv < nvec ? ldg_stream<false>(pv + rv) : make_uint4(0u, 0u, 0u, 0u);
+      }
+      double bm = -1.0;
+#pragma unroll
+      for (int u = 0; u < LTTB_PV; u++) {
+        const int rv = b * BV + u * 32 + lane;
+        const int re0 = r0 + rv * EPV;
+        const double dA = __dsub_rn(dA0, (double)re0);
+        if (re0 >= 0 && re0 + EPV <= len) {
+#pragma unroll
+          for (int ee = 0; ee < EPV; ee++) bm = fmax(bm, lttb_varea<YDT>(q[u], ee, dA, ay, K1, K2));
+        } else if (rv < nvec) {
+#pragma unroll
+          for (int ee = 0; ee < EPV; ee++)
+            if ((unsigned)(re0 + ee) < (unsigned)len) bm = fmax(bm, lttb_varea<YDT>(q[u], ee, dA, ay, K1, K2));
         }
       }
+      if (bm > best) { best = bm; bid = b; }
     }
-    best = warp_area_max(best);
-    if (lane == 0) sc[wid] = best;
-    __syncthreads();
-    if (tid == 0) {
-      AreaCand b = sc[0];
-      for (int w = 1; w < 8; w++)
-        if (area_better(sc[w], b)) b = sc[w];
-      part[c].a = b.a;
-      part[c].i = b.i;
+    // max over the warp, then the first element holding it
+    double W = best;
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) W = fmax(W, __shfl_xor_sync(0xffffffffu, W, m));
+    const unsigned tb = (best == W && bid >= 0) ? (unsigned)bid : 0xffffffffu;
+    const unsigned minb = __reduce_min_sync(0xffffffffu, tb);
+    int64_t found = IDX_NONE;
+    if (W > -1.0 && tb == minb) {
+      uint4 q[LTTB_PV];
+#pragma unroll
+      for (int u = 0; u < LTTB_PV; u++) {
+        const int rv = (int)minb * BV + u * 32 + lane;
+        q[u] = rv < nvec ? __ldg(pv + rv) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < LTTB_PV; u++) {
+        const int rv = (int)minb * BV + u * 32 + lane;
+        const int re0 = r0 + rv * EPV;
+        const double dA = __dsub_rn(dA0, (double)re0);
+#pragma unroll
+        for (int ee = 0; ee < EPV; ee++)
+          if (found == IDX_NONE && rv < nvec && (unsigned)(re0 + ee) < (unsigned)len &&
+              lttb_varea<YDT>(q[u], ee, dA, ay, K1, K2) == W)
+            found = cs + re0 + ee;
+      }
     }
-    __syncthreads();
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      const int64_t o = __shfl_xor_sync(0xffffffffu, found, m);
+      found = o < found ? o : found;
+    }
+    if (lane == 0) {
+      part[c].a = found == IDX_NONE ? -1.0 : W;
+      part[c].i = found;
+    }
   }
 }
 
-// warp per dirty bucket: merge chunk partials; on change store and dirty j+1
+// warp per bucket (round 1): merge piece partials; on change store the pick
+// and list bucket j+1 for re-verification
 __global__ void lttb_chunk_settle_kernel(const int64_t* off, const int64_t* cstart, const int32_t* nonempty,
                                          const int64_t* counts, const LttbAreaPart* part, int64_t* picks,
-                                         int32_t* dirty, int32_t* next_dirty, int32_t* ndirty) {
+                                         int32_t* next_list, int32_t* ndirty) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t L = counts[0];
   for (int64_t j = gw; j < L; j += nw) {
-    if (!dirty[j]) continue;
     const int64_t k = nonempty[j];
     const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-    const int64_t c0 = cstart[k], nch = (e - s + LTTB_CH - 1) / LTTB_CH;
-    AreaCand best{-1.0, IDX_NONE};
-    for (int64_t q = lane; q < nch; q += 32) {
-      AreaCand a{part[c0 + q].a, part[c0 + q].i};
-      if (area_better(a, best)) best = a;
-    }
-    best = warp_area_max(best);
-    if (lane == 0) {
-      dirty[j] = 0;
-      const int64_t p = best.i == IDX_NONE ? s : best.i;
-      if (p != picks[j]) {
-        picks[j] = p;
-        if (j + 1 < L) next_dirty[atomicAdd(ndirty, 1)] = (int32_t)(j + 1);  // work list
-      }
-    }
-  }
-}
-
-// Fix-up rounds run on a work list of buckets whose predecessor changed:
-// one CTA per (listed bucket, chunk); then one warp per listed bucket.
-template <int YDT>
-__global__ void __launch_bounds__(256)
-lttb_list_verify_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off,
-                        int64_t nb, const double2* cent, const int64_t* cstart, const int32_t* nonempty,
-                        const int64_t* picks, const int32_t* list, int64_t count, int64_t maxch, LttbAreaPart* part) {
-  const double* x = eff_x(xin, drop);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  __shared__ AreaCand sc[8];
-  for (int64_t t = blockIdx.x; t < count * maxch; t += gridDim.x) {
-    const int64_t j = list[t / maxch], q = t % maxch;
-    const int64_t k = nonempty[j];
-    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-    const int64_t cs = s + q * LTTB_CH;
-    if (cs >= e) continue;  // block-uniform
-    const int64_t ce = cs + LTTB_CH < e ? cs + LTTB_CH : e;
-    const int64_t prev = j == 0 ? 0 : picks[j - 1];
-    const double ax = xd(x, prev), ay = yd<YDT>(y, prev);
-    double cx, cy;
-    centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
-    AreaCand best{-1.0, IDX_NONE};
-    for (int64_t i0 = cs + tid; i0 < ce; i0 += 4 * 256) {
-      double vy[4], vx[4];
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int64_t i = i0 + u * 256;
-        vy[u] = i < ce ? yd<YDT>(y, i) : 0.0;
-        vx[u] = i < ce ? xd(x, i) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int64_t i = i0 + u * 256;
-        if (i < ce) {
-          AreaCand a{tri_area(ax, ay, cx, cy, vx[u], vy[u]), i};
-          if (area_better(a, best)) best = a;
-        }
-      }
-    }
-    best = warp_area_max(best);
-    if (lane == 0) sc[wid] = best;
-    __syncthreads();
-    if (tid == 0) {
-      AreaCand b = sc[0];
-      for (int w = 1; w < 8; w++)
-        if (area_better(sc[w], b)) b = sc[w];
-      part[cstart[k] + q].a = b.a;
-      part[cstart[k] + q].i = b.i;
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void lttb_list_settle_kernel(const int64_t* off, const int64_t* cstart, const int32_t* nonempty,
-                                        const int64_t* counts, const LttbAreaPart* part, int64_t* picks,
-                                        const int32_t* list, int64_t count, int32_t* next_list, int32_t* ndirty) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t L = counts[0];
-  for (int64_t t = gw; t < count; t += nw) {
-    const int64_t j = list[t];
-    const int64_t k = nonempty[j];
-    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-    const int64_t c0 = cstart[k], nch = (e - s + LTTB_CH - 1) / LTTB_CH;
+    const int64_t c0 = cstart[k], nch = lttb_npieces(s, e);
     AreaCand best{-1.0, IDX_NONE};
     for (int64_t q = lane; q < nch; q += 32) {
       AreaCand a{part[c0 + q].a, part[c0 + q].i};
@@ -589,6 +821,84 @@ __global__ void lttb_list_settle_kernel(const int64_t* off, const int64_t* cstar
       }
     }
   }
+}
+
+// Fix-up rounds in one cooperative launch (no host round trips): each round
+// re-verifies the listed buckets (one CTA per (entry, piece), exact area
+// with the current predecessor), grid barrier, settles them (warp per
+// entry; a changed pick lists its successor), grid barrier.  Data written by
+// other CTAs (picks, partials, lists, counters) is read with ld.cg.
+// ctr[0], ctr[1]: list lengths (ping-pong), ctr[2]: rounds, ctr[3]: length
+// after round 1.
+template <int YDT>
+__global__ void __launch_bounds__(256)
+lttb_fixup_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
+                  const double2* cent, const int64_t* cstart, const int32_t* nonempty, const int64_t* counts,
+                  int64_t* picks, int32_t* list_a, int32_t* list_b, int32_t* ctr, LttbAreaPart* part) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const double* x = eff_x(xin, drop);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  __shared__ AreaCand sc[8];
+  const int64_t L = counts[0];
+  const int64_t maxch = counts[2] > 0 ? counts[2] : 1;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int ci = 0, round = 1;
+  if (blockIdx.x == 0 && tid == 0) ctr[3] = __ldcg(ctr);
+  for (;; round++) {
+    const int64_t count = __ldcg(ctr + ci);
+    if (count == 0 || round > nb + 2) break;
+    const int32_t* cur = ci ? list_b : list_a;
+    int32_t* nxt = ci ? list_a : list_b;
+    for (int64_t t = blockIdx.x; t < count * maxch; t += gridDim.x) {
+      const int64_t j = __ldcg(cur + t / maxch), q = t % maxch;
+      const int64_t k = nonempty[j];
+      const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+      if (q >= lttb_npieces(s, e)) continue;  // block-uniform
+      int64_t cs, ce;
+      lttb_piece(s, e, q, cs, ce);
+      const int64_t prev = j == 0 ? 0 : __ldcg(picks + j - 1);
+      double cx, cy;
+      centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
+      AreaCand best = lttb_piece_area_scalar<YDT>(x, y, cs, ce, xd(x, prev), yd<YDT>(y, prev), cx, cy, tid, 256);
+      best = warp_area_max(best);
+      if (lane == 0) sc[wid] = best;
+      __syncthreads();
+      if (tid == 0) {
+        AreaCand b = sc[0];
+        for (int w = 1; w < 8; w++)
+          if (area_better(sc[w], b)) b = sc[w];
+        part[cstart[k] + q].a = b.a;
+        part[cstart[k] + q].i = b.i;
+      }
+      __syncthreads();
+    }
+    if (blockIdx.x == 0 && tid == 0) ctr[1 - ci] = 0;
+    grid.sync();
+    for (int64_t t = gw; t < count; t += nw) {
+      const int64_t j = __ldcg(cur + t);
+      const int64_t k = nonempty[j];
+      const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+      const int64_t c0 = cstart[k], nch = lttb_npieces(s, e);
+      AreaCand best{-1.0, IDX_NONE};
+      for (int64_t q = lane; q < nch; q += 32) {
+        AreaCand a{__ldcg(&part[c0 + q].a), __ldcg(&part[c0 + q].i)};
+        if (area_better(a, best)) best = a;
+      }
+      best = warp_area_max(best);
+      if (lane == 0) {
+        const int64_t p = best.i == IDX_NONE ? s : best.i;
+        if (p != __ldcg(picks + j)) {
+          picks[j] = p;
+          if (j + 1 < L) nxt[atomicAdd(ctr + 1 - ci, 1)] = (int32_t)(j + 1);
+        }
+      }
+    }
+    grid.sync();
+    ci = 1 - ci;
+  }
+  if (blockIdx.x == 0 && tid == 0) ctr[2] = round;
 }
 
 // out = [0, picks..., n-1] (+ count at out[-1]); optional index map
