@@ -558,13 +558,59 @@ int ensure_lstat(tsds_ctx* ctx) {
 
 // grid of exactly one resident wave of `kernel` (persistent kernels)
 template <typename K>
-unsigned one_wave(tsds_ctx* ctx, K kernel, int threads) {
+unsigned one_wave(tsds_ctx* ctx, K kernel, int threads, size_t smem = 0) {
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int b = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, 0) != cudaSuccess || b < 1) b = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem) != cudaSuccess || b < 1) b = 1;
   return (unsigned)(ctx->sms * b);
 }
 
-// Large buckets: prepass -> guess walk on the reduced problem -> verify/fix rounds.
+// launch with programmatic dependent launch: the kernel's launch and
+// prologue overlap the tail of its predecessor (the LTTB kernels start with
+// griddepcontrol.launch_dependents + griddepcontrol.wait)
+template <typename... KP, typename... A>
+int launch_pdl(tsds_ctx* ctx, void (*k)(KP...), unsigned grid, unsigned block, size_t smem, A... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(std::max(grid, 1u));
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, k, ((KP)args)...));
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
+// CUDA events around a whole composed call (tsds_ctx_profile)
+int prof_mark(tsds_ctx* ctx, std::pair<cudaEvent_t, cudaEvent_t>& ev, bool end) {
+  if (!ctx->profile) return TSDS_OK;
+  if (!end) {
+    if (ctx->ev_free.empty()) {
+      CUDA_TRY(cudaEventCreate(&ev.first));
+      CUDA_TRY(cudaEventCreate(&ev.second));
+    } else {
+      ev = ctx->ev_free.back();
+      ctx->ev_free.pop_back();
+    }
+    CUDA_TRY(cudaEventRecord(ev.first, ctx->stream));
+  } else {
+    CUDA_TRY(cudaEventRecord(ev.second, ctx->stream));
+    ctx->ev_used.push_back(ev);
+  }
+  return TSDS_OK;
+}
+
+static inline unsigned cap_grid(int64_t want, int64_t cap) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cap, want));
+}
+
+// Large buckets: prepass -> guess walk on the reduced problem -> verify/fix
+// rounds.  One stream-ordered sequence, no host round trip; consecutive
+// kernels are chained with programmatic dependent launch.
 int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
                    const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev) {
   RC_TRY(ensure(ctx, ctx->cent, (size_t)std::max<int64_t>(nb, 1) * sizeof(double2)));
@@ -572,19 +618,24 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   const int64_t NC = LTTB_NC;
   const int64_t maxch = (n + LTTB_CH - 1) / LTTB_CH + nb + 1;
   const int64_t maxseg = nb / LTTB_SEG + 2;
-  size_t need = 0;
+  const int64_t nlb = (nb + LTTB_LB - 1) / LTTB_LB;
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-  need += al(8 * (nb + 1)) + al(4 * maxch) + al(4 * nb) + al(4 * nb) + al(64) + al(32 * nb) + al(16 * nb) +
-          al(sizeof(LttbChunkPart) * maxch) + al(8 * NC * nb) + al(NC * nb) + al(NC * maxseg) + al(maxseg) +
-          al(8 * (nb + 4)) + al(4 * nb) * 2 + al(64) + al(sizeof(LttbAreaPart) * maxch);
+  const size_t zero_bytes = al(64) + al(64) + al(4 * nb) + al(24 * (nlb + 1));  // counts, ctr, arrive, link
+  const size_t need = zero_bytes + al(8 * (nb + 1)) + al(4 * maxch) + al(4 * nb) + al(4 * nb) + al(32 * nb) +
+                      al(16 * nb) + al(sizeof(LttbChunkPart) * maxch) + al(8 * NC * nb) + al(NC * nb) +
+                      al(NC * maxseg) + al(maxseg) + al(8 * (nb + 4)) + al(4 * nb) * 2 +
+                      al(sizeof(LttbAreaPart) * maxch);
   RC_TRY(ensure(ctx, ctx->lscr, need));
   char* p = (char*)ctx->lscr.p;
   auto take = [&](size_t bytes) { char* r = p; p += al(bytes); return r; };
+  int64_t* counts = (int64_t*)take(64);  // zeroed block: counts, ctr, arrive, link
+  int32_t* ctr = (int32_t*)take(64);
+  int32_t* arrive = (int32_t*)take(4 * nb);
+  unsigned long long* link = (unsigned long long*)take(24 * (nlb + 1));
   int64_t* cstart = (int64_t*)take(8 * (nb + 1));
   int32_t* cb = (int32_t*)take(4 * maxch);
   int32_t* rank = (int32_t*)take(4 * nb);
   int32_t* nonempty = (int32_t*)take(4 * nb);
-  int64_t* counts = (int64_t*)take(64);
   double4* bbox = (double4*)take(32 * nb);
   double2* slopes = (double2*)take(16 * nb);
   LttbChunkPart* cpart = (LttbChunkPart*)take(sizeof(LttbChunkPart) * maxch);
@@ -595,80 +646,67 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   int64_t* walkout = (int64_t*)take(8 * (nb + 4));
   int32_t* list_a = (int32_t*)take(4 * nb);
   int32_t* list_b = (int32_t*)take(4 * nb);
-  int32_t* ctr = (int32_t*)take(64);
   LttbAreaPart* apart = (LttbAreaPart*)take(sizeof(LttbAreaPart) * maxch);
   int64_t* picks = walkout + 2;
   const int mode = lttb_exact_mode();
   const int64_t avg = (n - 2) / std::max<int64_t>(nb, 1);
   const int exact = mode == 1 ? 1 : (mode == 2 ? 0 : (avg <= 1024 ? 1 : 0));
-  const unsigned gw8 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 16, (nb + 7) / 8));
-  // ---- layout, sampling, slopes
-  lttb_layout_kernel<<<1, 1024, 0, ctx->stream>>>(off, nb, cstart, cb, rank, nonempty, counts);
-  LAUNCH_CHECK();
-  YDT_SWITCH(ydt, (lttb_sample_kernel<YD><<<gw8, 256, 0, ctx->stream>>>(y, off, nb, bbox)));
-  LAUNCH_CHECK();
-  YDT_SWITCH(ydt, (lttb_slopes_kernel<YD><<<(unsigned)std::max<int64_t>(1, (nb + 255) / 256), 256, 0, ctx->stream>>>(
-                      xf, drop, y, off, nb, n, bbox, slopes)));
-  LAUNCH_CHECK();
-  // ---- chunk prepass + per-bucket merge (centroids, candidates)
+  const unsigned gw8 = cap_grid((nb + 7) / 8, (int64_t)ctx->sms * 16);
   const int vec_ok = ((uintptr_t)y & 15) == 0 ? 1 : 0;
-  YDT_SWITCH(ydt, (lttb_chunk_prepass_kernel<YD><<<one_wave(ctx, lttb_chunk_prepass_kernel<YD>, 256), 256, 0,
-                                                  ctx->stream>>>(xf, drop, y, off, cstart, cb, counts, slopes, cpart,
-                                                                 vec_ok)));
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  RC_TRY(prof_mark(ctx, ev, false));
+  CUDA_TRY(cudaMemsetAsync(counts, 0, zero_bytes, ctx->stream));
+  // ---- layout, sampling, slopes
+  RC_TRY(launch_pdl(ctx, lttb_layout_kernel, (unsigned)std::max<int64_t>(1, nlb), 1024, 0, off, nb, cstart, cb, rank,
+                    nonempty, counts, link));
+  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_sample_kernel<YD>, gw8, 256, 0, y, off, nb, bbox)));
+  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_slopes_kernel<YD>, cap_grid((nb + 255) / 256, 1 << 20), 256, 0, xf, drop,
+                                    y, off, nb, n, bbox, slopes)));
+  // ---- chunk prepass + per-bucket merge (centroids, candidates)
+  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_chunk_prepass_kernel<YD>,
+                                    one_wave(ctx, lttb_chunk_prepass_kernel<YD>, 256, LTTB_RING_BYTES), 256,
+                                    LTTB_RING_BYTES, xf, drop, y, off, cstart, cb, counts, slopes, cpart, vec_ok)));
+  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_chunk_merge_kernel<YD>, gw8, 256, 0, xf, drop, off, nb, cstart, cpart,
+                                    cent, ext)));
+  if (exact)
+    YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_centroid_kernel<YD>, cap_grid((nb + 7) / 8, (int64_t)ctx->sms * 16),
+                                      256, 0, xf, drop, y, off, nb, cent)));
+  // ---- guess chain on the candidates (composed transition tables); grids
+  //      are sized from nb, the kernels read the actual counts on the device
+  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_cand_table_kernel<YD>, cap_grid((nb * NC + 255) / 256, (int64_t)ctx->sms * 8),
+                                    256, 0, xf, drop, y, n, off, nb, cent, ext, nonempty, counts, T)));
+  const int64_t NS = (nb + LTTB_SEG - 1) / LTTB_SEG;
+  const unsigned gs = cap_grid((NS + 7) / 8, (int64_t)ctx->sms * 8);
+  RC_TRY(launch_pdl(ctx, lttb_seg_compose_kernel, gs, 256, 0, T, counts, C));
+  const int64_t cap = 40000;
+  RC_TRY(launch_pdl(ctx, lttb_seg_entry_kernel, 1, 1024, (size_t)(std::min<int64_t>(NS * NC, cap) + 16), T, C, counts,
+                    entry, cap));
+  RC_TRY(launch_pdl(ctx, lttb_seg_expand_kernel, gs, 256, 0, T, entry, ext, nonempty, counts, picks));
+  // ---- verify every bucket once (round 1), then the fix-up rounds on a work
+  //      list of buckets whose predecessor changed
+  int32_t* lcount = ctr + 2;  // round 1 lists into list_a / ctr[2]
+  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_chunk_verify_kernel<YD>,
+                                    one_wave(ctx, lttb_chunk_verify_kernel<YD>, 256, LTTB_RING_BYTES), 256,
+                                    LTTB_RING_BYTES, xf, drop, y, n, off, nb, cent, cstart, cb, rank, counts, picks,
+                                    apart, vec_ok)));
+  RC_TRY(launch_pdl(ctx, lttb_chunk_settle_kernel, cap_grid((nb + 7) / 8, (int64_t)ctx->sms * 8), 256, 0, off, cstart,
+                    nonempty, counts, apart, picks, list_a, lcount));
+  YDT_SWITCH(ydt, ({
+               const void* fx = (const void*)lttb_fixup_kernel<YD>;
+               const unsigned gf = one_wave(ctx, lttb_fixup_kernel<YD>, 256);
+               void* args[] = {(void*)&xf,     (void*)&drop,  (void*)&y,      (void*)&n,      (void*)&off,
+                               (void*)&nb,     (void*)&cent,  (void*)&cstart, (void*)&nonempty,
+                               (void*)&counts, (void*)&picks, (void*)&list_a, (void*)&list_b, (void*)&ctr,
+                               (void*)&arrive, (void*)&apart, (void*)&vec_ok};
+               CUDA_TRY(cudaLaunchCooperativeKernel(fx, dim3(gf), dim3(256), args, 0, ctx->stream));
+             }));
   LAUNCH_CHECK();
-  YDT_SWITCH(ydt, (lttb_chunk_merge_kernel<YD><<<gw8, 256, 0, ctx->stream>>>(xf, drop, off, nb, cstart, cpart, cent,
-                                                                           ext)));
-  LAUNCH_CHECK();
-  if (exact) {
-    unsigned gc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 16, (nb + 7) / 8));
-    YDT_SWITCH(ydt, (lttb_centroid_kernel<YD><<<gc, 256, 0, ctx->stream>>>(xf, drop, y, off, nb, cent)));
-    LAUNCH_CHECK();
-  }
-  // No host round trip from here on: grids are sized from nb (the kernels
-  // read the actual counts L, NCH from the device).
-  {
-    // ---- guess chain on the candidates (composed transition tables)
-    const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (nb * NC + 255) / 256));
-    YDT_SWITCH(ydt, (lttb_cand_table_kernel<YD><<<gt, 256, 0, ctx->stream>>>(xf, drop, y, n, off, nb, cent, ext,
-                                                                           nonempty, counts, T)));
-    LAUNCH_CHECK();
-    const int64_t NS = (nb + LTTB_SEG - 1) / LTTB_SEG;
-    const unsigned gs = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (NS + 7) / 8));
-    lttb_seg_compose_kernel<<<gs, 256, 0, ctx->stream>>>(T, counts, C);
-    LAUNCH_CHECK();
-    const int64_t cap = 40000;
-    lttb_seg_entry_kernel<<<1, 1024, (size_t)(std::min<int64_t>(NS * NC, cap) + 16), ctx->stream>>>(T, C, counts, entry,
-                                                                                                    cap);
-    LAUNCH_CHECK();
-    lttb_seg_expand_kernel<<<gs, 256, 0, ctx->stream>>>(T, entry, ext, nonempty, counts, picks);
-    LAUNCH_CHECK();
-    // ---- verify every bucket once (round 1), then the fix-up rounds on a
-    //      work list of buckets whose predecessor changed
-    CUDA_TRY(cudaMemsetAsync(ctr, 0, 16, ctx->stream));
-    const unsigned gl = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 8, (nb + 7) / 8));
-    YDT_SWITCH(ydt, (lttb_chunk_verify_kernel<YD><<<one_wave(ctx, lttb_chunk_verify_kernel<YD>, 256), 256, 0,
-                                                   ctx->stream>>>(xf, drop, y, n, off, nb, cent, cstart, cb, rank,
-                                                                  counts, picks, apart, vec_ok)));
-    LAUNCH_CHECK();
-    lttb_chunk_settle_kernel<<<gl, 256, 0, ctx->stream>>>(off, cstart, nonempty, counts, apart, picks, list_a, ctr);
-    LAUNCH_CHECK();
-    YDT_SWITCH(ydt, ({
-                 const void* fx = (const void*)lttb_fixup_kernel<YD>;
-                 const unsigned gf = one_wave(ctx, lttb_fixup_kernel<YD>, 256);
-                 void* args[] = {(void*)&xf,       (void*)&drop,     (void*)&y,    (void*)&n,      (void*)&off,
-                                 (void*)&nb,       (void*)&cent,     (void*)&cstart, (void*)&nonempty,
-                                 (void*)&counts,   (void*)&picks,    (void*)&list_a, (void*)&list_b, (void*)&ctr,
-                                 (void*)&apart};
-                 CUDA_TRY(cudaLaunchCooperativeKernel(fx, dim3(gf), dim3(256), args, 0, ctx->stream));
-               }));
-    LAUNCH_CHECK();
-    RC_TRY(ensure_lstat(ctx));
-    CUDA_TRY(cudaMemcpyAsync(ctx->h_lstat, ctr + 2, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    ctx->lstat_pending = true;
-  }
-  lttb_emit_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, (nb + 257) / 256)), 256, 0, ctx->stream>>>(
-      picks, counts, n, map, out_dev + 1, out_dev);
-  LAUNCH_CHECK();
+  RC_TRY(launch_pdl(ctx, lttb_emit_kernel, cap_grid((nb + 257) / 256, 1024), 256, 0, picks, counts, n, map,
+                    out_dev + 1, out_dev));
+  RC_TRY(prof_mark(ctx, ev, true));
+  RC_TRY(ensure_lstat(ctx));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_lstat, ctr + 3, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->lstat_pending = true;
   return TSDS_OK;
 }
 

@@ -59,10 +59,10 @@ __device__ __forceinline__ double vget(const uint4& q, int e) {
   using T = typename YT<YDT>::T;
   constexpr int ES = (int)sizeof(T);
   if constexpr (ES == 8) {
-    const unsigned long long b = e == 0 ? ((unsigned long long)q.y << 32 | q.x) : ((unsigned long long)q.w << 32 | q.z);
-    T v;
-    memcpy(&v, &b, 8);
-    return ycv<YDT>(v);
+    // register pairs, no shifts/ors: reinterpret through __hiloint2double
+    const double d = e == 0 ? __hiloint2double((int)q.y, (int)q.x) : __hiloint2double((int)q.w, (int)q.z);
+    if constexpr (YDT == DT_F64) return d;
+    else return ycv<YDT>((T)__double_as_longlong(d));
   } else {
     const int wi = e * ES / 4;
     const unsigned w = wi == 0 ? q.x : (wi == 1 ? q.y : (wi == 2 ? q.z : q.w));
@@ -96,6 +96,8 @@ __device__ __forceinline__ const double* eff_x(const double* x, const int* drop)
 template <int YDT>
 __global__ void lttb_centroid_kernel(const double* xin, const int* drop, const void* y,
                                      const int64_t* off, int64_t nb, double2* cent) {
+  pdl_launch_dependents();
+  pdl_wait();
   const double* x = eff_x(xin, drop);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;

@@ -25,7 +25,10 @@
 
 namespace tsds {
 
-constexpr int LTTB_K = 7;            // candidate slopes per bucket
+#ifndef LTTB_K_N
+#define LTTB_K_N 7
+#endif
+constexpr int LTTB_K = LTTB_K_N;     // candidate slopes per bucket
 constexpr int LTTB_NC = 2 * LTTB_K;  // candidates per bucket (argmax + argmin per slope)
 #ifndef LTTB_CH_N
 #define LTTB_CH_N 4096
@@ -56,53 +59,94 @@ struct LttbAreaPart {  // per-chunk partial of the verification
   int64_t i;
 };
 
-// chunk layout + non-empty bucket list (single CTA block scans):
-// cstart[k] = first chunk of bucket k, cb[c] = bucket of chunk c,
-// rank[k] = index among non-empty buckets, nonempty[j] = k, counts = {L, NCH}
+// piece layout + non-empty bucket list, one pass (chained scan): block t
+// (ticket order) takes LTTB_LB buckets, scans them, waits for block t-1's
+// inclusive prefix and publishes its own.
+// cstart[k] = first piece of bucket k, cb[c] = bucket of piece c,
+// rank[k] = index among non-empty buckets, nonempty[j] = k,
+// counts = {L, NCH, max pieces per bucket, ticket}; link[3t..3t+2] =
+// inclusive prefix of block t + ready flag, zeroed by the caller.
+constexpr int LTTB_LR = 4;                // buckets per thread
+constexpr int LTTB_LB = 1024 * LTTB_LR;   // buckets per block
 __global__ void __launch_bounds__(1024)
 lttb_layout_kernel(const int64_t* off, int64_t nb, int64_t* cstart, int32_t* cb, int32_t* rank, int32_t* nonempty,
-                   int64_t* counts) {
+                   int64_t* counts, unsigned long long* link) {
+  pdl_launch_dependents();
+  pdl_wait();
   __shared__ int64_t wt[2][32];
-  __shared__ int64_t run[2];
-  __shared__ unsigned long long smax;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  if (tid == 0) { run[0] = 0; run[1] = 0; smax = 0ull; }
+  __shared__ int64_t base[2];
+  __shared__ int tk;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) tk = (int)atomicAdd((unsigned long long*)&counts[3], 1ull);
   __syncthreads();
-  for (int64_t base = 0; base < nb; base += blockDim.x) {
-    const int64_t k = base + tid;
-    int64_t len = 0;
-    if (k < nb) len = __ldg(off + k + 1) - __ldg(off + k);
-    const int64_t nch = k < nb ? lttb_npieces(__ldg(off + k), __ldg(off + k + 1)) : 0;
-    const int64_t ne = len > 0 ? 1 : 0;
-    if (nch) atomicMax(&smax, (unsigned long long)nch);
-    int64_t a = nch, b = ne;
+  const int t = tk;
+  const int64_t k0 = (int64_t)t * LTTB_LB + (int64_t)tid * LTTB_LR;
+  int64_t np[LTTB_LR], a = 0, b = 0, mx = 0;
+#pragma unroll
+  for (int r = 0; r < LTTB_LR; r++) {
+    const int64_t k = k0 + r;
+    np[r] = k < nb ? lttb_npieces(__ldg(off + k), __ldg(off + k + 1)) : 0;
+    a += np[r];
+    b += np[r] > 0;
+    mx = np[r] > mx ? np[r] : mx;
+  }
+  if (mx) atomicMax((unsigned long long*)&counts[2], (unsigned long long)mx);
+  // block exclusive scan of (a, b)
+  int64_t ia = a, ib = b;
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    const int64_t ta = __shfl_up_sync(0xffffffffu, ia, m), tb = __shfl_up_sync(0xffffffffu, ib, m);
+    if (lane >= m) { ia += ta; ib += tb; }
+  }
+  if (lane == 31) { wt[0][wid] = ia; wt[1][wid] = ib; }
+  __syncthreads();
+  if (wid == 0) {
+    int64_t xa = wt[0][lane], xb = wt[1][lane];
 #pragma unroll
     for (int m = 1; m < 32; m <<= 1) {
-      const int64_t ta = __shfl_up_sync(0xffffffffu, a, m), tb = __shfl_up_sync(0xffffffffu, b, m);
-      if (lane >= m) { a += ta; b += tb; }
+      const int64_t ta = __shfl_up_sync(0xffffffffu, xa, m), tb = __shfl_up_sync(0xffffffffu, xb, m);
+      if (lane >= m) { xa += ta; xb += tb; }
     }
-    if (lane == 31) { wt[0][wid] = a; wt[1][wid] = b; }
-    __syncthreads();
-    int64_t pa = run[0], pb = run[1];
-    for (int w = 0; w < wid; w++) { pa += wt[0][w]; pb += wt[1][w]; }
-    pa += a - nch;
-    pb += b - ne;
-    if (k < nb) {
-      cstart[k] = pa;
-      rank[k] = ne ? (int32_t)pb : -1;
-      if (ne) nonempty[pb] = (int32_t)k;
-      for (int64_t c = 0; c < nch; c++) cb[pa + c] = (int32_t)k;
+    wt[0][lane] = xa;
+    wt[1][lane] = xb;
+    if (lane == 31) {
+      // chained prefix: wait for block t-1, publish ours
+      // (link[3t] = pieces, link[3t+1] = non-empty buckets, link[3t+2] = ready)
+      unsigned long long pa = 0, pb = 0;
+      if (t > 0) {
+        volatile unsigned long long* lp = link + 3 * (t - 1);
+        while (lp[2] == 0) {
+        }
+        __threadfence();
+        pa = lp[0];
+        pb = lp[1];
+      }
+      base[0] = (int64_t)pa;
+      base[1] = (int64_t)pb;
+      volatile unsigned long long* me = link + 3 * t;
+      me[0] = pa + (unsigned long long)xa;
+      me[1] = pb + (unsigned long long)xb;
+      __threadfence();
+      atomicExch(link + 3 * t + 2, 1ull);
+      if ((int64_t)(t + 1) * LTTB_LB >= nb) {
+        counts[0] = (int64_t)(pb + xb);
+        counts[1] = (int64_t)(pa + xa);
+      }
     }
-    __syncthreads();
-    if (tid == 0) {
-      for (int w = 0; w < nw; w++) { run[0] += wt[0][w]; run[1] += wt[1][w]; }
-    }
-    __syncthreads();
   }
-  if (tid == 0) {
-    counts[0] = run[1];
-    counts[1] = run[0];
-    counts[2] = (int64_t)smax;
+  __syncthreads();
+  int64_t pa = base[0] + (wid ? wt[0][wid - 1] : 0) + ia - a;
+  int64_t pb = base[1] + (wid ? wt[1][wid - 1] : 0) + ib - b;
+#pragma unroll
+  for (int r = 0; r < LTTB_LR; r++) {
+    const int64_t k = k0 + r;
+    if (k >= nb) break;
+    cstart[k] = pa;
+    rank[k] = np[r] ? (int32_t)pb : -1;
+    if (np[r]) nonempty[pb] = (int32_t)k;
+    for (int64_t c = 0; c < np[r]; c++) cb[pa + c] = (int32_t)k;
+    pa += np[r];
+    pb += np[r] > 0;
   }
 }
 
@@ -110,6 +154,8 @@ lttb_layout_kernel(const int64_t* off, int64_t nb, int64_t* cstart, int32_t* cb,
 // <= 64 strided samples; only steers the candidate slopes)
 template <int YDT>
 __global__ void lttb_sample_kernel(const void* y, const int64_t* off, int64_t nb, double4* bbox) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -139,6 +185,8 @@ __global__ void lttb_sample_kernel(const void* y, const int64_t* off, int64_t nb
 template <int YDT>
 __global__ void lttb_slopes_kernel(const double* xin, const int* drop, const void* y, const int64_t* off, int64_t nb,
                                    int64_t n, const double4* bbox, double2* slopes) {
+  pdl_launch_dependents();
+  pdl_wait();
   const double* x = eff_x(xin, drop);
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nb; k += (int64_t)gridDim.x * blockDim.x) {
     if (__ldg(off + k + 1) <= __ldg(off + k)) continue;
@@ -281,26 +329,88 @@ __device__ __forceinline__ void lttb_prepass_scalar(const double* x, const void*
 #ifndef LTTB_PV_N
 #define LTTB_PV_N 8
 #endif
-#ifndef LTTB_PMINB
-#define LTTB_PMINB 2
+constexpr int LTTB_PV = LTTB_PV_N;  // 128-bit vectors per lane per batch
+constexpr int LTTB_BV = 32 * LTTB_PV;  // vectors per warp batch
+#ifndef LTTB_RING_D
+#define LTTB_RING_D 3
 #endif
-#ifndef LTTB_VMINB
-#define LTTB_VMINB 2
-#endif
-constexpr int LTTB_PV = LTTB_PV_N;  // 128-bit vectors per lane in flight
+constexpr int LTTB_D = LTTB_RING_D;   // batches in flight per warp
+constexpr int LTTB_WARPS = 8;         // warps per CTA of the streaming kernels
+constexpr size_t LTTB_RING_BYTES = (size_t)LTTB_WARPS * LTTB_D * LTTB_BV * 16;
 
 __device__ __forceinline__ unsigned f32_key(float f) {  // order-preserving (no NaN)
   const unsigned b = __float_as_uint(f);
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-// Steering projection of a piece element (vector form): re = element index
-// relative to the piece start, dxb = x offset of the vector's first element
-// from the bucket start.  The locate pass recomputes it bit-identically.
-__device__ __forceinline__ float lttb_vx(float base, int rv0) { return __fadd_rn(base, (float)rv0); }
+__device__ __forceinline__ uint32_t lttb_smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
 
+// Per-warp streaming ring over the warp's contiguous vector range [V0, V1):
+// batch t (LTTB_BV vectors) is copied by cp.async (16 B per lane-vector,
+// L2 only) into slot t % LTTB_D, LTTB_D batches in flight.  Every lane
+// copies and later reads its own vectors, so completion is tracked per
+// lane with commit/wait groups and no warp synchronisation is needed.
+// Bytes in flight live in shared memory, not registers.
+struct LttbRing {
+  const uint4* src;
+  uint32_t sbase;
+  int64_t V0, V1;
+  __device__ __forceinline__ void fill(int64_t t, int lane) const {
+    const int64_t b = V0 + t * LTTB_BV;
+    const int64_t r = V1 - b;
+    const int rem = r < LTTB_BV ? (int)r : LTTB_BV;  // vectors of the batch inside the range (may be <= 0)
+    const uint32_t d = sbase + (uint32_t)((t % LTTB_D) * LTTB_BV + lane) * 16u;
+    const uint4* g = src + b + lane;
+#pragma unroll
+    for (int u = 0; u < LTTB_PV; u++)
+      if (u * 32 + lane < rem)
+        asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(d + (uint32_t)(u * 32) * 16u),
+                     "l"(g + u * 32)
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  __device__ __forceinline__ void wait() const { asm volatile("cp.async.wait_group %0;" ::"n"(LTTB_D - 1) : "memory"); }
+  __device__ __forceinline__ void drain() const { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+  __device__ __forceinline__ uint4 get(int64_t t, int u, int lane) const {
+    uint4 r;
+    const uint32_t a = sbase + (uint32_t)((t % LTTB_D) * LTTB_BV + u * 32 + lane) * 16u;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+    return r;
+  }
+};
+
+// piece c -> bucket k, bucket [s, e), piece [cs, ce)
+__device__ __forceinline__ void lttb_piece_of(const int64_t* off, const int64_t* cstart, const int32_t* cb, int64_t c,
+                                              int64_t& k, int64_t& s, int64_t& e, int64_t& cs, int64_t& ce) {
+  k = cb[c];
+  s = __ldg(off + k);
+  e = __ldg(off + k + 1);
+  lttb_piece(s, e, c - cstart[k], cs, ce);
+}
+
+// x offset (from the bucket start) of a lane's vector u in a batch, as the
+// steering projection uses it: dxl = (float)(batch start - s) + (float)(lane*EPV)
+__device__ __forceinline__ float lttb_dx(float dxl, int uoff) { return __fadd_rn(dxl, (float)uoff); }
+__device__ __forceinline__ float lttb_dxe(float dxb, int e) { return e == 0 ? dxb : __fadd_rn(dxb, (float)e); }
+
+// (a*b.x + c.x, a*b.y + c.y), each rounded once: fma.rn.f32x2
+__device__ __forceinline__ float2 lttb_ffma2(float a, float2 b, float2 c) {
+  float2 r;
+  asm("{.reg .b64 pa, pb, pc, pd;\n\t"
+      "mov.b64 pa, {%2, %2};\n\tmov.b64 pb, {%3, %4};\n\tmov.b64 pc, {%5, %6};\n\t"
+      "fma.rn.f32x2 pd, pa, pb, pc;\n\tmov.b64 {%0, %1}, pd;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+
+// fold one 128-bit vector (elements i0 .. i0+EPV-1) into the batch extrema;
+// with CHECK only the elements rl+e in [0, len) (relative to the window) count.
+// Steering projection: fmaf(-slope, (float)(i - s) [as dxb + e], (float)(y - yb)).
 template <int YDT, bool CHECK>
-__device__ __forceinline__ void lttb_pv_fold(const uint4& q, int re0, int len, float dxb, double yb,
+__device__ __forceinline__ void lttb_pv_fold(const uint4& q, int rl, int len, float dxb, double yb,
                                              const float (&sl)[LTTB_K], float (&bm)[LTTB_K], float (&bn)[LTTB_K],
                                              double& py) {
   constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
@@ -308,157 +418,202 @@ __device__ __forceinline__ void lttb_pv_fold(const uint4& q, int re0, int len, f
 #pragma unroll
   for (int e = 0; e < EPV; e++) {
     const double d = vget<YDT>(q, e);
-    const bool ok = !CHECK || (unsigned)(re0 + e) < (unsigned)len;
+    const bool ok = !CHECK || (unsigned)(rl + e) < (unsigned)len;
     if (ok) py = __dadd_rn(py, d);
     vf[e] = ok ? __double2float_rn(__dsub_rn(d, yb)) : __int_as_float(0x7fc00000);
   }
+  float dx[EPV];
+#pragma unroll
+  for (int e = 0; e < EPV; e++) dx[e] = lttb_dxe(dxb, e);
 #pragma unroll
   for (int j = 0; j < LTTB_K; j++) {
     float m = bm[j], n = bn[j];
 #pragma unroll
-    for (int e = 0; e < EPV; e++) {
-      const float t = fmaf(-sl[j], __fadd_rn(dxb, (float)e), vf[e]);
-      m = fmaxf(m, t);
-      n = fminf(n, t);
+    for (int e = 0; e < EPV; e += 2) {  // packed pair FMA (FFMA2), bit-identical to two fmaf
+      const float2 t = lttb_ffma2(-sl[j], make_float2(dx[e], dx[e + 1]), make_float2(vf[e], vf[e + 1]));
+      m = fmaxf(m, fmaxf(t.x, t.y));
+      n = fminf(n, fminf(t.x, t.y));
     }
     bm[j] = m;
     bn[j] = n;
   }
 }
 
-// Vector form (implicit x, aligned y): each warp streams a contiguous range
-// of pieces with LTTB_PV 128-bit loads per lane in flight.  Per lane and
-// batch only the extremum VALUES are folded (3-input min/max); the batch that
-// first improved a lane's extremum is remembered (8-bit ids) and the winning element is located afterwards by
-// re-reading that one batch.
+// Prepass, vector form (implicit x, 16-byte aligned y).  Each warp streams
+// a contiguous range of pieces through its LttbRing.  Per lane and batch only
+// the extremum VALUES are folded (3-input min/max); the batch that first
+// improved a lane's extremum is remembered (8-bit ids relative to the
+// piece's first batch) and the winning element is located afterwards by
+// re-reading that one batch from global memory (an L2 hit).  A batch that
+// straddles piece boundaries is folded once per piece, masked.
 template <int YDT>
-__global__ void __launch_bounds__(256, LTTB_PMINB)
+__device__ __forceinline__ void lttb_prepass_ring(const void* y, const int64_t* off, const int64_t* cstart,
+                                                  const int32_t* cb, int64_t NCH, const double2* slopes,
+                                                  LttbChunkPart* part, uint4* ring) {
+  constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
+  constexpr int BV = LTTB_BV;
+  const uint4* yv = (const uint4*)y;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t p0 = NCH * gw / nw, p1 = NCH * (gw + 1) / nw;
+  if (p0 >= p1) return;
+  int64_t k, s, e, cs, ce;
+  lttb_piece_of(off, cstart, cb, p1 - 1, k, s, e, cs, ce);
+  const int64_t V1 = (ce + EPV - 1) / EPV;
+  lttb_piece_of(off, cstart, cb, p0, k, s, e, cs, ce);
+  const int64_t V0 = cs / EPV;
+  const LttbRing R{yv, lttb_smem_u32(ring + (size_t)wl * LTTB_D * BV), V0, V1};
+  const int64_t NBt = (V1 - V0 + BV - 1) / BV;
+#pragma unroll
+  for (int t = 0; t < LTTB_D; t++) R.fill(t, lane);
+  float sl[LTTB_K];
+  double yb = 0.0;
+  auto bucket_header = [&]() {
+    const double2 sr = slopes[k];
+#pragma unroll
+    for (int j = 0; j < LTTB_K; j++) sl[j] = (float)(sr.x + (sr.y - sr.x) * ((double)j / (double)(LTTB_K - 1)));
+    const double ys0 = yd<YDT>(y, s);
+    yb = ys0 == ys0 ? ys0 : 0.0;
+  };
+  bucket_header();
+  float cmax[LTTB_K], cmin[LTTB_K];
+  constexpr int NW = (LTTB_K + 3) / 4;
+  unsigned bmx[NW], bmn[NW];  // 8-bit batch id per slope (4 per word), 0xff = none
+#pragma unroll
+  for (int w = 0; w < NW; w++) bmx[w] = bmn[w] = ~0u;
+  double py = 0.0;
+  int64_t tfirst = 0;
+#pragma unroll
+  for (int j = 0; j < LTTB_K; j++) { cmax[j] = -INFINITY; cmin[j] = INFINITY; }
+  int64_t c = p0;
+  for (int64_t t = 0; t < NBt; t++) {
+    R.wait();
+    const int64_t bs = (V0 + t * BV) * EPV, be = (V0 + (t + 1) * BV) * EPV;
+    bool done = false;
+    for (;;) {
+      const int64_t lo = cs > bs ? cs : bs, hi = ce < be ? ce : be;
+      if (lo < hi) {
+        float bm[LTTB_K], bn[LTTB_K];
+#pragma unroll
+        for (int j = 0; j < LTTB_K; j++) { bm[j] = -INFINITY; bn[j] = INFINITY; }
+        const int len = (int)(hi - lo);
+        const int rlb = (int)(bs - lo) + lane * EPV;  // lane's first element, relative to lo
+        const float dxl = __fadd_rn((float)(bs - s), (float)(lane * EPV));
+        if (bs >= lo && be <= hi) {  // whole batch inside the piece (warp-uniform)
+#pragma unroll
+          for (int u = 0; u < LTTB_PV; u++)
+            lttb_pv_fold<YDT, false>(R.get(t, u, lane), 0, 0, lttb_dx(dxl, u * 32 * EPV), yb, sl, bm, bn, py);
+        } else {
+#pragma unroll
+          for (int u = 0; u < LTTB_PV; u++) {
+            const int rl = rlb + u * 32 * EPV;
+            const float dxb = lttb_dx(dxl, u * 32 * EPV);
+            if (rl >= 0 && rl + EPV <= len) lttb_pv_fold<YDT, false>(R.get(t, u, lane), rl, len, dxb, yb, sl, bm, bn, py);
+            else if (rl < len && rl + EPV > 0) lttb_pv_fold<YDT, true>(R.get(t, u, lane), rl, len, dxb, yb, sl, bm, bn, py);
+          }
+        }
+        const unsigned bid4 = (unsigned)(t - tfirst) * 0x01010101u;
+#pragma unroll
+        for (int j = 0; j < LTTB_K; j++) {
+          const unsigned msk = 0xffu << (8 * (j & 3));
+          if (bm[j] > cmax[j]) bmx[j >> 2] = (bmx[j >> 2] & ~msk) | (bid4 & msk);
+          if (bn[j] < cmin[j]) bmn[j >> 2] = (bmn[j >> 2] & ~msk) | (bid4 & msk);
+          cmax[j] = fmaxf(cmax[j], bm[j]);
+          cmin[j] = fminf(cmin[j], bn[j]);
+        }
+      }
+      if (ce > be) break;  // piece continues in the next batch
+      // ---- piece c complete: sums, winners, locate, emit
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) py = __dadd_rn(py, __shfl_xor_sync(0xffffffffu, py, m));
+      float myW = 0.0f, mysl = 0.0f;
+      int myb = -1, mywl = 0;
+#pragma unroll
+      for (int q = 0; q < LTTB_NC; q++) {
+        const int j = q >> 1;
+        const bool mn = q & 1;
+        const float v = mn ? cmin[j] : cmax[j];
+        const unsigned bid = ((mn ? bmn[j >> 2] : bmx[j >> 2]) >> (8 * (j & 3))) & 0xffu;
+        const unsigned key = f32_key(v);
+        const unsigned W = mn ? __reduce_min_sync(0xffffffffu, key) : __reduce_max_sync(0xffffffffu, key);
+        const unsigned tie = (key == W && bid != 0xffu) ? (bid * 32u + (unsigned)lane) : 0xffffffffu;
+        const unsigned win = __reduce_min_sync(0xffffffffu, tie);
+        const float wv = __shfl_sync(0xffffffffu, v, (int)(win & 31u));
+        if (lane == q) {
+          myW = wv;
+          mysl = sl[j];
+          myb = win == 0xffffffffu ? -1 : (int)(win >> 5);
+          mywl = (int)(win & 31u);
+        }
+      }
+      int64_t found = -1;
+      if (lane < LTTB_NC && myb >= 0) {
+        const int64_t tb = tfirst + myb;
+        uint4 qv[LTTB_PV];
+#pragma unroll
+        for (int u = 0; u < LTTB_PV; u++) {
+          const int64_t v = V0 + tb * BV + u * 32 + mywl;
+          qv[u] = __ldg(yv + (v < V1 ? v : V1 - 1));
+        }
+        const int64_t tbs = (V0 + tb * BV) * EPV;
+        const float dxl = __fadd_rn((float)(tbs - s), (float)(mywl * EPV));
+#pragma unroll
+        for (int u = 0; u < LTTB_PV; u++) {
+          const int64_t i0 = tbs + (u * 32 + mywl) * EPV;
+          const float dxb = lttb_dx(dxl, u * 32 * EPV);
+#pragma unroll
+          for (int ee = 0; ee < EPV; ee++) {
+            const int64_t i = i0 + ee;
+            const double d = vget<YDT>(qv[u], ee);
+            const float vf = (i >= cs && i < ce) ? __double2float_rn(__dsub_rn(d, yb)) : __int_as_float(0x7fc00000);
+            const float tv = fmaf(-mysl, lttb_dxe(dxb, ee), vf);
+            if (found < 0 && tv == myW) found = i;
+          }
+        }
+      }
+      if (lane < LTTB_NC) {
+        part[c].v[lane] = myW;
+        part[c].i[lane] = found;
+      }
+      if (lane == 0) {
+        part[c].sx = 0.0;  // implicit x: the merge uses the closed form
+        part[c].sy = py;
+      }
+      // ---- next piece (may start inside this batch)
+      if (++c >= p1) { done = true; break; }
+      const int64_t kold = k;
+      lttb_piece_of(off, cstart, cb, c, k, s, e, cs, ce);
+      if (k != kold) bucket_header();
+#pragma unroll
+      for (int j = 0; j < LTTB_K; j++) { cmax[j] = -INFINITY; cmin[j] = INFINITY; }
+#pragma unroll
+      for (int w = 0; w < NW; w++) bmx[w] = bmn[w] = ~0u;
+      py = 0.0;
+      tfirst = t;
+    }
+    if (done) break;
+    R.fill(t + LTTB_D, lane);
+  }
+  R.drain();
+}
+
+// Prepass kernel: ring-streamed vector form when x is implicit and y is
+// 16-byte aligned, else the scalar form.
+template <int YDT>
+__global__ void __launch_bounds__(256, 2)
 lttb_chunk_prepass_kernel(const double* xin, const int* drop, const void* y, const int64_t* off,
                           const int64_t* cstart, const int32_t* cb, const int64_t* counts, const double2* slopes,
                           LttbChunkPart* part, int vec_ok) {
+  pdl_launch_dependents();
+  pdl_wait();
+  extern __shared__ uint4 lttb_ring[];
   const double* x = eff_x(xin, drop);
   if (x || !vec_ok) {
     lttb_prepass_scalar<YDT>(x, y, off, cstart, cb, counts, slopes, part);
     return;
   }
-  constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
-  constexpr int BV = 32 * LTTB_PV;  // vectors per warp batch
-  static_assert(LTTB_CH / (EPV * BV) <= 255, "batch ids must fit 8 bits");
-  const uint4* yv = (const uint4*)y;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t NCH = counts[1];
-  const int64_t p0 = NCH * gw / nw, p1 = NCH * (gw + 1) / nw;
-  int64_t kc = -1, s = 0, e = 0;
-  double yb = 0.0;
-  float sl[LTTB_K];
-#pragma unroll
-  for (int j = 0; j < LTTB_K; j++) sl[j] = 0.0f;
-  for (int64_t c = p0; c < p1; c++) {
-    const int64_t k = cb[c];
-    if (k != kc) {
-      kc = k;
-      s = __ldg(off + k);
-      e = __ldg(off + k + 1);
-      const double2 sr = slopes[k];
-#pragma unroll
-      for (int j = 0; j < LTTB_K; j++) sl[j] = (float)(sr.x + (sr.y - sr.x) * ((double)j / (double)(LTTB_K - 1)));
-      const double ys0 = yd<YDT>(y, s);
-      yb = ys0 == ys0 ? ys0 : 0.0;
-    }
-    int64_t cs, ce;
-    lttb_piece(s, e, c - cstart[k], cs, ce);
-    const int64_t v0 = cs / EPV;
-    const int nvec = (int)((ce + EPV - 1) / EPV - v0);
-    const int r0 = (int)(v0 * EPV - cs), len = (int)(ce - cs);  // r0 in (-EPV, 0]
-    const float base = (float)(cs - s);
-    const uint4* pv = yv + v0;
-    float cmax[LTTB_K], cmin[LTTB_K];
-    unsigned long long bmx = ~0ull, bmn = ~0ull;  // 8-bit batch id per slope, 0xff = none
-#pragma unroll
-    for (int j = 0; j < LTTB_K; j++) { cmax[j] = -INFINITY; cmin[j] = INFINITY; }
-    double py = 0.0;
-    const int nbat = (nvec + BV - 1) / BV;
-    for (int b = 0; b < nbat; b++) {
-      uint4 q[LTTB_PV];
-#pragma unroll
-      for (int u = 0; u < LTTB_PV; u++) {
-        const int rv = b * BV + u * 32 + lane;
-        q[u] = rv < nvec ? ldg_stream<false>(pv + rv) : make_uint4(0u, 0u, 0u, 0u);
-      }
-      float bm[LTTB_K], bn[LTTB_K];
-#pragma unroll
-      for (int j = 0; j < LTTB_K; j++) { bm[j] = -INFINITY; bn[j] = INFINITY; }
-#pragma unroll
-      for (int u = 0; u < LTTB_PV; u++) {
-        const int rv = b * BV + u * 32 + lane;
-        const int re0 = r0 + rv * EPV;
-        const float dxb = lttb_vx(base, re0);
-        if (re0 >= 0 && re0 + EPV <= len) lttb_pv_fold<YDT, false>(q[u], re0, len, dxb, yb, sl, bm, bn, py);
-        else if (rv < nvec) lttb_pv_fold<YDT, true>(q[u], re0, len, dxb, yb, sl, bm, bn, py);
-      }
-#pragma unroll
-      for (int j = 0; j < LTTB_K; j++) {
-        if (bm[j] > cmax[j]) { cmax[j] = bm[j]; bmx = (bmx & ~(0xffull << (8 * j))) | ((unsigned long long)b << (8 * j)); }
-        if (bn[j] < cmin[j]) { cmin[j] = bn[j]; bmn = (bmn & ~(0xffull << (8 * j))) | ((unsigned long long)b << (8 * j)); }
-      }
-    }
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) py = __dadd_rn(py, __shfl_xor_sync(0xffffffffu, py, m));
-    // winners: extreme value, then the lowest (batch, lane) holding it
-    float myW = 0.0f, mysl = 0.0f;
-    int myb = -1, mywl = 0;
-#pragma unroll
-    for (int t = 0; t < LTTB_NC; t++) {
-      const int j = t >> 1;
-      const bool mn = t & 1;
-      const float v = mn ? cmin[j] : cmax[j];
-      const unsigned bid = (unsigned)((mn ? bmn : bmx) >> (8 * j)) & 0xffu;
-      const unsigned key = f32_key(v);
-      const unsigned W = mn ? __reduce_min_sync(0xffffffffu, key) : __reduce_max_sync(0xffffffffu, key);
-      const unsigned tie = (key == W && bid != 0xffu) ? (bid * 32u + (unsigned)lane) : 0xffffffffu;
-      const unsigned win = __reduce_min_sync(0xffffffffu, tie);
-      const float wv = __shfl_sync(0xffffffffu, v, (int)(win & 31u));
-      if (lane == t) {
-        myW = wv;
-        mysl = sl[j];
-        myb = win == 0xffffffffu ? -1 : (int)(win >> 5);
-        mywl = (int)(win & 31u);
-      }
-    }
-    int64_t found = -1;
-    if (lane < LTTB_NC && myb >= 0) {
-      uint4 q[LTTB_PV];
-#pragma unroll
-      for (int u = 0; u < LTTB_PV; u++) {
-        const int rv = myb * BV + u * 32 + mywl;
-        q[u] = rv < nvec ? __ldg(pv + rv) : make_uint4(0u, 0u, 0u, 0u);
-      }
-#pragma unroll
-      for (int u = 0; u < LTTB_PV; u++) {
-        const int rv = myb * BV + u * 32 + mywl;
-        const int re0 = r0 + rv * EPV;
-        const float dxb = lttb_vx(base, re0);
-#pragma unroll
-        for (int ee = 0; ee < EPV; ee++) {
-          const double d = vget<YDT>(q[u], ee);
-          const bool ok = rv < nvec && (unsigned)(re0 + ee) < (unsigned)len;
-          const float vf = ok ? __double2float_rn(__dsub_rn(d, yb)) : __int_as_float(0x7fc00000);
-          const float t = fmaf(-mysl, __fadd_rn(dxb, (float)ee), vf);
-          if (found < 0 && t == myW) found = cs + re0 + ee;
-        }
-      }
-    }
-    if (lane < LTTB_NC) {
-      part[c].v[lane] = myW;
-      part[c].i[lane] = found;
-    }
-    if (lane == 0) {
-      part[c].sx = 0.0;  // implicit x: the merge uses the closed form
-      part[c].sy = py;
-    }
-  }
+  lttb_prepass_ring<YDT>(y, off, cstart, cb, counts[1], slopes, part, lttb_ring);
 }
 
 // warp per bucket: merge its chunk partials -> centroid (pairwise, chunk
@@ -466,6 +621,8 @@ lttb_chunk_prepass_kernel(const double* xin, const int* drop, const void* y, con
 template <int YDT>
 __global__ void lttb_chunk_merge_kernel(const double* xin, const int* drop, const int64_t* off, int64_t nb,
                                         const int64_t* cstart, const LttbChunkPart* part, double2* cent, int64_t* ext) {
+  pdl_launch_dependents();
+  pdl_wait();
   const double* x = eff_x(xin, drop);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -527,6 +684,8 @@ template <int YDT>
 __global__ void lttb_cand_table_kernel(const double* xin, const int* drop, const void* y, int64_t n,
                                        const int64_t* off, int64_t nb, const double2* cent, const int64_t* ext,
                                        const int32_t* nonempty, const int64_t* counts, uint8_t* T) {
+  pdl_launch_dependents();
+  pdl_wait();
   const double* x = eff_x(xin, drop);
   const int64_t L = counts[0];
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L * LTTB_NC;
@@ -552,6 +711,8 @@ __global__ void lttb_cand_table_kernel(const double* xin, const int* drop, const
 
 // warp per segment: compose the segment's tables (rows staged in smem)
 __global__ void __launch_bounds__(256) lttb_seg_compose_kernel(const uint8_t* T, const int64_t* counts, uint8_t* C) {
+  pdl_launch_dependents();
+  pdl_wait();
   __shared__ uint8_t rows[8][LTTB_SEG * LTTB_NC];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t L = counts[0];
@@ -575,6 +736,8 @@ __global__ void __launch_bounds__(256) lttb_seg_compose_kernel(const uint8_t* T,
 // one thread chains the segment entries (C staged in smem)
 __global__ void __launch_bounds__(1024) lttb_seg_entry_kernel(const uint8_t* T, const uint8_t* C, const int64_t* counts,
                                                               uint8_t* entry, int64_t cap) {
+  pdl_launch_dependents();
+  pdl_wait();
   extern __shared__ uint8_t sC[];
   const int64_t L = counts[0];
   const int64_t NS = (L + LTTB_SEG - 1) / LTTB_SEG;
@@ -595,6 +758,8 @@ __global__ void __launch_bounds__(1024) lttb_seg_entry_kernel(const uint8_t* T, 
 __global__ void __launch_bounds__(256) lttb_seg_expand_kernel(const uint8_t* T, const uint8_t* entry,
                                                                const int64_t* ext, const int32_t* nonempty,
                                                                const int64_t* counts, int64_t* picks) {
+  pdl_launch_dependents();
+  pdl_wait();
   __shared__ uint8_t rows[8][LTTB_SEG * LTTB_NC];
   __shared__ uint8_t cs[8][LTTB_SEG];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -658,19 +823,200 @@ __device__ __forceinline__ double lttb_varea(const uint4& q, int e, double dA, d
   return __dmul_rn(0.5, fabs(__dsub_rn(t1, t2)));
 }
 
-// Verification, round 1 (every bucket, predecessor = the guess): exact
-// first-max area per piece.  Vector form: persistent warps over contiguous
-// piece ranges, LTTB_PV 128-bit loads per lane in flight; per lane and
-// batch only the max AREA is folded, the first batch reaching a lane's max
-// is remembered, and the tying lanes re-read that batch to find their first
-// element (exact first-occurrence over the piece).  Scalar form: one CTA per
-// piece.  part[c] = (area, index) of piece c.
+// exact area partial of one piece, vector form (implicit x, aligned y): the
+// CTA's threads take 128-bit vectors, 8 loads in flight each; every thread
+// visits its elements in index order (strict > keeps the first max)
 template <int YDT>
-__global__ void __launch_bounds__(256, LTTB_VMINB)
+__device__ __forceinline__ AreaCand lttb_piece_area_vec(const void* y, int64_t cs, int64_t ce, int64_t prev,
+                                                        double ay, double K1, double K2, int tid, int nthr) {
+  constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
+  const int64_t v0 = cs / EPV;
+  const int nvec = (int)((ce + EPV - 1) / EPV - v0);
+  const int r0 = (int)(v0 * EPV - cs), len = (int)(ce - cs);
+  const double dA0 = (double)(prev - cs);
+  const uint4* pv = (const uint4*)y + v0;
+  AreaCand best{-1.0, IDX_NONE};
+  for (int rb = 0; rb < nvec; rb += 8 * nthr) {
+    uint4 q[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int rv = rb + tid + u * nthr;
+      q[u] = __ldg(pv + (rv < nvec ? rv : nvec - 1));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int rv = rb + tid + u * nthr;
+      const int re0 = r0 + rv * EPV;
+      const double dA = __dsub_rn(dA0, (double)re0);
+      if (rv < nvec) {
+#pragma unroll
+        for (int ee = 0; ee < EPV; ee++) {
+          const double a = lttb_varea<YDT>(q[u], ee, dA, ay, K1, K2);
+          if ((unsigned)(re0 + ee) < (unsigned)len && a > best.a) best = AreaCand{a, cs + re0 + ee};
+        }
+      }
+    }
+  }
+  return best;
+}
+
+// Settle bucket j once all its pieces have reported (called by the last
+// arriver, after a fence): merge the piece partials, store a changed pick
+// and list bucket j+1 (list `nxt`, length *cnt).
+__device__ __forceinline__ void lttb_settle_bucket(int64_t j, int64_t L, int64_t s, int64_t c0, int64_t nch,
+                                                   const LttbAreaPart* part, int64_t* picks, int32_t* nxt,
+                                                   int32_t* cnt) {
+  AreaCand best{-1.0, IDX_NONE};
+  for (int64_t q = 0; q < nch; q++) {
+    AreaCand a{__ldcg(&part[c0 + q].a), __ldcg(&part[c0 + q].i)};
+    if (area_better(a, best)) best = a;
+  }
+  const int64_t p = best.i == IDX_NONE ? s : best.i;
+  if (p != __ldcg(picks + j)) {
+    picks[j] = p;
+    if (j + 1 < L) nxt[atomicAdd(cnt, 1)] = (int32_t)(j + 1);
+  }
+}
+
+// Verification stream (vector form): like lttb_prepass_ring, per lane and
+// batch only the max AREA is folded and the first batch reaching a lane's
+// max is remembered; at the end of a piece the lanes holding the warp max in
+// the lowest such batch re-read it and the smallest index wins (exact
+// first occurrence over the piece).
+template <int YDT>
+__device__ __forceinline__ void lttb_verify_ring(const void* y, int64_t n, const int64_t* off, int64_t nb,
+                                                 const double2* cent, const int64_t* cstart, const int32_t* cb,
+                                                 const int32_t* rank, int64_t NCH, const int64_t* picks,
+                                                 LttbAreaPart* part, uint4* ring) {
+  constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
+  constexpr int BV = LTTB_BV;
+  const uint4* yv = (const uint4*)y;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t p0 = NCH * gw / nw, p1 = NCH * (gw + 1) / nw;
+  if (p0 >= p1) return;
+  int64_t k, s, e, cs, ce;
+  lttb_piece_of(off, cstart, cb, p1 - 1, k, s, e, cs, ce);
+  const int64_t V1 = (ce + EPV - 1) / EPV;
+  lttb_piece_of(off, cstart, cb, p0, k, s, e, cs, ce);
+  const int64_t V0 = cs / EPV;
+  const LttbRing R{yv, lttb_smem_u32(ring + (size_t)wl * LTTB_D * BV), V0, V1};
+  const int64_t NBt = (V1 - V0 + BV - 1) / BV;
+#pragma unroll
+  for (int t = 0; t < LTTB_D; t++) R.fill(t, lane);
+  int64_t prev = 0;
+  double ay = 0.0, K1 = 0.0, K2 = 0.0;
+  auto bucket_header = [&]() {
+    const int64_t j = rank[k];
+    prev = j == 0 ? 0 : __ldcg(picks + j - 1);
+    ay = yd<YDT>(y, prev);
+    double cx, cy;
+    centroid_for<YDT>(nullptr, y, off, nb, cent, k, n, cx, cy);
+    K1 = __dsub_rn((double)prev, cx);
+    K2 = __dsub_rn(cy, ay);
+  };
+  bucket_header();
+  double best = -1.0;
+  int bid = -1;
+  int64_t tfirst = 0;
+  int64_t c = p0;
+  for (int64_t t = 0; t < NBt; t++) {
+    R.wait();
+    const int64_t bs = (V0 + t * BV) * EPV, be = (V0 + (t + 1) * BV) * EPV;
+    bool done = false;
+    for (;;) {
+      const int64_t lo = cs > bs ? cs : bs, hi = ce < be ? ce : be;
+      if (lo < hi) {
+        double bm = -1.0;
+        const int len = (int)(hi - lo);
+        const int rlb = (int)(bs - lo) + lane * EPV;
+        const double dAl = (double)(prev - bs - lane * EPV);  // ax - x of the lane's first element (exact)
+        if (bs >= lo && be <= hi) {  // whole batch inside the piece (warp-uniform)
+#pragma unroll
+          for (int u = 0; u < LTTB_PV; u++) {
+            const uint4 q = R.get(t, u, lane);
+            const double dA = __dsub_rn(dAl, (double)(u * 32 * EPV));
+#pragma unroll
+            for (int ee = 0; ee < EPV; ee++) bm = fmax(bm, lttb_varea<YDT>(q, ee, dA, ay, K1, K2));
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < LTTB_PV; u++) {
+            const int rl = rlb + u * 32 * EPV;
+            const double dA = __dsub_rn(dAl, (double)(u * 32 * EPV));
+            if (rl < len && rl + EPV > 0) {
+              const uint4 q = R.get(t, u, lane);
+#pragma unroll
+              for (int ee = 0; ee < EPV; ee++)
+                if ((unsigned)(rl + ee) < (unsigned)len) bm = fmax(bm, lttb_varea<YDT>(q, ee, dA, ay, K1, K2));
+            }
+          }
+        }
+        if (bm > best) { best = bm; bid = (int)(t - tfirst); }
+      }
+      if (ce > be) break;
+      // ---- piece c complete: warp max, first element holding it
+      double W = best;
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) W = fmax(W, __shfl_xor_sync(0xffffffffu, W, m));
+      const unsigned tb = (best == W && bid >= 0) ? (unsigned)bid : 0xffffffffu;
+      const unsigned minb = __reduce_min_sync(0xffffffffu, tb);
+      int64_t found = IDX_NONE;
+      if (W > -1.0 && tb == minb) {
+        const int64_t tt = tfirst + minb;
+        uint4 qv[LTTB_PV];
+#pragma unroll
+        for (int u = 0; u < LTTB_PV; u++) {
+          const int64_t v = V0 + tt * BV + u * 32 + lane;
+          qv[u] = __ldg(yv + (v < V1 ? v : V1 - 1));
+        }
+#pragma unroll
+        for (int u = 0; u < LTTB_PV; u++) {
+          const int64_t i0 = (V0 + tt * BV + u * 32 + lane) * EPV;
+          const double dA = (double)(prev - i0);
+#pragma unroll
+          for (int ee = 0; ee < EPV; ee++)
+            if (found == IDX_NONE && i0 + ee >= cs && i0 + ee < ce &&
+                lttb_varea<YDT>(qv[u], ee, dA, ay, K1, K2) == W)
+              found = i0 + ee;
+        }
+      }
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) {
+        const int64_t o = __shfl_xor_sync(0xffffffffu, found, m);
+        found = o < found ? o : found;
+      }
+      if (lane == 0) {
+        part[c].a = found == IDX_NONE ? -1.0 : W;
+        part[c].i = found;
+      }
+      if (++c >= p1) { done = true; break; }
+      const int64_t kold = k;
+      lttb_piece_of(off, cstart, cb, c, k, s, e, cs, ce);
+      if (k != kold) bucket_header();
+      best = -1.0;
+      bid = -1;
+      tfirst = t;
+    }
+    if (done) break;
+    R.fill(t + LTTB_D, lane);
+  }
+  R.drain();
+}
+
+// Verification, round 1 (every bucket, predecessor = the guess): exact
+// first-max area per piece.  Vector form: lttb_verify_ring; scalar form
+// (explicit x / unaligned y): one CTA per piece.  part[c] = (area, index).
+template <int YDT>
+__global__ void __launch_bounds__(256, 2)
 lttb_chunk_verify_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off,
                          int64_t nb, const double2* cent, const int64_t* cstart, const int32_t* cb,
                          const int32_t* rank, const int64_t* counts, const int64_t* picks, LttbAreaPart* part,
                          int vec_ok) {
+  pdl_launch_dependents();
+  pdl_wait();
+  extern __shared__ uint4 lttb_ring[];
   const double* x = eff_x(xin, drop);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t NCH = counts[1];
@@ -682,7 +1028,7 @@ lttb_chunk_verify_kernel(const double* xin, const int* drop, const void* y, int6
       const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
       int64_t cs, ce;
       lttb_piece(s, e, c - cstart[k], cs, ce);
-      const int64_t prev = j == 0 ? 0 : picks[j - 1];
+      const int64_t prev = j == 0 ? 0 : __ldcg(picks + j - 1);
       double cx, cy;
       centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
       AreaCand best = lttb_piece_area_scalar<YDT>(x, y, cs, ce, xd(x, prev), yd<YDT>(y, prev), cx, cy, tid, 256);
@@ -700,105 +1046,16 @@ lttb_chunk_verify_kernel(const double* xin, const int* drop, const void* y, int6
     }
     return;
   }
-  constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
-  constexpr int BV = 32 * LTTB_PV;
-  const uint4* yv = (const uint4*)y;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t p0 = NCH * gw / nw, p1 = NCH * (gw + 1) / nw;
-  int64_t kc = -1, s = 0, e = 0, prev = 0;
-  double ay = 0.0, K1 = 0.0, K2 = 0.0;
-  for (int64_t c = p0; c < p1; c++) {
-    const int64_t k = cb[c];
-    if (k != kc) {
-      kc = k;
-      s = __ldg(off + k);
-      e = __ldg(off + k + 1);
-      const int64_t j = rank[k];
-      prev = j == 0 ? 0 : picks[j - 1];
-      ay = yd<YDT>(y, prev);
-      double cx, cy;
-      centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
-      K1 = __dsub_rn((double)prev, cx);
-      K2 = __dsub_rn(cy, ay);
-    }
-    int64_t cs, ce;
-    lttb_piece(s, e, c - cstart[k], cs, ce);
-    const int64_t v0 = cs / EPV;
-    const int nvec = (int)((ce + EPV - 1) / EPV - v0);
-    const int r0 = (int)(v0 * EPV - cs), len = (int)(ce - cs);
-    const double dA0 = (double)(prev - cs);  // ax - x at the piece start
-    const uint4* pv = yv + v0;
-    double best = -1.0;
-    int bid = -1;
-    const int nbat = (nvec + BV - 1) / BV;
-    for (int b = 0; b < nbat; b++) {
-      uint4 q[LTTB_PV];
-#pragma unroll
-      for (int u = 0; u < LTTB_PV; u++) {
-        const int rv = b * BV + u * 32 + lane;
-        q[u] = rv < nvec ? ldg_stream<false>(pv + rv) : make_uint4(0u, 0u, 0u, 0u);
-      }
-      double bm = -1.0;
-#pragma unroll
-      for (int u = 0; u < LTTB_PV; u++) {
-        const int rv = b * BV + u * 32 + lane;
-        const int re0 = r0 + rv * EPV;
-        const double dA = __dsub_rn(dA0, (double)re0);
-        if (re0 >= 0 && re0 + EPV <= len) {
-#pragma unroll
-          for (int ee = 0; ee < EPV; ee++) bm = fmax(bm, lttb_varea<YDT>(q[u], ee, dA, ay, K1, K2));
-        } else if (rv < nvec) {
-#pragma unroll
-          for (int ee = 0; ee < EPV; ee++)
-            if ((unsigned)(re0 + ee) < (unsigned)len) bm = fmax(bm, lttb_varea<YDT>(q[u], ee, dA, ay, K1, K2));
-        }
-      }
-      if (bm > best) { best = bm; bid = b; }
-    }
-    // max over the warp, then the first element holding it
-    double W = best;
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) W = fmax(W, __shfl_xor_sync(0xffffffffu, W, m));
-    const unsigned tb = (best == W && bid >= 0) ? (unsigned)bid : 0xffffffffu;
-    const unsigned minb = __reduce_min_sync(0xffffffffu, tb);
-    int64_t found = IDX_NONE;
-    if (W > -1.0 && tb == minb) {
-      uint4 q[LTTB_PV];
-#pragma unroll
-      for (int u = 0; u < LTTB_PV; u++) {
-        const int rv = (int)minb * BV + u * 32 + lane;
-        q[u] = rv < nvec ? __ldg(pv + rv) : make_uint4(0u, 0u, 0u, 0u);
-      }
-#pragma unroll
-      for (int u = 0; u < LTTB_PV; u++) {
-        const int rv = (int)minb * BV + u * 32 + lane;
-        const int re0 = r0 + rv * EPV;
-        const double dA = __dsub_rn(dA0, (double)re0);
-#pragma unroll
-        for (int ee = 0; ee < EPV; ee++)
-          if (found == IDX_NONE && rv < nvec && (unsigned)(re0 + ee) < (unsigned)len &&
-              lttb_varea<YDT>(q[u], ee, dA, ay, K1, K2) == W)
-            found = cs + re0 + ee;
-      }
-    }
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) {
-      const int64_t o = __shfl_xor_sync(0xffffffffu, found, m);
-      found = o < found ? o : found;
-    }
-    if (lane == 0) {
-      part[c].a = found == IDX_NONE ? -1.0 : W;
-      part[c].i = found;
-    }
-  }
+  lttb_verify_ring<YDT>(y, n, off, nb, cent, cstart, cb, rank, NCH, picks, part, lttb_ring);
 }
 
-// warp per bucket (round 1): merge piece partials; on change store the pick
-// and list bucket j+1 for re-verification
+// warp per bucket (round 1): merge piece partials, store a changed pick and
+// list bucket j+1
 __global__ void lttb_chunk_settle_kernel(const int64_t* off, const int64_t* cstart, const int32_t* nonempty,
                                          const int64_t* counts, const LttbAreaPart* part, int64_t* picks,
-                                         int32_t* next_list, int32_t* ndirty) {
+                                         int32_t* list, int32_t* lcount) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -814,27 +1071,33 @@ __global__ void lttb_chunk_settle_kernel(const int64_t* off, const int64_t* csta
     }
     best = warp_area_max(best);
     if (lane == 0) {
-      const int64_t p = best.i == IDX_NONE ? s : best.i;
-      if (p != picks[j]) {
-        picks[j] = p;
-        if (j + 1 < L) next_list[atomicAdd(ndirty, 1)] = (int32_t)(j + 1);
+      const int64_t pk = best.i == IDX_NONE ? s : best.i;
+      if (pk != picks[j]) {
+        picks[j] = pk;
+        if (j + 1 < L) list[atomicAdd(lcount, 1)] = (int32_t)(j + 1);
       }
     }
   }
 }
 
-// Fix-up rounds in one cooperative launch (no host round trips): each round
-// re-verifies the listed buckets (one CTA per (entry, piece), exact area
-// with the current predecessor), grid barrier, settles them (warp per
-// entry; a changed pick lists its successor), grid barrier.  Data written by
-// other CTAs (picks, partials, lists, counters) is read with ld.cg.
-// ctr[0], ctr[1]: list lengths (ping-pong), ctr[2]: rounds, ctr[3]: length
-// after round 1.
+// Fix-up rounds in one cooperative launch (no host round trips).  Round r
+// re-verifies the buckets listed by round r-1 (one CTA per (entry, piece),
+// exact area with the current predecessor); the CTA completing a bucket's
+// last piece settles it (arrival counters, fence) and lists its successor
+// if the pick changed; one grid barrier per round.  Round 1 is the
+// streaming verification (lttb_chunk_verify_kernel) and lists into
+// list_a / ctr[2].  Counters: ctr[r % 3] = length of the list round r reads;
+// ctr[3] = rounds, ctr[4] = list length after round 1.  A bucket read here
+// while its predecessor settles in the same round is listed again for the
+// next round, so the fixed point is exact.
 template <int YDT>
 __global__ void __launch_bounds__(256)
 lttb_fixup_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
                   const double2* cent, const int64_t* cstart, const int32_t* nonempty, const int64_t* counts,
-                  int64_t* picks, int32_t* list_a, int32_t* list_b, int32_t* ctr, LttbAreaPart* part) {
+                  int64_t* picks, int32_t* list_a, int32_t* list_b, int32_t* ctr, int32_t* arrive,
+                  LttbAreaPart* part, int vec_ok) {
+  pdl_launch_dependents();
+  pdl_wait();
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   const double* x = eff_x(xin, drop);
@@ -842,26 +1105,30 @@ lttb_fixup_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   __shared__ AreaCand sc[8];
   const int64_t L = counts[0];
   const int64_t maxch = counts[2] > 0 ? counts[2] : 1;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int ci = 0, round = 1;
-  if (blockIdx.x == 0 && tid == 0) ctr[3] = __ldcg(ctr);
-  for (;; round++) {
-    const int64_t count = __ldcg(ctr + ci);
-    if (count == 0 || round > nb + 2) break;
-    const int32_t* cur = ci ? list_b : list_a;
-    int32_t* nxt = ci ? list_a : list_b;
+  if (blockIdx.x == 0 && tid == 0) ctr[4] = __ldcg(ctr + 2);
+  int r = 2;
+  for (;; r++) {
+    const int64_t count = __ldcg(ctr + r % 3);
+    if (count == 0 || r > nb + 3) break;
+    const int32_t* cur = (r & 1) ? list_b : list_a;
+    int32_t* nxt = (r & 1) ? list_a : list_b;
+    if (blockIdx.x == 0 && tid == 0) ctr[(r + 2) % 3] = 0;
     for (int64_t t = blockIdx.x; t < count * maxch; t += gridDim.x) {
       const int64_t j = __ldcg(cur + t / maxch), q = t % maxch;
       const int64_t k = nonempty[j];
       const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-      if (q >= lttb_npieces(s, e)) continue;  // block-uniform
+      const int64_t nch = lttb_npieces(s, e);
+      if (q >= nch) continue;  // block-uniform
       int64_t cs, ce;
       lttb_piece(s, e, q, cs, ce);
       const int64_t prev = j == 0 ? 0 : __ldcg(picks + j - 1);
       double cx, cy;
       centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
-      AreaCand best = lttb_piece_area_scalar<YDT>(x, y, cs, ce, xd(x, prev), yd<YDT>(y, prev), cx, cy, tid, 256);
+      const double ay = yd<YDT>(y, prev);
+      AreaCand best = (x || !vec_ok)
+                          ? lttb_piece_area_scalar<YDT>(x, y, cs, ce, xd(x, prev), ay, cx, cy, tid, 256)
+                          : lttb_piece_area_vec<YDT>(y, cs, ce, prev, ay, __dsub_rn((double)prev, cx),
+                                                     __dsub_rn(cy, ay), tid, 256);
       best = warp_area_max(best);
       if (lane == 0) sc[wid] = best;
       __syncthreads();
@@ -869,41 +1136,27 @@ lttb_fixup_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
         AreaCand b = sc[0];
         for (int w = 1; w < 8; w++)
           if (area_better(sc[w], b)) b = sc[w];
-        part[cstart[k] + q].a = b.a;
-        part[cstart[k] + q].i = b.i;
+        const int64_t c0 = cstart[k];
+        part[c0 + q].a = b.a;
+        part[c0 + q].i = b.i;
+        __threadfence();
+        if ((atomicAdd(arrive + j, 1) + 1) % nch == 0) {
+          __threadfence();
+          lttb_settle_bucket(j, L, s, c0, nch, part, picks, nxt, ctr + (r + 1) % 3);
+        }
       }
       __syncthreads();
     }
-    if (blockIdx.x == 0 && tid == 0) ctr[1 - ci] = 0;
     grid.sync();
-    for (int64_t t = gw; t < count; t += nw) {
-      const int64_t j = __ldcg(cur + t);
-      const int64_t k = nonempty[j];
-      const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-      const int64_t c0 = cstart[k], nch = lttb_npieces(s, e);
-      AreaCand best{-1.0, IDX_NONE};
-      for (int64_t q = lane; q < nch; q += 32) {
-        AreaCand a{__ldcg(&part[c0 + q].a), __ldcg(&part[c0 + q].i)};
-        if (area_better(a, best)) best = a;
-      }
-      best = warp_area_max(best);
-      if (lane == 0) {
-        const int64_t p = best.i == IDX_NONE ? s : best.i;
-        if (p != __ldcg(picks + j)) {
-          picks[j] = p;
-          if (j + 1 < L) nxt[atomicAdd(ctr + 1 - ci, 1)] = (int32_t)(j + 1);
-        }
-      }
-    }
-    grid.sync();
-    ci = 1 - ci;
   }
-  if (blockIdx.x == 0 && tid == 0) ctr[2] = round;
+  if (blockIdx.x == 0 && tid == 0) ctr[3] = r - 1;
 }
 
 // out = [0, picks..., n-1] (+ count at out[-1]); optional index map
 __global__ void lttb_emit_kernel(const int64_t* picks, const int64_t* counts, int64_t n, const int64_t* map,
                                  int64_t* out, int64_t* m_out) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t L = counts[0];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L + 2; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t p = i == 0 ? 0 : (i == L + 1 ? n - 1 : picks[i - 1]);

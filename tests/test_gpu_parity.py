@@ -206,3 +206,34 @@ def test_lttb_large_bucket_modes(ts, oracle):
             assert 1 <= rounds <= 64
     finally:
         L.tsds_set_option(b"lttb_exact", 0)
+
+
+@pytest.mark.gpu
+def test_lttb_large_vector_paths(ts, oracle):
+    """Large-bucket LTTB through the 128-bit vector paths for every value
+    width, with exact ties (u8), NaNs, many buckets (multi-block layout scan)
+    and a misaligned device input (scalar fallback)."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    base = np.cumsum(rng.laplace(size=600_000))
+    withnan = base.copy()
+    withnan[rng.integers(0, base.size, 64)] = np.nan
+    cases = [
+        base,
+        withnan,
+        base.astype(np.float32),
+        base.astype(np.float16),
+        (base * 50).astype(np.int64),
+        np.clip(base * 3, -32768, 32767).astype(np.int16),
+        (np.abs(base) % 250).astype(np.uint8),
+        (np.abs(base) * 7).astype(np.uint32),
+    ]
+    for y in cases:
+        for n_out in (300, 15_000):  # avg bucket 2000 and 40: both on the large path
+            got = ts.downsample("lttb", y, n_out=n_out)
+            assert got.tolist() == oracle.downsample("lttb", y, n_out=n_out).tolist(), (y.dtype, n_out)
+    big = np.cumsum(rng.laplace(size=2_500_000))
+    assert ts.downsample("lttb", big, n_out=60_000).tolist() == oracle.downsample("lttb", big, n_out=60_000).tolist()
+    yd = torch.from_numpy(base).cuda()[1:]
+    assert ts.downsample("lttb", yd, n_out=1000).tolist() == oracle.downsample("lttb", base[1:], n_out=1000).tolist()

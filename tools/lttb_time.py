@@ -25,6 +25,25 @@ def timeit(fn, reps=5):
     return min(ts_) * 1e3, r
 
 
+def gpu_span(fn, reps=5):
+    """Device time of the large-bucket LTTB sequence (library profile events)."""
+    import ctypes
+
+    from paper_2307_05389_b200 import _lib
+
+    L, h = _lib.load(), _lib.context().handle
+    best = 1e9
+    for _ in range(reps):
+        L.tsds_ctx_profile(h, 1)
+        fn()
+        tot, cnt = ctypes.c_double(0), ctypes.c_int64(0)
+        L.tsds_ctx_profile_read(h, ctypes.byref(tot), ctypes.byref(cnt))
+        L.tsds_ctx_profile(h, 0)
+        if cnt.value:
+            best = min(best, tot.value)
+    return best
+
+
 def main():
     which = sys.argv[1:] or ["c3", "c4"]
     if "c3" in which:
@@ -35,6 +54,7 @@ def main():
             ms, r = timeit(lambda: ts.downsample("lttb", yd, n_out=n_out))
             from paper_2307_05389_b200 import _lib
             st = {k: _lib.load().tsds_ctx_stat(_lib.context().handle, k.encode()) for k in ("lttb_rounds", "lttb_dirty1")}
+            st["gpu_ms"] = round(gpu_span(lambda: ts.downsample("lttb", yd, n_out=n_out)), 3)
             g = np.load(os.path.join(ROOT, "tests", "golden", "configs.npz"))
             ok = np.array_equal(r, g[f"c3_lttb_{n_out}"]) if n == W.C3_N else None
             print(f"c3 lttb n_out={n_out}: {ms:.3f} ms  ({y.nbytes/ms/1e6:.0f} GB/s)  m={len(r)} {st} parity={ok}")
