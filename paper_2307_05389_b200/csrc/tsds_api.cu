@@ -63,6 +63,8 @@ struct tsds_ctx {
   DevBuf y, x, xf64, part, bincnt, res, off, out, misc, cent, scratch, y2, x2, x2f64, full, out2, rctr, lscr;
   int64_t lttb_rounds = 0;  // verification rounds of the last large-bucket LTTB
   int64_t lttb_dirty1 = 0;  // buckets whose guess was wrong in the first round
+  int64_t lttb_pieces = 0;  // pieces evaluated exactly (all rounds, after pruning)
+  int64_t lttb_pieces1 = 0; // ... in round 1
   int32_t* h_lstat = nullptr;  // pinned {rounds, dirty1} of the last large-bucket LTTB
   bool lstat_pending = false;
   void* h_pin = nullptr;
@@ -552,7 +554,7 @@ int run_lttb_walk_small(tsds_ctx* ctx, const double* xf, const int* drop, const 
                         const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev, bool have_cent = false);
 
 int ensure_lstat(tsds_ctx* ctx) {
-  if (!ctx->h_lstat) CUDA_TRY(cudaMallocHost(&ctx->h_lstat, 16));
+  if (!ctx->h_lstat) CUDA_TRY(cudaMallocHost(&ctx->h_lstat, 128));
   return TSDS_OK;
 }
 
@@ -580,6 +582,25 @@ int launch_pdl(tsds_ctx* ctx, void (*k)(KP...), unsigned grid, unsigned block, s
   cfg.stream = ctx->stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, k, ((KP)args)...));
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
+// cooperative launch (grid-wide barriers), also PDL-chained to its predecessor
+template <typename... KP, typename... A>
+int launch_coop(tsds_ctx* ctx, void (*k)(KP...), unsigned grid, unsigned block, A... args) {
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(std::max(grid, 1u));
+  cfg.blockDim = dim3(block);
+  cfg.stream = ctx->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
   CUDA_TRY(cudaLaunchKernelEx(&cfg, k, ((KP)args)...));
   LAUNCH_CHECK();
   return TSDS_OK;
@@ -620,18 +641,17 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   const int64_t maxseg = nb / LTTB_SEG + 2;
   const int64_t nlb = (nb + LTTB_LB - 1) / LTTB_LB;
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-  const size_t zero_bytes = al(64) + al(64) + al(4 * nb) + al(24 * (nlb + 1));  // counts, ctr, arrive, link
+  const size_t zero_bytes = al(64) + al(64) + al(24 * (nlb + 1)) + al(4 * nb);  // counts, ctr, link, lock
   const size_t need = zero_bytes + al(8 * (nb + 1)) + al(4 * maxch) + al(4 * nb) + al(4 * nb) + al(32 * nb) +
                       al(16 * nb) + al(sizeof(LttbChunkPart) * maxch) + al(8 * NC * nb) + al(NC * nb) +
-                      al(NC * maxseg) + al(maxseg) + al(8 * (nb + 4)) + al(4 * nb) * 2 +
-                      al(sizeof(LttbAreaPart) * maxch);
+                      al(NC * maxseg) + al(maxseg) + al(8 * (nb + 4)) + al(4 * nb);
   RC_TRY(ensure(ctx, ctx->lscr, need));
   char* p = (char*)ctx->lscr.p;
   auto take = [&](size_t bytes) { char* r = p; p += al(bytes); return r; };
-  int64_t* counts = (int64_t*)take(64);  // zeroed block: counts, ctr, arrive, link
+  int64_t* counts = (int64_t*)take(64);  // zeroed block: counts, ctr, link, lock
   int32_t* ctr = (int32_t*)take(64);
-  int32_t* arrive = (int32_t*)take(4 * nb);
   unsigned long long* link = (unsigned long long*)take(24 * (nlb + 1));
+  int32_t* lock = (int32_t*)take(4 * nb);
   int64_t* cstart = (int64_t*)take(8 * (nb + 1));
   int32_t* cb = (int32_t*)take(4 * maxch);
   int32_t* rank = (int32_t*)take(4 * nb);
@@ -645,8 +665,6 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   uint8_t* entry = (uint8_t*)take(maxseg);
   int64_t* walkout = (int64_t*)take(8 * (nb + 4));
   int32_t* list_a = (int32_t*)take(4 * nb);
-  int32_t* list_b = (int32_t*)take(4 * nb);
-  LttbAreaPart* apart = (LttbAreaPart*)take(sizeof(LttbAreaPart) * maxch);
   int64_t* picks = walkout + 2;
   const int mode = lttb_exact_mode();
   const int64_t avg = (n - 2) / std::max<int64_t>(nb, 1);
@@ -682,30 +700,23 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   RC_TRY(launch_pdl(ctx, lttb_seg_entry_kernel, 1, 1024, (size_t)(std::min<int64_t>(NS * NC, cap) + 16), T, C, counts,
                     entry, cap));
   RC_TRY(launch_pdl(ctx, lttb_seg_expand_kernel, gs, 256, 0, T, entry, ext, nonempty, counts, picks));
-  // ---- verify every bucket once (round 1), then the fix-up rounds on a work
-  //      list of buckets whose predecessor changed
-  int32_t* lcount = ctr + 2;  // round 1 lists into list_a / ctr[2]
-  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_chunk_verify_kernel<YD>,
-                                    one_wave(ctx, lttb_chunk_verify_kernel<YD>, 256, LTTB_RING_BYTES), 256,
-                                    LTTB_RING_BYTES, xf, drop, y, n, off, nb, cent, cstart, cb, rank, counts, picks,
-                                    apart, vec_ok)));
-  RC_TRY(launch_pdl(ctx, lttb_chunk_settle_kernel, cap_grid((nb + 7) / 8, (int64_t)ctx->sms * 8), 256, 0, off, cstart,
-                    nonempty, counts, apart, picks, list_a, lcount));
-  YDT_SWITCH(ydt, ({
-               const void* fx = (const void*)lttb_fixup_kernel<YD>;
-               const unsigned gf = one_wave(ctx, lttb_fixup_kernel<YD>, 256);
-               void* args[] = {(void*)&xf,     (void*)&drop,  (void*)&y,      (void*)&n,      (void*)&off,
-                               (void*)&nb,     (void*)&cent,  (void*)&cstart, (void*)&nonempty,
-                               (void*)&counts, (void*)&picks, (void*)&list_a, (void*)&list_b, (void*)&ctr,
-                               (void*)&arrive, (void*)&apart, (void*)&vec_ok};
-               CUDA_TRY(cudaLaunchCooperativeKernel(fx, dim3(gf), dim3(256), args, 0, ctx->stream));
-             }));
-  LAUNCH_CHECK();
-  RC_TRY(launch_pdl(ctx, lttb_emit_kernel, cap_grid((nb + 257) / 256, 1024), 256, 0, picks, counts, n, map,
-                    out_dev + 1, out_dev));
+  // ---- resolve: round 1 (every bucket, guessed predecessors, pruned exact
+  //      evaluation), then correction chains from the buckets whose
+  //      predecessor changed, then the output
+  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_round1_kernel<YD>, one_wave(ctx, lttb_round1_kernel<YD>, 256), 256, 0,
+                                    xf, drop, y, n, off, nb, (const double2*)cent, (const double2*)slopes,
+                                    (const int64_t*)cstart, (const int32_t*)nonempty, (const int64_t*)counts,
+                                    (const LttbChunkPart*)cpart, (const int64_t*)ext, picks, list_a, ctr, vec_ok)));
+  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_chain_kernel<YD>, one_wave(ctx, lttb_chain_kernel<YD>, 256), 256, 0,
+                                    xf, drop, y, n, off, nb, (const double2*)cent, (const double2*)slopes,
+                                    (const int64_t*)cstart, (const int32_t*)nonempty, (const int64_t*)counts,
+                                    (const LttbChunkPart*)cpart, (const int64_t*)ext, picks, (const int32_t*)list_a,
+                                    lock, ctr, vec_ok)));
+  RC_TRY(launch_pdl(ctx, lttb_emit_kernel, cap_grid((nb + 257) / 256, 1024), 256, 0, (const int64_t*)picks,
+                    (const int64_t*)counts, n, map, out_dev + 1, out_dev));
   RC_TRY(prof_mark(ctx, ev, true));
   RC_TRY(ensure_lstat(ctx));
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_lstat, ctr + 3, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_lstat, ctr, 10 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->lstat_pending = true;
   return TSDS_OK;
 }
@@ -1020,17 +1031,22 @@ int64_t tsds_ctx_stat(tsds_ctx* ctx, const char* name) {
   if (!ctx || !name) return -1;
   std::string n(name);
   if (n == "launches") return ctx->launches;
-  if (ctx->lstat_pending && (n == "lttb_rounds" || n == "lttb_dirty1")) {
+  const bool lt = n == "lttb_rounds" || n == "lttb_dirty1" || n == "lttb_pieces" || n == "lttb_pieces1";
+  if (ctx->lstat_pending && lt) {
     std::lock_guard<std::mutex> lk(ctx->mu);
     cudaSetDevice(ctx->device);
     if (cudaStreamSynchronize(ctx->stream) == cudaSuccess) {
-      ctx->lttb_rounds = ctx->h_lstat[0];
-      ctx->lttb_dirty1 = ctx->h_lstat[1];
+      ctx->lttb_rounds = ctx->h_lstat[3];   // correction-chain steps
+      ctx->lttb_dirty1 = ctx->h_lstat[2];   // |D|: buckets whose predecessor changed in round 1
+      ctx->lttb_pieces = ctx->h_lstat[8];   // pieces evaluated in the chains
+      ctx->lttb_pieces1 = ctx->h_lstat[9];  // pieces evaluated in round 1
     }
     ctx->lstat_pending = false;
   }
   if (n == "lttb_rounds") return ctx->lttb_rounds;
   if (n == "lttb_dirty1") return ctx->lttb_dirty1;
+  if (n == "lttb_pieces") return ctx->lttb_pieces;    // pieces evaluated exactly, all rounds
+  if (n == "lttb_pieces1") return ctx->lttb_pieces1;  // pieces evaluated exactly in round 1
   return -1;
 }
 

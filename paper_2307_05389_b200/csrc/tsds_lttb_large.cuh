@@ -35,6 +35,9 @@ constexpr int LTTB_NC = 2 * LTTB_K;  // candidates per bucket (argmax + argmin p
 #endif
 constexpr int64_t LTTB_CH = LTTB_CH_N;  // points per chunk
 constexpr int LTTB_SEG = 64;         // buckets per composed segment
+#ifndef LTTB_R1_U
+#define LTTB_R1_U 16
+#endif
 
 // Pieces: the series is cut into globally aligned chunks of LTTB_CH points;
 // piece q of bucket [s, e) is its intersection with chunk s/LTTB_CH + q
@@ -48,16 +51,17 @@ __device__ __forceinline__ void lttb_piece(int64_t s, int64_t e, int64_t q, int6
   ce = (g + 1) * LTTB_CH < e ? (g + 1) * LTTB_CH : e;
 }
 
+// slope j of bucket k's steering grid (prepass and pruning bounds)
+__device__ __forceinline__ float lttb_slope(double2 sr, int j) {
+  return __double2float_rn(__dadd_rn(sr.x, __dmul_rn(__dsub_rn(sr.y, sr.x), __ddiv_rn((double)j, (double)(LTTB_K - 1)))));
+}
+
 struct LttbChunkPart {  // per-chunk partial of the prepass
   float v[LTTB_NC];
   int64_t i[LTTB_NC];
   double sx, sy;
 };
 
-struct LttbAreaPart {  // per-chunk partial of the verification
-  double a;
-  int64_t i;
-};
 
 // piece layout + non-empty bucket list, one pass (chained scan): block t
 // (ticket order) takes LTTB_LB buckets, scans them, waits for block t-1's
@@ -250,7 +254,7 @@ __device__ __forceinline__ void lttb_prepass_scalar(const double* x, const void*
     const double2 sr = slopes[k];
     float sl[LTTB_K];
 #pragma unroll
-    for (int j = 0; j < LTTB_K; j++) sl[j] = (float)(sr.x + (sr.y - sr.x) * ((double)j / (double)(LTTB_K - 1)));
+    for (int j = 0; j < LTTB_K; j++) sl[j] = lttb_slope(sr, j);
     const double xs = xd(x, s), ys0 = yd<YDT>(y, s);
     const double yb = ys0 == ys0 ? ys0 : 0.0;
     float cmax[LTTB_K], cmin[LTTB_K];
@@ -472,7 +476,7 @@ __device__ __forceinline__ void lttb_prepass_ring(const void* y, const int64_t* 
   auto bucket_header = [&]() {
     const double2 sr = slopes[k];
 #pragma unroll
-    for (int j = 0; j < LTTB_K; j++) sl[j] = (float)(sr.x + (sr.y - sr.x) * ((double)j / (double)(LTTB_K - 1)));
+    for (int j = 0; j < LTTB_K; j++) sl[j] = lttb_slope(sr, j);
     const double ys0 = yd<YDT>(y, s);
     yb = ys0 == ys0 ? ys0 : 0.0;
   };
@@ -824,9 +828,9 @@ __device__ __forceinline__ double lttb_varea(const uint4& q, int e, double dA, d
 }
 
 // exact area partial of one piece, vector form (implicit x, aligned y): the
-// CTA's threads take 128-bit vectors, 8 loads in flight each; every thread
+// threads take 128-bit vectors, U loads in flight each; every thread
 // visits its elements in index order (strict > keeps the first max)
-template <int YDT>
+template <int YDT, int U = 8>
 __device__ __forceinline__ AreaCand lttb_piece_area_vec(const void* y, int64_t cs, int64_t ce, int64_t prev,
                                                         double ay, double K1, double K2, int tid, int nthr) {
   constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
@@ -836,15 +840,15 @@ __device__ __forceinline__ AreaCand lttb_piece_area_vec(const void* y, int64_t c
   const double dA0 = (double)(prev - cs);
   const uint4* pv = (const uint4*)y + v0;
   AreaCand best{-1.0, IDX_NONE};
-  for (int rb = 0; rb < nvec; rb += 8 * nthr) {
-    uint4 q[8];
+  for (int rb = 0; rb < nvec; rb += U * nthr) {
+    uint4 q[U];
 #pragma unroll
-    for (int u = 0; u < 8; u++) {
+    for (int u = 0; u < U; u++) {
       const int rv = rb + tid + u * nthr;
       q[u] = __ldg(pv + (rv < nvec ? rv : nvec - 1));
     }
 #pragma unroll
-    for (int u = 0; u < 8; u++) {
+    for (int u = 0; u < U; u++) {
       const int rv = rb + tid + u * nthr;
       const int re0 = r0 + rv * EPV;
       const double dA = __dsub_rn(dA0, (double)re0);
@@ -860,296 +864,286 @@ __device__ __forceinline__ AreaCand lttb_piece_area_vec(const void* y, int64_t c
   return best;
 }
 
-// Settle bucket j once all its pieces have reported (called by the last
-// arriver, after a fence): merge the piece partials, store a changed pick
-// and list bucket j+1 (list `nxt`, length *cnt).
-__device__ __forceinline__ void lttb_settle_bucket(int64_t j, int64_t L, int64_t s, int64_t c0, int64_t nch,
-                                                   const LttbAreaPart* part, int64_t* picks, int32_t* nxt,
-                                                   int32_t* cnt) {
-  AreaCand best{-1.0, IDX_NONE};
-  for (int64_t q = 0; q < nch; q++) {
-    AreaCand a{__ldcg(&part[c0 + q].a), __ldcg(&part[c0 + q].i)};
-    if (area_better(a, best)) best = a;
-  }
-  const int64_t p = best.i == IDX_NONE ? s : best.i;
-  if (p != __ldcg(picks + j)) {
-    picks[j] = p;
-    if (j + 1 < L) nxt[atomicAdd(cnt, 1)] = (int32_t)(j + 1);
-  }
-}
+// ---------------------------------------------------------------------------
+// Resolution: guess -> exact fixed point, with per-piece pruning.
+//
+// For bucket j with predecessor p (ax = p, ay = y[p]) and c = centroid of
+// the next bucket, the reference area of point i is
+//   A_i = 0.5*|K1*(y_i - ay) - (ax - i)*K2|,  K1 = ax - cx, K2 = cy - ay
+//       = 0.5*|K1*u_i + G|,  u_i = (y_i - yb) - sig*(i - s),  sig = -K2/K1,
+//   G = K1*(yb - ay) - (ax - s)*K2   (yb, s: the bucket's steering origin).
+// The prepass stored, per piece and steering slope s_j, the max M_j and min
+// m_j of t_j(i) ~ (y_i - yb) - s_j*(i - s) (fp32).  Since
+//   u_i = t_j(i) + (s_j - sig)*(i - s) +- E_j,
+// and max_i (y_i - yb - s*(i - s)) is convex in s (the min concave), u over
+// the piece lies in [U_lo, U_hi] (shifted single-slope bounds, and the chord
+// between the two grid slopes around sig), so
+//   max_i A_i <= 0.5*max(|K1*U_hi + G|, |K1*U_lo + G|) + slack.
+// E_j and slack over-estimate the fp32 / f64 rounding by x16 or more.  A
+// piece whose bound is below the best exact area among the bucket's
+// candidates cannot hold the first max, so only the remaining pieces are
+// evaluated exactly; the answer is the first max over candidates + unpruned
+// pieces (area desc, index asc).  Implicit x only; with explicit x every
+// piece is evaluated.
 
-// Verification stream (vector form): like lttb_prepass_ring, per lane and
-// batch only the max AREA is folded and the first batch reaching a lane's
-// max is remembered; at the end of a piece the lanes holding the warp max in
-// the lowest such batch re-read it and the smallest index wins (exact
-// first occurrence over the piece).
-template <int YDT>
-__device__ __forceinline__ void lttb_verify_ring(const void* y, int64_t n, const int64_t* off, int64_t nb,
-                                                 const double2* cent, const int64_t* cstart, const int32_t* cb,
-                                                 const int32_t* rank, int64_t NCH, const int64_t* picks,
-                                                 LttbAreaPart* part, uint4* ring) {
-  constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
-  constexpr int BV = LTTB_BV;
-  const uint4* yv = (const uint4*)y;
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t p0 = NCH * gw / nw, p1 = NCH * (gw + 1) / nw;
-  if (p0 >= p1) return;
-  int64_t k, s, e, cs, ce;
-  lttb_piece_of(off, cstart, cb, p1 - 1, k, s, e, cs, ce);
-  const int64_t V1 = (ce + EPV - 1) / EPV;
-  lttb_piece_of(off, cstart, cb, p0, k, s, e, cs, ce);
-  const int64_t V0 = cs / EPV;
-  const LttbRing R{yv, lttb_smem_u32(ring + (size_t)wl * LTTB_D * BV), V0, V1};
-  const int64_t NBt = (V1 - V0 + BV - 1) / BV;
+struct LttbPlan {  // constants of bucket j for one predecessor
+  int64_t prev;
+  double ay, K1, K2, sig;  // sig = -K2/K1 (steering slope of the area)
+};
+
+// upper bound of the reference area over piece [cs, ce) of bucket [s, e)
+__device__ __forceinline__ double lttb_piece_bound(const LttbChunkPart& P, double2 sr, int64_t s, int64_t cs,
+                                                   int64_t ce, double yb, double ax, double ay, double K1,
+                                                   double K2, double sig) {
+  if (!(K1 < 0.0) && !(K1 > 0.0)) return INFINITY;
+  const double dlo = (double)(cs - s), dhi = (double)(ce - 1 - s);
+  const double G = K1 * (yb - ay) - (ax - (double)s) * K2;
+  double uhi = INFINITY, ulo = -INFINITY;
+  double pM = 0.0, pm = 0.0, pE = 0.0, ps = 0.0;
 #pragma unroll
-  for (int t = 0; t < LTTB_D; t++) R.fill(t, lane);
-  int64_t prev = 0;
-  double ay = 0.0, K1 = 0.0, K2 = 0.0;
-  auto bucket_header = [&]() {
-    const int64_t j = rank[k];
-    prev = j == 0 ? 0 : __ldcg(picks + j - 1);
-    ay = yd<YDT>(y, prev);
-    double cx, cy;
-    centroid_for<YDT>(nullptr, y, off, nb, cent, k, n, cx, cy);
-    K1 = __dsub_rn((double)prev, cx);
-    K2 = __dsub_rn(cy, ay);
-  };
-  bucket_header();
-  double best = -1.0;
-  int bid = -1;
-  int64_t tfirst = 0;
-  int64_t c = p0;
-  for (int64_t t = 0; t < NBt; t++) {
-    R.wait();
-    const int64_t bs = (V0 + t * BV) * EPV, be = (V0 + (t + 1) * BV) * EPV;
-    bool done = false;
-    for (;;) {
-      const int64_t lo = cs > bs ? cs : bs, hi = ce < be ? ce : be;
-      if (lo < hi) {
-        double bm = -1.0;
-        const int len = (int)(hi - lo);
-        const int rlb = (int)(bs - lo) + lane * EPV;
-        const double dAl = (double)(prev - bs - lane * EPV);  // ax - x of the lane's first element (exact)
-        if (bs >= lo && be <= hi) {  // whole batch inside the piece (warp-uniform)
-#pragma unroll
-          for (int u = 0; u < LTTB_PV; u++) {
-            const uint4 q = R.get(t, u, lane);
-            const double dA = __dsub_rn(dAl, (double)(u * 32 * EPV));
-#pragma unroll
-            for (int ee = 0; ee < EPV; ee++) bm = fmax(bm, lttb_varea<YDT>(q, ee, dA, ay, K1, K2));
-          }
-        } else {
-#pragma unroll
-          for (int u = 0; u < LTTB_PV; u++) {
-            const int rl = rlb + u * 32 * EPV;
-            const double dA = __dsub_rn(dAl, (double)(u * 32 * EPV));
-            if (rl < len && rl + EPV > 0) {
-              const uint4 q = R.get(t, u, lane);
-#pragma unroll
-              for (int ee = 0; ee < EPV; ee++)
-                if ((unsigned)(rl + ee) < (unsigned)len) bm = fmax(bm, lttb_varea<YDT>(q, ee, dA, ay, K1, K2));
-            }
-          }
-        }
-        if (bm > best) { best = bm; bid = (int)(t - tfirst); }
-      }
-      if (ce > be) break;
-      // ---- piece c complete: warp max, first element holding it
-      double W = best;
-#pragma unroll
-      for (int m = 16; m >= 1; m >>= 1) W = fmax(W, __shfl_xor_sync(0xffffffffu, W, m));
-      const unsigned tb = (best == W && bid >= 0) ? (unsigned)bid : 0xffffffffu;
-      const unsigned minb = __reduce_min_sync(0xffffffffu, tb);
-      int64_t found = IDX_NONE;
-      if (W > -1.0 && tb == minb) {
-        const int64_t tt = tfirst + minb;
-        uint4 qv[LTTB_PV];
-#pragma unroll
-        for (int u = 0; u < LTTB_PV; u++) {
-          const int64_t v = V0 + tt * BV + u * 32 + lane;
-          qv[u] = __ldg(yv + (v < V1 ? v : V1 - 1));
-        }
-#pragma unroll
-        for (int u = 0; u < LTTB_PV; u++) {
-          const int64_t i0 = (V0 + tt * BV + u * 32 + lane) * EPV;
-          const double dA = (double)(prev - i0);
-#pragma unroll
-          for (int ee = 0; ee < EPV; ee++)
-            if (found == IDX_NONE && i0 + ee >= cs && i0 + ee < ce &&
-                lttb_varea<YDT>(qv[u], ee, dA, ay, K1, K2) == W)
-              found = i0 + ee;
-        }
-      }
-#pragma unroll
-      for (int m = 16; m >= 1; m >>= 1) {
-        const int64_t o = __shfl_xor_sync(0xffffffffu, found, m);
-        found = o < found ? o : found;
-      }
-      if (lane == 0) {
-        part[c].a = found == IDX_NONE ? -1.0 : W;
-        part[c].i = found;
-      }
-      if (++c >= p1) { done = true; break; }
-      const int64_t kold = k;
-      lttb_piece_of(off, cstart, cb, c, k, s, e, cs, ce);
-      if (k != kold) bucket_header();
-      best = -1.0;
-      bid = -1;
-      tfirst = t;
+  for (int j = 0; j < LTTB_K; j++) {
+    const double M = (double)P.v[2 * j], m = (double)P.v[2 * j + 1];
+    if (!(M >= m)) return INFINITY;  // no finite projection recorded (all-NaN piece): evaluate it
+    const double sj = (double)lttb_slope(sr, j);
+    const double dd = sj - sig;
+    const double a0 = dd * dlo, a1 = dd * dhi;
+    const double E = 0x1p-18 * (fmax(fabs(M), fabs(m)) + 2.0 * fabs(sj) * dhi);
+    // shifted single-slope bound (any sig)
+    uhi = fmin(uhi, M + fmax(a0, a1) + E);
+    ulo = fmax(ulo, m + fmin(a0, a1) - E);
+    // chord bound between the two grid slopes around sig
+    if (j > 0 && ps <= sig && sig <= sj && sj > ps) {
+      const double lam = (sj - sig) / (sj - ps);  // weight of the lower slope
+      const double r = 0x1p-40 * (fabs(pM) + fabs(M) + fabs(pm) + fabs(m));
+      uhi = fmin(uhi, lam * (pM + pE) + (1.0 - lam) * (M + E) + r);
+      ulo = fmax(ulo, lam * (pm - pE) + (1.0 - lam) * (m - E) - r);
     }
-    if (done) break;
-    R.fill(t + LTTB_D, lane);
+    pM = M;
+    pm = m;
+    pE = E;
+    ps = sj;
   }
-  R.drain();
+  const double b = fmax(fabs(K1 * uhi + G), fabs(K1 * ulo + G));
+  const double smax = fmax(fabs((double)lttb_slope(sr, 0)), fabs((double)lttb_slope(sr, LTTB_K - 1)));
+  const double slack = 0x1p-44 * (fabs(K1) * (fabs(uhi) + fabs(ulo) + fabs(yb - ay) + (smax + fabs(sig)) * dhi) +
+                                  fabs(K2) * (fabs(ax - (double)s) + dhi) + fabs(G));
+  return 0.5 * (b + slack);
 }
 
-// Verification, round 1 (every bucket, predecessor = the guess): exact
-// first-max area per piece.  Vector form: lttb_verify_ring; scalar form
-// (explicit x / unaligned y): one CTA per piece.  part[c] = (area, index).
+// Plan of bucket j (one warp): constants with the current predecessor and
+// the first max over the bucket's candidates (exact reference areas).
+template <int YDT>
+__device__ __forceinline__ void lttb_plan_bucket(const double* x, const void* y, int64_t n, const int64_t* off,
+                                                 int64_t nb, const double2* cent, const int32_t* nonempty,
+                                                 const int64_t* ext, const int64_t* picks, int64_t j, int lane,
+                                                 int64_t& k, int64_t& s, int64_t& e, LttbPlan& P, AreaCand& cb,
+                                                 double& cx, double& cy) {
+  k = nonempty[j];
+  s = __ldg(off + k);
+  e = __ldg(off + k + 1);
+  P.prev = j == 0 ? 0 : __ldcg(picks + j - 1);
+  centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
+  const double ax = xd(x, P.prev);
+  P.ay = yd<YDT>(y, P.prev);
+  P.K1 = __dsub_rn(ax, cx);
+  P.K2 = __dsub_rn(cy, P.ay);
+  P.sig = -P.K2 / P.K1;
+  cb = AreaCand{-1.0, IDX_NONE};
+  if (lane < LTTB_NC) {
+    const int64_t pi = __ldg(ext + k * LTTB_NC + lane);
+    const double a = tri_area(ax, P.ay, cx, cy, xd(x, pi), yd<YDT>(y, pi));
+    if (a > -1.0) cb = AreaCand{a, pi};
+  }
+  cb = warp_area_max(cb);
+}
+
+// must piece q of bucket [s, e) be evaluated exactly? (pruning bound vs the
+// best candidate area; explicit x: always)
+__device__ __forceinline__ bool lttb_keep_piece(const double* x, const LttbChunkPart* cpart, double2 sr, int64_t c0,
+                                                int64_t q, int64_t s, int64_t e, double yb, const LttbPlan& P,
+                                                double best) {
+  if (x) return true;
+  int64_t cs, ce;
+  lttb_piece(s, e, q, cs, ce);
+  const double bnd =
+      lttb_piece_bound(cpart[c0 + q], sr, s, cs, ce, yb, (double)P.prev, P.ay, P.K1, P.K2, P.sig);
+  return !(bnd < best);
+}
+
+// steering origin of bucket [s, e): y[s] (0 if NaN), as in the prepass
+template <int YDT>
+__device__ __forceinline__ double lttb_yb(const void* y, int64_t s) {
+  const double v = yd<YDT>(y, s);
+  return v == v ? v : 0.0;
+}
+
+// Round 1 (every bucket with its guessed predecessor), warp per bucket: plan,
+// exact evaluation of the unpruned pieces by the same warp, settle.  A pick
+// that differs from the guess lists bucket j+1 in D (list, ctr[2]).  A
+// bucket evaluated after its predecessor changed is still listed, so after
+// this kernel every bucket not in D satisfies picks[j] = f_j(picks[j-1]).
 template <int YDT>
 __global__ void __launch_bounds__(256, 2)
-lttb_chunk_verify_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off,
-                         int64_t nb, const double2* cent, const int64_t* cstart, const int32_t* cb,
-                         const int32_t* rank, const int64_t* counts, const int64_t* picks, LttbAreaPart* part,
-                         int vec_ok) {
+lttb_round1_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
+                   const double2* cent, const double2* slopes, const int64_t* cstart, const int32_t* nonempty,
+                   const int64_t* counts, const LttbChunkPart* cpart, const int64_t* ext, int64_t* picks,
+                   int32_t* list, int32_t* ctr, int vec_ok) {
   pdl_launch_dependents();
   pdl_wait();
-  extern __shared__ uint4 lttb_ring[];
   const double* x = eff_x(xin, drop);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t NCH = counts[1];
-  if (x || !vec_ok) {
-    __shared__ AreaCand sc[8];
-    for (int64_t c = blockIdx.x; c < NCH; c += gridDim.x) {
-      const int64_t k = cb[c];
-      const int64_t j = rank[k];
-      const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-      int64_t cs, ce;
-      lttb_piece(s, e, c - cstart[k], cs, ce);
-      const int64_t prev = j == 0 ? 0 : __ldcg(picks + j - 1);
-      double cx, cy;
-      centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
-      AreaCand best = lttb_piece_area_scalar<YDT>(x, y, cs, ce, xd(x, prev), yd<YDT>(y, prev), cx, cy, tid, 256);
-      best = warp_area_max(best);
-      if (lane == 0) sc[wid] = best;
-      __syncthreads();
-      if (tid == 0) {
-        AreaCand bb = sc[0];
-        for (int w = 1; w < 8; w++)
-          if (area_better(sc[w], bb)) bb = sc[w];
-        part[c].a = bb.a;
-        part[c].i = bb.i;
-      }
-      __syncthreads();
-    }
-    return;
-  }
-  lttb_verify_ring<YDT>(y, n, off, nb, cent, cstart, cb, rank, NCH, picks, part, lttb_ring);
-}
-
-// warp per bucket (round 1): merge piece partials, store a changed pick and
-// list bucket j+1
-__global__ void lttb_chunk_settle_kernel(const int64_t* off, const int64_t* cstart, const int32_t* nonempty,
-                                         const int64_t* counts, const LttbAreaPart* part, int64_t* picks,
-                                         int32_t* list, int32_t* lcount) {
-  pdl_launch_dependents();
-  pdl_wait();
   const int lane = threadIdx.x & 31;
+  const int64_t L = counts[0];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t L = counts[0];
+  int evals = 0;
   for (int64_t j = gw; j < L; j += nw) {
-    const int64_t k = nonempty[j];
-    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+    int64_t k, s, e;
+    LttbPlan P;
+    AreaCand best;
+    double cx, cy;
+    lttb_plan_bucket<YDT>(x, y, n, off, nb, cent, nonempty, ext, picks, j, lane, k, s, e, P, best, cx, cy);
     const int64_t c0 = cstart[k], nch = lttb_npieces(s, e);
-    AreaCand best{-1.0, IDX_NONE};
-    for (int64_t q = lane; q < nch; q += 32) {
-      AreaCand a{part[c0 + q].a, part[c0 + q].i};
-      if (area_better(a, best)) best = a;
+    const double2 sr = slopes[k];
+    const double yb = lttb_yb<YDT>(y, s);
+    for (int64_t q0 = 0; q0 < nch; q0 += 32) {
+      const int64_t q = q0 + lane;
+      const bool keep = q < nch && lttb_keep_piece(x, cpart, sr, c0, q, s, e, yb, P, best.a);
+      unsigned bal = __ballot_sync(0xffffffffu, keep);
+      evals += __popc(bal);
+      while (bal) {
+        const int b = __ffs(bal) - 1;
+        bal &= bal - 1;
+        int64_t cs, ce;
+        lttb_piece(s, e, q0 + b, cs, ce);
+        AreaCand a = (x || !vec_ok)
+                         ? lttb_piece_area_scalar<YDT>(x, y, cs, ce, xd(x, P.prev), P.ay, cx, cy, lane, 32)
+                         : lttb_piece_area_vec<YDT, LTTB_R1_U>(y, cs, ce, P.prev, P.ay, P.K1, P.K2, lane, 32);
+        a = warp_area_max(a);
+        if (area_better(a, best)) best = a;
+      }
     }
-    best = warp_area_max(best);
     if (lane == 0) {
       const int64_t pk = best.i == IDX_NONE ? s : best.i;
-      if (pk != picks[j]) {
-        picks[j] = pk;
-        if (j + 1 < L) list[atomicAdd(lcount, 1)] = (int32_t)(j + 1);
+      if (pk != __ldcg(picks + j)) {
+        __stcg(picks + j, pk);
+        if (j + 1 < L) list[atomicAdd(ctr + 2, 1)] = (int32_t)(j + 1);
       }
     }
   }
+  if (lane == 0 && evals) atomicAdd(ctr + 9, evals);
 }
 
-// Fix-up rounds in one cooperative launch (no host round trips).  Round r
-// re-verifies the buckets listed by round r-1 (one CTA per (entry, piece),
-// exact area with the current predecessor); the CTA completing a bucket's
-// last piece settles it (arrival counters, fence) and lists its successor
-// if the pick changed; one grid barrier per round.  Round 1 is the
-// streaming verification (lttb_chunk_verify_kernel) and lists into
-// list_a / ctr[2].  Counters: ctr[r % 3] = length of the list round r reads;
-// ctr[3] = rounds, ctr[4] = list length after round 1.  A bucket read here
-// while its predecessor settles in the same round is listed again for the
-// next round, so the fixed point is exact.
+__device__ __forceinline__ void lttb_lock(int32_t* l) {
+  int old;
+  do {
+    asm volatile("atom.acquire.gpu.cas.b32 %0, [%1], 0, 1;" : "=r"(old) : "l"(l) : "memory");
+  } while (old != 0);
+}
+__device__ __forceinline__ void lttb_unlock(int32_t* l) {
+  asm volatile("st.release.gpu.b32 [%0], 0;" ::"l"(l) : "memory");
+}
+__device__ __forceinline__ int64_t lttb_ld_relaxed(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.relaxed.gpu.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Correction chains, CTA per entry of D: re-plan bucket j with the current
+// predecessor, evaluate its unpruned pieces (CTA per piece), then under
+// bucket j's lock: if picks[j-1] still equals the predecessor used, store
+// the pick; a changed pick continues the chain at j+1, an outdated
+// predecessor abandons it (whoever changed picks[j-1] continues at j).  The
+// last write to picks[j] therefore always carries f_j(final picks[j-1]): the
+// fixed point is exactly the reference's sequence.
+// ctr: [2] |D|, [3] chain steps, [8] pieces evaluated in chains.
 template <int YDT>
-__global__ void __launch_bounds__(256)
-lttb_fixup_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
-                  const double2* cent, const int64_t* cstart, const int32_t* nonempty, const int64_t* counts,
-                  int64_t* picks, int32_t* list_a, int32_t* list_b, int32_t* ctr, int32_t* arrive,
-                  LttbAreaPart* part, int vec_ok) {
+__global__ void __launch_bounds__(256, 2)
+lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
+                  const double2* cent, const double2* slopes, const int64_t* cstart, const int32_t* nonempty,
+                  const int64_t* counts, const LttbChunkPart* cpart, const int64_t* ext, int64_t* picks,
+                  const int32_t* list, int32_t* lock, int32_t* ctr, int vec_ok) {
   pdl_launch_dependents();
   pdl_wait();
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
   const double* x = eff_x(xin, drop);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  __shared__ AreaCand sc[8];
   const int64_t L = counts[0];
-  const int64_t maxch = counts[2] > 0 ? counts[2] : 1;
-  if (blockIdx.x == 0 && tid == 0) ctr[4] = __ldcg(ctr + 2);
-  int r = 2;
-  for (;; r++) {
-    const int64_t count = __ldcg(ctr + r % 3);
-    if (count == 0 || r > nb + 3) break;
-    const int32_t* cur = (r & 1) ? list_b : list_a;
-    int32_t* nxt = (r & 1) ? list_a : list_b;
-    if (blockIdx.x == 0 && tid == 0) ctr[(r + 2) % 3] = 0;
-    for (int64_t t = blockIdx.x; t < count * maxch; t += gridDim.x) {
-      const int64_t j = __ldcg(cur + t / maxch), q = t % maxch;
-      const int64_t k = nonempty[j];
-      const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-      const int64_t nch = lttb_npieces(s, e);
-      if (q >= nch) continue;  // block-uniform
-      int64_t cs, ce;
-      lttb_piece(s, e, q, cs, ce);
-      const int64_t prev = j == 0 ? 0 : __ldcg(picks + j - 1);
-      double cx, cy;
-      centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
-      const double ay = yd<YDT>(y, prev);
-      AreaCand best = (x || !vec_ok)
-                          ? lttb_piece_area_scalar<YDT>(x, y, cs, ce, xd(x, prev), ay, cx, cy, tid, 256)
-                          : lttb_piece_area_vec<YDT>(y, cs, ce, prev, ay, __dsub_rn((double)prev, cx),
-                                                     __dsub_rn(cy, ay), tid, 256);
-      best = warp_area_max(best);
-      if (lane == 0) sc[wid] = best;
-      __syncthreads();
-      if (tid == 0) {
-        AreaCand b = sc[0];
-        for (int w = 1; w < 8; w++)
-          if (area_better(sc[w], b)) b = sc[w];
-        const int64_t c0 = cstart[k];
-        part[c0 + q].a = b.a;
-        part[c0 + q].i = b.i;
-        __threadfence();
-        if ((atomicAdd(arrive + j, 1) + 1) % nch == 0) {
-          __threadfence();
-          lttb_settle_bucket(j, L, s, c0, nch, part, picks, nxt, ctr + (r + 1) % 3);
+  __shared__ LttbPlan sP;
+  __shared__ AreaCand sCb, sW[8];
+  __shared__ double sc[3];   // cx, cy, yb
+  __shared__ int64_t sk[3];  // k, s, e
+  __shared__ int32_t sq[256];
+  __shared__ int sn, sgo;
+  const int64_t nD = __ldcg(ctr + 2);
+  for (int64_t t = blockIdx.x; t < nD; t += gridDim.x) {
+    int64_t j = __ldcg(list + t);
+    for (;;) {
+      if (wid == 0) {
+        int64_t k, s, e;
+        LttbPlan P;
+        AreaCand cb;
+        double cx, cy;
+        lttb_plan_bucket<YDT>(x, y, n, off, nb, cent, nonempty, ext, picks, j, lane, k, s, e, P, cb, cx, cy);
+        if (lane == 0) {
+          sP = P;
+          sCb = cb;
+          sc[0] = cx;
+          sc[1] = cy;
+          sc[2] = lttb_yb<YDT>(y, s);
+          sk[0] = k;
+          sk[1] = s;
+          sk[2] = e;
+          atomicAdd(ctr + 3, 1);
         }
       }
       __syncthreads();
+      const LttbPlan P = sP;
+      const int64_t k = sk[0], s = sk[1], e = sk[2];
+      const int64_t c0 = cstart[k], nch = lttb_npieces(s, e);
+      const double2 sr = slopes[k];
+      AreaCand wb{-1.0, IDX_NONE};
+      for (int64_t q0 = 0; q0 < nch; q0 += 256) {
+        if (tid == 0) sn = 0;
+        __syncthreads();
+        const int64_t q = q0 + tid;
+        if (q < nch && lttb_keep_piece(x, cpart, sr, c0, q, s, e, sc[2], P, sCb.a)) sq[atomicAdd(&sn, 1)] = (int32_t)tid;
+        __syncthreads();
+        const int m = sn;
+        for (int i = 0; i < m; i++) {  // CTA per piece
+          int64_t cs, ce;
+          lttb_piece(s, e, q0 + sq[i], cs, ce);
+          const AreaCand a = (x || !vec_ok)
+                                 ? lttb_piece_area_scalar<YDT>(x, y, cs, ce, xd(x, P.prev), P.ay, sc[0], sc[1], tid, 256)
+                                 : lttb_piece_area_vec<YDT, 8>(y, cs, ce, P.prev, P.ay, P.K1, P.K2, tid, 256);
+          if (area_better(a, wb)) wb = a;
+        }
+        if (tid == 0) atomicAdd(ctr + 8, m);
+        __syncthreads();
+      }
+      wb = warp_area_max(wb);
+      if (lane == 0) sW[wid] = wb;
+      __syncthreads();
+      if (tid == 0) {
+        AreaCand b = sCb;
+        for (int w = 0; w < 8; w++)
+          if (area_better(sW[w], b)) b = sW[w];
+        const int64_t pk = b.i == IDX_NONE ? s : b.i;
+        int go = 0;
+        lttb_lock(lock + j);
+        const int64_t cur = j == 0 ? 0 : lttb_ld_relaxed(picks + j - 1);
+        if (cur == P.prev && pk != lttb_ld_relaxed(picks + j)) {
+          asm volatile("st.relaxed.gpu.b64 [%0], %1;" ::"l"(picks + j), "l"(pk) : "memory");
+          go = j + 1 < L;
+        }
+        lttb_unlock(lock + j);
+        sgo = go;
+      }
+      __syncthreads();
+      const int go = sgo;
+      __syncthreads();
+      if (!go) break;
+      j++;
     }
-    grid.sync();
   }
-  if (blockIdx.x == 0 && tid == 0) ctr[3] = r - 1;
 }
 
 // out = [0, picks..., n-1] (+ count at out[-1]); optional index map
@@ -1159,7 +1153,7 @@ __global__ void lttb_emit_kernel(const int64_t* picks, const int64_t* counts, in
   pdl_wait();
   const int64_t L = counts[0];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L + 2; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t p = i == 0 ? 0 : (i == L + 1 ? n - 1 : picks[i - 1]);
+    const int64_t p = i == 0 ? 0 : (i == L + 1 ? n - 1 : __ldcg(picks + i - 1));
     out[i] = map ? __ldg(map + p) : p;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *m_out = L + 2;
