@@ -589,7 +589,7 @@ int launch_pdl(tsds_ctx* ctx, void (*k)(KP...), unsigned grid, unsigned block, s
 
 // cooperative launch (grid-wide barriers), also PDL-chained to its predecessor
 template <typename... KP, typename... A>
-int launch_coop(tsds_ctx* ctx, void (*k)(KP...), unsigned grid, unsigned block, A... args) {
+int launch_coop(tsds_ctx* ctx, void (*k)(KP...), unsigned grid, unsigned block, size_t smem, A... args) {
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
@@ -598,6 +598,7 @@ int launch_coop(tsds_ctx* ctx, void (*k)(KP...), unsigned grid, unsigned block, 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(std::max(grid, 1u));
   cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx->stream;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
@@ -641,15 +642,16 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   const int64_t maxseg = nb / LTTB_SEG + 2;
   const int64_t nlb = (nb + LTTB_LB - 1) / LTTB_LB;
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-  const size_t zero_bytes = al(64) + al(64) + al(24 * (nlb + 1)) + al(4 * nb);  // counts, ctr, link, lock
+  const size_t zero_bytes = al(64) + al(256) + al(24 * (nlb + 1)) + al(4 * nb);  // counts, ctr, link, lock
   const size_t need = zero_bytes + al(8 * (nb + 1)) + al(4 * maxch) + al(4 * nb) + al(4 * nb) + al(32 * nb) +
                       al(16 * nb) + al(sizeof(LttbChunkPart) * maxch) + al(8 * NC * nb) + al(NC * nb) +
-                      al(NC * maxseg) + al(maxseg) + al(8 * (nb + 4)) + al(4 * nb);
+                      al(NC * maxseg) + al(maxseg) + al(8 * (nb + 4)) + al(4 * nb) + al(sizeof(LttbPlan) * nb) +
+                      al(sizeof(AreaCand) * nb) + al(4 * nb) + al(sizeof(AreaCand) * maxch) + al(sizeof(int2) * maxch);
   RC_TRY(ensure(ctx, ctx->lscr, need));
   char* p = (char*)ctx->lscr.p;
   auto take = [&](size_t bytes) { char* r = p; p += al(bytes); return r; };
   int64_t* counts = (int64_t*)take(64);  // zeroed block: counts, ctr, link, lock
-  int32_t* ctr = (int32_t*)take(64);
+  int32_t* ctr = (int32_t*)take(256);
   unsigned long long* link = (unsigned long long*)take(24 * (nlb + 1));
   int32_t* lock = (int32_t*)take(4 * nb);
   int64_t* cstart = (int64_t*)take(8 * (nb + 1));
@@ -665,6 +667,11 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   uint8_t* entry = (uint8_t*)take(maxseg);
   int64_t* walkout = (int64_t*)take(8 * (nb + 4));
   int32_t* list_a = (int32_t*)take(4 * nb);
+  LttbPlan* plan = (LttbPlan*)take(sizeof(LttbPlan) * nb);
+  AreaCand* cbest = (AreaCand*)take(sizeof(AreaCand) * nb);
+  int32_t* arrive = (int32_t*)take(4 * nb);
+  AreaCand* apart = (AreaCand*)take(sizeof(AreaCand) * maxch);
+  int2* plist = (int2*)take(sizeof(int2) * maxch);
   int64_t* picks = walkout + 2;
   const int mode = lttb_exact_mode();
   const int64_t avg = (n - 2) / std::max<int64_t>(nb, 1);
@@ -684,29 +691,23 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_chunk_prepass_kernel<YD>,
                                     one_wave(ctx, lttb_chunk_prepass_kernel<YD>, 256, LTTB_RING_BYTES), 256,
                                     LTTB_RING_BYTES, xf, drop, y, off, cstart, cb, counts, slopes, cpart, vec_ok)));
-  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_chunk_merge_kernel<YD>, gw8, 256, 0, xf, drop, off, nb, cstart, cpart,
-                                    cent, ext)));
-  if (exact)
-    YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_centroid_kernel<YD>, cap_grid((nb + 7) / 8, (int64_t)ctx->sms * 16),
-                                      256, 0, xf, drop, y, off, nb, cent)));
-  // ---- guess chain on the candidates (composed transition tables); grids
-  //      are sized from nb, the kernels read the actual counts on the device
-  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_cand_table_kernel<YD>, cap_grid((nb * NC + 255) / 256, (int64_t)ctx->sms * 8),
-                                    256, 0, xf, drop, y, n, off, nb, cent, ext, nonempty, counts, T)));
-  const int64_t NS = (nb + LTTB_SEG - 1) / LTTB_SEG;
-  const unsigned gs = cap_grid((NS + 7) / 8, (int64_t)ctx->sms * 8);
-  RC_TRY(launch_pdl(ctx, lttb_seg_compose_kernel, gs, 256, 0, T, counts, C));
-  const int64_t cap = 40000;
-  RC_TRY(launch_pdl(ctx, lttb_seg_entry_kernel, 1, 1024, (size_t)(std::min<int64_t>(NS * NC, cap) + 16), T, C, counts,
-                    entry, cap));
-  RC_TRY(launch_pdl(ctx, lttb_seg_expand_kernel, gs, 256, 0, T, entry, ext, nonempty, counts, picks));
-  // ---- resolve: round 1 (every bucket, guessed predecessors, pruned exact
-  //      evaluation), then correction chains from the buckets whose
-  //      predecessor changed, then the output
-  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_round1_kernel<YD>, one_wave(ctx, lttb_round1_kernel<YD>, 256), 256, 0,
-                                    xf, drop, y, n, off, nb, (const double2*)cent, (const double2*)slopes,
-                                    (const int64_t*)cstart, (const int32_t*)nonempty, (const int64_t*)counts,
-                                    (const LttbChunkPart*)cpart, (const int64_t*)ext, picks, list_a, ctr, vec_ok)));
+  // ---- guess (merge, transition tables, composed chain) + round-1 plan:
+  //      one cooperative launch; then round-1 evaluation of the unpruned
+  //      pieces, the correction chains and the output
+  const int64_t cap = 32768;
+  YDT_SWITCH(ydt, ({
+               auto kg = lttb_guess_kernel<YD>;
+               cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(cap + 16));
+               RC_TRY(launch_coop(ctx, kg, one_wave(ctx, kg, 256, (size_t)(cap + 16)), 256, (size_t)(cap + 16), xf,
+                                  drop, y, n, off, nb, cent, (const double2*)slopes, (const int64_t*)cstart,
+                                  (const int32_t*)nonempty, (const int64_t*)counts, (const LttbChunkPart*)cpart, ext,
+                                  T, C, entry, picks, plan, cbest, arrive, apart, plist, list_a, ctr, exact, cap));
+             }));
+  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_eval_kernel<YD>, one_wave(ctx, lttb_eval_kernel<YD>, 256), 256, 0, xf,
+                                    drop, y, n, off, nb, (const double2*)cent, (const int64_t*)cstart,
+                                    (const int32_t*)nonempty, (const int64_t*)counts, (const LttbPlan*)plan,
+                                    (const AreaCand*)cbest, arrive, apart, (const int2*)plist, picks, list_a, ctr,
+                                    vec_ok)));
   YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_chain_kernel<YD>, one_wave(ctx, lttb_chain_kernel<YD>, 256), 256, 0,
                                     xf, drop, y, n, off, nb, (const double2*)cent, (const double2*)slopes,
                                     (const int64_t*)cstart, (const int32_t*)nonempty, (const int64_t*)counts,
@@ -716,7 +717,7 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
                     (const int64_t*)counts, n, map, out_dev + 1, out_dev));
   RC_TRY(prof_mark(ctx, ev, true));
   RC_TRY(ensure_lstat(ctx));
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_lstat, ctr, 10 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_lstat, ctr, 32 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->lstat_pending = true;
   return TSDS_OK;
 }
@@ -1042,6 +1043,12 @@ int64_t tsds_ctx_stat(tsds_ctx* ctx, const char* name) {
       ctx->lttb_pieces1 = ctx->h_lstat[9];  // pieces evaluated in round 1
     }
     ctx->lstat_pending = false;
+  }
+  if (n.rfind("lttb_ts", 0) == 0 && n.size() == 8 && ctx->h_lstat) {  // debug: guess-kernel phase times (ns)
+    cudaStreamSynchronize(ctx->stream);
+    const unsigned long long* t = (const unsigned long long*)(ctx->h_lstat + 16);
+    const int i = n[7] - '0';
+    return (i >= 1 && i <= 5) ? (int64_t)(t[i] - t[i - 1]) : -1;
   }
   if (n == "lttb_rounds") return ctx->lttb_rounds;
   if (n == "lttb_dirty1") return ctx->lttb_dirty1;

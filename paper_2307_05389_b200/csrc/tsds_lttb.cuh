@@ -94,10 +94,8 @@ __device__ __forceinline__ const double* eff_x(const double* x, const int* drop)
 // Centroid of every bucket, reference summation order: one warp per bucket,
 // lanes fetch 32 consecutive points, every lane replays the sequential sum.
 template <int YDT>
-__global__ void lttb_centroid_kernel(const double* xin, const int* drop, const void* y,
-                                     const int64_t* off, int64_t nb, double2* cent) {
-  pdl_launch_dependents();
-  pdl_wait();
+__device__ __forceinline__ void lttb_centroid_phase(const double* xin, const int* drop, const void* y,
+                                                    const int64_t* off, int64_t nb, double2* cent) {
   const double* x = eff_x(xin, drop);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -121,6 +119,13 @@ __global__ void lttb_centroid_kernel(const double* xin, const int* drop, const v
       cent[k] = make_double2(__ddiv_rn(sx, cw), __ddiv_rn(sy, cw));
     }
   }
+}
+template <int YDT>
+__global__ void lttb_centroid_kernel(const double* xin, const int* drop, const void* y,
+                                     const int64_t* off, int64_t nb, double2* cent) {
+  pdl_launch_dependents();
+  pdl_wait();
+  lttb_centroid_phase<YDT>(xin, drop, y, off, nb, cent);
 }
 
 struct AreaCand {

@@ -94,7 +94,8 @@ lttb_layout_kernel(const int64_t* off, int64_t nb, int64_t* cstart, int32_t* cb,
     b += np[r] > 0;
     mx = np[r] > mx ? np[r] : mx;
   }
-  if (mx) atomicMax((unsigned long long*)&counts[2], (unsigned long long)mx);
+  const unsigned long long wmx = __reduce_max_sync(0xffffffffu, (unsigned)mx);  // one atomic per warp
+  if (lane == 0 && wmx) atomicMax((unsigned long long*)&counts[2], wmx);
   // block exclusive scan of (a, b)
   int64_t ia = a, ib = b;
 #pragma unroll
@@ -623,10 +624,8 @@ lttb_chunk_prepass_kernel(const double* xin, const int* drop, const void* y, con
 // warp per bucket: merge its chunk partials -> centroid (pairwise, chunk
 // order) and the LTTB_NC candidates in index order
 template <int YDT>
-__global__ void lttb_chunk_merge_kernel(const double* xin, const int* drop, const int64_t* off, int64_t nb,
+__device__ __forceinline__ void lttb_merge_phase(const double* xin, const int* drop, const int64_t* off, int64_t nb,
                                         const int64_t* cstart, const LttbChunkPart* part, double2* cent, int64_t* ext) {
-  pdl_launch_dependents();
-  pdl_wait();
   const double* x = eff_x(xin, drop);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -652,10 +651,21 @@ __global__ void lttb_chunk_merge_kernel(const double* xin, const int* drop, cons
       const bool mx = (lane & 1) == 0;
       float bv = 0.0f;
       int64_t bi = -1;
-      for (int64_t q = 0; q < nch; q++) {
-        const float ov = part[c0 + q].v[lane];
-        const int64_t oi = part[c0 + q].i[lane];
-        if (oi >= 0 && (bi < 0 || (mx ? ov > bv : ov < bv) || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+      for (int64_t q0 = 0; q0 < nch; q0 += 4) {  // 4 pieces' loads in flight
+        float ov[4];
+        int64_t oi[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const bool in = q0 + u < nch;
+          ov[u] = in ? part[c0 + q0 + u].v[lane] : 0.0f;
+          oi[u] = in ? part[c0 + q0 + u].i[lane] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          if (oi[u] >= 0 && (bi < 0 || (mx ? ov[u] > bv : ov[u] < bv) || (ov[u] == bv && oi[u] < bi))) {
+            bv = ov[u];
+            bi = oi[u];
+          }
       }
       cand = bi < 0 ? s : bi;
     }
@@ -685,11 +695,9 @@ __global__ void lttb_chunk_merge_kernel(const double* xin, const int* drop, cons
 // picked when the predecessor is candidate i of non-empty bucket j (row 0:
 // predecessor = point 0)
 template <int YDT>
-__global__ void lttb_cand_table_kernel(const double* xin, const int* drop, const void* y, int64_t n,
+__device__ __forceinline__ void lttb_cand_table_phase(const double* xin, const int* drop, const void* y, int64_t n,
                                        const int64_t* off, int64_t nb, const double2* cent, const int64_t* ext,
                                        const int32_t* nonempty, const int64_t* counts, uint8_t* T) {
-  pdl_launch_dependents();
-  pdl_wait();
   const double* x = eff_x(xin, drop);
   const int64_t L = counts[0];
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L * LTTB_NC;
@@ -704,20 +712,36 @@ __global__ void lttb_cand_table_kernel(const double* xin, const int* drop, const
     const int64_t* cbp = ext + b * LTTB_NC;
     int best = 0;
     double besta = -1.0;
+    double vx[LTTB_NC], vy[LTTB_NC];
+#pragma unroll
     for (int q = 0; q < LTTB_NC; q++) {
       const int64_t pi = __ldg(cbp + q);
-      const double a = tri_area(ax, ay, cx, cy, xd(x, pi), yd<YDT>(y, pi));
+      vx[q] = xd(x, pi);
+      vy[q] = yd<YDT>(y, pi);
+    }
+#pragma unroll
+    for (int q = 0; q < LTTB_NC; q++) {
+      const double a = tri_area(ax, ay, cx, cy, vx[q], vy[q]);
       if (a > besta) { besta = a; best = q; }
     }
     T[t] = (uint8_t)best;
   }
 }
 
+// copy len bytes of global src into warp-private smem with 16-byte vector
+// loads (one round trip); returns the offset of src[0] inside dst
+__device__ __forceinline__ int lttb_stage_bytes(uint8_t* dst, const uint8_t* src, int64_t len, int lane) {
+  const uintptr_t a = (uintptr_t)src, base = a & ~(uintptr_t)15;
+  const int shift = (int)(a - base);
+  const int nv = (int)((shift + len + 15) / 16);
+  for (int v = lane; v < nv; v += 32) ((uint4*)dst)[v] = __ldcg((const uint4*)base + v);
+  __syncwarp();
+  return shift;
+}
+
 // warp per segment: compose the segment's tables (rows staged in smem)
-__global__ void __launch_bounds__(256) lttb_seg_compose_kernel(const uint8_t* T, const int64_t* counts, uint8_t* C) {
-  pdl_launch_dependents();
-  pdl_wait();
-  __shared__ uint8_t rows[8][LTTB_SEG * LTTB_NC];
+__device__ __forceinline__ void lttb_seg_compose_phase(const uint8_t* T, const int64_t* counts, uint8_t* C) {
+  __shared__ __align__(16) uint8_t rows[8][LTTB_SEG * LTTB_NC + 32];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t L = counts[0];
   const int64_t NS = (L + LTTB_SEG - 1) / LTTB_SEG;
@@ -726,23 +750,19 @@ __global__ void __launch_bounds__(256) lttb_seg_compose_kernel(const uint8_t* T,
   for (int64_t s = gw; s < NS; s += nw) {
     const int64_t j0 = s * LTTB_SEG, j1 = (s + 1) * LTTB_SEG < L - 1 ? (s + 1) * LTTB_SEG : L - 1;
     const int64_t nr = j1 > j0 ? j1 - j0 : 0;
-    for (int64_t t = lane; t < nr * LTTB_NC; t += 32) rows[wl][t] = T[(j0 + 1) * LTTB_NC + t];
-    __syncwarp();
+    const int sh = lttb_stage_bytes(rows[wl], T + (j0 + 1) * LTTB_NC, nr * LTTB_NC, lane);
     if (lane < LTTB_NC) {
       int c = lane;
-      for (int64_t r = 0; r < nr; r++) c = rows[wl][r * LTTB_NC + c];
+      for (int64_t r = 0; r < nr; r++) c = rows[wl][sh + r * LTTB_NC + c];
       C[s * LTTB_NC + lane] = (uint8_t)c;
     }
     __syncwarp();
   }
 }
 
-// one thread chains the segment entries (C staged in smem)
-__global__ void __launch_bounds__(1024) lttb_seg_entry_kernel(const uint8_t* T, const uint8_t* C, const int64_t* counts,
-                                                              uint8_t* entry, int64_t cap) {
-  pdl_launch_dependents();
-  pdl_wait();
-  extern __shared__ uint8_t sC[];
+// one thread chains the segment entries (C staged in smem; one CTA)
+__device__ __forceinline__ void lttb_seg_entry_phase(const uint8_t* T, const uint8_t* C, const int64_t* counts,
+                                                     uint8_t* entry, uint8_t* sC, int64_t cap) {
   const int64_t L = counts[0];
   const int64_t NS = (L + LTTB_SEG - 1) / LTTB_SEG;
   const bool staged = NS * LTTB_NC <= cap;
@@ -759,12 +779,10 @@ __global__ void __launch_bounds__(1024) lttb_seg_entry_kernel(const uint8_t* T, 
 }
 
 // warp per segment: expand the picks
-__global__ void __launch_bounds__(256) lttb_seg_expand_kernel(const uint8_t* T, const uint8_t* entry,
+__device__ __forceinline__ void lttb_seg_expand_phase(const uint8_t* T, const uint8_t* entry,
                                                                const int64_t* ext, const int32_t* nonempty,
                                                                const int64_t* counts, int64_t* picks) {
-  pdl_launch_dependents();
-  pdl_wait();
-  __shared__ uint8_t rows[8][LTTB_SEG * LTTB_NC];
+  __shared__ __align__(16) uint8_t rows[8][LTTB_SEG * LTTB_NC + 32];
   __shared__ uint8_t cs[8][LTTB_SEG];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t L = counts[0];
@@ -775,13 +793,12 @@ __global__ void __launch_bounds__(256) lttb_seg_expand_kernel(const uint8_t* T, 
     const int64_t j0 = s * LTTB_SEG, j1 = (s + 1) * LTTB_SEG < L ? (s + 1) * LTTB_SEG : L;
     const int64_t nr = j1 - j0;
     const int64_t rlim = (j1 < L ? nr : nr - 1) * LTTB_NC;  // transitions j0->j0+1 .. j1-1->j1
-    for (int64_t t = lane; t < rlim; t += 32) rows[wl][t] = T[(j0 + 1) * LTTB_NC + t];
-    __syncwarp();
+    const int sh = lttb_stage_bytes(rows[wl], T + (j0 + 1) * LTTB_NC, rlim, lane);
     if (lane == 0) {
       int c = entry[s];
       for (int64_t r = 0; r < nr; r++) {
         cs[wl][r] = (uint8_t)c;
-        if (r + 1 < nr) c = rows[wl][r * LTTB_NC + c];
+        if (r + 1 < nr) c = rows[wl][sh + r * LTTB_NC + c];
       }
     }
     __syncwarp();
@@ -977,17 +994,125 @@ __device__ __forceinline__ double lttb_yb(const void* y, int64_t s) {
   return v == v ? v : 0.0;
 }
 
-// Round 1 (every bucket with its guessed predecessor), warp per bucket: plan,
-// exact evaluation of the unpruned pieces by the same warp, settle.  A pick
-// that differs from the guess lists bucket j+1 in D (list, ctr[2]).  A
-// bucket evaluated after its predecessor changed is still listed, so after
-// this kernel every bucket not in D satisfies picks[j] = f_j(picks[j-1]).
+// settle bucket j (pick = first max of its candidate best and its piece
+// partials); a pick that differs from picks[j] lists bucket j+1 in D
+__device__ __forceinline__ void lttb_settle(int64_t j, int64_t L, int64_t s, int64_t c0, int64_t nch,
+                                            const AreaCand* cbest, const AreaCand* part, int64_t* picks,
+                                            int32_t* list, int32_t* cnt) {
+  AreaCand best{__ldcg(&cbest[j].a), __ldcg(&cbest[j].i)};
+  for (int64_t q = 0; q < nch; q++) {
+    const AreaCand a{__ldcg(&part[c0 + q].a), __ldcg(&part[c0 + q].i)};
+    if (area_better(a, best)) best = a;
+  }
+  const int64_t p = best.i == IDX_NONE ? s : best.i;
+  if (p != __ldcg(picks + j)) {
+    __stcg(picks + j, p);
+    if (j + 1 < L) list[atomicAdd(cnt, 1)] = (int32_t)(j + 1);
+  }
+}
+
+// The guess and round-1 plan in one cooperative launch (grid barriers
+// between the phases, no kernel boundaries):
+//   merge      warp per bucket: centroid (+ exact sequential centroids in
+//              exact mode) and the LTTB_NC candidates from the piece partials
+//   cand_table thread per (bucket, candidate): transition tables T
+//   compose    warp per segment of LTTB_SEG buckets: composed tables C
+//   entry      one thread: entry candidate of every segment
+//   expand     warp per segment: the guessed pick of every bucket
+//   plan       warp per bucket, predecessor = the guess: constants, exact
+//              candidate best, piece bounds -> unpruned pieces listed for
+//              lttb_eval_kernel; a bucket with none settles at once.
+// ctr: [2] |D| (list), [6] pieces listed.
 template <int YDT>
 __global__ void __launch_bounds__(256, 2)
-lttb_round1_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
-                   const double2* cent, const double2* slopes, const int64_t* cstart, const int32_t* nonempty,
-                   const int64_t* counts, const LttbChunkPart* cpart, const int64_t* ext, int64_t* picks,
-                   int32_t* list, int32_t* ctr, int vec_ok) {
+lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
+                  double2* cent, const double2* slopes, const int64_t* cstart, const int32_t* nonempty,
+                  const int64_t* counts, const LttbChunkPart* cpart, int64_t* ext, uint8_t* T, uint8_t* C,
+                  uint8_t* entry, int64_t* picks, LttbPlan* plan, AreaCand* cbest, int32_t* arrive, AreaCand* part,
+                  int2* plist, int32_t* list, int32_t* ctr, int exact, int64_t cap) {
+  pdl_launch_dependents();
+  pdl_wait();
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ uint8_t lttb_dsm[];
+  const double* x = eff_x(xin, drop);
+  unsigned long long* tsb = (unsigned long long*)(ctr + 16);  // debug phase timestamps
+  auto stamp = [&](int i) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      tsb[i] = t;
+    }
+  };
+  stamp(0);
+  lttb_merge_phase<YDT>(xin, drop, off, nb, cstart, cpart, cent, ext);
+  if (exact) {
+    grid.sync();
+    lttb_centroid_phase<YDT>(xin, drop, y, off, nb, cent);
+  }
+  grid.sync();
+  stamp(1);
+  lttb_cand_table_phase<YDT>(xin, drop, y, n, off, nb, cent, ext, nonempty, counts, T);
+  grid.sync();
+  stamp(2);
+  lttb_seg_compose_phase(T, counts, C);
+  grid.sync();
+  stamp(3);
+  if (blockIdx.x == 0) lttb_seg_entry_phase(T, C, counts, entry, lttb_dsm, cap);
+  grid.sync();
+  stamp(4);
+  lttb_seg_expand_phase(T, entry, ext, nonempty, counts, picks);
+  grid.sync();
+  stamp(5);
+  // ---- plan (round 1)
+  const int lane = threadIdx.x & 31;
+  const int64_t L = counts[0];
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = gw; j < L; j += nw) {
+    int64_t k, s, e;
+    LttbPlan P;
+    AreaCand cb;
+    double cx, cy;
+    lttb_plan_bucket<YDT>(x, y, n, off, nb, cent, nonempty, ext, picks, j, lane, k, s, e, P, cb, cx, cy);
+    const int64_t c0 = cstart[k], nch = lttb_npieces(s, e);
+    const double2 sr = slopes[k];
+    const double yb = lttb_yb<YDT>(y, s);
+    int nun = 0;
+    for (int64_t q0 = 0; q0 < nch; q0 += 32) {
+      const int64_t q = q0 + lane;
+      const bool keep = q < nch && lttb_keep_piece(x, cpart, sr, c0, q, s, e, yb, P, cb.a);
+      if (q < nch && !keep) part[c0 + q] = AreaCand{-1.0, IDX_NONE};
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      int base = 0;
+      if (lane == 0 && bal) base = atomicAdd(ctr + 6, __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (keep) plist[base + __popc(bal & ((1u << lane) - 1u))] = make_int2((int)(c0 + q), (int)j);
+      nun += __popc(bal);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      plan[j] = P;
+      cbest[j] = cb;
+      arrive[j] = nun;
+      if (nun == 0) {
+        __threadfence();
+        lttb_settle(j, L, s, c0, nch, cbest, part, picks, list, ctr + 2);
+      }
+    }
+  }
+}
+
+// Round 1 evaluation, warp per listed piece: exact first max with the
+// guessed predecessor; the warp completing a bucket's last piece settles it.
+// After this kernel every bucket not in D satisfies picks[j] = f_j(picks[j-1])
+// (a bucket whose predecessor changed during round 1 is in D).
+template <int YDT>
+__global__ void __launch_bounds__(256, 2)
+lttb_eval_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
+                 const double2* cent, const int64_t* cstart, const int32_t* nonempty, const int64_t* counts,
+                 const LttbPlan* plan, const AreaCand* cbest, int32_t* arrive, AreaCand* part, const int2* plist,
+                 int64_t* picks, int32_t* list, int32_t* ctr, int vec_ok) {
   pdl_launch_dependents();
   pdl_wait();
   const double* x = eff_x(xin, drop);
@@ -995,42 +1120,36 @@ lttb_round1_kernel(const double* xin, const int* drop, const void* y, int64_t n,
   const int64_t L = counts[0];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int evals = 0;
-  for (int64_t j = gw; j < L; j += nw) {
-    int64_t k, s, e;
-    LttbPlan P;
-    AreaCand best;
-    double cx, cy;
-    lttb_plan_bucket<YDT>(x, y, n, off, nb, cent, nonempty, ext, picks, j, lane, k, s, e, P, best, cx, cy);
-    const int64_t c0 = cstart[k], nch = lttb_npieces(s, e);
-    const double2 sr = slopes[k];
-    const double yb = lttb_yb<YDT>(y, s);
-    for (int64_t q0 = 0; q0 < nch; q0 += 32) {
-      const int64_t q = q0 + lane;
-      const bool keep = q < nch && lttb_keep_piece(x, cpart, sr, c0, q, s, e, yb, P, best.a);
-      unsigned bal = __ballot_sync(0xffffffffu, keep);
-      evals += __popc(bal);
-      while (bal) {
-        const int b = __ffs(bal) - 1;
-        bal &= bal - 1;
-        int64_t cs, ce;
-        lttb_piece(s, e, q0 + b, cs, ce);
-        AreaCand a = (x || !vec_ok)
-                         ? lttb_piece_area_scalar<YDT>(x, y, cs, ce, xd(x, P.prev), P.ay, cx, cy, lane, 32)
-                         : lttb_piece_area_vec<YDT, LTTB_R1_U>(y, cs, ce, P.prev, P.ay, P.K1, P.K2, lane, 32);
-        a = warp_area_max(a);
-        if (area_better(a, best)) best = a;
-      }
+  const int64_t np = __ldcg(ctr + 6);
+  for (int64_t t = gw; t < np; t += nw) {
+    const int2 pc = __ldcg(plist + t);
+    const int64_t c = pc.x, j = pc.y;
+    const int64_t k = nonempty[j];
+    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+    const int64_t c0 = cstart[k];
+    int64_t cs, ce;
+    lttb_piece(s, e, c - c0, cs, ce);
+    const LttbPlan P = plan[j];
+    AreaCand a;
+    if (x || !vec_ok) {
+      double cx, cy;
+      centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
+      a = lttb_piece_area_scalar<YDT>(x, y, cs, ce, xd(x, P.prev), P.ay, cx, cy, lane, 32);
+    } else {
+      a = lttb_piece_area_vec<YDT, LTTB_R1_U>(y, cs, ce, P.prev, P.ay, P.K1, P.K2, lane, 32);
     }
+    a = warp_area_max(a);
     if (lane == 0) {
-      const int64_t pk = best.i == IDX_NONE ? s : best.i;
-      if (pk != __ldcg(picks + j)) {
-        __stcg(picks + j, pk);
-        if (j + 1 < L) list[atomicAdd(ctr + 2, 1)] = (int32_t)(j + 1);
+      part[c] = a;
+      __threadfence();
+      if (atomicSub(arrive + j, 1) == 1) {
+        __threadfence();
+        lttb_settle(j, L, s, c0, lttb_npieces(s, e), cbest, part, picks, list, ctr + 2);
       }
     }
+    __syncwarp();
   }
-  if (lane == 0 && evals) atomicAdd(ctr + 9, evals);
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctr[9] = (int32_t)np;
 }
 
 __device__ __forceinline__ void lttb_lock(int32_t* l) {
