@@ -494,6 +494,10 @@ int run_minmax_m4(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y
   const int64_t nb = n_out / width;
   BinSpec bins{0, nullptr, n, nb, 0};
   ScanArgs A = scan_args(nullptr, bins, 0, nb, 0, n);
+  // host y: enqueue its (asynchronous, pinned) upload first so that the host
+  // binning of x below overlaps the transfer
+  const void* dy;
+  RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
   if (x) {
     if (mem == TSDS_MEM_HOST) {
       if (!tsds_host_is_uniform_spaced(x, xdt, n)) {
@@ -516,8 +520,6 @@ int run_minmax_m4(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y
       A.status_out = &misc(ctx)->status_copy;
     }
   }
-  const void* dy;
-  RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
   A.y = dy;
   A.epi = algo == TSDS_MINMAX ? EPI_MINMAX : EPI_M4;
   A.out = out_dev;
