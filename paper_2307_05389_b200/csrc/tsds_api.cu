@@ -157,7 +157,16 @@ int begin_call(tsds_ctx* ctx) {
 int dtype_ok(int dt) { return dt >= 0 && dt < DT_COUNT; }
 
 // tuning knobs: environment defaults, overridable with tsds_set_option
-int64_t g_dyn_percent = -1, g_tma_min_bytes = -1;
+int64_t g_dyn_percent = -1, g_tma_min_bytes = -1, g_cta_bins_max = -1;
+
+// CTA-per-bin scan for inputs up to this many bytes (latency-bound sizes)
+int64_t cta_bins_max_bytes() {
+  if (g_cta_bins_max < 0) {
+    const char* e = getenv("TSDS_CTA_BINS_MAX_BYTES");
+    g_cta_bins_max = e ? atoll(e) : ((int64_t)128 << 20);
+  }
+  return g_cta_bins_max;
+}
 
 int64_t dyn_percent() {
   if (g_dyn_percent < 0) {
@@ -311,6 +320,9 @@ int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
   }
   const int64_t nchunks = A.n_static + A.n_dyn;
   const int64_t nbins = A.g1 - A.g0;
+  // small inputs split into many bins: CTA per bin (TSDS option cta_bins_max_bytes)
+  A.cta_bins = !A.independent && tv * ES <= cta_bins_max_bytes() && nbins >= (int64_t)ctx->sms &&
+               tv / std::max<int64_t>(nbins, 1) >= 256 / ES;
   RC_TRY(ensure(ctx, ctx->part, (size_t)nchunks * 2 * sizeof(MinMaxCand)));
   RC_TRY(ensure(ctx, ctx->bincnt, (size_t)nbins * sizeof(unsigned), true));
   RC_TRY(ensure(ctx, ctx->res, (size_t)nbins * 2 * sizeof(int64_t)));
@@ -319,6 +331,7 @@ int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
   A.res = (int64_t*)ctx->res.p;
   A.flags = &misc(ctx)->F;
   int64_t grid = std::min<int64_t>(W / SCAN_WARPS, (nchunks + SCAN_WARPS - 1) / SCAN_WARPS);
+  if (A.cta_bins) grid = std::min<int64_t>(nbins, W / SCAN_WARPS);
   if (A.independent || A.check_flags)
     grid = std::max<int64_t>(grid, std::min<int64_t>(W / SCAN_WARPS, (nbins + SCAN_WARPS - 1) / SCAN_WARPS));
   grid = std::max<int64_t>(grid, 1);
@@ -962,6 +975,7 @@ int tsds_set_option(const char* name, int64_t value) {
   std::string n(name);
   if (n == "tma_min_bytes") g_tma_min_bytes = std::max<int64_t>(0, value);
   else if (n == "dyn_percent") g_dyn_percent = std::max<int64_t>(0, std::min<int64_t>(90, value));
+  else if (n == "cta_bins_max_bytes") g_cta_bins_max = std::max<int64_t>(0, value);
   else if (n == "lttb_exact") g_lttb_exact = std::max<int64_t>(0, std::min<int64_t>(2, value));
   else return set_err(TSDS_ERR_ARG, "unknown option " + n);
   return TSDS_OK;
