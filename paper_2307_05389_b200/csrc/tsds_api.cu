@@ -157,7 +157,16 @@ int begin_call(tsds_ctx* ctx) {
 int dtype_ok(int dt) { return dt >= 0 && dt < DT_COUNT; }
 
 // tuning knobs: environment defaults, overridable with tsds_set_option
-int64_t g_dyn_percent = -1, g_tma_min_bytes = -1;
+int64_t g_dyn_percent = -1, g_tma_min_bytes = -1, g_cta_bins_max = -1;
+
+// CTA-per-bin scan for inputs up to this many bytes (latency-bound sizes)
+int64_t cta_bins_max_bytes() {
+  if (g_cta_bins_max < 0) {
+    const char* e = getenv("TSDS_CTA_BINS_MAX_BYTES");
+    g_cta_bins_max = e ? atoll(e) : ((int64_t)128 << 20);
+  }
+  return g_cta_bins_max;
+}
 
 int64_t dyn_percent() {
   if (g_dyn_percent < 0) {
@@ -311,6 +320,9 @@ int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
   }
   const int64_t nchunks = A.n_static + A.n_dyn;
   const int64_t nbins = A.g1 - A.g0;
+  // small inputs split into many bins: CTA per bin (TSDS option cta_bins_max_bytes)
+  A.cta_bins = !A.independent && tv * ES <= cta_bins_max_bytes() && nbins >= (int64_t)ctx->sms &&
+               tv / std::max<int64_t>(nbins, 1) >= 256 / ES;
   RC_TRY(ensure(ctx, ctx->part, (size_t)nchunks * 2 * sizeof(MinMaxCand)));
   RC_TRY(ensure(ctx, ctx->bincnt, (size_t)nbins * sizeof(unsigned), true));
   RC_TRY(ensure(ctx, ctx->res, (size_t)nbins * 2 * sizeof(int64_t)));
@@ -319,6 +331,7 @@ int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
   A.res = (int64_t*)ctx->res.p;
   A.flags = &misc(ctx)->F;
   int64_t grid = std::min<int64_t>(W / SCAN_WARPS, (nchunks + SCAN_WARPS - 1) / SCAN_WARPS);
+  if (A.cta_bins) grid = std::min<int64_t>(nbins, W / SCAN_WARPS);
   if (A.independent || A.check_flags)
     grid = std::max<int64_t>(grid, std::min<int64_t>(W / SCAN_WARPS, (nbins + SCAN_WARPS - 1) / SCAN_WARPS));
   grid = std::max<int64_t>(grid, 1);
@@ -494,6 +507,10 @@ int run_minmax_m4(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y
   const int64_t nb = n_out / width;
   BinSpec bins{0, nullptr, n, nb, 0};
   ScanArgs A = scan_args(nullptr, bins, 0, nb, 0, n);
+  // host y: enqueue its (asynchronous, pinned) upload first so that the host
+  // binning of x below overlaps the transfer
+  const void* dy;
+  RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
   if (x) {
     if (mem == TSDS_MEM_HOST) {
       if (!tsds_host_is_uniform_spaced(x, xdt, n)) {
@@ -516,8 +533,6 @@ int run_minmax_m4(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y
       A.status_out = &misc(ctx)->status_copy;
     }
   }
-  const void* dy;
-  RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
   A.y = dy;
   A.epi = algo == TSDS_MINMAX ? EPI_MINMAX : EPI_M4;
   A.out = out_dev;
@@ -954,6 +969,7 @@ int tsds_set_option(const char* name, int64_t value) {
   std::string n(name);
   if (n == "tma_min_bytes") g_tma_min_bytes = std::max<int64_t>(0, value);
   else if (n == "dyn_percent") g_dyn_percent = std::max<int64_t>(0, std::min<int64_t>(90, value));
+  else if (n == "cta_bins_max_bytes") g_cta_bins_max = std::max<int64_t>(0, value);
   else if (n == "lttb_exact") g_lttb_exact = std::max<int64_t>(0, std::min<int64_t>(2, value));
   else return set_err(TSDS_ERR_ARG, "unknown option " + n);
   return TSDS_OK;

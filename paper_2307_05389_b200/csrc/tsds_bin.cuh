@@ -281,15 +281,15 @@ __global__ void binning_kernel(const BinJob J) {
   (void)nwarps;
 
   __shared__ int s_last, s_mode;
-  __threadfence();
-  __syncthreads();
+  __syncthreads();  // + thread 0's release-acquire fence (see scan_epilogue)
   if (threadIdx.x == 0) {
+    fence_acq_rel_gpu();
     unsigned t = atomicAdd(&F->bin_blocks_done, 1u);
     s_last = (t == gridDim.x - 1);
+    if (s_last) fence_acq_rel_gpu();
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   if (threadIdx.x == 0) {
     const bool api_uniform = J.xapi && *(volatile int*)&F->mis_api == 0;
     const bool sl_uniform = *(volatile int*)&F->mis_slice == 0;

@@ -117,6 +117,7 @@ struct ScanArgs {
   int reset_flags;     // clear the binning flags at the end (pipeline consumer)
   int* status_out;     // nullable: receives flags->status before the reset
   int independent;     // host-known non-monotone offsets
+  int cta_bins;        // small inputs: CTA per bin (its warps split the bin), no cross-CTA merges
   // epilogue
   int epi;
   int64_t* out;        // compacted output (or idx slots)
@@ -339,36 +340,46 @@ __device__ __forceinline__ int bin_emit(const ScanArgs& A, const BinSpec& B, int
   return m;
 }
 
-// One CTA compacts bins [ga, gb) into out[...]; returns the count.
+// One CTA compacts bins [ga, gb) into out[...]; returns the count.  Each
+// thread takes 4 consecutive bins per pass (their loads issued together),
+// so a pass covers 4 * blockDim bins with one block-wide exclusive scan.
 __device__ int64_t cta_compact(const ScanArgs& A, const BinSpec& B, int64_t ga, int64_t gb, int64_t* out,
                                int64_t sub) {
-  __shared__ int64_t warp_tot[32];
+  constexpr int PB = 4;  // bins per thread per pass
+  __shared__ int warp_tot[32];
   __shared__ int64_t running;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
   if (tid == 0) running = 0;
   __syncthreads();
-  for (int64_t base = ga; base < gb; base += blockDim.x) {
-    int64_t g = base + tid;
-    int64_t v[4];
-    int c = g < gb ? bin_emit(A, B, g, v) : 0;
-    int incl = c;
+  for (int64_t base = ga; base < gb; base += (int64_t)PB * blockDim.x) {
+    int64_t v[PB][4];
+    int c[PB], tot = 0;
+#pragma unroll
+    for (int r = 0; r < PB; r++) {
+      const int64_t g = base + (int64_t)PB * tid + r;
+      c[r] = g < gb ? bin_emit(A, B, g, v[r]) : 0;
+      tot += c[r];
+    }
+    int incl = tot;
 #pragma unroll
     for (int m = 1; m < 32; m <<= 1) {
-      int t = __shfl_up_sync(0xffffffffu, incl, m);
+      const int t = __shfl_up_sync(0xffffffffu, incl, m);
       if (lane >= m) incl += t;
     }
     if (lane == 31) warp_tot[wid] = incl;
     __syncthreads();
-    int64_t before = running;
-    for (int w = 0; w < wid; w++) before += warp_tot[w];
-    int64_t pos = before + incl - c;
-    for (int t = 0; t < c; t++) out[pos + t] = v[t] - sub;
-    __syncthreads();
-    if (tid == 0) {
-      int64_t tot = 0;
-      for (int w = 0; w < nw; w++) tot += warp_tot[w];
-      running += tot;
+    int64_t pos = running + incl - tot;
+    int all = 0;
+    for (int w = 0; w < nw; w++) {
+      const int t = warp_tot[w];
+      if (w < wid) pos += t;
+      all += t;
     }
+#pragma unroll
+    for (int r = 0; r < PB; r++)
+      for (int t = 0; t < c[r]; t++) out[pos++] = v[r][t] - sub;
+    __syncthreads();
+    if (tid == 0) running += all;
     __syncthreads();
   }
   return running;
@@ -408,13 +419,14 @@ __device__ __forceinline__ void process_chunk(const ScanArgs& A, const BinSpec& 
         MinMaxCand* slot = A.part + 2 * w + (before ? 0 : 1);
         slot->mn = r.mn;
         slot->mx = r.mx;
-        __threadfence();
+        fence_acq_rel_gpu();
         old = atomicAdd(A.bin_cnt + (g - A.g0), 1u);
+        if ((int64_t)old == chunk_of(A, e - 1) - chunk_of(A, s)) fence_acq_rel_gpu();
       }
       old = __shfl_sync(0xffffffffu, old, 0);
       int64_t wa = chunk_of(A, s), wb = chunk_of(A, e - 1);
       if ((int64_t)old == wb - wa) {  // last arriver merges the partials
-        __threadfence();
+        __syncwarp();
         MinMaxCand acc{cand_none_min(), cand_none_max()};
         for (int64_t ww = wa + lane; ww <= wb; ww += 32) {
           const MinMaxCand* sl = A.part + 2 * ww + (ww == wa ? 1 : 0);
@@ -437,18 +449,33 @@ __device__ __forceinline__ void process_chunk(const ScanArgs& A, const BinSpec& 
 
 // Last CTA of a launch: compaction epilogue, counter and flag reset.
 // Every CTA of the grid must call it exactly once.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted) {
   PipeFlags* F = A.flags;
   __shared__ int is_last;
-  __threadfence();
+#ifdef TSDS_SCAN_TIMING
+  if (threadIdx.x == 0) atomicMax(&F->pad1[1], gtimer());
+#endif
+  // the CTA's writes are ordered before the ticket by the barrier plus one
+  // release-acquire fence of thread 0 (cumulative); the last CTA acquires
+  // the same way.  A per-thread __threadfence() (fence.sc) here cost ~20 us
+  // per launch across the grid.
   __syncthreads();
   if (threadIdx.x == 0) {
+    fence_acq_rel_gpu();
     unsigned t = atomicAdd(&F->scan_blocks_done, 1u);
     is_last = (t == gridDim.x - 1);
+    if (is_last) fence_acq_rel_gpu();
   }
   __syncthreads();
   if (!is_last) return;
-  __threadfence();
+#ifdef TSDS_SCAN_TIMING
+  if (threadIdx.x == 0) F->pad1[2] = gtimer();
+#endif
   if (aborted) {
     if (threadIdx.x == 0) {
       if (A.epi == EPI_SLOTS_MINMAX || A.epi == EPI_SLOTS_M4) {
@@ -476,6 +503,15 @@ __device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted)
       *A.out_count = tot;
     }
   }
+#ifdef TSDS_SCAN_TIMING
+  if (threadIdx.x == 0) {
+    const unsigned long long t3 = gtimer();
+    printf("scan timing: main %.1f us, last-CTA wait %.1f us, epilogue %.1f us, grid %d\n",
+           (F->pad1[1] - F->pad1[0]) * 1e-3, (F->pad1[2] - F->pad1[1]) * 1e-3, (t3 - F->pad1[2]) * 1e-3, gridDim.x);
+    F->pad1[0] = ~0ull;
+    F->pad1[1] = 0;
+  }
+#endif
   if (threadIdx.x == 0) {
     if (A.status_out) *A.status_out = *(volatile int*)&F->status;
     if (A.reset_flags) {
@@ -498,6 +534,9 @@ scan_kernel(const ScanArgs A) {
   // programmatic dependent launch: everything below may read what the
   // binning kernel (the primary grid) wrote
   pdl_wait();
+#ifdef TSDS_SCAN_TIMING
+  if (threadIdx.x == 0) atomicMin(&A.flags->pad1[0], gtimer());
+#endif
   const int lane = threadIdx.x & 31;
   const int64_t gw = (int64_t)blockIdx.x * SCAN_WARPS + (threadIdx.x >> 5);
   const int64_t nwarps_grid = (int64_t)gridDim.x * SCAN_WARPS;
@@ -507,6 +546,36 @@ scan_kernel(const ScanArgs A) {
   const bool aborted = A.check_flags && *(volatile int*)&F->status;
   const bool indep = A.independent || (A.check_flags && *(volatile int*)&F->nonmono);
 
+#ifndef TSDS_NO_CTA_BINS
+  if (!aborted && A.cta_bins) {
+    // CTA per bin: every warp reduces a contiguous eighth of the bin, the
+    // partials merge in shared memory (lexicographic (key, index) merges,
+    // so the first occurrence wins in any order); one round trip per bin
+    // instead of a chain of warp batches, and no cross-CTA merge.
+    __shared__ MinMaxCand part_s[SCAN_WARPS];
+    const int wid = threadIdx.x >> 5;
+    for (int64_t g = A.g0 + blockIdx.x; g < A.g1; g += gridDim.x) {
+      const int64_t s = bin_off(B, g), e = bin_off(B, g + 1);
+      if (e > s) {
+        const int64_t len = e - s;
+        const int64_t a = s + len * wid / SCAN_WARPS, c = s + len * (wid + 1) / SCAN_WARPS;
+        MinMaxCand r{cand_none_min(), cand_none_max()};
+        if (c > a) r = seg_reduce<DT, PROP, U>(A, a, c);
+        if (lane == 0) part_s[wid] = r;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && e > s) {
+        MinMaxCand acc = part_s[0];
+        for (int w = 1; w < SCAN_WARPS; w++) {
+          merge_min(acc.mn, part_s[w].mn);
+          merge_max(acc.mx, part_s[w].mx);
+        }
+        finalize<DT, PROP>(A, B, g, acc);
+      }
+      __syncthreads();
+    }
+  } else
+#endif
   if (!aborted && indep) {
     // non-monotone offsets (x violated its documented precondition): bins
     // may overlap, so every bin is reduced on its own, like the reference.
