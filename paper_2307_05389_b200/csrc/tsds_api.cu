@@ -655,7 +655,12 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   RC_TRY(ensure(ctx, ctx->cent, (size_t)std::max<int64_t>(nb, 1) * sizeof(double2)));
   double2* cent = (double2*)ctx->cent.p;
   const int64_t NC = LTTB_NC;
-  const int64_t SB = 512 / dtype_size(ydt);
+  // sub-block size: 32 or 64 vectors of 16 bytes (>= 64 sub-blocks per bucket)
+  const int64_t EPV = 16 / dtype_size(ydt);
+  const int64_t vpb = (n / std::max<int64_t>(nb, 1)) / EPV;  // vectors per bucket
+  int SBV = 32;  // <= 64: a warp's group (32 sub-blocks) stays short enough to balance the grid
+  while (SBV < 64 && (int64_t)SBV * 2 * 64 <= vpb) SBV *= 2;
+  const int64_t SB = (int64_t)SBV * EPV;
   const int64_t NG = (n + SB - 1) / SB;
   const int64_t maxsb = NG + nb + 1;  // sub-blocks touched by the buckets (boundaries twice)
   const int64_t maxseg = nb / LTTB_SEG + 2;
@@ -673,6 +678,8 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   int32_t* ctr = (int32_t*)take(256);
   int32_t* lock = (int32_t*)take(4 * nb);
   LttbSBArrays A;
+  A.SB = SB;
+  A.SBV = SBV;
   A.mm = (float2*)take(8 * NG);
   A.am = (uint32_t*)take(4 * NG);
   A.sy = (double*)take(8 * NG);
@@ -701,8 +708,9 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   RC_TRY(prof_mark(ctx, ev, false));
   CUDA_TRY(cudaMemsetAsync(counts, 0, zero_bytes, ctx->stream));
   // ---- 1. sub-block summaries (the one streaming pass over y)
-  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_sb_kernel<YD>, one_wave(ctx, lttb_sb_kernel<YD>, 256), 256, 0, xf, drop,
-                                    y, n, vec_ok, A)));
+  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_sb_kernel<YD>,
+                                    one_wave(ctx, lttb_sb_kernel<YD>, LTTB_SB_WARPS * 32, LTTB_SB_SMEM),
+                                    LTTB_SB_WARPS * 32, LTTB_SB_SMEM, xf, drop, y, n, vec_ok, A)));
   // ---- 2. guess + round-1 plan (cooperative)
   const int64_t cap = 32768;
   YDT_SWITCH(ydt, ({
@@ -715,7 +723,7 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
              }));
   // ---- 3. round-1 evaluation, 4. correction chains, 5. output
   YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_eval_kernel<YD>, one_wave(ctx, lttb_eval_kernel<YD>, 256), 256, 0, xf,
-                                    drop, y, n, off, nb, (const double2*)cent, (const int32_t*)nonempty,
+                                    drop, y, n, off, nb, A, (const double2*)cent, (const int32_t*)nonempty,
                                     (const int64_t*)counts, (const LttbRound1*)r1, arrive, part,
                                     (const int64_t*)slots, (const int64_t*)wl, picks, list_a, ctr, vec_ok)));
   YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_chain_kernel<YD>, one_wave(ctx, lttb_chain_kernel<YD>, 256), 256, 0,

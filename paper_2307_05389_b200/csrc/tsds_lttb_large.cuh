@@ -40,11 +40,10 @@ constexpr int LTTB_K = 7;            // steering slopes per bucket
 constexpr int LTTB_NC = 2 * LTTB_K;  // candidates per bucket (argmax + argmin per slope)
 constexpr int LTTB_SEG = 64;         // buckets per composed segment
 
-// sub-block geometry: one warp-wide 128-bit load (32 lanes x 16 bytes)
+// elements per 16-byte vector
 template <int YDT>
 struct SBG {
-  static constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);  // elements per 16-byte vector
-  static constexpr int SB = 32 * EPV;                                // points per sub-block
+  static constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
 };
 
 // order-preserving u32 key of a float (no NaN)
@@ -57,6 +56,8 @@ __device__ __forceinline__ float f32_unkey(unsigned k) {
 }
 
 struct LttbSBArrays {
+  int64_t SB;     // points per sub-block = SBV * EPV (chosen per call from the bucket size)
+  int SBV;        // 16-byte vectors per sub-block: a power of two in [32, 512]
   float2* mm;     // (max rounded up, min rounded down) over non-NaN points; (-inf, +inf) if none
   uint32_t* am;   // offset of the first max | offset of the first min << 16 (0xffff each if none)
   double* sy;     // sum of y (NaN propagates, like the reference's centroid sums)
@@ -65,65 +66,149 @@ struct LttbSBArrays {
 
 // ---------------------------------------------------------------------------
 // 1. sub-block summaries.  Lane-owned sub-blocks: warp w takes 32
-// consecutive sub-blocks, lane l sub-block 32w + l, streamed in 4 rounds of
-// 8 contiguous 16-byte loads (each lane reads its own 512 bytes; the 128-byte
-// lines are reused from L1).  Everything is lane-local: running sum in index
-// order, first max / first min of the outward-rounded f32 values.
+// consecutive sub-blocks at a time, lane l sub-block 32w + l.  A round is
+// the next 8 vectors (128 bytes) of each of the 32 sub-blocks: it is copied
+// by cp.async as 8 warp instructions of four full 128-byte lines each into a
+// per-warp ring (LTTB_SB_D rounds = 12 KB in flight per warp, bytes in
+// shared memory rather than registers; XOR-swizzled so that the lane-owned
+// reads are conflict-free), then every lane folds its own 8 vectors: running
+// sum in index order, first max / first min of the outward-rounded values.
+constexpr int LTTB_SB_D = 3;          // rounds in flight per warp
+constexpr int LTTB_SB_WARPS = 8;      // warps per CTA
+constexpr int LTTB_SB_SMEM = LTTB_SB_WARPS * LTTB_SB_D * 4096;
+
+// running first max / first min in f64 (NaN never compares true); the
+// max/min start at -inf/+inf, so a sub-block whose non-NaN values are all
+// -inf (+inf) keeps the "none" offset and is resolved by lttb_sb_store
+struct SbAcc {
+  double mx, mn, s0, s1;
+  int amx, amn;
+  __device__ __forceinline__ void reset() {
+    mx = -INFINITY;
+    mn = INFINITY;
+    s0 = s1 = 0.0;
+    amx = amn = 0xffff;
+  }
+  __device__ __forceinline__ void fold(double d, int o, bool odd) {
+    if (odd) s1 = __dadd_rn(s1, d);
+    else s0 = __dadd_rn(s0, d);
+    if (d > mx) { mx = d; amx = o; }
+    if (d < mn) { mn = d; amn = o; }
+  }
+};
+
+// write sub-block g's summary (outward-rounded f32 extremes)
 template <int YDT>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ void lttb_sb_store(const LttbSBArrays& A, const void* y, int64_t n, int64_t g, SbAcc& a) {
+  if (a.amx == 0xffff || a.amn == 0xffff) {  // rare: no point beat the +-inf start (all NaN or all +-inf)
+    for (int o = 0; o < A.SB && g * A.SB + o < n; o++) {
+      const double d = yd<YDT>(y, g * A.SB + o);
+      if (a.amx == 0xffff && d == -INFINITY) { a.mx = d; a.amx = o; }
+      if (a.amn == 0xffff && d == INFINITY) { a.mn = d; a.amn = o; }
+    }
+  }
+  A.mm[g] = make_float2(a.amx == 0xffff ? -INFINITY : __double2float_ru(a.mx),
+                        a.amn == 0xffff ? INFINITY : __double2float_rd(a.mn));
+  A.am[g] = (uint32_t)a.amx | ((uint32_t)a.amn << 16);
+  A.sy[g] = __dadd_rn(a.s0, a.s1);
+}
+
+template <int YDT>
+__global__ void __launch_bounds__(LTTB_SB_WARPS * 32)
 lttb_sb_kernel(const double* xin, const int* drop, const void* y, int64_t n, int vec_ok, LttbSBArrays A) {
   pdl_launch_dependents();
   pdl_wait();
-  using G = SBG<YDT>;
-  constexpr int EPV = G::EPV, SB = G::SB;
+  constexpr int EPV = SBG<YDT>::EPV;
+  extern __shared__ uint4 sb_ring[];
+  const int64_t SB = A.SB;
+  const int SBV = A.SBV, RPG = SBV / 8;  // rounds per group of 32 sub-blocks
   const double* x = eff_x(xin, drop);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t NG = (n + SB - 1) / SB;
   const int64_t nvec = (n + EPV - 1) / EPV;
   const uint4* yv = (const uint4*)y;
-  for (int64_t gb = gw * 32; gb < NG; gb += nw * 32) {
-    const int64_t g = gb + lane;
-    float mx = -INFINITY, mn = INFINITY;
-    int amx = 0xffff, amn = 0xffff;
-    double sum = 0.0, sumx = 0.0;
-#pragma unroll 1
-    for (int it = 0; it < 4; it++) {
-      uint4 q[8];
-      if (vec_ok) {
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-          const int64_t v = g * 32 + it * 8 + u;
-          q[u] = (g < NG && v < nvec) ? __ldg(yv + v) : make_uint4(0, 0, 0, 0);
-        }
+  if (!vec_ok || x) {  // unaligned y or explicit x: plain lane-owned loads
+    for (int64_t gb = gw * 32; gb < NG; gb += nw * 32) {
+      const int64_t g = gb + lane;
+      SbAcc acc;
+      acc.reset();
+      double sumx = 0.0;
+      for (int o = 0; o < SB && g < NG; o++) {
+        const int64_t i = g * SB + o;
+        if (i >= n) break;
+        acc.fold(yd<YDT>(y, i), o, o & 1);
+        if (x) sumx = __dadd_rn(sumx, __ldg(x + i));
       }
+      if (g < NG) {
+        lttb_sb_store<YDT>(A, y, n, g, acc);
+        if (x) A.sx[g] = sumx;
+      }
+    }
+    return;
+  }
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sb_ring + (size_t)wl * LTTB_SB_D * 256);
+  const int64_t ngroups = NG > gw * 32 ? (NG - gw * 32 + nw * 32 - 1) / (nw * 32) : 0;
+  // fill / consume cursors: (group base, round in group, ring slot) advanced
+  // incrementally (no 64-bit divisions in the loop)
+  int64_t fgb = gw * 32, fleft = ngroups;
+  int fit = 0, fslot = 0;
+  auto fill = [&]() {
+    if (fleft > 0) {
+      const uint32_t dst = sbase + (uint32_t)(fslot * 4096);
 #pragma unroll
       for (int u = 0; u < 8; u++) {
+        const int L = u * 4 + (lane >> 3), w = lane & 7;
+        const int64_t v = (fgb + L) * SBV + fit * 8 + w;
+        const bool in = fgb + L < NG && v < nvec;
+        const uint32_t d = dst + (uint32_t)((L * 8 + (w ^ (L & 7))) * 16);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(yv + (in ? v : 0)),
+                     "r"(in ? 16 : 0)
+                     : "memory");
+      }
+      if (++fit == RPG) { fit = 0; fgb += nw * 32; fleft--; }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    fslot = fslot == LTTB_SB_D - 1 ? 0 : fslot + 1;
+  };
 #pragma unroll
-        for (int e = 0; e < EPV; e++) {
-          const int o = (it * 8 + u) * EPV + e;  // offset inside the sub-block
-          const int64_t i = g * SB + o;
-          if (g < NG && i < n) {
-            const double d = vec_ok ? vget<YDT>(q[u], e) : yd<YDT>(y, i);
-            sum = __dadd_rn(sum, d);
-            if (x) sumx = __dadd_rn(sumx, __ldg(x + i));
-            if (d == d) {
-              const float fu = __double2float_ru(d), fd = __double2float_rd(d);
-              if (fu > mx || amx == 0xffff) { mx = fu; amx = o; }
-              if (fd < mn || amn == 0xffff) { mn = fd; amn = o; }
-            }
-          }
-        }
+  for (int r = 0; r < LTTB_SB_D; r++) fill();
+  SbAcc acc;
+  acc.reset();
+  int64_t cgb = gw * 32;
+  int cit = 0, cslot = 0;
+  for (int64_t left = ngroups; left > 0;) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(LTTB_SB_D - 1) : "memory");
+    __syncwarp();
+    const int64_t g = cgb + lane;
+    const uint32_t src = sbase + (uint32_t)(cslot * 4096);
+    const int ob = cit * 8 * EPV;                                 // offset of the round in the sub-block
+    const bool full = g < NG && g * SB + ob + 8 * EPV <= n;       // whole round inside the series
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+      uint4 q;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
+                   : "r"(src + (uint32_t)((lane * 8 + (w ^ (lane & 7))) * 16)));
+#pragma unroll
+      for (int e = 0; e < EPV; e++) {
+        const int o = ob + w * EPV + e;
+        if (full || (g < NG && g * SB + o < n)) acc.fold(vget<YDT>(q, e), o, (w * EPV + e) & 1);
       }
     }
-    if (g < NG) {
-      A.mm[g] = make_float2(mx, mn);
-      A.am[g] = (uint32_t)amx | ((uint32_t)amn << 16);
-      A.sy[g] = sum;
-      if (x) A.sx[g] = sumx;
+    __syncwarp();
+    fill();
+    cslot = cslot == LTTB_SB_D - 1 ? 0 : cslot + 1;
+    if (++cit == RPG) {
+      if (g < NG) lttb_sb_store<YDT>(A, y, n, g, acc);
+      acc.reset();
+      cit = 0;
+      cgb += nw * 32;
+      left--;
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -190,7 +275,7 @@ template <int YDT>
 __device__ __forceinline__ void lttb_cent_phase(const double* x, const void* y, const int64_t* off,
                                                 const int32_t* nonempty, const int64_t* counts,
                                                 const LttbSBArrays A, double2* cent, float2* yr) {
-  constexpr int SB = SBG<YDT>::SB;
+  const int64_t SB = A.SB;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -296,7 +381,7 @@ __device__ __forceinline__ void lttb_cand_phase(const double* x, const void* y, 
                                                 int64_t n, const double2* cent, const float2* yr,
                                                 const int32_t* nonempty, const int64_t* counts,
                                                 const LttbSBArrays A, int64_t* ext) {
-  constexpr int SB = SBG<YDT>::SB;
+  const int64_t SB = A.SB;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -340,19 +425,17 @@ __device__ __forceinline__ void lttb_cand_phase(const double* x, const void* y, 
         }
       }
     }
+    // warp-wide winners: the rounded value by REDUX, then the lowest index
+    // holding it (a candidate only steers the guess, so rounding is harmless)
     int64_t cand = s;
 #pragma unroll
     for (int c = 0; c < LTTB_NC; c++) {
-      double v = bv[c];
-      int64_t i = bi[c];
-#pragma unroll
-      for (int m = 16; m >= 1; m >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, v, m);
-        const int64_t oi = __shfl_xor_sync(0xffffffffu, i, m);
-        const bool better = (c & 1) ? (ov < v) : (ov > v);
-        if (oi >= 0 && (i < 0 || better || (ov == v && oi < i))) { v = ov; i = oi; }
-      }
-      if (lane == c) cand = i < 0 ? s : i;
+      const bool mx = (c & 1) == 0;
+      const unsigned key = bi[c] >= 0 ? f32_key(__double2float_rn(bv[c])) : (mx ? 0u : 0xffffffffu);
+      const unsigned w = mx ? __reduce_max_sync(0xffffffffu, key) : __reduce_min_sync(0xffffffffu, key);
+      const unsigned rel = (bi[c] >= 0 && key == w) ? (unsigned)(bi[c] - s) : 0xffffffffu;
+      const unsigned r = __reduce_min_sync(0xffffffffu, rel);
+      if (lane == c) cand = r == 0xffffffffu ? s : s + (int64_t)r;
     }
     // sort the NC candidates by index (odd-even transposition over lanes)
     for (int r = 0; r < LTTB_NC; r++) {
@@ -543,9 +626,8 @@ __device__ __forceinline__ void lttb_plan_bucket(const double* x, const void* y,
 }
 
 // sub-block g restricted to bucket [s, e)
-template <int YDT>
-__device__ __forceinline__ void lttb_sb_range(int64_t g, int64_t s, int64_t e, int64_t& cs, int64_t& ce) {
-  constexpr int SB = SBG<YDT>::SB;
+__device__ __forceinline__ void lttb_sb_range(int64_t SB, int64_t g, int64_t s, int64_t e, int64_t& cs,
+                                              int64_t& ce) {
   cs = g * SB > s ? g * SB : s;
   ce = (g + 1) * SB < e ? (g + 1) * SB : e;
 }
@@ -555,7 +637,7 @@ __device__ __forceinline__ bool lttb_keep_sb(const double* x, const LttbSBArrays
                                              const LttbPlan& P, double best) {
   if (x) return true;
   int64_t cs, ce;
-  lttb_sb_range<YDT>(g, s, e, cs, ce);
+  lttb_sb_range(A.SB, g, s, e, cs, ce);
   return !(lttb_sb_bound(A.mm[g], s, cs, ce, P) < best);
 }
 
@@ -568,31 +650,44 @@ __device__ __forceinline__ double lttb_varea(const uint4& q, int e, double dA, d
   return __dmul_rn(0.5, fabs(__dsub_rn(t1, t2)));
 }
 
-// exact first max over [cs, ce) inside sub-block g, one warp (lane l takes
-// the sub-block's vector l); explicit x / unaligned y: point by point
+// exact first max over [cs, ce) inside sub-block g, one warp: lane l takes
+// the sub-block's vectors l, l+32, ... (all loads in flight, then the areas
+// in index order); explicit x / unaligned y: point by point
 template <int YDT>
-__device__ __forceinline__ AreaCand lttb_eval_sb(const double* x, const void* y, int vec_ok, int64_t g, int64_t cs,
-                                                 int64_t ce, const LttbPlan& P, double cx, double cy, int lane) {
-  constexpr int EPV = SBG<YDT>::EPV, SB = SBG<YDT>::SB;
+__device__ __forceinline__ AreaCand lttb_eval_sb(const double* x, const void* y, int vec_ok, const LttbSBArrays& A,
+                                                 int64_t g, int64_t cs, int64_t ce, const LttbPlan& P, double cx,
+                                                 double cy, int lane) {
+  constexpr int EPV = SBG<YDT>::EPV;
   AreaCand best{-1.0, IDX_NONE};
-  const int64_t i0 = g * SB + lane * EPV;
   if (x || !vec_ok) {
     const double ax = xd(x, P.prev);
-#pragma unroll
-    for (int e = 0; e < EPV; e++) {
-      const int64_t i = i0 + e;
-      if (i >= cs && i < ce) {
-        const AreaCand a{tri_area(ax, P.ay, cx, cy, xd(x, i), yd<YDT>(y, i)), i};
-        if (area_better(a, best)) best = a;
-      }
+    for (int64_t i = cs + lane; i < ce; i += 32) {
+      const AreaCand a{tri_area(ax, P.ay, cx, cy, xd(x, i), yd<YDT>(y, i)), i};
+      if (area_better(a, best)) best = a;
     }
-  } else if (i0 < ce && i0 + EPV > cs) {
-    const uint4 q = __ldg((const uint4*)y + g * 32 + lane);
-    const double dA = (double)(P.prev - i0);
+    return warp_area_max(best);
+  }
+  const int64_t v0 = cs / EPV, v1 = (ce + EPV - 1) / EPV;  // vectors overlapping [cs, ce) (<= SBV + 1)
+  const uint4* yv = (const uint4*)y;
+  for (int64_t vb = v0; vb < v1; vb += 32 * 16) {
+    uint4 q[16];
 #pragma unroll
-    for (int e = 0; e < EPV; e++) {
-      const double a = lttb_varea<YDT>(q, e, dA, P.ay, P.K1, P.K2);
-      if (i0 + e >= cs && i0 + e < ce && a > best.a) best = AreaCand{a, i0 + e};
+    for (int u = 0; u < 16; u++) {
+      const int64_t v = vb + u * 32 + lane;
+      if (v < v1) q[u] = __ldg(yv + v);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const int64_t v = vb + u * 32 + lane;
+      if (v < v1) {
+        const int64_t i0 = v * EPV;
+        const double dA = (double)(P.prev - i0);
+#pragma unroll
+        for (int e = 0; e < EPV; e++) {
+          const double a = lttb_varea<YDT>(q[u], e, dA, P.ay, P.K1, P.K2);
+          if (i0 + e >= cs && i0 + e < ce && a > best.a) best = AreaCand{a, i0 + e};
+        }
+      }
     }
   }
   return warp_area_max(best);
@@ -693,7 +788,7 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   grid.sync();
   stamp(4);
   // ---- round-1 plan
-  constexpr int SB = SBG<YDT>::SB;
+  const int64_t SB = A.SB;
   const int lane = threadIdx.x & 31;
   const int64_t L = counts[0];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -726,7 +821,7 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
           if (x) keep = true;
           else {
             int64_t cs, ce;
-            lttb_sb_range<YDT>(g, s, e, cs, ce);
+            lttb_sb_range(A.SB, g, s, e, cs, ce);
             keep = !(lttb_sb_bound(m4[u], s, cs, ce, P) < cb.a);
           }
         }
@@ -762,7 +857,7 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
 template <int YDT>
 __global__ void __launch_bounds__(256)
 lttb_eval_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
-                 const double2* cent, const int32_t* nonempty, const int64_t* counts, const LttbRound1* r1,
+                 const LttbSBArrays A, const double2* cent, const int32_t* nonempty, const int64_t* counts, const LttbRound1* r1,
                  int32_t* arrive, AreaCand* part, const int64_t* slots, const int64_t* wl, int64_t* picks,
                  int32_t* list, int32_t* ctr, int vec_ok) {
   pdl_launch_dependents();
@@ -783,8 +878,8 @@ lttb_eval_kernel(const double* xin, const int* drop, const void* y, int64_t n, c
     double cx = 0.0, cy = 0.0;
     if (x || !vec_ok) centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
     int64_t cs, ce;
-    lttb_sb_range<YDT>(g, s, e, cs, ce);
-    const AreaCand a = lttb_eval_sb<YDT>(x, y, vec_ok, g, cs, ce, P, cx, cy, lane);
+    lttb_sb_range(A.SB, g, s, e, cs, ce);
+    const AreaCand a = lttb_eval_sb<YDT>(x, y, vec_ok, A, g, cs, ce, P, cx, cy, lane);
     int last = 0;
     if (lane == 0) {
       part[pos] = a;
@@ -827,7 +922,7 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
                   const int64_t* ext, int64_t* picks, const int32_t* list, int32_t* lock, int32_t* ctr, int vec_ok) {
   pdl_launch_dependents();
   pdl_wait();
-  constexpr int SB = SBG<YDT>::SB;
+  const int64_t SB = A.SB;
   const double* x = eff_x(xin, drop);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t L = counts[0];
@@ -872,8 +967,8 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
         const int m = sn;
         for (int i = wid; i < m; i += 8) {  // warp per sub-block
           int64_t cs, ce;
-          lttb_sb_range<YDT>(sq[i], s, e, cs, ce);
-          const AreaCand a = lttb_eval_sb<YDT>(x, y, vec_ok, sq[i], cs, ce, P, sc[0], sc[1], lane);
+          lttb_sb_range(A.SB, sq[i], s, e, cs, ce);
+          const AreaCand a = lttb_eval_sb<YDT>(x, y, vec_ok, A, sq[i], cs, ce, P, sc[0], sc[1], lane);
           if (area_better(a, wb)) wb = a;
         }
         if (tid == 0) atomicAdd(ctr + 8, m);
