@@ -390,14 +390,14 @@ __device__ __forceinline__ void lttb_cand_phase(const double* x, const void* y, 
     const int64_t k = nonempty[j];
     const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
     const double2 sr = lttb_slope_range<YDT>(x, y, off, nb, n, cent, yr, nonempty, j, k);
-    double sl[LTTB_K];
+    float sl[LTTB_K];  // candidates only steer the guess: f32 scores, bucket-relative u32 positions
 #pragma unroll
-    for (int t = 0; t < LTTB_K; t++) sl[t] = sr.x + (sr.y - sr.x) * ((double)t / (double)(LTTB_K - 1));
+    for (int t = 0; t < LTTB_K; t++) sl[t] = (float)(sr.x + (sr.y - sr.x) * ((double)t / (double)(LTTB_K - 1)));
     const double xs = xd(x, s);
-    double bv[LTTB_NC];
-    int64_t bi[LTTB_NC];
+    float bv[LTTB_NC];
+    unsigned bi[LTTB_NC];
 #pragma unroll
-    for (int c = 0; c < LTTB_NC; c++) { bv[c] = (c & 1) ? INFINITY : -INFINITY; bi[c] = -1; }
+    for (int c = 0; c < LTTB_NC; c++) { bv[c] = (c & 1) ? INFINITY : -INFINITY; bi[c] = 0xffffffffu; }
     const int64_t g0 = s / SB, g1 = (e - 1) / SB;
     for (int64_t gb = g0; gb <= g1; gb += 32 * 4) {  // 4 sub-blocks per lane in flight
       float2 m4[4];
@@ -416,25 +416,24 @@ __device__ __forceinline__ void lttb_cand_phase(const double* x, const void* y, 
         const int64_t px = g * SB + (am & 0xffff), pn = g * SB + (am >> 16);
         const bool okx = (am & 0xffff) != 0xffff && px >= s && px < e;
         const bool okn = (am >> 16) != 0xffff && pn >= s && pn < e;
-        const double dxx = okx ? xd(x, px) - xs : 0.0, dxn = okn ? xd(x, pn) - xs : 0.0;
+        const float dxx = okx ? (float)(xd(x, px) - xs) : 0.0f, dxn = okn ? (float)(xd(x, pn) - xs) : 0.0f;
 #pragma unroll
         for (int t = 0; t < LTTB_K; t++) {
-          const double vx = (double)m.x - sl[t] * dxx, vn = (double)m.y - sl[t] * dxn;
-          if (okx && vx > bv[2 * t]) { bv[2 * t] = vx; bi[2 * t] = px; }
-          if (okn && vn < bv[2 * t + 1]) { bv[2 * t + 1] = vn; bi[2 * t + 1] = pn; }
+          const float vx = fmaf(-sl[t], dxx, m.x), vn = fmaf(-sl[t], dxn, m.y);
+          if (okx && vx > bv[2 * t]) { bv[2 * t] = vx; bi[2 * t] = (unsigned)(px - s); }
+          if (okn && vn < bv[2 * t + 1]) { bv[2 * t + 1] = vn; bi[2 * t + 1] = (unsigned)(pn - s); }
         }
       }
     }
-    // warp-wide winners: the rounded value by REDUX, then the lowest index
-    // holding it (a candidate only steers the guess, so rounding is harmless)
+    // warp-wide winners: the value by REDUX, then the lowest position holding it
     int64_t cand = s;
 #pragma unroll
     for (int c = 0; c < LTTB_NC; c++) {
       const bool mx = (c & 1) == 0;
-      const unsigned key = bi[c] >= 0 ? f32_key(__double2float_rn(bv[c])) : (mx ? 0u : 0xffffffffu);
+      const bool has = bi[c] != 0xffffffffu;
+      const unsigned key = has ? f32_key(bv[c]) : (mx ? 0u : 0xffffffffu);
       const unsigned w = mx ? __reduce_max_sync(0xffffffffu, key) : __reduce_min_sync(0xffffffffu, key);
-      const unsigned rel = (bi[c] >= 0 && key == w) ? (unsigned)(bi[c] - s) : 0xffffffffu;
-      const unsigned r = __reduce_min_sync(0xffffffffu, rel);
+      const unsigned r = __reduce_min_sync(0xffffffffu, (has && key == w) ? bi[c] : 0xffffffffu);
       if (lane == c) cand = r == 0xffffffffu ? s : s + (int64_t)r;
     }
     // sort the NC candidates by index (odd-even transposition over lanes)
@@ -738,7 +737,7 @@ struct LttbRound1 {  // per non-empty bucket: round-1 plan and its sub-block lis
 //               settles at once.
 // ctr: [2] |D|, [6..7] sub-blocks listed (int64).
 template <int YDT>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, 3)
 lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
                   const LttbSBArrays A, double2* cent, float2* yr, int32_t* bcnt, int32_t* nonempty, int32_t* rank,
                   int64_t* counts, int64_t* ext, uint8_t* T, uint8_t* C, uint8_t* entry, int64_t* picks,
