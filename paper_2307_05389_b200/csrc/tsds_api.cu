@@ -645,88 +645,90 @@ static inline unsigned cap_grid(int64_t want, int64_t cap) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cap, want));
 }
 
-// Large buckets: prepass -> guess walk on the reduced problem -> verify/fix
-// rounds.  One stream-ordered sequence, no host round trip; consecutive
-// kernels are chained with programmatic dependent launch.
+// Large buckets (tsds_lttb_large.cuh): sub-block summaries -> guess +
+// round-1 plan (cooperative) -> round-1 evaluation of the surviving
+// sub-blocks -> correction chains -> output.  One stream-ordered sequence,
+// no host round trip; consecutive kernels are chained with programmatic
+// dependent launch.
 int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
                    const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev) {
   RC_TRY(ensure(ctx, ctx->cent, (size_t)std::max<int64_t>(nb, 1) * sizeof(double2)));
   double2* cent = (double2*)ctx->cent.p;
   const int64_t NC = LTTB_NC;
-  const int64_t maxch = (n + LTTB_CH - 1) / LTTB_CH + nb + 1;
+  // sub-block size: 32 or 64 vectors of 16 bytes (>= 64 sub-blocks per bucket)
+  const int64_t EPV = 16 / dtype_size(ydt);
+  const int64_t vpb = (n / std::max<int64_t>(nb, 1)) / EPV;  // vectors per bucket
+  int SBV = 32;  // <= 64: a warp's group (32 sub-blocks) stays short enough to balance the grid
+  while (SBV < 64 && (int64_t)SBV * 2 * 64 <= vpb) SBV *= 2;
+  const int64_t SB = (int64_t)SBV * EPV;
+  const int64_t NG = (n + SB - 1) / SB;
+  const int64_t maxsb = NG + nb + 1;  // sub-blocks touched by the buckets (boundaries twice)
   const int64_t maxseg = nb / LTTB_SEG + 2;
-  const int64_t nlb = (nb + LTTB_LB - 1) / LTTB_LB;
+  const int64_t nbl = (int64_t)ctx->sms * 16;  // >= blocks of the cooperative guess kernel
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-  const size_t zero_bytes = al(64) + al(256) + al(24 * (nlb + 1)) + al(4 * nb);  // counts, ctr, link, lock
-  const size_t need = zero_bytes + al(8 * (nb + 1)) + al(4 * maxch) + al(4 * nb) + al(4 * nb) + al(32 * nb) +
-                      al(16 * nb) + al(sizeof(LttbChunkPart) * maxch) + al(8 * NC * nb) + al(NC * nb) +
-                      al(NC * maxseg) + al(maxseg) + al(8 * (nb + 4)) + al(4 * nb) + al(sizeof(LttbPlan) * nb) +
-                      al(sizeof(AreaCand) * nb) + al(4 * nb) + al(sizeof(AreaCand) * maxch) + al(sizeof(int2) * maxch);
+  const size_t zero_bytes = al(64) + al(256) + al(4 * nb);  // counts, ctr, lock
+  const size_t need = zero_bytes + al(8 * NG) + al(4 * NG) + al(8 * NG) + (xf ? al(8 * NG) : 0) + al(8 * nb) +
+                      al(4 * nbl) + al(4 * nb) * 4 + al(8 * NC * nb) + al(NC * nb) + al(NC * maxseg) + al(maxseg) +
+                      al(8 * (nb + 4)) + al(sizeof(LttbRound1) * nb) + al(sizeof(AreaCand) * maxsb) +
+                      al(8 * maxsb) * 2;
   RC_TRY(ensure(ctx, ctx->lscr, need));
   char* p = (char*)ctx->lscr.p;
   auto take = [&](size_t bytes) { char* r = p; p += al(bytes); return r; };
-  int64_t* counts = (int64_t*)take(64);  // zeroed block: counts, ctr, link, lock
+  int64_t* counts = (int64_t*)take(64);  // zeroed block: counts, ctr, lock
   int32_t* ctr = (int32_t*)take(256);
-  unsigned long long* link = (unsigned long long*)take(24 * (nlb + 1));
   int32_t* lock = (int32_t*)take(4 * nb);
-  int64_t* cstart = (int64_t*)take(8 * (nb + 1));
-  int32_t* cb = (int32_t*)take(4 * maxch);
-  int32_t* rank = (int32_t*)take(4 * nb);
+  LttbSBArrays A;
+  A.SB = SB;
+  A.SBV = SBV;
+  A.mm = (float2*)take(8 * NG);
+  A.am = (uint32_t*)take(4 * NG);
+  A.sy = (double*)take(8 * NG);
+  A.sx = xf ? (double*)take(8 * NG) : nullptr;
+  float2* yr = (float2*)take(8 * nb);
+  int32_t* bcnt = (int32_t*)take(4 * nbl);
   int32_t* nonempty = (int32_t*)take(4 * nb);
-  double4* bbox = (double4*)take(32 * nb);
-  double2* slopes = (double2*)take(16 * nb);
-  LttbChunkPart* cpart = (LttbChunkPart*)take(sizeof(LttbChunkPart) * maxch);
+  int32_t* rank = (int32_t*)take(4 * nb);
+  int32_t* arrive = (int32_t*)take(4 * nb);
+  int32_t* list_a = (int32_t*)take(4 * nb);
   int64_t* ext = (int64_t*)take(8 * NC * nb);
   uint8_t* T = (uint8_t*)take(NC * nb);
   uint8_t* C = (uint8_t*)take(NC * maxseg);
   uint8_t* entry = (uint8_t*)take(maxseg);
   int64_t* walkout = (int64_t*)take(8 * (nb + 4));
-  int32_t* list_a = (int32_t*)take(4 * nb);
-  LttbPlan* plan = (LttbPlan*)take(sizeof(LttbPlan) * nb);
-  AreaCand* cbest = (AreaCand*)take(sizeof(AreaCand) * nb);
-  int32_t* arrive = (int32_t*)take(4 * nb);
-  AreaCand* apart = (AreaCand*)take(sizeof(AreaCand) * maxch);
-  int2* plist = (int2*)take(sizeof(int2) * maxch);
+  LttbRound1* r1 = (LttbRound1*)take(sizeof(LttbRound1) * nb);
+  AreaCand* part = (AreaCand*)take(sizeof(AreaCand) * maxsb);
+  int64_t* slots = (int64_t*)take(8 * maxsb);
+  int64_t* wl = (int64_t*)take(8 * maxsb);
   int64_t* picks = walkout + 2;
   const int mode = lttb_exact_mode();
   const int64_t avg = (n - 2) / std::max<int64_t>(nb, 1);
   const int exact = mode == 1 ? 1 : (mode == 2 ? 0 : (avg <= 1024 ? 1 : 0));
-  const unsigned gw8 = cap_grid((nb + 7) / 8, (int64_t)ctx->sms * 16);
   const int vec_ok = ((uintptr_t)y & 15) == 0 ? 1 : 0;
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
   RC_TRY(prof_mark(ctx, ev, false));
   CUDA_TRY(cudaMemsetAsync(counts, 0, zero_bytes, ctx->stream));
-  // ---- layout, sampling, slopes
-  RC_TRY(launch_pdl(ctx, lttb_layout_kernel, (unsigned)std::max<int64_t>(1, nlb), 1024, 0, off, nb, cstart, cb, rank,
-                    nonempty, counts, link));
-  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_sample_kernel<YD>, gw8, 256, 0, y, off, nb, bbox)));
-  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_slopes_kernel<YD>, cap_grid((nb + 255) / 256, 1 << 20), 256, 0, xf, drop,
-                                    y, off, nb, n, bbox, slopes)));
-  // ---- chunk prepass + per-bucket merge (centroids, candidates)
-  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_chunk_prepass_kernel<YD>,
-                                    one_wave(ctx, lttb_chunk_prepass_kernel<YD>, 256, LTTB_RING_BYTES), 256,
-                                    LTTB_RING_BYTES, xf, drop, y, off, cstart, cb, counts, slopes, cpart, vec_ok)));
-  // ---- guess (merge, transition tables, composed chain) + round-1 plan:
-  //      one cooperative launch; then round-1 evaluation of the unpruned
-  //      pieces, the correction chains and the output
+  // ---- 1. sub-block summaries (the one streaming pass over y)
+  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_sb_kernel<YD>,
+                                    one_wave(ctx, lttb_sb_kernel<YD>, LTTB_SB_WARPS * 32, LTTB_SB_SMEM),
+                                    LTTB_SB_WARPS * 32, LTTB_SB_SMEM, xf, drop, y, n, vec_ok, A)));
+  // ---- 2. guess + round-1 plan (cooperative)
   const int64_t cap = 32768;
   YDT_SWITCH(ydt, ({
                auto kg = lttb_guess_kernel<YD>;
                cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(cap + 16));
-               RC_TRY(launch_coop(ctx, kg, one_wave(ctx, kg, 256, (size_t)(cap + 16)), 256, (size_t)(cap + 16), xf,
-                                  drop, y, n, off, nb, cent, (const double2*)slopes, (const int64_t*)cstart,
-                                  (const int32_t*)nonempty, (const int64_t*)counts, (const LttbChunkPart*)cpart, ext,
-                                  T, C, entry, picks, plan, cbest, arrive, apart, plist, list_a, ctr, exact, cap));
+               const unsigned gg = std::min<unsigned>(one_wave(ctx, kg, 256, (size_t)(cap + 16)), (unsigned)nbl);
+               RC_TRY(launch_coop(ctx, kg, gg, 256, (size_t)(cap + 16), xf, drop, y, n, off, nb, A, cent, yr, bcnt,
+                                  nonempty, rank, counts, ext, T, C, entry, picks, r1, arrive, slots, wl, list_a, ctr,
+                                  exact, cap));
              }));
+  // ---- 3. round-1 evaluation, 4. correction chains, 5. output
   YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_eval_kernel<YD>, one_wave(ctx, lttb_eval_kernel<YD>, 256), 256, 0, xf,
-                                    drop, y, n, off, nb, (const double2*)cent, (const int64_t*)cstart,
-                                    (const int32_t*)nonempty, (const int64_t*)counts, (const LttbPlan*)plan,
-                                    (const AreaCand*)cbest, arrive, apart, (const int2*)plist, picks, list_a, ctr,
-                                    vec_ok)));
+                                    drop, y, n, off, nb, A, (const double2*)cent, (const int32_t*)nonempty,
+                                    (const int64_t*)counts, (const LttbRound1*)r1, arrive, part,
+                                    (const int64_t*)slots, (const int64_t*)wl, picks, list_a, ctr, vec_ok)));
   YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_chain_kernel<YD>, one_wave(ctx, lttb_chain_kernel<YD>, 256), 256, 0,
-                                    xf, drop, y, n, off, nb, (const double2*)cent, (const double2*)slopes,
-                                    (const int64_t*)cstart, (const int32_t*)nonempty, (const int64_t*)counts,
-                                    (const LttbChunkPart*)cpart, (const int64_t*)ext, picks, (const int32_t*)list_a,
+                                    xf, drop, y, n, off, nb, (const double2*)cent, (const int32_t*)nonempty,
+                                    (const int64_t*)counts, A, (const int64_t*)ext, picks, (const int32_t*)list_a,
                                     lock, ctr, vec_ok)));
   RC_TRY(launch_pdl(ctx, lttb_emit_kernel, cap_grid((nb + 257) / 256, 1024), 256, 0, (const int64_t*)picks,
                     (const int64_t*)counts, n, map, out_dev + 1, out_dev));
@@ -1055,12 +1057,12 @@ int64_t tsds_ctx_stat(tsds_ctx* ctx, const char* name) {
     if (cudaStreamSynchronize(ctx->stream) == cudaSuccess) {
       ctx->lttb_rounds = ctx->h_lstat[3];   // correction-chain steps
       ctx->lttb_dirty1 = ctx->h_lstat[2];   // |D|: buckets whose predecessor changed in round 1
-      ctx->lttb_pieces = ctx->h_lstat[8];   // pieces evaluated in the chains
-      ctx->lttb_pieces1 = ctx->h_lstat[9];  // pieces evaluated in round 1
+      ctx->lttb_pieces = ctx->h_lstat[8];   // sub-blocks evaluated in the chains
+      ctx->lttb_pieces1 = ctx->h_lstat[6];  // sub-blocks evaluated in round 1 (low word)
     }
     ctx->lstat_pending = false;
   }
-  if (n.rfind("lttb_ts", 0) == 0 && n.size() == 8 && ctx->h_lstat) {  // debug: guess-kernel phase times (ns)
+  if (n.rfind("lttb_ts", 0) == 0 && n.size() == 8 && ctx->h_lstat) {  // guess-kernel phase times (ns)
     cudaStreamSynchronize(ctx->stream);
     const unsigned long long* t = (const unsigned long long*)(ctx->h_lstat + 16);
     const int i = n[7] - '0';

@@ -1,23 +1,34 @@
-// tsds_lttb_large.cuh -- LTTB for large buckets: guess, verify, fix.
+// tsds_lttb_large.cuh -- LTTB for large buckets: summarise, guess, prune, fix.
 //
-// The reference walk (_kernels.py:375-480) is a chain pick_k = f_k(pick_{k-1})
-// over buckets of up to ~50k points.  Instead of walking them one after
-// another:
-//   1. chunk-parallel prepass (one pass over the data): every bucket's
-//      centroid and LTTB_NC candidate picks -- argmax / argmin of
-//      y - s*x for LTTB_K slopes s spanning the slopes (cy-ay)/(cx-ax) the
-//      bucket can see (from a sampled bounding box of its neighbours);
-//   2. the chain restricted to the candidates is solved exactly by composing
-//      per-bucket transition tables (parallel segments + a short sequential
-//      pass over segment entries) -- a guess for every pick;
-//   3. chunk-parallel verification: f_k evaluated exactly over ALL points of
-//      every bucket with the guessed predecessor; buckets whose exact pick
-//      differs are corrected and their successors re-verified, round by
-//      round, until pick_k = f_k(pick_{k-1}) everywhere.
-// The fixed point is exactly the reference's sequence (same area formula,
-// first max, NaN never wins).  Centroids: the reference's sequential order
-// for small buckets (exact mode), a fixed pairwise tree otherwise (can only
-// move an area in its last bits: a pick differs only at a 1e-15 tie).
+// The reference walk (_kernels.py:375-480) is a chain
+// pick_k = f_k(pick_{k-1}) over buckets of up to ~50k points.  Instead of
+// walking the buckets one after another:
+//   1. lttb_sb_kernel -- ONE streaming pass over y: for every sub-block of
+//      SB = 512 bytes of y (64 f64 / 128 f32 / ... points, aligned to the
+//      series start) its max (rounded up to f32), min (rounded down), the
+//      offsets of its first max / min and its f64 sum (explicit x: also the
+//      sum of x).  ~4% extra bytes written.
+//   2. lttb_guess_kernel (cooperative, grid barriers between phases):
+//      non-empty bucket list; per bucket the centroid and y-range; LTTB_NC
+//      candidate points (the sub-block extremes that maximise / minimise
+//      y - s*x for LTTB_K slopes s spanning the slopes the bucket can see);
+//      the chain restricted to the candidates is solved exactly by composing
+//      per-bucket transition tables -> a guessed pick for every bucket; then
+//      the round-1 plan: with the guessed predecessor, the exact best
+//      candidate area B and, per sub-block, a rigorous upper bound of the
+//      area (from its max/min); sub-blocks whose bound is below B cannot
+//      hold the first max and are pruned.
+//   3. lttb_eval_kernel -- exact reference areas over the surviving
+//      sub-blocks (warp per sub-block); the warp completing a bucket settles
+//      it; buckets whose predecessor changed form the list D.
+//   4. lttb_chain_kernel -- correction chains from D (re-plan with the
+//      current predecessor, evaluate, lock-protected store, continue while
+//      the pick changes).
+// The fixed point is exactly the reference's sequence (same area formula in
+// the same f64 operation order without FMA, first max, NaN never wins).
+// Centroids: the reference's sequential order for small buckets (exact
+// mode), otherwise a fixed tree order over sub-block sums (moves an area only
+// in its last bits: a pick can differ only at a ~1e-15 relative tie).
 #pragma once
 
 #include "tsds_lttb.cuh"
@@ -25,649 +36,405 @@
 
 namespace tsds {
 
-#ifndef LTTB_K_N
-#define LTTB_K_N 7
-#endif
-constexpr int LTTB_K = LTTB_K_N;     // candidate slopes per bucket
+constexpr int LTTB_K = 7;            // steering slopes per bucket
 constexpr int LTTB_NC = 2 * LTTB_K;  // candidates per bucket (argmax + argmin per slope)
-#ifndef LTTB_CH_N
-#define LTTB_CH_N 4096
-#endif
-constexpr int64_t LTTB_CH = LTTB_CH_N;  // points per chunk
 constexpr int LTTB_SEG = 64;         // buckets per composed segment
-#ifndef LTTB_R1_U
-#define LTTB_R1_U 16
-#endif
 
-// Pieces: the series is cut into globally aligned chunks of LTTB_CH points;
-// piece q of bucket [s, e) is its intersection with chunk s/LTTB_CH + q
-// (aligned starts let the scans use 128-bit loads).
-__device__ __forceinline__ int64_t lttb_npieces(int64_t s, int64_t e) {
-  return e > s ? (e - 1) / LTTB_CH - s / LTTB_CH + 1 : 0;
-}
-__device__ __forceinline__ void lttb_piece(int64_t s, int64_t e, int64_t q, int64_t& cs, int64_t& ce) {
-  const int64_t g = s / LTTB_CH + q;
-  cs = g * LTTB_CH > s ? g * LTTB_CH : s;
-  ce = (g + 1) * LTTB_CH < e ? (g + 1) * LTTB_CH : e;
-}
-
-// slope j of bucket k's steering grid (prepass and pruning bounds)
-__device__ __forceinline__ float lttb_slope(double2 sr, int j) {
-  return __double2float_rn(__dadd_rn(sr.x, __dmul_rn(__dsub_rn(sr.y, sr.x), __ddiv_rn((double)j, (double)(LTTB_K - 1)))));
-}
-
-struct LttbChunkPart {  // per-chunk partial of the prepass
-  float v[LTTB_NC];
-  int64_t i[LTTB_NC];
-  double sx, sy;
+// elements per 16-byte vector
+template <int YDT>
+struct SBG {
+  static constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
 };
 
-
-// piece layout + non-empty bucket list, one pass (chained scan): block t
-// (ticket order) takes LTTB_LB buckets, scans them, waits for block t-1's
-// inclusive prefix and publishes its own.
-// cstart[k] = first piece of bucket k, cb[c] = bucket of piece c,
-// rank[k] = index among non-empty buckets, nonempty[j] = k,
-// counts = {L, NCH, max pieces per bucket, ticket}; link[3t..3t+2] =
-// inclusive prefix of block t + ready flag, zeroed by the caller.
-constexpr int LTTB_LR = 4;                // buckets per thread
-constexpr int LTTB_LB = 1024 * LTTB_LR;   // buckets per block
-__global__ void __launch_bounds__(1024)
-lttb_layout_kernel(const int64_t* off, int64_t nb, int64_t* cstart, int32_t* cb, int32_t* rank, int32_t* nonempty,
-                   int64_t* counts, unsigned long long* link) {
-  pdl_launch_dependents();
-  pdl_wait();
-  __shared__ int64_t wt[2][32];
-  __shared__ int64_t base[2];
-  __shared__ int tk;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) tk = (int)atomicAdd((unsigned long long*)&counts[3], 1ull);
-  __syncthreads();
-  const int t = tk;
-  const int64_t k0 = (int64_t)t * LTTB_LB + (int64_t)tid * LTTB_LR;
-  int64_t np[LTTB_LR], a = 0, b = 0, mx = 0;
-#pragma unroll
-  for (int r = 0; r < LTTB_LR; r++) {
-    const int64_t k = k0 + r;
-    np[r] = k < nb ? lttb_npieces(__ldg(off + k), __ldg(off + k + 1)) : 0;
-    a += np[r];
-    b += np[r] > 0;
-    mx = np[r] > mx ? np[r] : mx;
-  }
-  const unsigned long long wmx = __reduce_max_sync(0xffffffffu, (unsigned)mx);  // one atomic per warp
-  if (lane == 0 && wmx) atomicMax((unsigned long long*)&counts[2], wmx);
-  // block exclusive scan of (a, b)
-  int64_t ia = a, ib = b;
-#pragma unroll
-  for (int m = 1; m < 32; m <<= 1) {
-    const int64_t ta = __shfl_up_sync(0xffffffffu, ia, m), tb = __shfl_up_sync(0xffffffffu, ib, m);
-    if (lane >= m) { ia += ta; ib += tb; }
-  }
-  if (lane == 31) { wt[0][wid] = ia; wt[1][wid] = ib; }
-  __syncthreads();
-  if (wid == 0) {
-    int64_t xa = wt[0][lane], xb = wt[1][lane];
-#pragma unroll
-    for (int m = 1; m < 32; m <<= 1) {
-      const int64_t ta = __shfl_up_sync(0xffffffffu, xa, m), tb = __shfl_up_sync(0xffffffffu, xb, m);
-      if (lane >= m) { xa += ta; xb += tb; }
-    }
-    wt[0][lane] = xa;
-    wt[1][lane] = xb;
-    if (lane == 31) {
-      // chained prefix: wait for block t-1, publish ours
-      // (link[3t] = pieces, link[3t+1] = non-empty buckets, link[3t+2] = ready)
-      unsigned long long pa = 0, pb = 0;
-      if (t > 0) {
-        volatile unsigned long long* lp = link + 3 * (t - 1);
-        while (lp[2] == 0) {
-        }
-        __threadfence();
-        pa = lp[0];
-        pb = lp[1];
-      }
-      base[0] = (int64_t)pa;
-      base[1] = (int64_t)pb;
-      volatile unsigned long long* me = link + 3 * t;
-      me[0] = pa + (unsigned long long)xa;
-      me[1] = pb + (unsigned long long)xb;
-      __threadfence();
-      atomicExch(link + 3 * t + 2, 1ull);
-      if ((int64_t)(t + 1) * LTTB_LB >= nb) {
-        counts[0] = (int64_t)(pb + xb);
-        counts[1] = (int64_t)(pa + xa);
-      }
-    }
-  }
-  __syncthreads();
-  int64_t pa = base[0] + (wid ? wt[0][wid - 1] : 0) + ia - a;
-  int64_t pb = base[1] + (wid ? wt[1][wid - 1] : 0) + ib - b;
-#pragma unroll
-  for (int r = 0; r < LTTB_LR; r++) {
-    const int64_t k = k0 + r;
-    if (k >= nb) break;
-    cstart[k] = pa;
-    rank[k] = np[r] ? (int32_t)pb : -1;
-    if (np[r]) nonempty[pb] = (int32_t)k;
-    for (int64_t c = 0; c < np[r]; c++) cb[pa + c] = (int32_t)k;
-    pa += np[r];
-    pb += np[r] > 0;
-  }
-}
-
-// sampled bounding box {ymin, ymax, ymean} of every bucket (warp per bucket,
-// <= 64 strided samples; only steers the candidate slopes)
-template <int YDT>
-__global__ void lttb_sample_kernel(const void* y, const int64_t* off, int64_t nb, double4* bbox) {
-  pdl_launch_dependents();
-  pdl_wait();
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t k = gw; k < nb; k += nw) {
-    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-    if (e <= s) continue;
-    const int64_t st = (e - s + 63) / 64;
-    double mn = 1e300, mx = -1e300, sum = 0.0;
-    int cnt = 0;
-    const int64_t i0 = s + lane * st, i1 = s + (lane + 32) * st;
-    const double v0 = i0 < e ? yd<YDT>(y, i0) : __longlong_as_double(0x7ff8000000000000ll);
-    const double v1 = i1 < e ? yd<YDT>(y, i1) : __longlong_as_double(0x7ff8000000000000ll);
-    if (v0 == v0) { mn = fmin(mn, v0); mx = fmax(mx, v0); sum += v0; cnt++; }
-    if (v1 == v1) { mn = fmin(mn, v1); mx = fmax(mx, v1); sum += v1; cnt++; }
-    for (int m = 16; m >= 1; m >>= 1) {
-      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, m));
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, m));
-      sum += __shfl_xor_sync(0xffffffffu, sum, m);
-      cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
-    }
-    if (lane == 0) bbox[k] = make_double4(mn, mx, cnt ? sum / cnt : 0.0, 0.0);
-  }
-}
-
-// slope interval of bucket k: a in the previous non-empty bucket's widened
-// box, c the next bucket's centroid box (or the last point)
-template <int YDT>
-__global__ void lttb_slopes_kernel(const double* xin, const int* drop, const void* y, const int64_t* off, int64_t nb,
-                                   int64_t n, const double4* bbox, double2* slopes) {
-  pdl_launch_dependents();
-  pdl_wait();
-  const double* x = eff_x(xin, drop);
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nb; k += (int64_t)gridDim.x * blockDim.x) {
-    if (__ldg(off + k + 1) <= __ldg(off + k)) continue;
-    int64_t kp = k - 1;
-    while (kp >= 0 && __ldg(off + kp + 1) <= __ldg(off + kp)) kp--;
-    double ax0, ax1, ay0, ay1;
-    if (kp < 0) {
-      ax0 = ax1 = xd(x, 0);
-      ay0 = ay1 = yd<YDT>(y, 0);
-    } else {
-      const double4 b = bbox[kp];
-      const double w = 0.5 * (b.y - b.x);
-      ax0 = xd(x, __ldg(off + kp));
-      ax1 = xd(x, __ldg(off + kp + 1) - 1);
-      ay0 = b.x - w;
-      ay1 = b.y + w;
-    }
-    double cx0, cx1, cy0, cy1;
-    if (k == nb - 1 || __ldg(off + k + 2) <= __ldg(off + k + 1)) {
-      cx0 = cx1 = xd(x, n - 1);
-      cy0 = cy1 = yd<YDT>(y, n - 1);
-    } else {
-      const double4 b = bbox[k + 1];
-      const double w = 0.5 * (b.y - b.x);
-      cx0 = xd(x, __ldg(off + k + 1));
-      cx1 = xd(x, __ldg(off + k + 2) - 1);
-      cy0 = b.z - w;
-      cy1 = b.z + w;
-    }
-    double lo = 1e300, hi = -1e300;
-    for (int i = 0; i < 16; i++) {
-      const double ax = (i & 1) ? ax1 : ax0, ay = (i & 2) ? ay1 : ay0;
-      const double cx = (i & 4) ? cx1 : cx0, cy = (i & 8) ? cy1 : cy0;
-      const double dx = cx - ax;
-      if (!(dx > 0.0)) continue;
-      const double sl = (cy - ay) / dx;
-      lo = fmin(lo, sl);
-      hi = fmax(hi, sl);
-    }
-    if (!(lo <= hi)) { lo = 0.0; hi = 0.0; }
-    slopes[k] = make_double2(lo, hi);
-  }
-}
-
-// warp per piece: candidate partials (fp32 projections relative to the
-// bucket's first point; they only steer the guess) and fixed-order sums.
-// Scalar form: explicit x or a y base that is not 16-byte aligned.
-template <int YDT>
-__device__ __forceinline__ void lttb_prepass_scalar(const double* x, const void* y, const int64_t* off,
-                                                    const int64_t* cstart, const int32_t* cb, const int64_t* counts,
-                                                    const double2* slopes, LttbChunkPart* part) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t NCH = counts[1];
-  for (int64_t c = gw; c < NCH; c += nw) {
-    const int64_t k = cb[c];
-    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-    int64_t cs, ce;
-    lttb_piece(s, e, c - cstart[k], cs, ce);
-    const double2 sr = slopes[k];
-    float sl[LTTB_K];
-#pragma unroll
-    for (int j = 0; j < LTTB_K; j++) sl[j] = lttb_slope(sr, j);
-    const double xs = xd(x, s), ys0 = yd<YDT>(y, s);
-    const double yb = ys0 == ys0 ? ys0 : 0.0;
-    float cmax[LTTB_K], cmin[LTTB_K];
-    int32_t imax[LTTB_K], imin[LTTB_K];
-#pragma unroll
-    for (int j = 0; j < LTTB_K; j++) { cmax[j] = -INFINITY; cmin[j] = INFINITY; imax[j] = -1; imin[j] = -1; }
-    double px = 0.0, py = 0.0;
-    // 8 loads in flight per lane; the doubles are folded into the sums and
-    // narrowed to fp32 right away to keep the register footprint small
-    for (int64_t i0 = cs + lane; i0 < ce; i0 += 8 * 32) {
-      float vf[8], dxf[8];
-      {
-        double vy[8];
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-          const int64_t i = i0 + u * 32;
-          vy[u] = i < ce ? yd<YDT>(y, i) : __longlong_as_double(0x7ff8000000000000ll);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-          const int64_t i = i0 + u * 32;
-          double vx = 0.0;
-          if (i < ce) {
-            py = __dadd_rn(py, vy[u]);
-            vx = xd(x, i);
-            if (x) px = __dadd_rn(px, vx);
-          }
-          vf[u] = vy[u] == vy[u] ? (float)(vy[u] - yb) : __int_as_float(0x7fc00000);
-          dxf[u] = (float)(vx - xs);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; u++) {
-        if (vf[u] == vf[u]) {
-          const int32_t ii = (int32_t)(i0 + u * 32 - s);
-#pragma unroll
-          for (int j = 0; j < LTTB_K; j++) {
-            const float t = fmaf(-sl[j], dxf[u], vf[u]);
-            if (t > cmax[j]) { cmax[j] = t; imax[j] = ii; }
-            if (t < cmin[j]) { cmin[j] = t; imin[j] = ii; }
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) {
-      px = __dadd_rn(px, __shfl_xor_sync(0xffffffffu, px, m));
-      py = __dadd_rn(py, __shfl_xor_sync(0xffffffffu, py, m));
-#pragma unroll
-      for (int j = 0; j < LTTB_K; j++) {
-        float ov = __shfl_xor_sync(0xffffffffu, cmax[j], m);
-        int32_t oi = __shfl_xor_sync(0xffffffffu, imax[j], m);
-        if (oi >= 0 && (imax[j] < 0 || ov > cmax[j] || (ov == cmax[j] && oi < imax[j]))) { cmax[j] = ov; imax[j] = oi; }
-        ov = __shfl_xor_sync(0xffffffffu, cmin[j], m);
-        oi = __shfl_xor_sync(0xffffffffu, imin[j], m);
-        if (oi >= 0 && (imin[j] < 0 || ov < cmin[j] || (ov == cmin[j] && oi < imin[j]))) { cmin[j] = ov; imin[j] = oi; }
-      }
-    }
-    if (lane < LTTB_NC) {
-      const int j = lane >> 1;
-      float v = 0.0f;
-      int32_t ii = -1;
-#pragma unroll
-      for (int q = 0; q < LTTB_K; q++)
-        if (q == j) { v = (lane & 1) ? cmin[q] : cmax[q]; ii = (lane & 1) ? imin[q] : imax[q]; }
-      part[c].v[lane] = v;
-      part[c].i[lane] = ii < 0 ? -1 : s + ii;
-    }
-    if (lane == 0) {
-      part[c].sx = px;
-      part[c].sy = py;
-    }
-  }
-}
-
-#ifndef LTTB_PV_N
-#define LTTB_PV_N 8
-#endif
-constexpr int LTTB_PV = LTTB_PV_N;  // 128-bit vectors per lane per batch
-constexpr int LTTB_BV = 32 * LTTB_PV;  // vectors per warp batch
-#ifndef LTTB_RING_D
-#define LTTB_RING_D 3
-#endif
-constexpr int LTTB_D = LTTB_RING_D;   // batches in flight per warp
-constexpr int LTTB_WARPS = 8;         // warps per CTA of the streaming kernels
-constexpr size_t LTTB_RING_BYTES = (size_t)LTTB_WARPS * LTTB_D * LTTB_BV * 16;
-
-__device__ __forceinline__ unsigned f32_key(float f) {  // order-preserving (no NaN)
+// order-preserving u32 key of a float (no NaN)
+__device__ __forceinline__ unsigned f32_key(float f) {
   const unsigned b = __float_as_uint(f);
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
-
-__device__ __forceinline__ uint32_t lttb_smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
+__device__ __forceinline__ float f32_unkey(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
-// Per-warp streaming ring over the warp's contiguous vector range [V0, V1):
-// batch t (LTTB_BV vectors) is copied by cp.async (16 B per lane-vector,
-// L2 only) into slot t % LTTB_D, LTTB_D batches in flight.  Every lane
-// copies and later reads its own vectors, so completion is tracked per
-// lane with commit/wait groups and no warp synchronisation is needed.
-// Bytes in flight live in shared memory, not registers.
-struct LttbRing {
-  const uint4* src;
-  uint32_t sbase;
-  int64_t V0, V1;
-  __device__ __forceinline__ void fill(int64_t t, int lane) const {
-    const int64_t b = V0 + t * LTTB_BV;
-    const int64_t r = V1 - b;
-    const int rem = r < LTTB_BV ? (int)r : LTTB_BV;  // vectors of the batch inside the range (may be <= 0)
-    const uint32_t d = sbase + (uint32_t)((t % LTTB_D) * LTTB_BV + lane) * 16u;
-    const uint4* g = src + b + lane;
-#pragma unroll
-    for (int u = 0; u < LTTB_PV; u++)
-      if (u * 32 + lane < rem)
-        asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(d + (uint32_t)(u * 32) * 16u),
-                     "l"(g + u * 32)
-                     : "memory");
-    asm volatile("cp.async.commit_group;" ::: "memory");
+struct LttbSBArrays {
+  int64_t SB;     // points per sub-block = SBV * EPV (chosen per call from the bucket size)
+  int SBV;        // 16-byte vectors per sub-block: a power of two in [32, 512]
+  float2* mm;     // (max rounded up, min rounded down) over non-NaN points; (-inf, +inf) if none
+  uint32_t* am;   // offset of the first max | offset of the first min << 16 (0xffff each if none)
+  double* sy;     // sum of y (NaN propagates, like the reference's centroid sums)
+  double* sx;     // sum of x (explicit x only)
+};
+
+// ---------------------------------------------------------------------------
+// 1. sub-block summaries.  Lane-owned sub-blocks: warp w takes 32
+// consecutive sub-blocks at a time, lane l sub-block 32w + l.  A round is
+// the next 8 vectors (128 bytes) of each of the 32 sub-blocks: it is copied
+// by cp.async as 8 warp instructions of four full 128-byte lines each into a
+// per-warp ring (LTTB_SB_D rounds = 12 KB in flight per warp, bytes in
+// shared memory rather than registers; XOR-swizzled so that the lane-owned
+// reads are conflict-free), then every lane folds its own 8 vectors: running
+// sum in index order, first max / first min of the outward-rounded values.
+constexpr int LTTB_SB_D = 3;          // rounds in flight per warp
+constexpr int LTTB_SB_WARPS = 8;      // warps per CTA
+constexpr int LTTB_SB_SMEM = LTTB_SB_WARPS * LTTB_SB_D * 4096;
+
+// running first max / first min in f64 (NaN never compares true); the
+// max/min start at -inf/+inf, so a sub-block whose non-NaN values are all
+// -inf (+inf) keeps the "none" offset and is resolved by lttb_sb_store
+struct SbAcc {
+  double mx, mn, s0, s1;
+  int amx, amn;
+  __device__ __forceinline__ void reset() {
+    mx = -INFINITY;
+    mn = INFINITY;
+    s0 = s1 = 0.0;
+    amx = amn = 0xffff;
   }
-  __device__ __forceinline__ void wait() const { asm volatile("cp.async.wait_group %0;" ::"n"(LTTB_D - 1) : "memory"); }
-  __device__ __forceinline__ void drain() const { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-  __device__ __forceinline__ uint4 get(int64_t t, int u, int lane) const {
-    uint4 r;
-    const uint32_t a = sbase + (uint32_t)((t % LTTB_D) * LTTB_BV + u * 32 + lane) * 16u;
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
-    return r;
+  __device__ __forceinline__ void fold(double d, int o, bool odd) {
+    if (odd) s1 = __dadd_rn(s1, d);
+    else s0 = __dadd_rn(s0, d);
+    if (d > mx) { mx = d; amx = o; }
+    if (d < mn) { mn = d; amn = o; }
   }
 };
 
-// piece c -> bucket k, bucket [s, e), piece [cs, ce)
-__device__ __forceinline__ void lttb_piece_of(const int64_t* off, const int64_t* cstart, const int32_t* cb, int64_t c,
-                                              int64_t& k, int64_t& s, int64_t& e, int64_t& cs, int64_t& ce) {
-  k = cb[c];
-  s = __ldg(off + k);
-  e = __ldg(off + k + 1);
-  lttb_piece(s, e, c - cstart[k], cs, ce);
-}
-
-// x offset (from the bucket start) of a lane's vector u in a batch, as the
-// steering projection uses it: dxl = (float)(batch start - s) + (float)(lane*EPV)
-__device__ __forceinline__ float lttb_dx(float dxl, int uoff) { return __fadd_rn(dxl, (float)uoff); }
-__device__ __forceinline__ float lttb_dxe(float dxb, int e) { return e == 0 ? dxb : __fadd_rn(dxb, (float)e); }
-
-// (a*b.x + c.x, a*b.y + c.y), each rounded once: fma.rn.f32x2
-__device__ __forceinline__ float2 lttb_ffma2(float a, float2 b, float2 c) {
-  float2 r;
-  asm("{.reg .b64 pa, pb, pc, pd;\n\t"
-      "mov.b64 pa, {%2, %2};\n\tmov.b64 pb, {%3, %4};\n\tmov.b64 pc, {%5, %6};\n\t"
-      "fma.rn.f32x2 pd, pa, pb, pc;\n\tmov.b64 {%0, %1}, pd;\n\t}"
-      : "=f"(r.x), "=f"(r.y)
-      : "f"(a), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-  return r;
-}
-
-// fold one 128-bit vector (elements i0 .. i0+EPV-1) into the batch extrema;
-// with CHECK only the elements rl+e in [0, len) (relative to the window) count.
-// Steering projection: fmaf(-slope, (float)(i - s) [as dxb + e], (float)(y - yb)).
-template <int YDT, bool CHECK>
-__device__ __forceinline__ void lttb_pv_fold(const uint4& q, int rl, int len, float dxb, double yb,
-                                             const float (&sl)[LTTB_K], float (&bm)[LTTB_K], float (&bn)[LTTB_K],
-                                             double& py) {
-  constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
-  float vf[EPV];
-#pragma unroll
-  for (int e = 0; e < EPV; e++) {
-    const double d = vget<YDT>(q, e);
-    const bool ok = !CHECK || (unsigned)(rl + e) < (unsigned)len;
-    if (ok) py = __dadd_rn(py, d);
-    vf[e] = ok ? __double2float_rn(__dsub_rn(d, yb)) : __int_as_float(0x7fc00000);
-  }
-  float dx[EPV];
-#pragma unroll
-  for (int e = 0; e < EPV; e++) dx[e] = lttb_dxe(dxb, e);
-#pragma unroll
-  for (int j = 0; j < LTTB_K; j++) {
-    float m = bm[j], n = bn[j];
-#pragma unroll
-    for (int e = 0; e < EPV; e += 2) {  // packed pair FMA (FFMA2), bit-identical to two fmaf
-      const float2 t = lttb_ffma2(-sl[j], make_float2(dx[e], dx[e + 1]), make_float2(vf[e], vf[e + 1]));
-      m = fmaxf(m, fmaxf(t.x, t.y));
-      n = fminf(n, fminf(t.x, t.y));
-    }
-    bm[j] = m;
-    bn[j] = n;
-  }
-}
-
-// Prepass, vector form (implicit x, 16-byte aligned y).  Each warp streams
-// a contiguous range of pieces through its LttbRing.  Per lane and batch only
-// the extremum VALUES are folded (3-input min/max); the batch that first
-// improved a lane's extremum is remembered (8-bit ids relative to the
-// piece's first batch) and the winning element is located afterwards by
-// re-reading that one batch from global memory (an L2 hit).  A batch that
-// straddles piece boundaries is folded once per piece, masked.
+// write sub-block g's summary (outward-rounded f32 extremes)
 template <int YDT>
-__device__ __forceinline__ void lttb_prepass_ring(const void* y, const int64_t* off, const int64_t* cstart,
-                                                  const int32_t* cb, int64_t NCH, const double2* slopes,
-                                                  LttbChunkPart* part, uint4* ring) {
-  constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
-  constexpr int BV = LTTB_BV;
-  const uint4* yv = (const uint4*)y;
+__device__ __forceinline__ void lttb_sb_store(const LttbSBArrays& A, const void* y, int64_t n, int64_t g, SbAcc& a) {
+  if (a.amx == 0xffff || a.amn == 0xffff) {  // rare: no point beat the +-inf start (all NaN or all +-inf)
+    for (int o = 0; o < A.SB && g * A.SB + o < n; o++) {
+      const double d = yd<YDT>(y, g * A.SB + o);
+      if (a.amx == 0xffff && d == -INFINITY) { a.mx = d; a.amx = o; }
+      if (a.amn == 0xffff && d == INFINITY) { a.mn = d; a.amn = o; }
+    }
+  }
+  A.mm[g] = make_float2(a.amx == 0xffff ? -INFINITY : __double2float_ru(a.mx),
+                        a.amn == 0xffff ? INFINITY : __double2float_rd(a.mn));
+  A.am[g] = (uint32_t)a.amx | ((uint32_t)a.amn << 16);
+  A.sy[g] = __dadd_rn(a.s0, a.s1);
+}
+
+template <int YDT>
+__global__ void __launch_bounds__(LTTB_SB_WARPS * 32)
+lttb_sb_kernel(const double* xin, const int* drop, const void* y, int64_t n, int vec_ok, LttbSBArrays A) {
+  pdl_launch_dependents();
+  pdl_wait();
+  constexpr int EPV = SBG<YDT>::EPV;
+  extern __shared__ uint4 sb_ring[];
+  const int64_t SB = A.SB;
+  const int SBV = A.SBV, RPG = SBV / 8;  // rounds per group of 32 sub-blocks
+  const double* x = eff_x(xin, drop);
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t p0 = NCH * gw / nw, p1 = NCH * (gw + 1) / nw;
-  if (p0 >= p1) return;
-  int64_t k, s, e, cs, ce;
-  lttb_piece_of(off, cstart, cb, p1 - 1, k, s, e, cs, ce);
-  const int64_t V1 = (ce + EPV - 1) / EPV;
-  lttb_piece_of(off, cstart, cb, p0, k, s, e, cs, ce);
-  const int64_t V0 = cs / EPV;
-  const LttbRing R{yv, lttb_smem_u32(ring + (size_t)wl * LTTB_D * BV), V0, V1};
-  const int64_t NBt = (V1 - V0 + BV - 1) / BV;
-#pragma unroll
-  for (int t = 0; t < LTTB_D; t++) R.fill(t, lane);
-  float sl[LTTB_K];
-  double yb = 0.0;
-  auto bucket_header = [&]() {
-    const double2 sr = slopes[k];
-#pragma unroll
-    for (int j = 0; j < LTTB_K; j++) sl[j] = lttb_slope(sr, j);
-    const double ys0 = yd<YDT>(y, s);
-    yb = ys0 == ys0 ? ys0 : 0.0;
-  };
-  bucket_header();
-  float cmax[LTTB_K], cmin[LTTB_K];
-  constexpr int NW = (LTTB_K + 3) / 4;
-  unsigned bmx[NW], bmn[NW];  // 8-bit batch id per slope (4 per word), 0xff = none
-#pragma unroll
-  for (int w = 0; w < NW; w++) bmx[w] = bmn[w] = ~0u;
-  double py = 0.0;
-  int64_t tfirst = 0;
-#pragma unroll
-  for (int j = 0; j < LTTB_K; j++) { cmax[j] = -INFINITY; cmin[j] = INFINITY; }
-  int64_t c = p0;
-  for (int64_t t = 0; t < NBt; t++) {
-    R.wait();
-    const int64_t bs = (V0 + t * BV) * EPV, be = (V0 + (t + 1) * BV) * EPV;
-    bool done = false;
-    for (;;) {
-      const int64_t lo = cs > bs ? cs : bs, hi = ce < be ? ce : be;
-      if (lo < hi) {
-        float bm[LTTB_K], bn[LTTB_K];
-#pragma unroll
-        for (int j = 0; j < LTTB_K; j++) { bm[j] = -INFINITY; bn[j] = INFINITY; }
-        const int len = (int)(hi - lo);
-        const int rlb = (int)(bs - lo) + lane * EPV;  // lane's first element, relative to lo
-        const float dxl = __fadd_rn((float)(bs - s), (float)(lane * EPV));
-        if (bs >= lo && be <= hi) {  // whole batch inside the piece (warp-uniform)
-#pragma unroll
-          for (int u = 0; u < LTTB_PV; u++)
-            lttb_pv_fold<YDT, false>(R.get(t, u, lane), 0, 0, lttb_dx(dxl, u * 32 * EPV), yb, sl, bm, bn, py);
-        } else {
-#pragma unroll
-          for (int u = 0; u < LTTB_PV; u++) {
-            const int rl = rlb + u * 32 * EPV;
-            const float dxb = lttb_dx(dxl, u * 32 * EPV);
-            if (rl >= 0 && rl + EPV <= len) lttb_pv_fold<YDT, false>(R.get(t, u, lane), rl, len, dxb, yb, sl, bm, bn, py);
-            else if (rl < len && rl + EPV > 0) lttb_pv_fold<YDT, true>(R.get(t, u, lane), rl, len, dxb, yb, sl, bm, bn, py);
-          }
-        }
-        const unsigned bid4 = (unsigned)(t - tfirst) * 0x01010101u;
-#pragma unroll
-        for (int j = 0; j < LTTB_K; j++) {
-          const unsigned msk = 0xffu << (8 * (j & 3));
-          if (bm[j] > cmax[j]) bmx[j >> 2] = (bmx[j >> 2] & ~msk) | (bid4 & msk);
-          if (bn[j] < cmin[j]) bmn[j >> 2] = (bmn[j >> 2] & ~msk) | (bid4 & msk);
-          cmax[j] = fmaxf(cmax[j], bm[j]);
-          cmin[j] = fminf(cmin[j], bn[j]);
-        }
+  const int64_t NG = (n + SB - 1) / SB;
+  const int64_t nvec = (n + EPV - 1) / EPV;
+  const uint4* yv = (const uint4*)y;
+  if (!vec_ok || x) {  // unaligned y or explicit x: plain lane-owned loads
+    for (int64_t gb = gw * 32; gb < NG; gb += nw * 32) {
+      const int64_t g = gb + lane;
+      SbAcc acc;
+      acc.reset();
+      double sumx = 0.0;
+      for (int o = 0; o < SB && g < NG; o++) {
+        const int64_t i = g * SB + o;
+        if (i >= n) break;
+        acc.fold(yd<YDT>(y, i), o, o & 1);
+        if (x) sumx = __dadd_rn(sumx, __ldg(x + i));
       }
-      if (ce > be) break;  // piece continues in the next batch
-      // ---- piece c complete: sums, winners, locate, emit
-#pragma unroll
-      for (int m = 16; m >= 1; m >>= 1) py = __dadd_rn(py, __shfl_xor_sync(0xffffffffu, py, m));
-      float myW = 0.0f, mysl = 0.0f;
-      int myb = -1, mywl = 0;
-#pragma unroll
-      for (int q = 0; q < LTTB_NC; q++) {
-        const int j = q >> 1;
-        const bool mn = q & 1;
-        const float v = mn ? cmin[j] : cmax[j];
-        const unsigned bid = ((mn ? bmn[j >> 2] : bmx[j >> 2]) >> (8 * (j & 3))) & 0xffu;
-        const unsigned key = f32_key(v);
-        const unsigned W = mn ? __reduce_min_sync(0xffffffffu, key) : __reduce_max_sync(0xffffffffu, key);
-        const unsigned tie = (key == W && bid != 0xffu) ? (bid * 32u + (unsigned)lane) : 0xffffffffu;
-        const unsigned win = __reduce_min_sync(0xffffffffu, tie);
-        const float wv = __shfl_sync(0xffffffffu, v, (int)(win & 31u));
-        if (lane == q) {
-          myW = wv;
-          mysl = sl[j];
-          myb = win == 0xffffffffu ? -1 : (int)(win >> 5);
-          mywl = (int)(win & 31u);
-        }
+      if (g < NG) {
+        lttb_sb_store<YDT>(A, y, n, g, acc);
+        if (x) A.sx[g] = sumx;
       }
-      int64_t found = -1;
-      if (lane < LTTB_NC && myb >= 0) {
-        const int64_t tb = tfirst + myb;
-        uint4 qv[LTTB_PV];
-#pragma unroll
-        for (int u = 0; u < LTTB_PV; u++) {
-          const int64_t v = V0 + tb * BV + u * 32 + mywl;
-          qv[u] = __ldg(yv + (v < V1 ? v : V1 - 1));
-        }
-        const int64_t tbs = (V0 + tb * BV) * EPV;
-        const float dxl = __fadd_rn((float)(tbs - s), (float)(mywl * EPV));
-#pragma unroll
-        for (int u = 0; u < LTTB_PV; u++) {
-          const int64_t i0 = tbs + (u * 32 + mywl) * EPV;
-          const float dxb = lttb_dx(dxl, u * 32 * EPV);
-#pragma unroll
-          for (int ee = 0; ee < EPV; ee++) {
-            const int64_t i = i0 + ee;
-            const double d = vget<YDT>(qv[u], ee);
-            const float vf = (i >= cs && i < ce) ? __double2float_rn(__dsub_rn(d, yb)) : __int_as_float(0x7fc00000);
-            const float tv = fmaf(-mysl, lttb_dxe(dxb, ee), vf);
-            if (found < 0 && tv == myW) found = i;
-          }
-        }
-      }
-      if (lane < LTTB_NC) {
-        part[c].v[lane] = myW;
-        part[c].i[lane] = found;
-      }
-      if (lane == 0) {
-        part[c].sx = 0.0;  // implicit x: the merge uses the closed form
-        part[c].sy = py;
-      }
-      // ---- next piece (may start inside this batch)
-      if (++c >= p1) { done = true; break; }
-      const int64_t kold = k;
-      lttb_piece_of(off, cstart, cb, c, k, s, e, cs, ce);
-      if (k != kold) bucket_header();
-#pragma unroll
-      for (int j = 0; j < LTTB_K; j++) { cmax[j] = -INFINITY; cmin[j] = INFINITY; }
-#pragma unroll
-      for (int w = 0; w < NW; w++) bmx[w] = bmn[w] = ~0u;
-      py = 0.0;
-      tfirst = t;
     }
-    if (done) break;
-    R.fill(t + LTTB_D, lane);
-  }
-  R.drain();
-}
-
-// Prepass kernel: ring-streamed vector form when x is implicit and y is
-// 16-byte aligned, else the scalar form.
-template <int YDT>
-__global__ void __launch_bounds__(256, 2)
-lttb_chunk_prepass_kernel(const double* xin, const int* drop, const void* y, const int64_t* off,
-                          const int64_t* cstart, const int32_t* cb, const int64_t* counts, const double2* slopes,
-                          LttbChunkPart* part, int vec_ok) {
-  pdl_launch_dependents();
-  pdl_wait();
-  extern __shared__ uint4 lttb_ring[];
-  const double* x = eff_x(xin, drop);
-  if (x || !vec_ok) {
-    lttb_prepass_scalar<YDT>(x, y, off, cstart, cb, counts, slopes, part);
     return;
   }
-  lttb_prepass_ring<YDT>(y, off, cstart, cb, counts[1], slopes, part, lttb_ring);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sb_ring + (size_t)wl * LTTB_SB_D * 256);
+  const int64_t ngroups = NG > gw * 32 ? (NG - gw * 32 + nw * 32 - 1) / (nw * 32) : 0;
+  // fill / consume cursors: (group base, round in group, ring slot) advanced
+  // incrementally (no 64-bit divisions in the loop)
+  int64_t fgb = gw * 32, fleft = ngroups;
+  int fit = 0, fslot = 0;
+  auto fill = [&]() {
+    if (fleft > 0) {
+      const uint32_t dst = sbase + (uint32_t)(fslot * 4096);
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int L = u * 4 + (lane >> 3), w = lane & 7;
+        const int64_t v = (fgb + L) * SBV + fit * 8 + w;
+        const bool in = fgb + L < NG && v < nvec;
+        const uint32_t d = dst + (uint32_t)((L * 8 + (w ^ (L & 7))) * 16);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(yv + (in ? v : 0)),
+                     "r"(in ? 16 : 0)
+                     : "memory");
+      }
+      if (++fit == RPG) { fit = 0; fgb += nw * 32; fleft--; }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    fslot = fslot == LTTB_SB_D - 1 ? 0 : fslot + 1;
+  };
+#pragma unroll
+  for (int r = 0; r < LTTB_SB_D; r++) fill();
+  SbAcc acc;
+  acc.reset();
+  int64_t cgb = gw * 32;
+  int cit = 0, cslot = 0;
+  for (int64_t left = ngroups; left > 0;) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(LTTB_SB_D - 1) : "memory");
+    __syncwarp();
+    const int64_t g = cgb + lane;
+    const uint32_t src = sbase + (uint32_t)(cslot * 4096);
+    const int ob = cit * 8 * EPV;                                 // offset of the round in the sub-block
+    const bool full = g < NG && g * SB + ob + 8 * EPV <= n;       // whole round inside the series
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+      uint4 q;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
+                   : "r"(src + (uint32_t)((lane * 8 + (w ^ (lane & 7))) * 16)));
+#pragma unroll
+      for (int e = 0; e < EPV; e++) {
+        const int o = ob + w * EPV + e;
+        if (full || (g < NG && g * SB + o < n)) acc.fold(vget<YDT>(q, e), o, (w * EPV + e) & 1);
+      }
+    }
+    __syncwarp();
+    fill();
+    cslot = cslot == LTTB_SB_D - 1 ? 0 : cslot + 1;
+    if (++cit == RPG) {
+      if (g < NG) lttb_sb_store<YDT>(A, y, n, g, acc);
+      acc.reset();
+      cit = 0;
+      cgb += nw * 32;
+      left--;
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-// warp per bucket: merge its chunk partials -> centroid (pairwise, chunk
-// order) and the LTTB_NC candidates in index order
+// ---------------------------------------------------------------------------
+// 2. guess kernel phases
+
+// non-empty buckets: block b owns buckets [b*nb/B, (b+1)*nb/B) and counts
+// them into bcnt[b]; after a grid barrier every block writes its part of
+// nonempty[] and rank[]; counts[0] = L.
+__device__ __forceinline__ void lttb_count_phase(const int64_t* off, int64_t nb, int32_t* bcnt, int* s_red) {
+  const int64_t k0 = nb * blockIdx.x / gridDim.x, k1 = nb * (blockIdx.x + 1) / gridDim.x;
+  int c = 0;
+  for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) c += __ldg(off + k + 1) > __ldg(off + k);
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += s_red[w];
+    bcnt[blockIdx.x] = t;
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void lttb_list_phase(const int64_t* off, int64_t nb, const int32_t* bcnt, int32_t* nonempty,
+                                                int32_t* rank, int64_t* counts, int* s_red, int* s_base) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
+  int pre = 0;
+  for (int b = tid; b < (int)blockIdx.x; b += blockDim.x) pre += __ldcg(bcnt + b);
+  pre = __reduce_add_sync(0xffffffffu, pre);
+  if (lane == 0) s_red[wid] = pre;
+  __syncthreads();
+  if (tid == 0) {
+    int t = 0;
+    for (int w = 0; w < nwarp; w++) t += s_red[w];
+    *s_base = t;
+    if (blockIdx.x == gridDim.x - 1) counts[0] = t + __ldcg(bcnt + blockIdx.x);
+  }
+  __syncthreads();
+  const int64_t k0 = nb * blockIdx.x / gridDim.x, k1 = nb * (blockIdx.x + 1) / gridDim.x;
+  for (int64_t kb = k0; kb < k1; kb += blockDim.x) {  // block-wide ordered compaction
+    const int64_t k = kb + tid;
+    const bool ne = k < k1 && __ldg(off + k + 1) > __ldg(off + k);
+    const unsigned bal = __ballot_sync(0xffffffffu, ne);
+    if (lane == 0) s_red[wid] = __popc(bal);
+    __syncthreads();
+    int before = *s_base, tot = 0;
+    for (int w = 0; w < nwarp; w++) {
+      const int c = s_red[w];
+      if (w < wid) before += c;
+      tot += c;
+    }
+    const int j = before + __popc(bal & ((1u << lane) - 1u));
+    if (k < k1) rank[k] = ne ? j : -1;
+    if (ne) nonempty[j] = (int32_t)k;
+    __syncthreads();
+    if (tid == 0) *s_base += tot;
+    __syncthreads();
+  }
+}
+
+// warp per non-empty bucket: centroid (fixed tree order over sub-block sums;
+// the partial boundary sub-blocks are summed point by point) and the
+// y-range (from the sub-block maxima/minima, a superset at the boundaries)
 template <int YDT>
-__device__ __forceinline__ void lttb_merge_phase(const double* xin, const int* drop, const int64_t* off, int64_t nb,
-                                        const int64_t* cstart, const LttbChunkPart* part, double2* cent, int64_t* ext) {
-  const double* x = eff_x(xin, drop);
+__device__ __forceinline__ void lttb_cent_phase(const double* x, const void* y, const int64_t* off,
+                                                const int32_t* nonempty, const int64_t* counts,
+                                                const LttbSBArrays A, double2* cent, float2* yr) {
+  const int64_t SB = A.SB;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t k = gw; k < nb; k += nw) {
+  const int64_t L = counts[0];
+  for (int64_t j = gw; j < L; j += nw) {
+    const int64_t k = nonempty[j];
     const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-    if (e <= s) continue;
-    const int64_t c0 = cstart[k], nch = lttb_npieces(s, e);
-    // sums: lane-strided over chunks, then butterfly (fixed order)
-    double sx = 0.0, sy = 0.0;
-    for (int64_t q = lane; q < nch; q += 32) {
-      sx = __dadd_rn(sx, part[c0 + q].sx);
-      sy = __dadd_rn(sy, part[c0 + q].sy);
+    const int64_t g0 = s / SB, g1 = (e - 1) / SB;
+    double sy = 0.0, sx = 0.0;
+    float hi = -INFINITY, lo = INFINITY;
+    for (int64_t gb = g0; gb <= g1; gb += 32 * 4) {  // 4 sub-blocks per lane in flight
+      float2 m[4];
+      double vy[4], vx[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t g = gb + u * 32 + lane;
+        const bool full = g <= g1 && g * SB >= s && (g + 1) * SB <= e;
+        m[u] = g <= g1 ? A.mm[g] : make_float2(-INFINITY, INFINITY);
+        vy[u] = full ? A.sy[g] : 0.0;
+        vx[u] = (full && x) ? A.sx[g] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        hi = fmaxf(hi, m[u].x);
+        lo = fminf(lo, m[u].y);
+        sy = __dadd_rn(sy, vy[u]);
+        sx = __dadd_rn(sx, vx[u]);
+      }
+    }
+    // partial boundary sub-blocks: point by point
+    const int64_t h0e = (g0 + 1) * SB < e ? (g0 + 1) * SB : e;
+    if (s % SB != 0 || h0e < (g0 + 1) * SB) {
+      for (int64_t i = s + lane; i < h0e; i += 32) {
+        sy = __dadd_rn(sy, yd<YDT>(y, i));
+        if (x) sx = __dadd_rn(sx, __ldg(x + i));
+      }
+    }
+    if (g1 > g0 && e % SB != 0) {
+      for (int64_t i = g1 * SB + lane; i < e; i += 32) {
+        sy = __dadd_rn(sy, yd<YDT>(y, i));
+        if (x) sx = __dadd_rn(sx, __ldg(x + i));
+      }
     }
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) {
-      sx = __dadd_rn(sx, __shfl_xor_sync(0xffffffffu, sx, m));
       sy = __dadd_rn(sy, __shfl_xor_sync(0xffffffffu, sy, m));
+      sx = __dadd_rn(sx, __shfl_xor_sync(0xffffffffu, sx, m));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, m));
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, m));
     }
-    // candidates: lane q < NC merges slot q over the chunks
-    int64_t cand = s;
-    if (lane < LTTB_NC) {
-      const bool mx = (lane & 1) == 0;
-      float bv = 0.0f;
-      int64_t bi = -1;
-      for (int64_t q0 = 0; q0 < nch; q0 += 4) {  // 4 pieces' loads in flight
-        float ov[4];
-        int64_t oi[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const bool in = q0 + u < nch;
-          ov[u] = in ? part[c0 + q0 + u].v[lane] : 0.0f;
-          oi[u] = in ? part[c0 + q0 + u].i[lane] : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; u++)
-          if (oi[u] >= 0 && (bi < 0 || (mx ? ov[u] > bv : ov[u] < bv) || (ov[u] == bv && oi[u] < bi))) {
-            bv = ov[u];
-            bi = oi[u];
-          }
+    if (lane == 0) {
+      const double cw = (double)(e - s);
+      if (!x) {
+        sx = (double)(s + e - 1) * cw < 9007199254740992.0 ? (double)((s + e - 1) * (e - s) / 2)
+                                                           : 0.5 * ((double)(s + e - 1) * cw);
       }
-      cand = bi < 0 ? s : bi;
+      cent[k] = make_double2(__ddiv_rn(sx, cw), __ddiv_rn(sy, cw));
+      yr[k] = make_float2(hi, lo);
+    }
+  }
+}
+
+// slope interval of bucket k (rank j): a anywhere in the previous non-empty
+// bucket's box (x range x its y range), c = the centroid of bucket k+1 (or
+// the last point)
+template <int YDT>
+__device__ __forceinline__ double2 lttb_slope_range(const double* x, const void* y, const int64_t* off, int64_t nb,
+                                                    int64_t n, const double2* cent, const float2* yr,
+                                                    const int32_t* nonempty, int64_t j, int64_t k) {
+  double ax0, ax1, ay0, ay1;
+  if (j == 0) {
+    ax0 = ax1 = xd(x, 0);
+    ay0 = ay1 = yd<YDT>(y, 0);
+  } else {
+    const int64_t kp = nonempty[j - 1];
+    const float2 r = yr[kp];
+    ax0 = xd(x, __ldg(off + kp));
+    ax1 = xd(x, __ldg(off + kp + 1) - 1);
+    ay0 = (double)r.y;
+    ay1 = (double)r.x;
+  }
+  double cx, cy;
+  centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
+  double lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const double ax = (i & 1) ? ax1 : ax0, ay = (i & 2) ? ay1 : ay0;
+    const double dx = cx - ax;
+    if (!(dx > 0.0)) continue;
+    const double sl = (cy - ay) / dx;
+    lo = fmin(lo, sl);
+    hi = fmax(hi, sl);
+  }
+  if (!(lo <= hi)) lo = hi = 0.0;
+  return make_double2(lo, hi);
+}
+
+// warp per non-empty bucket: LTTB_NC candidates -- for each steering slope
+// s_t, the sub-block extreme point maximising (minimising) y - s_t*x, using
+// the sub-block's rounded max (min) -- sorted by index into ext[k*NC ..]
+template <int YDT>
+__device__ __forceinline__ void lttb_cand_phase(const double* x, const void* y, const int64_t* off, int64_t nb,
+                                                int64_t n, const double2* cent, const float2* yr,
+                                                const int32_t* nonempty, const int64_t* counts,
+                                                const LttbSBArrays A, int64_t* ext) {
+  const int64_t SB = A.SB;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t L = counts[0];
+  for (int64_t j = gw; j < L; j += nw) {
+    const int64_t k = nonempty[j];
+    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+    const double2 sr = lttb_slope_range<YDT>(x, y, off, nb, n, cent, yr, nonempty, j, k);
+    float sl[LTTB_K];  // candidates only steer the guess: f32 scores, bucket-relative u32 positions
+#pragma unroll
+    for (int t = 0; t < LTTB_K; t++) sl[t] = (float)(sr.x + (sr.y - sr.x) * ((double)t / (double)(LTTB_K - 1)));
+    const double xs = xd(x, s);
+    float bv[LTTB_NC];
+    unsigned bi[LTTB_NC];
+#pragma unroll
+    for (int c = 0; c < LTTB_NC; c++) { bv[c] = (c & 1) ? INFINITY : -INFINITY; bi[c] = 0xffffffffu; }
+    const int64_t g0 = s / SB, g1 = (e - 1) / SB;
+    for (int64_t gb = g0; gb <= g1; gb += 32 * 4) {  // 4 sub-blocks per lane in flight
+      float2 m4[4];
+      unsigned am4[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t g = gb + u * 32 + lane;
+        m4[u] = g <= g1 ? A.mm[g] : make_float2(-INFINITY, INFINITY);
+        am4[u] = g <= g1 ? A.am[g] : 0xffffffffu;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t g = gb + u * 32 + lane;
+        const float2 m = m4[u];
+        const unsigned am = am4[u];
+        const int64_t px = g * SB + (am & 0xffff), pn = g * SB + (am >> 16);
+        const bool okx = (am & 0xffff) != 0xffff && px >= s && px < e;
+        const bool okn = (am >> 16) != 0xffff && pn >= s && pn < e;
+        const float dxx = okx ? (float)(xd(x, px) - xs) : 0.0f, dxn = okn ? (float)(xd(x, pn) - xs) : 0.0f;
+#pragma unroll
+        for (int t = 0; t < LTTB_K; t++) {
+          const float vx = fmaf(-sl[t], dxx, m.x), vn = fmaf(-sl[t], dxn, m.y);
+          if (okx && vx > bv[2 * t]) { bv[2 * t] = vx; bi[2 * t] = (unsigned)(px - s); }
+          if (okn && vn < bv[2 * t + 1]) { bv[2 * t + 1] = vn; bi[2 * t + 1] = (unsigned)(pn - s); }
+        }
+      }
+    }
+    // warp-wide winners: the value by REDUX, then the lowest position holding it
+    int64_t cand = s;
+#pragma unroll
+    for (int c = 0; c < LTTB_NC; c++) {
+      const bool mx = (c & 1) == 0;
+      const bool has = bi[c] != 0xffffffffu;
+      const unsigned key = has ? f32_key(bv[c]) : (mx ? 0u : 0xffffffffu);
+      const unsigned w = mx ? __reduce_max_sync(0xffffffffu, key) : __reduce_min_sync(0xffffffffu, key);
+      const unsigned r = __reduce_min_sync(0xffffffffu, (has && key == w) ? bi[c] : 0xffffffffu);
+      if (lane == c) cand = r == 0xffffffffu ? s : s + (int64_t)r;
     }
     // sort the NC candidates by index (odd-even transposition over lanes)
     for (int r = 0; r < LTTB_NC; r++) {
@@ -679,15 +446,6 @@ __device__ __forceinline__ void lttb_merge_phase(const double* xin, const int* d
       }
     }
     if (lane < LTTB_NC) ext[k * LTTB_NC + lane] = cand;
-    if (lane == 0) {
-      if (!x) {
-        const double cnt = (double)(e - s);
-        sx = (double)(s + e - 1) * cnt < 9007199254740992.0 ? (double)((s + e - 1) * (e - s) / 2)
-                                                            : 0.5 * ((double)(s + e - 1) * cnt);
-      }
-      const double cw = (double)(e - s);
-      cent[k] = make_double2(__ddiv_rn(sx, cw), __ddiv_rn(sy, cw));
-    }
   }
 }
 
@@ -695,10 +453,9 @@ __device__ __forceinline__ void lttb_merge_phase(const double* xin, const int* d
 // picked when the predecessor is candidate i of non-empty bucket j (row 0:
 // predecessor = point 0)
 template <int YDT>
-__device__ __forceinline__ void lttb_cand_table_phase(const double* xin, const int* drop, const void* y, int64_t n,
-                                       const int64_t* off, int64_t nb, const double2* cent, const int64_t* ext,
-                                       const int32_t* nonempty, const int64_t* counts, uint8_t* T) {
-  const double* x = eff_x(xin, drop);
+__device__ __forceinline__ void lttb_cand_table_phase(const double* x, const void* y, int64_t n, const int64_t* off,
+                                                      int64_t nb, const double2* cent, const int64_t* ext,
+                                                      const int32_t* nonempty, const int64_t* counts, uint8_t* T) {
   const int64_t L = counts[0];
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L * LTTB_NC;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -739,9 +496,10 @@ __device__ __forceinline__ int lttb_stage_bytes(uint8_t* dst, const uint8_t* src
   return shift;
 }
 
-// warp per segment: compose the segment's tables (rows staged in smem)
-__device__ __forceinline__ void lttb_seg_compose_phase(const uint8_t* T, const int64_t* counts, uint8_t* C) {
-  __shared__ __align__(16) uint8_t rows[8][LTTB_SEG * LTTB_NC + 32];
+// warp per segment of LTTB_SEG buckets: composed tables C (segment entry
+// candidate -> exit candidate)
+__device__ __forceinline__ void lttb_seg_compose_phase(const uint8_t* T, const int64_t* counts, uint8_t* C,
+                                                       uint8_t (*rows)[LTTB_SEG * LTTB_NC + 32]) {
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t L = counts[0];
   const int64_t NS = (L + LTTB_SEG - 1) / LTTB_SEG;
@@ -778,12 +536,11 @@ __device__ __forceinline__ void lttb_seg_entry_phase(const uint8_t* T, const uin
   }
 }
 
-// warp per segment: expand the picks
-__device__ __forceinline__ void lttb_seg_expand_phase(const uint8_t* T, const uint8_t* entry,
-                                                               const int64_t* ext, const int32_t* nonempty,
-                                                               const int64_t* counts, int64_t* picks) {
-  __shared__ __align__(16) uint8_t rows[8][LTTB_SEG * LTTB_NC + 32];
-  __shared__ uint8_t cs[8][LTTB_SEG];
+// warp per segment: expand the guessed picks
+__device__ __forceinline__ void lttb_seg_expand_phase(const uint8_t* T, const uint8_t* entry, const int64_t* ext,
+                                                      const int32_t* nonempty, const int64_t* counts, int64_t* picks,
+                                                      uint8_t (*rows)[LTTB_SEG * LTTB_NC + 32],
+                                                      uint8_t (*cs)[LTTB_SEG]) {
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t L = counts[0];
   const int64_t NS = (L + LTTB_SEG - 1) / LTTB_SEG;
@@ -808,142 +565,35 @@ __device__ __forceinline__ void lttb_seg_expand_phase(const uint8_t* T, const ui
   }
 }
 
-// exact area partial of one piece, scalar form (explicit x / unaligned y):
-// the CTA's warps stride over the piece
-template <int YDT>
-__device__ __forceinline__ AreaCand lttb_piece_area_scalar(const double* x, const void* y, int64_t cs, int64_t ce,
-                                                           double ax, double ay, double cx, double cy, int tid,
-                                                           int nthreads) {
-  AreaCand best{-1.0, IDX_NONE};
-  for (int64_t i0 = cs + tid; i0 < ce; i0 += 4 * nthreads) {
-    double vy[4], vx[4];
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int64_t i = i0 + u * nthreads;
-      vy[u] = i < ce ? yd<YDT>(y, i) : 0.0;
-      vx[u] = i < ce ? xd(x, i) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int64_t i = i0 + u * nthreads;
-      if (i < ce) {
-        AreaCand a{tri_area(ax, ay, cx, cy, vx[u], vy[u]), i};
-        if (area_better(a, best)) best = a;
-      }
-    }
-  }
-  return best;
-}
-
-// the reference area of element e of a vector (implicit x): dA = ax - x of
-// the vector's first element (an exact integer in f64)
-template <int YDT>
-__device__ __forceinline__ double lttb_varea(const uint4& q, int e, double dA, double ay, double K1, double K2) {
-  const double t1 = __dmul_rn(K1, __dsub_rn(vget<YDT>(q, e), ay));
-  const double t2 = __dmul_rn(__dsub_rn(dA, (double)e), K2);
-  return __dmul_rn(0.5, fabs(__dsub_rn(t1, t2)));
-}
-
-// exact area partial of one piece, vector form (implicit x, aligned y): the
-// threads take 128-bit vectors, U loads in flight each; every thread
-// visits its elements in index order (strict > keeps the first max)
-template <int YDT, int U = 8>
-__device__ __forceinline__ AreaCand lttb_piece_area_vec(const void* y, int64_t cs, int64_t ce, int64_t prev,
-                                                        double ay, double K1, double K2, int tid, int nthr) {
-  constexpr int EPV = 16 / (int)sizeof(typename YT<YDT>::T);
-  const int64_t v0 = cs / EPV;
-  const int nvec = (int)((ce + EPV - 1) / EPV - v0);
-  const int r0 = (int)(v0 * EPV - cs), len = (int)(ce - cs);
-  const double dA0 = (double)(prev - cs);
-  const uint4* pv = (const uint4*)y + v0;
-  AreaCand best{-1.0, IDX_NONE};
-  for (int rb = 0; rb < nvec; rb += U * nthr) {
-    uint4 q[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      const int rv = rb + tid + u * nthr;
-      q[u] = __ldg(pv + (rv < nvec ? rv : nvec - 1));
-    }
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      const int rv = rb + tid + u * nthr;
-      const int re0 = r0 + rv * EPV;
-      const double dA = __dsub_rn(dA0, (double)re0);
-      if (rv < nvec) {
-#pragma unroll
-        for (int ee = 0; ee < EPV; ee++) {
-          const double a = lttb_varea<YDT>(q[u], ee, dA, ay, K1, K2);
-          if ((unsigned)(re0 + ee) < (unsigned)len && a > best.a) best = AreaCand{a, cs + re0 + ee};
-        }
-      }
-    }
-  }
-  return best;
-}
-
 // ---------------------------------------------------------------------------
-// Resolution: guess -> exact fixed point, with per-piece pruning.
-//
-// For bucket j with predecessor p (ax = p, ay = y[p]) and c = centroid of
-// the next bucket, the reference area of point i is
+// Pruning.  For bucket j with predecessor p (ax = p, ay = y[p]) and c the
+// centroid of the next bucket, the reference area of point i is
 //   A_i = 0.5*|K1*(y_i - ay) - (ax - i)*K2|,  K1 = ax - cx, K2 = cy - ay
-//       = 0.5*|K1*u_i + G|,  u_i = (y_i - yb) - sig*(i - s),  sig = -K2/K1,
-//   G = K1*(yb - ay) - (ax - s)*K2   (yb, s: the bucket's steering origin).
-// The prepass stored, per piece and steering slope s_j, the max M_j and min
-// m_j of t_j(i) ~ (y_i - yb) - s_j*(i - s) (fp32).  Since
-//   u_i = t_j(i) + (s_j - sig)*(i - s) +- E_j,
-// and max_i (y_i - yb - s*(i - s)) is convex in s (the min concave), u over
-// the piece lies in [U_lo, U_hi] (shifted single-slope bounds, and the chord
-// between the two grid slopes around sig), so
-//   max_i A_i <= 0.5*max(|K1*U_hi + G|, |K1*U_lo + G|) + slack.
-// E_j and slack over-estimate the fp32 / f64 rounding by x16 or more.  A
-// piece whose bound is below the best exact area among the bucket's
-// candidates cannot hold the first max, so only the remaining pieces are
-// evaluated exactly; the answer is the first max over candidates + unpruned
-// pieces (area desc, index asc).  Implicit x only; with explicit x every
-// piece is evaluated.
+//       = 0.5*|K1*u_i + G|,  u_i = y_i - sig*(i - s),  sig = -K2/K1,
+//   G = -K1*ay - (ax - s)*K2.
+// Over a sub-block with y in [mn, mx] (outward-rounded) and i - s in
+// [dlo, dhi], u lies in [mn - max(sig*dlo, sig*dhi), mx - min(sig*dlo,
+// sig*dhi)], so max A <= 0.5*max(|K1*U_hi + G|, |K1*U_lo + G|) + slack, the
+// slack over-estimating every f64 rounding (x100).  A sub-block whose bound
+// is below the best exact candidate area cannot hold the first max.
+// Implicit x only (explicit x: every sub-block is evaluated).
 
 struct LttbPlan {  // constants of bucket j for one predecessor
   int64_t prev;
-  double ay, K1, K2, sig;  // sig = -K2/K1 (steering slope of the area)
+  double ay, K1, K2, sig;
 };
 
-// upper bound of the reference area over piece [cs, ce) of bucket [s, e)
-__device__ __forceinline__ double lttb_piece_bound(const LttbChunkPart& P, double2 sr, int64_t s, int64_t cs,
-                                                   int64_t ce, double yb, double ax, double ay, double K1,
-                                                   double K2, double sig) {
-  if (!(K1 < 0.0) && !(K1 > 0.0)) return INFINITY;
+__device__ __forceinline__ double lttb_sb_bound(float2 m, int64_t s, int64_t cs, int64_t ce, const LttbPlan& P) {
+  if (!(m.x >= m.y)) return -INFINITY;  // no non-NaN point: nothing can win here
+  if (!(P.K1 < 0.0) && !(P.K1 > 0.0)) return INFINITY;
   const double dlo = (double)(cs - s), dhi = (double)(ce - 1 - s);
-  const double G = K1 * (yb - ay) - (ax - (double)s) * K2;
-  double uhi = INFINITY, ulo = -INFINITY;
-  double pM = 0.0, pm = 0.0, pE = 0.0, ps = 0.0;
-#pragma unroll
-  for (int j = 0; j < LTTB_K; j++) {
-    const double M = (double)P.v[2 * j], m = (double)P.v[2 * j + 1];
-    if (!(M >= m)) return INFINITY;  // no finite projection recorded (all-NaN piece): evaluate it
-    const double sj = (double)lttb_slope(sr, j);
-    const double dd = sj - sig;
-    const double a0 = dd * dlo, a1 = dd * dhi;
-    const double E = 0x1p-18 * (fmax(fabs(M), fabs(m)) + 2.0 * fabs(sj) * dhi);
-    // shifted single-slope bound (any sig)
-    uhi = fmin(uhi, M + fmax(a0, a1) + E);
-    ulo = fmax(ulo, m + fmin(a0, a1) - E);
-    // chord bound between the two grid slopes around sig
-    if (j > 0 && ps <= sig && sig <= sj && sj > ps) {
-      const double lam = (sj - sig) / (sj - ps);  // weight of the lower slope
-      const double r = 0x1p-40 * (fabs(pM) + fabs(M) + fabs(pm) + fabs(m));
-      uhi = fmin(uhi, lam * (pM + pE) + (1.0 - lam) * (M + E) + r);
-      ulo = fmax(ulo, lam * (pm - pE) + (1.0 - lam) * (m - E) - r);
-    }
-    pM = M;
-    pm = m;
-    pE = E;
-    ps = sj;
-  }
-  const double b = fmax(fabs(K1 * uhi + G), fabs(K1 * ulo + G));
-  const double smax = fmax(fabs((double)lttb_slope(sr, 0)), fabs((double)lttb_slope(sr, LTTB_K - 1)));
-  const double slack = 0x1p-44 * (fabs(K1) * (fabs(uhi) + fabs(ulo) + fabs(yb - ay) + (smax + fabs(sig)) * dhi) +
-                                  fabs(K2) * (fabs(ax - (double)s) + dhi) + fabs(G));
+  const double a0 = P.sig * dlo, a1 = P.sig * dhi;
+  const double uhi = (double)m.x - fmin(a0, a1), ulo = (double)m.y - fmax(a0, a1);
+  const double ax = (double)P.prev;
+  const double G = -P.K1 * P.ay - (ax - (double)s) * P.K2;
+  const double b = fmax(fabs(P.K1 * uhi + G), fabs(P.K1 * ulo + G));
+  const double slack = 0x1p-44 * (fabs(P.K1) * (fabs(uhi) + fabs(ulo) + fabs(P.ay) + fabs(P.sig) * dhi) +
+                                  fabs(P.K2) * (fabs(ax - (double)s) + dhi) + fabs(G));
   return 0.5 * (b + slack);
 }
 
@@ -974,69 +624,136 @@ __device__ __forceinline__ void lttb_plan_bucket(const double* x, const void* y,
   cb = warp_area_max(cb);
 }
 
-// must piece q of bucket [s, e) be evaluated exactly? (pruning bound vs the
-// best candidate area; explicit x: always)
-__device__ __forceinline__ bool lttb_keep_piece(const double* x, const LttbChunkPart* cpart, double2 sr, int64_t c0,
-                                                int64_t q, int64_t s, int64_t e, double yb, const LttbPlan& P,
-                                                double best) {
+// sub-block g restricted to bucket [s, e)
+__device__ __forceinline__ void lttb_sb_range(int64_t SB, int64_t g, int64_t s, int64_t e, int64_t& cs,
+                                              int64_t& ce) {
+  cs = g * SB > s ? g * SB : s;
+  ce = (g + 1) * SB < e ? (g + 1) * SB : e;
+}
+
+template <int YDT>
+__device__ __forceinline__ bool lttb_keep_sb(const double* x, const LttbSBArrays& A, int64_t g, int64_t s, int64_t e,
+                                             const LttbPlan& P, double best) {
   if (x) return true;
   int64_t cs, ce;
-  lttb_piece(s, e, q, cs, ce);
-  const double bnd =
-      lttb_piece_bound(cpart[c0 + q], sr, s, cs, ce, yb, (double)P.prev, P.ay, P.K1, P.K2, P.sig);
-  return !(bnd < best);
+  lttb_sb_range(A.SB, g, s, e, cs, ce);
+  return !(lttb_sb_bound(A.mm[g], s, cs, ce, P) < best);
 }
 
-// steering origin of bucket [s, e): y[s] (0 if NaN), as in the prepass
+// the reference area of element e of a vector (implicit x): dA = ax - x of
+// the vector's first element (an exact integer in f64)
 template <int YDT>
-__device__ __forceinline__ double lttb_yb(const void* y, int64_t s) {
-  const double v = yd<YDT>(y, s);
-  return v == v ? v : 0.0;
+__device__ __forceinline__ double lttb_varea(const uint4& q, int e, double dA, double ay, double K1, double K2) {
+  const double t1 = __dmul_rn(K1, __dsub_rn(vget<YDT>(q, e), ay));
+  const double t2 = __dmul_rn(__dsub_rn(dA, (double)e), K2);
+  return __dmul_rn(0.5, fabs(__dsub_rn(t1, t2)));
 }
 
-// settle bucket j (pick = first max of its candidate best and its piece
-// partials); a pick that differs from picks[j] lists bucket j+1 in D
-__device__ __forceinline__ void lttb_settle(int64_t j, int64_t L, int64_t s, int64_t c0, int64_t nch,
-                                            const AreaCand* cbest, const AreaCand* part, int64_t* picks,
-                                            int32_t* list, int32_t* cnt) {
-  AreaCand best{__ldcg(&cbest[j].a), __ldcg(&cbest[j].i)};
-  for (int64_t q = 0; q < nch; q++) {
-    const AreaCand a{__ldcg(&part[c0 + q].a), __ldcg(&part[c0 + q].i)};
+// exact first max over [cs, ce) inside sub-block g, one warp: lane l takes
+// the sub-block's vectors l, l+32, ... (all loads in flight, then the areas
+// in index order); explicit x / unaligned y: point by point
+template <int YDT>
+__device__ __forceinline__ AreaCand lttb_eval_sb(const double* x, const void* y, int vec_ok, const LttbSBArrays& A,
+                                                 int64_t g, int64_t cs, int64_t ce, const LttbPlan& P, double cx,
+                                                 double cy, int lane) {
+  constexpr int EPV = SBG<YDT>::EPV;
+  AreaCand best{-1.0, IDX_NONE};
+  if (x || !vec_ok) {
+    const double ax = xd(x, P.prev);
+    for (int64_t i = cs + lane; i < ce; i += 32) {
+      const AreaCand a{tri_area(ax, P.ay, cx, cy, xd(x, i), yd<YDT>(y, i)), i};
+      if (area_better(a, best)) best = a;
+    }
+    return warp_area_max(best);
+  }
+  const int64_t v0 = cs / EPV, v1 = (ce + EPV - 1) / EPV;  // vectors overlapping [cs, ce) (<= SBV + 1)
+  const uint4* yv = (const uint4*)y;
+  for (int64_t vb = v0; vb < v1; vb += 32 * 16) {
+    uint4 q[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const int64_t v = vb + u * 32 + lane;
+      if (v < v1) q[u] = __ldg(yv + v);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const int64_t v = vb + u * 32 + lane;
+      if (v < v1) {
+        const int64_t i0 = v * EPV;
+        const double dA = (double)(P.prev - i0);
+#pragma unroll
+        for (int e = 0; e < EPV; e++) {
+          const double a = lttb_varea<YDT>(q[u], e, dA, P.ay, P.K1, P.K2);
+          if (i0 + e >= cs && i0 + e < ce && a > best.a) best = AreaCand{a, i0 + e};
+        }
+      }
+    }
+  }
+  return warp_area_max(best);
+}
+
+// settle bucket j (warp-wide): first max of its candidate best and its
+// evaluated sub-blocks (part[base .. base+cnt)); a pick that differs from
+// picks[j] lists bucket j+1 in D
+__device__ __forceinline__ void lttb_settle_warp(int64_t j, int64_t L, int64_t s, const AreaCand& cbj,
+                                                 const AreaCand* part, int64_t base, int64_t cnt, int64_t* picks,
+                                                 int32_t* list, int32_t* dcnt, int lane) {
+  AreaCand best = lane == 0 ? cbj : AreaCand{-1.0, IDX_NONE};
+  for (int64_t t = lane; t < cnt; t += 32) {
+    const AreaCand a{__ldcg(&part[base + t].a), __ldcg(&part[base + t].i)};
     if (area_better(a, best)) best = a;
   }
-  const int64_t p = best.i == IDX_NONE ? s : best.i;
-  if (p != __ldcg(picks + j)) {
-    __stcg(picks + j, p);
-    if (j + 1 < L) list[atomicAdd(cnt, 1)] = (int32_t)(j + 1);
+  best = warp_area_max(best);
+  if (lane == 0) {
+    const int64_t p = best.i == IDX_NONE ? s : best.i;
+    if (p != __ldcg(picks + j)) {
+      __stcg(picks + j, p);
+      if (j + 1 < L) list[atomicAdd(dcnt, 1)] = (int32_t)(j + 1);
+    }
   }
 }
 
-// The guess and round-1 plan in one cooperative launch (grid barriers
-// between the phases, no kernel boundaries):
-//   merge      warp per bucket: centroid (+ exact sequential centroids in
-//              exact mode) and the LTTB_NC candidates from the piece partials
-//   cand_table thread per (bucket, candidate): transition tables T
-//   compose    warp per segment of LTTB_SEG buckets: composed tables C
-//   entry      one thread: entry candidate of every segment
-//   expand     warp per segment: the guessed pick of every bucket
-//   plan       warp per bucket, predecessor = the guess: constants, exact
-//              candidate best, piece bounds -> unpruned pieces listed for
-//              lttb_eval_kernel; a bucket with none settles at once.
-// ctr: [2] |D| (list), [6] pieces listed.
+struct LttbRound1 {  // per non-empty bucket: round-1 plan and its sub-block list
+  LttbPlan P;
+  AreaCand cb;
+  int64_t base, cnt;
+};
+
+// The guess and the round-1 plan in one cooperative launch (grid barriers
+// between the phases):
+//   count/list  non-empty bucket list (nonempty, rank, counts[0] = L)
+//   cent        warp per bucket: centroid + y range
+//   [exact]     sequential-order centroids (small buckets)
+//   cand        warp per bucket: LTTB_NC candidates
+//   cand_table  thread per (bucket, candidate): transition tables T
+//   compose     warp per segment: composed tables C
+//   entry       one thread: entry candidate of every segment
+//   expand      warp per segment: the guessed pick of every bucket
+//   plan        warp per bucket, predecessor = the guess: constants, exact
+//               candidate best, sub-block bounds -> the bucket's surviving
+//               sub-blocks, compacted into the bucket's slot range
+//               (slots[g0 + j ..], entry = sub-block << 24 | bucket rank)
+//               and appended to the work list wl; a bucket with none
+//               settles at once.
+// ctr: [2] |D|, [6..7] sub-blocks listed (int64).
 template <int YDT>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, 3)
 lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
-                  double2* cent, const double2* slopes, const int64_t* cstart, const int32_t* nonempty,
-                  const int64_t* counts, const LttbChunkPart* cpart, int64_t* ext, uint8_t* T, uint8_t* C,
-                  uint8_t* entry, int64_t* picks, LttbPlan* plan, AreaCand* cbest, int32_t* arrive, AreaCand* part,
-                  int2* plist, int32_t* list, int32_t* ctr, int exact, int64_t cap) {
+                  const LttbSBArrays A, double2* cent, float2* yr, int32_t* bcnt, int32_t* nonempty, int32_t* rank,
+                  int64_t* counts, int64_t* ext, uint8_t* T, uint8_t* C, uint8_t* entry, int64_t* picks,
+                  LttbRound1* r1, int32_t* arrive, int64_t* slots, int64_t* wl, int32_t* list, int32_t* ctr,
+                  int exact, int64_t cap) {
   pdl_launch_dependents();
   pdl_wait();
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ uint8_t lttb_dsm[];
+  __shared__ __align__(16) uint8_t rows[8][LTTB_SEG * LTTB_NC + 32];
+  __shared__ uint8_t segc[8][LTTB_SEG];
+  __shared__ int s_red[32];
+  __shared__ int s_base;
   const double* x = eff_x(xin, drop);
-  unsigned long long* tsb = (unsigned long long*)(ctr + 16);  // debug phase timestamps
+  unsigned long long* tsb = (unsigned long long*)(ctr + 16);  // phase timestamps (tsds_ctx_stat "lttb_tsN")
   auto stamp = [&](int i) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       unsigned long long t;
@@ -1045,74 +762,103 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
     }
   };
   stamp(0);
-  lttb_merge_phase<YDT>(xin, drop, off, nb, cstart, cpart, cent, ext);
-  if (exact) {
-    grid.sync();
-    lttb_centroid_phase<YDT>(xin, drop, y, off, nb, cent);
-  }
+  lttb_count_phase(off, nb, bcnt, s_red);
+  grid.sync();
+  lttb_list_phase(off, nb, bcnt, nonempty, rank, counts, s_red, &s_base);
   grid.sync();
   stamp(1);
-  lttb_cand_table_phase<YDT>(xin, drop, y, n, off, nb, cent, ext, nonempty, counts, T);
+  lttb_cent_phase<YDT>(x, y, off, nonempty, counts, A, cent, yr);
   grid.sync();
+  if (exact) {
+    lttb_centroid_phase<YDT>(xin, drop, y, off, nb, cent);
+    grid.sync();
+  }
   stamp(2);
-  lttb_seg_compose_phase(T, counts, C);
+  lttb_cand_phase<YDT>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext);
   grid.sync();
   stamp(3);
+  lttb_cand_table_phase<YDT>(x, y, n, off, nb, cent, ext, nonempty, counts, T);
+  grid.sync();
+  lttb_seg_compose_phase(T, counts, C, rows);
+  grid.sync();
   if (blockIdx.x == 0) lttb_seg_entry_phase(T, C, counts, entry, lttb_dsm, cap);
   grid.sync();
-  stamp(4);
-  lttb_seg_expand_phase(T, entry, ext, nonempty, counts, picks);
+  lttb_seg_expand_phase(T, entry, ext, nonempty, counts, picks, rows, segc);
   grid.sync();
-  stamp(5);
-  // ---- plan (round 1)
+  stamp(4);
+  // ---- round-1 plan
+  const int64_t SB = A.SB;
   const int lane = threadIdx.x & 31;
   const int64_t L = counts[0];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long* nsb = (unsigned long long*)(ctr + 6);
   for (int64_t j = gw; j < L; j += nw) {
     int64_t k, s, e;
     LttbPlan P;
     AreaCand cb;
     double cx, cy;
     lttb_plan_bucket<YDT>(x, y, n, off, nb, cent, nonempty, ext, picks, j, lane, k, s, e, P, cb, cx, cy);
-    const int64_t c0 = cstart[k], nch = lttb_npieces(s, e);
-    const double2 sr = slopes[k];
-    const double yb = lttb_yb<YDT>(y, s);
-    int nun = 0;
-    for (int64_t q0 = 0; q0 < nch; q0 += 32) {
-      const int64_t q = q0 + lane;
-      const bool keep = q < nch && lttb_keep_piece(x, cpart, sr, c0, q, s, e, yb, P, cb.a);
-      if (q < nch && !keep) part[c0 + q] = AreaCand{-1.0, IDX_NONE};
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      int base = 0;
-      if (lane == 0 && bal) base = atomicAdd(ctr + 6, __popc(bal));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (keep) plist[base + __popc(bal & ((1u << lane) - 1u))] = make_int2((int)(c0 + q), (int)j);
-      nun += __popc(bal);
-    }
-    __syncwarp();
-    if (lane == 0) {
-      plan[j] = P;
-      cbest[j] = cb;
-      arrive[j] = nun;
-      if (nun == 0) {
-        __threadfence();
-        lttb_settle(j, L, s, c0, nch, cbest, part, picks, list, ctr + 2);
+    const int64_t g0 = s / SB, g1 = (e - 1) / SB;
+    // surviving sub-blocks compacted into the bucket's own slot range
+    // [g0 + j, g1 + j] (disjoint across buckets); their slot positions are
+    // appended to the work list wl
+    const int64_t base = g0 + j;
+    int64_t cnt = 0;
+    for (int64_t gb = g0; gb <= g1; gb += 32 * 4) {
+      float2 m4[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t g = gb + u * 32 + lane;
+        m4[u] = g <= g1 ? A.mm[g] : make_float2(-INFINITY, INFINITY);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t g = gb + u * 32 + lane;
+        bool keep = false;
+        if (g <= g1) {
+          if (x) keep = true;
+          else {
+            int64_t cs, ce;
+            lttb_sb_range(A.SB, g, s, e, cs, ce);
+            keep = !(lttb_sb_bound(m4[u], s, cs, ce, P) < cb.a);
+          }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (bal) {
+          const int64_t pos = base + cnt + __popc(bal & ((1u << lane) - 1u));
+          int64_t w0 = 0;
+          if (lane == 0) w0 = (int64_t)atomicAdd(nsb, (unsigned long long)__popc(bal));
+          w0 = __shfl_sync(0xffffffffu, w0, 0);
+          if (keep) {
+            slots[pos] = (g << 24) | j;
+            wl[w0 + __popc(bal & ((1u << lane) - 1u))] = pos;
+          }
+          cnt += __popc(bal);
+        }
       }
     }
+    if (lane == 0) {
+      r1[j] = LttbRound1{P, cb, base, cnt};
+      arrive[j] = (int32_t)cnt;
+    }
+    if (cnt == 0) lttb_settle_warp(j, L, s, cb, nullptr, 0, 0, picks, list, ctr + 2, lane);
   }
+  grid.sync();
+  stamp(5);
 }
 
-// Round 1 evaluation, warp per listed piece: exact first max with the
-// guessed predecessor; the warp completing a bucket's last piece settles it.
-// After this kernel every bucket not in D satisfies picks[j] = f_j(picks[j-1])
-// (a bucket whose predecessor changed during round 1 is in D).
+// Round-1 evaluation, warp per work-list entry (a sub-block slot): exact
+// first max with the guessed predecessor into part[slot]; the warp completing a bucket's last
+// sub-block settles it.  Afterwards every bucket not in D satisfies
+// picks[j] = f_j(picks[j-1]) (a bucket whose predecessor changed during
+// round 1 is in D).
 template <int YDT>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256)
 lttb_eval_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
-                 const double2* cent, const int64_t* cstart, const int32_t* nonempty, const int64_t* counts,
-                 const LttbPlan* plan, const AreaCand* cbest, int32_t* arrive, AreaCand* part, const int2* plist,
-                 int64_t* picks, int32_t* list, int32_t* ctr, int vec_ok) {
+                 const LttbSBArrays A, const double2* cent, const int32_t* nonempty, const int64_t* counts, const LttbRound1* r1,
+                 int32_t* arrive, AreaCand* part, const int64_t* slots, const int64_t* wl, int64_t* picks,
+                 int32_t* list, int32_t* ctr, int vec_ok) {
   pdl_launch_dependents();
   pdl_wait();
   const double* x = eff_x(xin, drop);
@@ -1120,36 +866,29 @@ lttb_eval_kernel(const double* xin, const int* drop, const void* y, int64_t n, c
   const int64_t L = counts[0];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t np = __ldcg(ctr + 6);
+  const int64_t np = (int64_t)__ldcg((const unsigned long long*)(ctr + 6));
   for (int64_t t = gw; t < np; t += nw) {
-    const int2 pc = __ldcg(plist + t);
-    const int64_t c = pc.x, j = pc.y;
+    const int64_t pos = __ldcg(wl + t);
+    const int64_t ent = __ldcg(slots + pos);
+    const int64_t g = ent >> 24, j = ent & 0xffffff;
     const int64_t k = nonempty[j];
     const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-    const int64_t c0 = cstart[k];
+    const LttbPlan P = r1[j].P;
+    double cx = 0.0, cy = 0.0;
+    if (x || !vec_ok) centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
     int64_t cs, ce;
-    lttb_piece(s, e, c - c0, cs, ce);
-    const LttbPlan P = plan[j];
-    AreaCand a;
-    if (x || !vec_ok) {
-      double cx, cy;
-      centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
-      a = lttb_piece_area_scalar<YDT>(x, y, cs, ce, xd(x, P.prev), P.ay, cx, cy, lane, 32);
-    } else {
-      a = lttb_piece_area_vec<YDT, LTTB_R1_U>(y, cs, ce, P.prev, P.ay, P.K1, P.K2, lane, 32);
-    }
-    a = warp_area_max(a);
+    lttb_sb_range(A.SB, g, s, e, cs, ce);
+    const AreaCand a = lttb_eval_sb<YDT>(x, y, vec_ok, A, g, cs, ce, P, cx, cy, lane);
+    int last = 0;
     if (lane == 0) {
-      part[c] = a;
+      part[pos] = a;
       __threadfence();
-      if (atomicSub(arrive + j, 1) == 1) {
-        __threadfence();
-        lttb_settle(j, L, s, c0, lttb_npieces(s, e), cbest, part, picks, list, ctr + 2);
-      }
+      last = atomicSub(arrive + j, 1) == 1;
+      if (last) __threadfence();
     }
-    __syncwarp();
+    if (__shfl_sync(0xffffffffu, last, 0))
+      lttb_settle_warp(j, L, s, r1[j].cb, part, r1[j].base, r1[j].cnt, picks, list, ctr + 2, lane);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctr[9] = (int32_t)np;
 }
 
 __device__ __forceinline__ void lttb_lock(int32_t* l) {
@@ -1168,29 +907,29 @@ __device__ __forceinline__ int64_t lttb_ld_relaxed(const int64_t* p) {
 }
 
 // Correction chains, CTA per entry of D: re-plan bucket j with the current
-// predecessor, evaluate its unpruned pieces (CTA per piece), then under
-// bucket j's lock: if picks[j-1] still equals the predecessor used, store
-// the pick; a changed pick continues the chain at j+1, an outdated
+// predecessor, evaluate its surviving sub-blocks (warp per sub-block), then
+// under bucket j's lock: if picks[j-1] still equals the predecessor used,
+// store the pick; a changed pick continues the chain at j+1, an outdated
 // predecessor abandons it (whoever changed picks[j-1] continues at j).  The
 // last write to picks[j] therefore always carries f_j(final picks[j-1]): the
 // fixed point is exactly the reference's sequence.
-// ctr: [2] |D|, [3] chain steps, [8] pieces evaluated in chains.
+// ctr: [2] |D|, [3] chain steps, [8] sub-blocks evaluated in chains.
 template <int YDT>
 __global__ void __launch_bounds__(256, 2)
 lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
-                  const double2* cent, const double2* slopes, const int64_t* cstart, const int32_t* nonempty,
-                  const int64_t* counts, const LttbChunkPart* cpart, const int64_t* ext, int64_t* picks,
-                  const int32_t* list, int32_t* lock, int32_t* ctr, int vec_ok) {
+                  const double2* cent, const int32_t* nonempty, const int64_t* counts, const LttbSBArrays A,
+                  const int64_t* ext, int64_t* picks, const int32_t* list, int32_t* lock, int32_t* ctr, int vec_ok) {
   pdl_launch_dependents();
   pdl_wait();
+  const int64_t SB = A.SB;
   const double* x = eff_x(xin, drop);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t L = counts[0];
   __shared__ LttbPlan sP;
   __shared__ AreaCand sCb, sW[8];
-  __shared__ double sc[3];   // cx, cy, yb
+  __shared__ double sc[2];   // cx, cy
   __shared__ int64_t sk[3];  // k, s, e
-  __shared__ int32_t sq[256];
+  __shared__ int64_t sq[256];
   __shared__ int sn, sgo;
   const int64_t nD = __ldcg(ctr + 2);
   for (int64_t t = blockIdx.x; t < nD; t += gridDim.x) {
@@ -1207,7 +946,6 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
           sCb = cb;
           sc[0] = cx;
           sc[1] = cy;
-          sc[2] = lttb_yb<YDT>(y, s);
           sk[0] = k;
           sk[1] = s;
           sk[2] = e;
@@ -1216,29 +954,25 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
       }
       __syncthreads();
       const LttbPlan P = sP;
-      const int64_t k = sk[0], s = sk[1], e = sk[2];
-      const int64_t c0 = cstart[k], nch = lttb_npieces(s, e);
-      const double2 sr = slopes[k];
+      const int64_t s = sk[1], e = sk[2];
+      const int64_t g0 = s / SB, g1 = (e - 1) / SB;
       AreaCand wb{-1.0, IDX_NONE};
-      for (int64_t q0 = 0; q0 < nch; q0 += 256) {
+      for (int64_t gb = g0; gb <= g1; gb += 256) {
         if (tid == 0) sn = 0;
         __syncthreads();
-        const int64_t q = q0 + tid;
-        if (q < nch && lttb_keep_piece(x, cpart, sr, c0, q, s, e, sc[2], P, sCb.a)) sq[atomicAdd(&sn, 1)] = (int32_t)tid;
+        const int64_t g = gb + tid;
+        if (g <= g1 && lttb_keep_sb<YDT>(x, A, g, s, e, P, sCb.a)) sq[atomicAdd(&sn, 1)] = g;
         __syncthreads();
         const int m = sn;
-        for (int i = 0; i < m; i++) {  // CTA per piece
+        for (int i = wid; i < m; i += 8) {  // warp per sub-block
           int64_t cs, ce;
-          lttb_piece(s, e, q0 + sq[i], cs, ce);
-          const AreaCand a = (x || !vec_ok)
-                                 ? lttb_piece_area_scalar<YDT>(x, y, cs, ce, xd(x, P.prev), P.ay, sc[0], sc[1], tid, 256)
-                                 : lttb_piece_area_vec<YDT, 8>(y, cs, ce, P.prev, P.ay, P.K1, P.K2, tid, 256);
+          lttb_sb_range(A.SB, sq[i], s, e, cs, ce);
+          const AreaCand a = lttb_eval_sb<YDT>(x, y, vec_ok, A, sq[i], cs, ce, P, sc[0], sc[1], lane);
           if (area_better(a, wb)) wb = a;
         }
         if (tid == 0) atomicAdd(ctr + 8, m);
         __syncthreads();
       }
-      wb = warp_area_max(wb);
       if (lane == 0) sW[wid] = wb;
       __syncthreads();
       if (tid == 0) {

@@ -202,8 +202,8 @@ def test_lttb_large_bucket_modes(ts, oracle):
             for n_out in (50, 1000):
                 assert ts.downsample("lttb", y, n_out=n_out).tolist() == oracle.downsample("lttb", y, n_out=n_out).tolist()
                 assert ts.downsample("lttb", x, y, n_out=n_out).tolist() == oracle.downsample("lttb", x, y, n_out=n_out).tolist()
-            rounds = L.tsds_ctx_stat(_lib.context().handle, b"lttb_rounds")
-            assert 1 <= rounds <= 64
+            steps = L.tsds_ctx_stat(_lib.context().handle, b"lttb_rounds")  # correction-chain steps
+            assert 0 <= steps <= 4 * 1000
     finally:
         L.tsds_set_option(b"lttb_exact", 0)
 
