@@ -726,7 +726,8 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
                                     drop, y, n, off, nb, A, (const double2*)cent, (const int32_t*)nonempty,
                                     (const int64_t*)counts, (const LttbRound1*)r1, arrive, part,
                                     (const int64_t*)slots, (const int64_t*)wl, picks, list_a, ctr, vec_ok)));
-  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_chain_kernel<YD>, one_wave(ctx, lttb_chain_kernel<YD>, 256), 256, 0,
+  YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_chain_kernel<YD>, one_wave(ctx, lttb_chain_kernel<YD>, LTTB_CH_THREADS),
+                                    LTTB_CH_THREADS, 0,
                                     xf, drop, y, n, off, nb, (const double2*)cent, (const int32_t*)nonempty,
                                     (const int64_t*)counts, A, (const int64_t*)ext, picks, (const int32_t*)list_a,
                                     lock, ctr, vec_ok)));

@@ -268,6 +268,37 @@ __device__ __forceinline__ void lttb_list_phase(const int64_t* off, int64_t nb, 
   }
 }
 
+// bucket cursor for warp-strided loops: the next bucket's (k, s, e) is
+// loaded one iteration ahead, so its two dependent round trips overlap the
+// current bucket's work
+struct BucketCursor {
+  const int32_t* nonempty;
+  const int64_t* off;
+  int64_t L, step, j, kn, sn, en;
+  __device__ __forceinline__ void load(int64_t jj) {
+    if (jj < L) {
+      kn = nonempty[jj];
+      sn = __ldg(off + kn);
+      en = __ldg(off + kn + 1);
+    }
+  }
+  __device__ __forceinline__ BucketCursor(const int32_t* ne, const int64_t* o, int64_t L_, int64_t j0, int64_t st)
+      : nonempty(ne), off(o), L(L_), step(st), j(j0), kn(0), sn(0), en(0) {
+    load(j0);
+  }
+  // current bucket -> (k, s, e); prefetch the next
+  __device__ __forceinline__ bool next(int64_t& jj, int64_t& k, int64_t& s, int64_t& e) {
+    if (j >= L) return false;
+    jj = j;
+    k = kn;
+    s = sn;
+    e = en;
+    j += step;
+    load(j);
+    return true;
+  }
+};
+
 // warp per non-empty bucket: centroid (fixed tree order over sub-block sums;
 // the partial boundary sub-blocks are summed point by point) and the
 // y-range (from the sub-block maxima/minima, a superset at the boundaries)
@@ -280,9 +311,8 @@ __device__ __forceinline__ void lttb_cent_phase(const double* x, const void* y, 
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t L = counts[0];
-  for (int64_t j = gw; j < L; j += nw) {
-    const int64_t k = nonempty[j];
-    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+  BucketCursor cur(nonempty, off, L, gw, nw);
+  for (int64_t j, k, s, e; cur.next(j, k, s, e);) {
     const int64_t g0 = s / SB, g1 = (e - 1) / SB;
     double sy = 0.0, sx = 0.0;
     float hi = -INFINITY, lo = INFINITY;
@@ -386,9 +416,8 @@ __device__ __forceinline__ void lttb_cand_phase(const double* x, const void* y, 
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t L = counts[0];
-  for (int64_t j = gw; j < L; j += nw) {
-    const int64_t k = nonempty[j];
-    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+  BucketCursor cur(nonempty, off, L, gw, nw);
+  for (int64_t j, k, s, e; cur.next(j, k, s, e);) {
     const double2 sr = lttb_slope_range<YDT>(x, y, off, nb, n, cent, yr, nonempty, j, k);
     float sl[LTTB_K];  // candidates only steer the guess: f32 scores, bucket-relative u32 positions
 #pragma unroll
@@ -604,10 +633,12 @@ __device__ __forceinline__ void lttb_plan_bucket(const double* x, const void* y,
                                                  int64_t nb, const double2* cent, const int32_t* nonempty,
                                                  const int64_t* ext, const int64_t* picks, int64_t j, int lane,
                                                  int64_t& k, int64_t& s, int64_t& e, LttbPlan& P, AreaCand& cb,
-                                                 double& cx, double& cy) {
-  k = nonempty[j];
-  s = __ldg(off + k);
-  e = __ldg(off + k + 1);
+                                                 double& cx, double& cy, bool known = false) {
+  if (!known) {
+    k = nonempty[j];
+    s = __ldg(off + k);
+    e = __ldg(off + k + 1);
+  }
   P.prev = j == 0 ? 0 : __ldcg(picks + j - 1);
   centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
   const double ax = xd(x, P.prev);
@@ -668,15 +699,15 @@ __device__ __forceinline__ AreaCand lttb_eval_sb(const double* x, const void* y,
   }
   const int64_t v0 = cs / EPV, v1 = (ce + EPV - 1) / EPV;  // vectors overlapping [cs, ce) (<= SBV + 1)
   const uint4* yv = (const uint4*)y;
-  for (int64_t vb = v0; vb < v1; vb += 32 * 16) {
-    uint4 q[16];
+  for (int64_t vb = v0; vb < v1; vb += 32 * 4) {  // sub-blocks are <= 64 vectors: one pass
+    uint4 q[4];
 #pragma unroll
-    for (int u = 0; u < 16; u++) {
+    for (int u = 0; u < 4; u++) {
       const int64_t v = vb + u * 32 + lane;
       if (v < v1) q[u] = __ldg(yv + v);
     }
 #pragma unroll
-    for (int u = 0; u < 16; u++) {
+    for (int u = 0; u < 4; u++) {
       const int64_t v = vb + u * 32 + lane;
       if (v < v1) {
         const int64_t i0 = v * EPV;
@@ -793,12 +824,12 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long* nsb = (unsigned long long*)(ctr + 6);
-  for (int64_t j = gw; j < L; j += nw) {
-    int64_t k, s, e;
+  BucketCursor cur(nonempty, off, L, gw, nw);
+  for (int64_t j, k, s, e; cur.next(j, k, s, e);) {
     LttbPlan P;
     AreaCand cb;
     double cx, cy;
-    lttb_plan_bucket<YDT>(x, y, n, off, nb, cent, nonempty, ext, picks, j, lane, k, s, e, P, cb, cx, cy);
+    lttb_plan_bucket<YDT>(x, y, n, off, nb, cent, nonempty, ext, picks, j, lane, k, s, e, P, cb, cx, cy, true);
     const int64_t g0 = s / SB, g1 = (e - 1) / SB;
     // surviving sub-blocks compacted into the bucket's own slot range
     // [g0 + j, g1 + j] (disjoint across buckets); their slot positions are
@@ -914,8 +945,10 @@ __device__ __forceinline__ int64_t lttb_ld_relaxed(const int64_t* p) {
 // last write to picks[j] therefore always carries f_j(final picks[j-1]): the
 // fixed point is exactly the reference's sequence.
 // ctr: [2] |D|, [3] chain steps, [8] sub-blocks evaluated in chains.
+constexpr int LTTB_CH_THREADS = 128;  // chain CTA: 4 warps (6 CTAs / SM -> ~every dirty bucket its own CTA)
+
 template <int YDT>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(LTTB_CH_THREADS, 6)
 lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
                   const double2* cent, const int32_t* nonempty, const int64_t* counts, const LttbSBArrays A,
                   const int64_t* ext, int64_t* picks, const int32_t* list, int32_t* lock, int32_t* ctr, int vec_ok) {
@@ -926,10 +959,10 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t L = counts[0];
   __shared__ LttbPlan sP;
-  __shared__ AreaCand sCb, sW[8];
+  __shared__ AreaCand sCb, sW[LTTB_CH_THREADS / 32];
   __shared__ double sc[2];   // cx, cy
   __shared__ int64_t sk[3];  // k, s, e
-  __shared__ int64_t sq[256];
+  __shared__ int64_t sq[LTTB_CH_THREADS];
   __shared__ int sn, sgo;
   const int64_t nD = __ldcg(ctr + 2);
   for (int64_t t = blockIdx.x; t < nD; t += gridDim.x) {
@@ -957,14 +990,14 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
       const int64_t s = sk[1], e = sk[2];
       const int64_t g0 = s / SB, g1 = (e - 1) / SB;
       AreaCand wb{-1.0, IDX_NONE};
-      for (int64_t gb = g0; gb <= g1; gb += 256) {
+      for (int64_t gb = g0; gb <= g1; gb += LTTB_CH_THREADS) {
         if (tid == 0) sn = 0;
         __syncthreads();
         const int64_t g = gb + tid;
         if (g <= g1 && lttb_keep_sb<YDT>(x, A, g, s, e, P, sCb.a)) sq[atomicAdd(&sn, 1)] = g;
         __syncthreads();
         const int m = sn;
-        for (int i = wid; i < m; i += 8) {  // warp per sub-block
+        for (int i = wid; i < m; i += LTTB_CH_THREADS / 32) {  // warp per sub-block
           int64_t cs, ce;
           lttb_sb_range(A.SB, sq[i], s, e, cs, ce);
           const AreaCand a = lttb_eval_sb<YDT>(x, y, vec_ok, A, sq[i], cs, ce, P, sc[0], sc[1], lane);
@@ -977,7 +1010,7 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
       __syncthreads();
       if (tid == 0) {
         AreaCand b = sCb;
-        for (int w = 0; w < 8; w++)
+        for (int w = 0; w < LTTB_CH_THREADS / 32; w++)
           if (area_better(sW[w], b)) b = sW[w];
         const int64_t pk = b.i == IDX_NONE ? s : b.i;
         int go = 0;

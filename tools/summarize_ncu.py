@@ -11,7 +11,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
-PROF = os.path.join(ROOT, "profiles")
+PROF = os.environ.get("PROF_DIR") or os.path.join(ROOT, "profiles")
 
 RAW = [
     "gpu__time_duration.sum",
@@ -80,6 +80,52 @@ def main():
         det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
         with open(os.path.join(PROF, f"{tag}_scan_c2_details.csv"), "w") as f:
             f.write(det)
+    # LTTB (C3) launch lists with DRAM bytes (warm caches: --cache-control none)
+    for n_out in (1000, 10000):
+        lp = os.path.join(OUT, f"{tag}_lttb_launches_{n_out}.csv")
+        if not os.path.exists(lp):
+            continue
+        rows = list(csv.reader(open(lp)))
+        start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+        h = rows[start]
+        idi, kn, mn, mv, mu = (h.index("ID"), h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"),
+                               h.index("Metric Unit"))
+        per = {}
+        for r in rows[start + 1:]:
+            per.setdefault(int(r[idi]), {"name": r[kn].split("(")[0].replace("void ", "")})[r[mn]] = (r[mv], r[mu])
+        ids = sorted(per)
+        last = ids[len(ids) // 2:]  # the second of the two calls
+        lines += [f"## LTTB C3 n_out={n_out}: one call, per kernel (ncu, serialised, warm L2)", "",
+                  "| kernel | us | DRAM read MB | DRAM write MB |", "|---|---|---|---|"]
+        tot = 0.0
+        for i in last:
+            d = per[i]
+            t = d.get("gpu__time_duration.sum", ("0", "ns"))
+            us = float(t[0].replace(",", "")) * {"ns": 1e-3, "nsecond": 1e-3, "us": 1, "usecond": 1, "ms": 1e3,
+                                                  "msecond": 1e3}.get(t[1], 1e-3)
+            tot += us
+            rd = unit_bytes(*d.get("dram__bytes_read.sum", ("0", "byte"))) / 1e6
+            wr = unit_bytes(*d.get("dram__bytes_write.sum", ("0", "byte"))) / 1e6
+            lines.append(f"| {d['name']} | {us:.1f} | {rd:.1f} | {wr:.1f} |")
+        lines += [f"| total | {tot:.1f} | | |", ""]
+        with open(os.path.join(PROF, f"{tag}_lttb_launches_{n_out}.csv"), "w") as f:
+            f.write(open(lp).read())
+    rep = os.path.join(OUT, f"{tag}_lttb_sb.ncu-rep")
+    if os.path.exists(rep):
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(out.splitlines()))
+        h, units, v = rows[0], rows[1], rows[2]
+        lines += ["## lttb_sb_kernel (C3 summary pass, ncu --set full, 1 launch)", ""]
+        for m in RAW:
+            if m in h:
+                i = h.index(m)
+                lines.append(f"- `{m}` = {v[i]} {units[i]}")
+        lines.append("")
+    for extra in (f"{tag}_configs.md", f"{tag}_bench.json"):
+        ep = os.path.join(OUT, extra)
+        if os.path.exists(ep):
+            with open(os.path.join(PROF, extra), "w") as f:
+                f.write(open(ep).read())
     with open(os.path.join(PROF, f"{tag}_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     print("\n".join(lines))
