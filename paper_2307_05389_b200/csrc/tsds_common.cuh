@@ -145,7 +145,14 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
 // 8-byte types 24 warps/SM (80 registers, all U loads hoisted) past L1.
 template <int ES>
 struct ScanCfg {
-  static constexpr int MIN_BLOCKS = ES <= 2 ? 4 : 3;
+#ifdef TSDS_KEEP_VECTORS
+  // keep the extremum vectors in registers (no locate re-read); costs the
+  // 1/2-byte kernels a quarter of their occupancy -- measured slower on C5
+  static constexpr bool KEEP = ES <= 2;
+#else
+  static constexpr bool KEEP = false;
+#endif
+  static constexpr int MIN_BLOCKS = (ES <= 2 && !KEEP) ? 4 : 3;
   static constexpr bool L1ALLOC = ES <= 2;
 };
 

@@ -158,12 +158,14 @@ __device__ __forceinline__ void chunk_range(const ScanArgs& A, int64_t w, int64_
 // vector sources: global memory (streaming loads) or a shared-memory tile
 template <bool L1ALLOC>
 struct GlobalSrc {
+  static constexpr bool SMEM = false;
   const uint4* yv;  // virtual vector 0
   __device__ __forceinline__ const uint4* base(int64_t jb) const { return yv + jb; }
   __device__ __forceinline__ uint4 stream(const uint4* p, int j) const { return ldg_stream<L1ALLOC>(p + j); }
   __device__ __forceinline__ uint4 again(const uint4* p, int j) const { return __ldg(p + j); }
 };
 struct SmemSrc {
+  static constexpr bool SMEM = true;
   uint32_t sv;  // shared-memory address of the tile copy; it starts at virtual vector v0
   int64_t v0;
   __device__ __forceinline__ const uint4* base(int64_t jb) const {
@@ -217,11 +219,21 @@ __device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, co
     const uint4* p = src.base(jb);
     R rmn = O::min_init(), rmx = O::max_init();
     int jmn = -1, jmx = -1, jnan = -1;
+    // KEEP: the vectors holding the lane's extrema stay in registers, so no
+    // re-read round trip is needed to locate the element (small bins)
+    constexpr bool KEEP = ScanCfg<sizeof(E)>::KEEP && !Src::SMEM;
+    uint4 kmn = make_uint4(0, 0, 0, 0), kmx = kmn;
     auto step = [&](const uint4& v, int jj) {
       R vmn, vmx;
       O::vminmax(v, vmn, vmx);
-      if (O::upd_min(vmn, rmn)) jmn = jj;
-      if (O::upd_max(vmx, rmx)) jmx = jj;
+      if (O::upd_min(vmn, rmn)) {
+        jmn = jj;
+        if constexpr (KEEP) kmn = v;
+      }
+      if (O::upd_max(vmx, rmx)) {
+        jmx = jj;
+        if constexpr (KEEP) kmx = v;
+      }
       if constexpr (PROP && O::NANABLE) {
         if (jnan < 0 && O::vec_hasnan(v)) jnan = jj;
       }
@@ -238,6 +250,9 @@ __device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, co
       uint4 buf[U];
 #pragma unroll
       for (int u = 0; u < U; u++) buf[u] = src.stream(p, j + 32 * u);
+      if constexpr (KEEP && O::FALLBACK) {
+        if (jb0 == 0) kmn = kmx = buf[0];  // the fallback vector (the lane's first)
+      }
 #pragma unroll
       for (int u = 0; u < U; u++) step(buf[u], j + 32 * u);
     }
@@ -246,6 +261,9 @@ __device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, co
       uint4 buf[U];
 #pragma unroll
       for (int u = 0; u < U; u++) buf[u] = src.stream(p, min(j + 32 * u, last));
+      if constexpr (KEEP && O::FALLBACK) {
+        if (jb0 == 0) kmn = kmx = buf[0];
+      }
 #pragma unroll
       for (int u = 0; u < U; u++) step(buf[u], min(j + 32 * u, last));
     }
@@ -259,8 +277,14 @@ __device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, co
     const int64_t i0 = jb * VEC - A.shift;  // element index of vector jb
     // re-read the (at most three) vectors holding this lane's extrema; all
     // loads are issued before any is used so they overlap
-    const uint4 vmn = src.again(p, jmn >= 0 ? jmn : 0);
-    const uint4 vmx = src.again(p, jmx >= 0 ? jmx : 0);
+    uint4 vmn, vmx;
+    if constexpr (KEEP) {
+      vmn = kmn;
+      vmx = kmx;
+    } else {
+      vmn = src.again(p, jmn >= 0 ? jmn : 0);
+      vmx = src.again(p, jmx >= 0 ? jmx : 0);
+    }
     uint4 vnan = vmn;
     if constexpr (PROP && O::NANABLE) vnan = src.again(p, jnan >= 0 ? jnan : 0);
     if (jmn >= 0 && O::valid(rmn)) {
