@@ -478,6 +478,97 @@ __device__ __forceinline__ void lttb_cand_phase(const double* x, const void* y, 
   }
 }
 
+// CTA per non-empty bucket (few large buckets): the CTA's warps split the
+// bucket's sub-blocks, reduce their LTTB_NC candidates by REDUX, and the
+// per-warp winners merge in shared memory (same selection rule as the warp
+// version: best rounded score, then the lowest position)
+template <int YDT>
+__device__ __forceinline__ void lttb_cand_phase_cta(const double* x, const void* y, const int64_t* off, int64_t nb,
+                                                    int64_t n, const double2* cent, const float2* yr,
+                                                    const int32_t* nonempty, const int64_t* counts,
+                                                    const LttbSBArrays A, int64_t* ext) {
+  __shared__ unsigned s_key[8][LTTB_NC], s_pos[8][LTTB_NC];
+  const int64_t SB = A.SB;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nthr = blockDim.x;
+  const int64_t L = counts[0];
+  for (int64_t j = blockIdx.x; j < L; j += gridDim.x) {
+    const int64_t k = nonempty[j];
+    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+    const double2 sr = lttb_slope_range<YDT>(x, y, off, nb, n, cent, yr, nonempty, j, k);
+    float sl[LTTB_K];
+#pragma unroll
+    for (int t = 0; t < LTTB_K; t++) sl[t] = (float)(sr.x + (sr.y - sr.x) * ((double)t / (double)(LTTB_K - 1)));
+    const double xs = xd(x, s);
+    float bv[LTTB_NC];
+    unsigned bi[LTTB_NC];
+#pragma unroll
+    for (int c = 0; c < LTTB_NC; c++) { bv[c] = (c & 1) ? INFINITY : -INFINITY; bi[c] = 0xffffffffu; }
+    const int64_t g0 = s / SB, g1 = (e - 1) / SB;
+    for (int64_t gb = g0; gb <= g1; gb += (int64_t)nthr * 2) {  // 2 sub-blocks per thread in flight
+      float2 m2[2];
+      unsigned am2[2];
+#pragma unroll
+      for (int u = 0; u < 2; u++) {
+        const int64_t g = gb + u * nthr + tid;
+        m2[u] = g <= g1 ? A.mm[g] : make_float2(-INFINITY, INFINITY);
+        am2[u] = g <= g1 ? A.am[g] : 0xffffffffu;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; u++) {
+        const int64_t g = gb + u * nthr + tid;
+        const unsigned am = am2[u];
+        const int64_t px = g * SB + (am & 0xffff), pn = g * SB + (am >> 16);
+        const bool okx = (am & 0xffff) != 0xffff && px >= s && px < e;
+        const bool okn = (am >> 16) != 0xffff && pn >= s && pn < e;
+        const float dxx = okx ? (float)(xd(x, px) - xs) : 0.0f, dxn = okn ? (float)(xd(x, pn) - xs) : 0.0f;
+#pragma unroll
+        for (int t = 0; t < LTTB_K; t++) {
+          const float vx = fmaf(-sl[t], dxx, m2[u].x), vn = fmaf(-sl[t], dxn, m2[u].y);
+          if (okx && vx > bv[2 * t]) { bv[2 * t] = vx; bi[2 * t] = (unsigned)(px - s); }
+          if (okn && vn < bv[2 * t + 1]) { bv[2 * t + 1] = vn; bi[2 * t + 1] = (unsigned)(pn - s); }
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < LTTB_NC; c++) {
+      const bool mx = (c & 1) == 0;
+      const bool has = bi[c] != 0xffffffffu;
+      const unsigned key = has ? f32_key(bv[c]) : (mx ? 0u : 0xffffffffu);
+      const unsigned w = mx ? __reduce_max_sync(0xffffffffu, key) : __reduce_min_sync(0xffffffffu, key);
+      const unsigned r = __reduce_min_sync(0xffffffffu, (has && key == w) ? bi[c] : 0xffffffffu);
+      if (lane == 0) {
+        s_key[wid][c] = w;
+        s_pos[wid][c] = r;
+      }
+    }
+    __syncthreads();
+    if (wid == 0) {
+      int64_t cand = s;
+      if (lane < LTTB_NC) {
+        const bool mx = (lane & 1) == 0;
+        unsigned bk = mx ? 0u : 0xffffffffu, bp = 0xffffffffu;
+        for (int w = 0; w < (nthr >> 5); w++) {
+          const unsigned kk = s_key[w][lane], pp = s_pos[w][lane];
+          if (pp == 0xffffffffu) continue;
+          if (bp == 0xffffffffu || (mx ? kk > bk : kk < bk) || (kk == bk && pp < bp)) { bk = kk; bp = pp; }
+        }
+        cand = bp == 0xffffffffu ? s : s + (int64_t)bp;
+      }
+      for (int r = 0; r < LTTB_NC; r++) {  // sort by index (odd-even transposition)
+        const int partner = ((lane & 1) == (r & 1)) ? lane + 1 : lane - 1;
+        const int64_t o = __shfl_sync(0xffffffffu, cand, partner & 31);
+        if (lane < LTTB_NC && partner >= 0 && partner < LTTB_NC) {
+          const bool low = lane < partner;
+          cand = low ? (o < cand ? o : cand) : (o > cand ? o : cand);
+        }
+      }
+      if (lane < LTTB_NC) ext[k * LTTB_NC + lane] = cand;
+    }
+    __syncthreads();
+  }
+}
+
 // T[(j+1)*NC + i], j in [-1, L-2]: the candidate of non-empty bucket j+1
 // picked when the predecessor is candidate i of non-empty bucket j (row 0:
 // predecessor = point 0)
@@ -805,7 +896,8 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
     grid.sync();
   }
   stamp(2);
-  lttb_cand_phase<YDT>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext);
+  if (counts[0] <= 4 * (int64_t)gridDim.x) lttb_cand_phase_cta<YDT>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext);
+  else lttb_cand_phase<YDT>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext);
   grid.sync();
   stamp(3);
   lttb_cand_table_phase<YDT>(x, y, n, off, nb, cent, ext, nonempty, counts, T);
@@ -962,7 +1054,7 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   __shared__ AreaCand sCb, sW[LTTB_CH_THREADS / 32];
   __shared__ double sc[2];   // cx, cy
   __shared__ int64_t sk[3];  // k, s, e
-  __shared__ int64_t sq[LTTB_CH_THREADS];
+  __shared__ int64_t sq[LTTB_CH_THREADS * 4];
   __shared__ int sn, sgo;
   const int64_t nD = __ldcg(ctr + 2);
   for (int64_t t = blockIdx.x; t < nD; t += gridDim.x) {
@@ -990,11 +1082,27 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
       const int64_t s = sk[1], e = sk[2];
       const int64_t g0 = s / SB, g1 = (e - 1) / SB;
       AreaCand wb{-1.0, IDX_NONE};
-      for (int64_t gb = g0; gb <= g1; gb += LTTB_CH_THREADS) {
+      for (int64_t gb = g0; gb <= g1; gb += LTTB_CH_THREADS * 4) {
         if (tid == 0) sn = 0;
         __syncthreads();
-        const int64_t g = gb + tid;
-        if (g <= g1 && lttb_keep_sb<YDT>(x, A, g, s, e, P, sCb.a)) sq[atomicAdd(&sn, 1)] = g;
+        float2 m4[4];  // all loads first (one round trip for up to 4 * CTA sub-blocks)
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int64_t g = gb + u * LTTB_CH_THREADS + tid;
+          m4[u] = g <= g1 ? A.mm[g] : make_float2(-INFINITY, INFINITY);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int64_t g = gb + u * LTTB_CH_THREADS + tid;
+          if (g > g1) continue;
+          bool keep = true;
+          if (!x) {
+            int64_t cs, ce;
+            lttb_sb_range(A.SB, g, s, e, cs, ce);
+            keep = !(lttb_sb_bound(m4[u], s, cs, ce, P) < sCb.a);
+          }
+          if (keep) sq[atomicAdd(&sn, 1)] = g;
+        }
         __syncthreads();
         const int m = sn;
         for (int i = wid; i < m; i += LTTB_CH_THREADS / 32) {  // warp per sub-block
