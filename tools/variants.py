@@ -83,7 +83,8 @@ def main():
         L.tsds_ctx_profile_read(ctx.handle, ctypes.byref(tot), ctypes.byref(k))
         L.tsds_ctx_profile(ctx.handle, 0)
         scan = tot.value / max(1, k.value)
-        print(f"{wl} {name}: step {ms*1e3:8.1f} us ({nbytes/ms/1e6:7.0f} GB/s)   scan {scan*1e3:8.1f} us ({nbytes/scan/1e6:7.0f} GB/s)")
+        sc = f"scan {scan*1e3:8.1f} us ({nbytes/scan/1e6:7.0f} GB/s)" if scan > 0 else "scan (not profiled)"
+        print(f"{wl} {name}: step {ms*1e3:8.1f} us ({nbytes/ms/1e6:7.0f} GB/s)   {sc}")
 
 
 if __name__ == "__main__":
