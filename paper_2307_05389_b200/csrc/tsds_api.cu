@@ -158,7 +158,16 @@ int begin_call(tsds_ctx* ctx) {
 int dtype_ok(int dt) { return dt >= 0 && dt < DT_COUNT; }
 
 // tuning knobs: environment defaults, overridable with tsds_set_option
-int64_t g_dyn_percent = -1, g_tma_min_bytes = -1, g_cta_bins_max = -1;
+int64_t g_dyn_percent = -1, g_tma_min_bytes = -1, g_cta_bins_max = -1, g_lane_bins = -1;
+
+// thread-per-bin batched kernel: 0 off, 1 auto (default), 2 whenever eligible
+int64_t lane_bins_mode() {
+  if (g_lane_bins < 0) {
+    const char* e = getenv("TSDS_LANE_BINS");
+    g_lane_bins = e ? std::max(0, std::min(2, atoi(e))) : 1;
+  }
+  return g_lane_bins;
+}
 
 // CTA-per-bin scan for inputs up to this many bytes (latency-bound sizes)
 int64_t cta_bins_max_bytes() {
@@ -1023,6 +1032,7 @@ int tsds_set_option(const char* name, int64_t value) {
   std::string n(name);
   if (n == "tma_min_bytes") g_tma_min_bytes = std::max<int64_t>(0, value);
   else if (n == "dyn_percent") g_dyn_percent = std::max<int64_t>(0, std::min<int64_t>(90, value));
+  else if (n == "lane_bins") g_lane_bins = std::max<int64_t>(0, std::min<int64_t>(2, value));
   else if (n == "cta_bins_max_bytes") g_cta_bins_max = std::max<int64_t>(0, value);
   else if (n == "lttb_exact") g_lttb_exact = std::max<int64_t>(0, std::min<int64_t>(2, value));
   else return set_err(TSDS_ERR_ARG, "unknown option " + n);
@@ -1265,11 +1275,12 @@ static int batched_enqueue(tsds_ctx* ctx, const void* dy, int ydt, int64_t S, in
   // many short bins (4 .. 256 vectors each, enough of them to fill the GPU
   // with one thread per bin): thread-per-bin kernel.  Measured on C5 (1024
   // series): u8 (250 vectors/bin) 749 -> 477 us; i16/f16 (500 vectors/bin)
-  // are faster on the warp scan.  Env TSDS_LANE_BINS=0 disables it.
+  // are faster on the warp scan.  Option / env "lane_bins" (TSDS_LANE_BINS).
   const int64_t es = dtype_size(ydt), bin_bytes = (L / nb) * es;
-  const char* lb = getenv("TSDS_LANE_BINS");
-  const bool lane_ok = !nan_mode && ((uintptr_t)dy % 16) == 0 && bin_bytes >= 64 && bin_bytes <= 4096 &&
-                       S * nb >= (int64_t)ctx->sms * 1024 && !(lb && atoi(lb) == 0);
+  const int64_t mode = lane_bins_mode();  // 0 off, 1 auto, 2 whenever eligible (tests)
+  const bool eligible = !nan_mode && ((uintptr_t)dy % 16) == 0;
+  const bool lane_ok = eligible && (mode == 2 || (mode == 1 && bin_bytes >= 64 && bin_bytes <= 4096 &&
+                                                  S * nb >= (int64_t)ctx->sms * 1024));
   if (lane_ok) RC_TRY(launch_lane_bins(ctx, ydt, A));
   else RC_TRY(launch_scan(ctx, ydt, nan_mode, A));
   A.epi = EPI_MINMAX;

@@ -148,6 +148,37 @@ def test_batched_rows_equal_single(ts, oracle):
             assert idx[s, : cnt[s]].tolist() == want[s, : wcnt[s]].tolist(), (tag, s)
 
 
+def test_batched_thread_per_bin_kernel(ts, oracle):
+    """The thread-per-bin batched kernel (forced on for small inputs): every
+    width, ties, f16 +-0/NaN ordering, f32 NaNs, and bins that do not start
+    or end on a 16-byte boundary (head/tail elements)."""
+    from paper_2307_05389_b200 import _lib
+
+    L = _lib.load()
+    rng = np.random.default_rng(12)
+    try:
+        L.tsds_set_option(b"lane_bins", 2)
+        for tag in ("u8", "i8", "i16", "u16", "f16", "f32", "i32", "u64", "f64"):
+            for length, n_out in ((20_000, 100), (20_011, 98), (4_003, 1000)):
+                Y = np.stack([W.random_series(tag, length, int(rng.integers(1 << 30)), ties=True) for _ in range(5)])
+                if tag in ("f32", "f64"):
+                    Y[1, ::97] = np.nan
+                    Y[2, :] = np.nan
+                if tag == "f16":
+                    Y[1, ::53] = -0.0
+                    Y[1, 7::61] = 0.0
+                    Y[2, ::71] = np.float16("nan")
+                    Y[3].view(np.uint16)[5::89] = 0xFE00  # negative NaN pattern (ordinal: below -inf)
+                    Y[4, ::37] = -np.inf
+                idx, cnt = ts.minmax_batched(Y, n_out=n_out)
+                want, wcnt = oracle.minmax_batched(Y, n_out=n_out)
+                assert np.array_equal(cnt, wcnt), (tag, length)
+                for s in range(Y.shape[0]):
+                    assert idx[s, : cnt[s]].tolist() == want[s, : wcnt[s]].tolist(), (tag, length, s)
+    finally:
+        L.tsds_set_option(b"lane_bins", 1)
+
+
 def test_c1_config(ts):
     g = G.configs()
     y = W.config1()
