@@ -1274,12 +1274,13 @@ static int batched_enqueue(tsds_ctx* ctx, const void* dy, int ydt, int64_t S, in
   A.out = nullptr;
   // many short bins (4 .. 256 vectors each, enough of them to fill the GPU
   // with one thread per bin): thread-per-bin kernel.  Measured on C5 (1024
-  // series): u8 (250 vectors/bin) 749 -> 477 us; i16/f16 (500 vectors/bin)
-  // are faster on the warp scan.  Option / env "lane_bins" (TSDS_LANE_BINS).
+  // series, 4000-point bins): u8 749 -> 405 us, f16 887 -> 809 us; i16 stays
+  // on the warp scan (745 vs 806 us).  Option / env "lane_bins" (TSDS_LANE_BINS).
   const int64_t es = dtype_size(ydt), bin_bytes = (L / nb) * es;
   const int64_t mode = lane_bins_mode();  // 0 off, 1 auto, 2 whenever eligible (tests)
   const bool eligible = !nan_mode && ((uintptr_t)dy % 16) == 0;
-  const bool lane_ok = eligible && (mode == 2 || (mode == 1 && bin_bytes >= 64 && bin_bytes <= 4096 &&
+  const int64_t max_bytes = ydt == DT_F16 ? 16384 : 4096;  // f16: the warp scan's ordinal keys cost more
+  const bool lane_ok = eligible && (mode == 2 || (mode == 1 && bin_bytes >= 64 && bin_bytes <= max_bytes &&
                                                   S * nb >= (int64_t)ctx->sms * 1024));
   if (lane_ok) RC_TRY(launch_lane_bins(ctx, ydt, A));
   else RC_TRY(launch_scan(ctx, ydt, nan_mode, A));

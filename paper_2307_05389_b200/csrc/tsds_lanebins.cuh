@@ -49,19 +49,28 @@ lane_bins_kernel(const ScanArgs A) {
       R rmn = O::min_init(), rmx = O::max_init();
       int64_t jmn = -1, jmx = -1;
       uint4 kmn = make_uint4(0, 0, 0, 0), kmx = kmn;
-      for (int64_t j = jb; j < je; j += 8) {
-        uint4 buf[8];
+      // software pipeline: the next LB_U vectors are in flight while the
+      // current ones are folded
+      constexpr int LB_U = 4;
+      uint4 cur[LB_U];
 #pragma unroll
-        for (int u = 0; u < 8; u++) buf[u] = __ldg(yv + (j + u < je ? j + u : je - 1));
+      for (int u = 0; u < LB_U; u++) cur[u] = __ldg(yv + (jb + u < je ? jb + u : je - 1));
+      for (int64_t j = jb; j < je; j += LB_U) {
+        uint4 nxt[LB_U];
+        const int64_t jn = j + LB_U;
 #pragma unroll
-        for (int u = 0; u < 8; u++) {
+        for (int u = 0; u < LB_U; u++) nxt[u] = __ldg(yv + (jn + u < je ? jn + u : je - 1));
+#pragma unroll
+        for (int u = 0; u < LB_U; u++) {
           if (j + u < je) {
             R vmn, vmx;
-            O::vminmax(buf[u], vmn, vmx);
-            if (O::upd_min(vmn, rmn)) { jmn = j + u; kmn = buf[u]; }
-            if (O::upd_max(vmx, rmx)) { jmx = j + u; kmx = buf[u]; }
+            O::vminmax(cur[u], vmn, vmx);
+            if (O::upd_min(vmn, rmn)) { jmn = j + u; kmn = cur[u]; }
+            if (O::upd_max(vmx, rmx)) { jmx = j + u; kmx = cur[u]; }
           }
         }
+#pragma unroll
+        for (int u = 0; u < LB_U; u++) cur[u] = nxt[u];
       }
       if constexpr (O::FALLBACK) {  // nothing beat the init sentinel: the first vector holds it
         if (jmn < 0) { jmn = jb; kmn = __ldg(yv + jb); }
