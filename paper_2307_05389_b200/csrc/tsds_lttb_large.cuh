@@ -685,6 +685,58 @@ __device__ __forceinline__ void lttb_seg_expand_phase(const uint8_t* T, const ui
   }
 }
 
+// Few buckets (L * LTTB_NC fits the dynamic shared memory): compose, entry
+// and expand inside ONE CTA with the whole transition table staged in
+// shared memory -- block barriers instead of three grid barriers.
+__device__ __forceinline__ bool lttb_chain_fits(int64_t L, int64_t cap) {
+  const int64_t NS = (L + LTTB_SEG - 1) / LTTB_SEG;
+  return ((L * LTTB_NC + 15) & ~(int64_t)15) + NS * LTTB_NC + NS <= cap;
+}
+__device__ __forceinline__ void lttb_chain_small_cta(const uint8_t* T, const int64_t* ext, const int32_t* nonempty,
+                                                     int64_t L, int64_t* picks, uint8_t* sm,
+                                                     uint8_t (*segc)[LTTB_SEG]) {
+  const int tid = threadIdx.x, lane = tid & 31, wl = tid >> 5, nwarp = blockDim.x >> 5;
+  const int64_t NS = (L + LTTB_SEG - 1) / LTTB_SEG;
+  const int64_t tb = (L * LTTB_NC + 15) & ~(int64_t)15;
+  uint8_t* sT = sm;
+  uint8_t* sC = sm + tb;
+  uint8_t* sE = sC + NS * LTTB_NC;
+  for (int64_t v = tid; v < tb / 16; v += blockDim.x) ((uint4*)sT)[v] = __ldcg((const uint4*)T + v);
+  __syncthreads();
+  for (int64_t sg = wl; sg < NS; sg += nwarp) {  // compose
+    const int64_t j0 = sg * LTTB_SEG, j1 = (sg + 1) * LTTB_SEG < L - 1 ? (sg + 1) * LTTB_SEG : L - 1;
+    if (lane < LTTB_NC) {
+      int c = lane;
+      for (int64_t r = j0; r < j1; r++) c = sT[(r + 1) * LTTB_NC + c];
+      sC[sg * LTTB_NC + lane] = (uint8_t)c;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {  // entry candidate of every segment
+    int c = sT[0];
+    for (int64_t sg = 0; sg < NS; sg++) {
+      sE[sg] = (uint8_t)c;
+      c = sC[sg * LTTB_NC + c];
+    }
+  }
+  __syncthreads();
+  for (int64_t sg = wl; sg < NS; sg += nwarp) {  // expand
+    const int64_t j0 = sg * LTTB_SEG, j1 = (sg + 1) * LTTB_SEG < L ? (sg + 1) * LTTB_SEG : L;
+    const int64_t nr = j1 - j0;
+    if (lane == 0) {
+      int c = sE[sg];
+      for (int64_t r = 0; r < nr; r++) {
+        segc[wl][r] = (uint8_t)c;
+        if (r + 1 < nr) c = sT[(j0 + r + 1) * LTTB_NC + c];
+      }
+    }
+    __syncwarp();
+    for (int64_t r = lane; r < nr; r += 32)
+      picks[j0 + r] = __ldg(ext + (int64_t)nonempty[j0 + r] * LTTB_NC + segc[wl][r]);
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Pruning.  For bucket j with predecessor p (ax = p, ay = y[p]) and c the
 // centroid of the next bucket, the reference area of point i is
@@ -902,11 +954,15 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   stamp(3);
   lttb_cand_table_phase<YDT>(x, y, n, off, nb, cent, ext, nonempty, counts, T);
   grid.sync();
-  lttb_seg_compose_phase(T, counts, C, rows);
-  grid.sync();
-  if (blockIdx.x == 0) lttb_seg_entry_phase(T, C, counts, entry, lttb_dsm, cap);
-  grid.sync();
-  lttb_seg_expand_phase(T, entry, ext, nonempty, counts, picks, rows, segc);
+  if (lttb_chain_fits(counts[0], cap)) {
+    if (blockIdx.x == 0) lttb_chain_small_cta(T, ext, nonempty, counts[0], picks, lttb_dsm, segc);
+  } else {
+    lttb_seg_compose_phase(T, counts, C, rows);
+    grid.sync();
+    if (blockIdx.x == 0) lttb_seg_entry_phase(T, C, counts, entry, lttb_dsm, cap);
+    grid.sync();
+    lttb_seg_expand_phase(T, entry, ext, nonempty, counts, picks, rows, segc);
+  }
   grid.sync();
   stamp(4);
   // ---- round-1 plan
