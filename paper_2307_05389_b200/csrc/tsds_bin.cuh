@@ -175,6 +175,18 @@ __device__ int64_t lower_bound_fast_cta(const void* x, int64_t n, double e, doub
   double t = __ddiv_rn(__dsub_rn(e, x0), span);
   t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
   int64_t g = (int64_t)(t * (double)(n - 1));
+  // one secant step from the probe at g: linear interpolation alone misses by
+  // thousands of elements on jittered timestamps (config 2), which sends the
+  // search to the slow exact fallback; the corrected guess lands in the window
+  {
+    const double slope = span / (double)(n - 1);
+    const double xg = xf64<XDT>(x, g);
+    const double d = (e - xg) / slope;
+    if (d == d && fabs(d) < (double)n) {
+      int64_t g2 = g + (int64_t)d;
+      g = g2 < 0 ? 0 : (g2 > n - 1 ? n - 1 : g2);
+    }
+  }
   int64_t ws = g - W / 2;
   if (ws > n - W) ws = n - W;
   if (ws < 0) ws = 0;
