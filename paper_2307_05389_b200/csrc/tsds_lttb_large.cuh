@@ -1102,6 +1102,7 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
                   const int64_t* ext, int64_t* picks, const int32_t* list, int32_t* lock, int32_t* ctr, int vec_ok) {
   pdl_launch_dependents();
   pdl_wait();
+  constexpr int NSQ = LTTB_CH_THREADS * 4;  // sub-blocks tested per pass
   const int64_t SB = A.SB;
   const double* x = eff_x(xin, drop);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1110,18 +1111,46 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   __shared__ AreaCand sCb, sW[LTTB_CH_THREADS / 32];
   __shared__ double sc[2];   // cx, cy
   __shared__ int64_t sk[3];  // k, s, e
-  __shared__ int64_t sq[LTTB_CH_THREADS * 4];
+  __shared__ int64_t sq[NSQ];
   __shared__ int sn, sgo;
+  // static data of the chain's next bucket, prefetched while the current
+  // bucket is being settled (everything but the predecessor is known)
+  __shared__ int64_t pf_j, pf_k[3], pf_ci[LTTB_NC];
+  __shared__ double pf_c[2], pf_cx[LTTB_NC], pf_cy[LTTB_NC];
+  __shared__ float2 pf_mm[NSQ];
+  __shared__ int64_t pf_mmj;
   const int64_t nD = __ldcg(ctr + 2);
   for (int64_t t = blockIdx.x; t < nD; t += gridDim.x) {
     int64_t j = __ldcg(list + t);
+    if (tid == 0) pf_j = pf_mmj = -1;
+    __syncthreads();
     for (;;) {
       if (wid == 0) {
         int64_t k, s, e;
         LttbPlan P;
         AreaCand cb;
         double cx, cy;
-        lttb_plan_bucket<YDT>(x, y, n, off, nb, cent, nonempty, ext, picks, j, lane, k, s, e, P, cb, cx, cy);
+        if (pf_j == j) {  // prefetched: only the predecessor's point is new
+          k = pf_k[0];
+          s = pf_k[1];
+          e = pf_k[2];
+          cx = pf_c[0];
+          cy = pf_c[1];
+          P.prev = j == 0 ? 0 : __ldcg(picks + j - 1);
+          const double ax = xd(x, P.prev);
+          P.ay = yd<YDT>(y, P.prev);
+          P.K1 = __dsub_rn(ax, cx);
+          P.K2 = __dsub_rn(cy, P.ay);
+          P.sig = -P.K2 / P.K1;
+          cb = AreaCand{-1.0, IDX_NONE};
+          if (lane < LTTB_NC) {
+            const double a = tri_area(ax, P.ay, cx, cy, pf_cx[lane], pf_cy[lane]);
+            if (a > -1.0) cb = AreaCand{a, pf_ci[lane]};
+          }
+          cb = warp_area_max(cb);
+        } else {
+          lttb_plan_bucket<YDT>(x, y, n, off, nb, cent, nonempty, ext, picks, j, lane, k, s, e, P, cb, cx, cy);
+        }
         if (lane == 0) {
           sP = P;
           sCb = cb;
@@ -1138,14 +1167,15 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
       const int64_t s = sk[1], e = sk[2];
       const int64_t g0 = s / SB, g1 = (e - 1) / SB;
       AreaCand wb{-1.0, IDX_NONE};
-      for (int64_t gb = g0; gb <= g1; gb += LTTB_CH_THREADS * 4) {
+      for (int64_t gb = g0; gb <= g1; gb += NSQ) {
         if (tid == 0) sn = 0;
         __syncthreads();
+        const bool pre = gb == g0 && pf_mmj == j;
         float2 m4[4];  // all loads first (one round trip for up to 4 * CTA sub-blocks)
 #pragma unroll
         for (int u = 0; u < 4; u++) {
           const int64_t g = gb + u * LTTB_CH_THREADS + tid;
-          m4[u] = g <= g1 ? A.mm[g] : make_float2(-INFINITY, INFINITY);
+          m4[u] = g <= g1 ? (pre ? pf_mm[u * LTTB_CH_THREADS + tid] : A.mm[g]) : make_float2(-INFINITY, INFINITY);
         }
 #pragma unroll
         for (int u = 0; u < 4; u++) {
@@ -1186,9 +1216,38 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
         }
         lttb_unlock(lock + j);
         sgo = go;
+      } else if (wid > 0 && j + 1 < L) {
+        // meanwhile warps 1.. prefetch bucket j+1 (used only if the chain goes on)
+        const int64_t jn = j + 1;
+        const int64_t kn = nonempty[jn];
+        const int64_t sn_ = __ldg(off + kn), en = __ldg(off + kn + 1);
+        if (wid == 1) {
+          double cx, cy;
+          centroid_for<YDT>(x, y, off, nb, cent, kn, n, cx, cy);
+          if (lane < LTTB_NC) {
+            const int64_t pi = __ldg(ext + kn * LTTB_NC + lane);
+            pf_ci[lane] = pi;
+            pf_cx[lane] = xd(x, pi);
+            pf_cy[lane] = yd<YDT>(y, pi);
+          }
+          if (lane == 0) {
+            pf_k[0] = kn;
+            pf_k[1] = sn_;
+            pf_k[2] = en;
+            pf_c[0] = cx;
+            pf_c[1] = cy;
+          }
+          __syncwarp();
+          if (lane == 0) pf_j = jn;
+        } else {
+          const int64_t gn0 = sn_ / SB, gn1 = (en - 1) / SB;
+          for (int i = tid - 64; i < NSQ; i += LTTB_CH_THREADS - 64)
+            if (gn0 + i <= gn1) pf_mm[i] = A.mm[gn0 + i];
+        }
       }
       __syncthreads();
       const int go = sgo;
+      if (tid == 0) pf_mmj = j + 1;  // pf_mm (warps 2..) holds bucket j+1's first sub-blocks
       __syncthreads();
       if (!go) break;
       j++;
