@@ -580,6 +580,10 @@ scan_kernel(const ScanArgs A) {
     const int wid = threadIdx.x >> 5;
     for (int64_t g = A.g0 + blockIdx.x; g < A.g1; g += gridDim.x) {
       const int64_t s = bin_off(B, g), e = bin_off(B, g + 1);
+      bool nan0 = false;  // the NaN-first-slot probe (A.3), issued before the reduction
+      if constexpr (!PROP && Ops<DT>::IEEE) {
+        if (threadIdx.x == 0 && e > s) nan0 = elem_is_nan<DT>(A.y, s);
+      }
       if (e > s) {
         const int64_t len = e - s;
         const int64_t a = s + len * wid / SCAN_WARPS, c = s + len * (wid + 1) / SCAN_WARPS;
@@ -594,7 +598,9 @@ scan_kernel(const ScanArgs A) {
           merge_min(acc.mn, part_s[w].mn);
           merge_max(acc.mx, part_s[w].mx);
         }
-        finalize<DT, PROP>(A, B, g, acc);
+        int64_t* o = A.res + 2 * (g - A.g0);
+        o[0] = nan0 ? s : acc.mn.idx;
+        o[1] = nan0 ? s : acc.mx.idx;
       }
       __syncthreads();
     }
