@@ -347,8 +347,9 @@ __device__ __forceinline__ void finalize(const ScanArgs& A, const BinSpec& B, in
 __device__ __forceinline__ int bin_emit(const ScanArgs& A, const BinSpec& B, int64_t g, int64_t v[4]) {
   int64_t s = bin_off(B, g), e = bin_off(B, g + 1);
   if (e <= s) return 0;
-  int64_t lo = ld_cg_i64(A.res + 2 * (g - A.g0));
-  int64_t hi = ld_cg_i64(A.res + 2 * (g - A.g0) + 1);
+  // plain L2 loads (not volatile asm): the compaction's bins can overlap
+  int64_t lo = (int64_t)__ldcg((const long long*)A.res + 2 * (g - A.g0));
+  int64_t hi = (int64_t)__ldcg((const long long*)A.res + 2 * (g - A.g0) + 1);
   int64_t p = lo < hi ? lo : hi, q = lo < hi ? hi : lo;
   if (A.epi == EPI_MINMAX || A.epi == EPI_SLOTS_MINMAX) {
     v[0] = p;
