@@ -267,6 +267,10 @@ def test_lttb_large_vector_paths(ts, oracle):
         (np.abs(base) % 250).astype(np.uint8),
         (np.abs(base) * 7).astype(np.uint32),
     ]
+    withinf = base.copy()
+    withinf[rng.integers(0, base.size, 8)] = np.inf
+    withinf[rng.integers(0, base.size, 8)] = -np.inf
+    cases += [withinf, np.full(200_000, 3.25), np.full(200_000, np.nan)]
     for y in cases:
         for n_out in (300, 15_000):  # avg bucket 2000 and 40: both on the large path
             got = ts.downsample("lttb", y, n_out=n_out)
