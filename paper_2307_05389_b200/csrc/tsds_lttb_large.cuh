@@ -335,20 +335,27 @@ __device__ __forceinline__ void lttb_cent_phase(const double* x, const void* y, 
         sx = __dadd_rn(sx, vx[u]);
       }
     }
-    // partial boundary sub-blocks: point by point
+    // partial boundary sub-blocks: point by point (a lane's points loaded
+    // together, then summed in index order)
+    auto partial = [&](int64_t a, int64_t b) {
+      for (int64_t i0 = a; i0 < b; i0 += 32 * 4) {
+        double vy[4], vx[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int64_t i = i0 + u * 32 + lane;
+          vy[u] = i < b ? yd<YDT>(y, i) : 0.0;
+          vx[u] = (i < b && x) ? __ldg(x + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          sy = __dadd_rn(sy, vy[u]);
+          sx = __dadd_rn(sx, vx[u]);
+        }
+      }
+    };
     const int64_t h0e = (g0 + 1) * SB < e ? (g0 + 1) * SB : e;
-    if (s % SB != 0 || h0e < (g0 + 1) * SB) {
-      for (int64_t i = s + lane; i < h0e; i += 32) {
-        sy = __dadd_rn(sy, yd<YDT>(y, i));
-        if (x) sx = __dadd_rn(sx, __ldg(x + i));
-      }
-    }
-    if (g1 > g0 && e % SB != 0) {
-      for (int64_t i = g1 * SB + lane; i < e; i += 32) {
-        sy = __dadd_rn(sy, yd<YDT>(y, i));
-        if (x) sx = __dadd_rn(sx, __ldg(x + i));
-      }
-    }
+    if (s % SB != 0 || h0e < (g0 + 1) * SB) partial(s, h0e);
+    if (g1 > g0 && e % SB != 0) partial(g1 * SB, e);
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) {
       sy = __dadd_rn(sy, __shfl_xor_sync(0xffffffffu, sy, m));
