@@ -73,8 +73,14 @@ struct LttbSBArrays {
 // shared memory rather than registers; XOR-swizzled so that the lane-owned
 // reads are conflict-free), then every lane folds its own 8 vectors: running
 // sum in index order, first max / first min of the outward-rounded values.
-constexpr int LTTB_SB_D = 3;          // rounds in flight per warp
-constexpr int LTTB_SB_WARPS = 8;      // warps per CTA
+#ifndef LTTB_SB_D_N
+#define LTTB_SB_D_N 3
+#endif
+#ifndef LTTB_SB_WARPS_N
+#define LTTB_SB_WARPS_N 8
+#endif
+constexpr int LTTB_SB_D = LTTB_SB_D_N;          // rounds in flight per warp
+constexpr int LTTB_SB_WARPS = LTTB_SB_WARPS_N;  // warps per CTA
 constexpr int LTTB_SB_SMEM = LTTB_SB_WARPS * LTTB_SB_D * 4096;
 
 // running first max / first min in f64 (NaN never compares true); the
