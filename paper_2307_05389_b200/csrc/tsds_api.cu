@@ -706,6 +706,8 @@ static inline unsigned cap_grid(int64_t want, int64_t cap) {
 // dependent launch.
 int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
                    const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev) {
+  if (nb >= ((int64_t)1 << 24))  // work-list entries pack the bucket rank into 24 bits
+    return set_err(TSDS_ERR_ARG, "large-bucket LTTB supports fewer than 2^24 buckets");
   RC_TRY(ensure(ctx, ctx->cent, (size_t)std::max<int64_t>(nb, 1) * sizeof(double2)));
   double2* cent = (double2*)ctx->cent.p;
   const int64_t NC = LTTB_NC;
