@@ -66,6 +66,7 @@ struct tsds_ctx {
   int64_t lttb_dirty1 = 0;  // buckets whose guess was wrong in the first round
   int64_t lttb_pieces = 0;  // pieces evaluated exactly (all rounds, after pruning)
   int64_t lttb_pieces1 = 0; // ... in round 1
+  int64_t lttb_longest = 0; // longest correction chain of the last large-bucket LTTB
   int32_t* h_lstat = nullptr;  // pinned {rounds, dirty1} of the last large-bucket LTTB
   bool lstat_pending = false;
   void* h_pin = nullptr;
@@ -1108,7 +1109,8 @@ int64_t tsds_ctx_stat(tsds_ctx* ctx, const char* name) {
   if (!ctx || !name) return -1;
   std::string n(name);
   if (n == "launches") return ctx->launches;
-  const bool lt = n == "lttb_rounds" || n == "lttb_dirty1" || n == "lttb_pieces" || n == "lttb_pieces1";
+  const bool lt = n == "lttb_rounds" || n == "lttb_dirty1" || n == "lttb_pieces" || n == "lttb_pieces1" ||
+                  n == "lttb_longest_chain";
   if (ctx->lstat_pending && lt) {
     std::lock_guard<std::mutex> lk(ctx->mu);
     cudaSetDevice(ctx->device);
@@ -1117,6 +1119,7 @@ int64_t tsds_ctx_stat(tsds_ctx* ctx, const char* name) {
       ctx->lttb_dirty1 = ctx->h_lstat[2];   // |D|: buckets whose predecessor changed in round 1
       ctx->lttb_pieces = ctx->h_lstat[8];   // sub-blocks evaluated in the chains
       ctx->lttb_pieces1 = ctx->h_lstat[6];  // sub-blocks evaluated in round 1 (low word)
+      ctx->lttb_longest = ctx->h_lstat[10]; // longest correction chain (steps)
     }
     ctx->lstat_pending = false;
   }
@@ -1130,6 +1133,7 @@ int64_t tsds_ctx_stat(tsds_ctx* ctx, const char* name) {
   if (n == "lttb_dirty1") return ctx->lttb_dirty1;
   if (n == "lttb_pieces") return ctx->lttb_pieces;    // pieces evaluated exactly, all rounds
   if (n == "lttb_pieces1") return ctx->lttb_pieces1;  // pieces evaluated exactly in round 1
+  if (n == "lttb_longest_chain") return ctx->lttb_longest;
   return -1;
 }
 

@@ -1135,9 +1135,11 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   const int64_t nD = __ldcg(ctr + 2);
   for (int64_t t = blockIdx.x; t < nD; t += gridDim.x) {
     int64_t j = __ldcg(list + t);
+    int clen = 0;  // steps of this chain (stat: longest chain, ctr[10])
     if (tid == 0) pf_j = pf_mmj = -1;
     __syncthreads();
     for (;;) {
+      clen++;
       if (wid == 0) {
         int64_t k, s, e;
         LttbPlan P;
@@ -1262,7 +1264,10 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
       const int go = sgo;
       if (tid == 0) pf_mmj = j + 1;  // pf_mm (warps 2..) holds bucket j+1's first sub-blocks
       __syncthreads();
-      if (!go) break;
+      if (!go) {
+        if (tid == 0) atomicMax(ctr + 10, clen);
+        break;
+      }
       j++;
     }
   }

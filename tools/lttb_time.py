@@ -53,7 +53,7 @@ def main():
         for n_out in (1000, 10000):
             ms, r = timeit(lambda: ts.downsample("lttb", yd, n_out=n_out))
             from paper_2307_05389_b200 import _lib
-            st = {k: _lib.load().tsds_ctx_stat(_lib.context().handle, k.encode()) for k in ("lttb_rounds", "lttb_dirty1", "lttb_pieces1", "lttb_pieces", "lttb_ts1", "lttb_ts2", "lttb_ts3", "lttb_ts4", "lttb_ts5")}
+            st = {k: _lib.load().tsds_ctx_stat(_lib.context().handle, k.encode()) for k in ("lttb_rounds", "lttb_dirty1", "lttb_pieces1", "lttb_pieces", "lttb_longest_chain", "lttb_ts1", "lttb_ts2", "lttb_ts3", "lttb_ts4", "lttb_ts5")}
             st["gpu_ms"] = round(gpu_span(lambda: ts.downsample("lttb", yd, n_out=n_out)), 3)
             g = np.load(os.path.join(ROOT, "tests", "golden", "configs.npz"))
             ok = np.array_equal(r, g[f"c3_lttb_{n_out}"]) if n == W.C3_N else None
