@@ -179,6 +179,23 @@ def test_batched_thread_per_bin_kernel(ts, oracle):
         L.tsds_set_option(b"lane_bins", 1)
 
 
+def test_cta_per_bin_scan_mode(ts, oracle):
+    """Small inputs with >= #SM bins take the CTA-per-bin scan (C1's path):
+    MinMax / M4 / NaN-propagating, with and without x, every width."""
+    rng = np.random.default_rng(21)
+    for tag in ("f32", "f64", "f16", "i64", "u8", "i16", "u32"):
+        y = W.random_series(tag, 300_001, int(rng.integers(1 << 30)), ties=True)
+        if tag in ("f32", "f64"):
+            y[rng.integers(0, y.size, 300)] = np.nan
+        x = np.cumsum(rng.integers(1, 9, y.size)).astype(np.int64)
+        for algo in ("minmax", "m4"):
+            assert ts.downsample(algo, y, n_out=2000).tolist() == oracle.downsample(algo, y, n_out=2000).tolist(), (tag, algo)
+            assert ts.downsample(algo, x, y, n_out=2000).tolist() == oracle.downsample(algo, x, y, n_out=2000).tolist(), (tag, algo, "x")
+        if tag in ("f32", "f64", "f16"):
+            got = ts.downsample("nanm4", y, n_out=2000).tolist()
+            assert got == oracle.downsample("m4", y, n_out=2000, nan=True).tolist(), (tag, "nanm4")
+
+
 def test_c1_config(ts):
     g = G.configs()
     y = W.config1()
