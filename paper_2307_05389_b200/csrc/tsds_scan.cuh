@@ -344,12 +344,15 @@ __device__ __forceinline__ void finalize(const ScanArgs& A, const BinSpec& B, in
 }
 
 // values emitted for bin g, sorted ascending; returns count
-__device__ __forceinline__ int bin_emit(const ScanArgs& A, const BinSpec& B, int64_t g, int64_t v[4]) {
+// plain L2 loads (not volatile asm): the compaction's bins can overlap
+__device__ __forceinline__ longlong2 bin_res(const ScanArgs& A, int64_t g) {
+  return __ldcg((const longlong2*)A.res + (g - A.g0));
+}
+// (lo, hi) already loaded by the caller; an empty bin ignores them
+__device__ __forceinline__ int bin_emit_r(const ScanArgs& A, const BinSpec& B, int64_t g, longlong2 r, int64_t v[4]) {
   int64_t s = bin_off(B, g), e = bin_off(B, g + 1);
   if (e <= s) return 0;
-  // plain L2 loads (not volatile asm): the compaction's bins can overlap
-  int64_t lo = (int64_t)__ldcg((const long long*)A.res + 2 * (g - A.g0));
-  int64_t hi = (int64_t)__ldcg((const long long*)A.res + 2 * (g - A.g0) + 1);
+  int64_t lo = (int64_t)r.x, hi = (int64_t)r.y;
   int64_t p = lo < hi ? lo : hi, q = lo < hi ? hi : lo;
   if (A.epi == EPI_MINMAX || A.epi == EPI_SLOTS_MINMAX) {
     v[0] = p;
@@ -363,6 +366,9 @@ __device__ __forceinline__ int bin_emit(const ScanArgs& A, const BinSpec& B, int
   if (q > v[m - 1]) v[m++] = q;
   if (e - 1 > v[m - 1]) v[m++] = e - 1;
   return m;
+}
+__device__ __forceinline__ int bin_emit(const ScanArgs& A, const BinSpec& B, int64_t g, int64_t v[4]) {
+  return bin_emit_r(A, B, g, bin_res(A, g), v);
 }
 
 // One CTA compacts bins [ga, gb) into out[...]; returns the count.  Each
@@ -379,10 +385,18 @@ __device__ int64_t cta_compact(const ScanArgs& A, const BinSpec& B, int64_t ga, 
   for (int64_t base = ga; base < gb; base += (int64_t)PB * blockDim.x) {
     int64_t v[PB][4];
     int c[PB], tot = 0;
+    // all PB result loads issued before any is used (one L2 round trip per
+    // pass, not one per bin); out-of-range bins load bin ga and are dropped
+    longlong2 rr[PB];
 #pragma unroll
     for (int r = 0; r < PB; r++) {
       const int64_t g = base + (int64_t)PB * tid + r;
-      c[r] = g < gb ? bin_emit(A, B, g, v[r]) : 0;
+      rr[r] = bin_res(A, g < gb ? g : ga);
+    }
+#pragma unroll
+    for (int r = 0; r < PB; r++) {
+      const int64_t g = base + (int64_t)PB * tid + r;
+      c[r] = g < gb ? bin_emit_r(A, B, g, rr[r], v[r]) : 0;
       tot += c[r];
     }
     int incl = tot;
