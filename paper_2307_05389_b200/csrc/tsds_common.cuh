@@ -44,7 +44,7 @@ struct PipeFlags {
   unsigned scan_blocks_done;
   int pad0;
   unsigned long long work_ctr;  // dynamic work units handed out by the scan
-  unsigned long long pad1[3];
+  unsigned long long pad1[4];  // TSDS_SCAN_TIMING stamps
 };
 
 __device__ __forceinline__ void pdl_launch_dependents() {

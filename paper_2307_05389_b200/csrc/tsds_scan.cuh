@@ -371,6 +371,13 @@ __device__ __forceinline__ int bin_emit(const ScanArgs& A, const BinSpec& B, int
   return bin_emit_r(A, B, g, bin_res(A, g), v);
 }
 
+// global nanosecond timer (TSDS_SCAN_TIMING stamps)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // One CTA compacts bins [ga, gb) into out[...]; returns the count.  Each
 // thread takes 4 consecutive bins per pass (their loads issued together),
 // so a pass covers 4 * blockDim bins with one block-wide exclusive scan.
@@ -393,6 +400,13 @@ __device__ int64_t cta_compact(const ScanArgs& A, const BinSpec& B, int64_t ga, 
       const int64_t g = base + (int64_t)PB * tid + r;
       rr[r] = bin_res(A, g < gb ? g : ga);
     }
+#ifdef TSDS_SCAN_TIMING
+    if (tid == 0 && base == ga && A.flags) {
+      volatile long long sink = rr[0].x;
+      (void)sink;
+      A.flags->pad1[3] = gtimer();
+    }
+#endif
 #pragma unroll
     for (int r = 0; r < PB; r++) {
       const int64_t g = base + (int64_t)PB * tid + r;
@@ -488,11 +502,6 @@ __device__ __forceinline__ void process_chunk(const ScanArgs& A, const BinSpec& 
 
 // Last CTA of a launch: compaction epilogue, counter and flag reset.
 // Every CTA of the grid must call it exactly once.
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 __device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted) {
   PipeFlags* F = A.flags;
   __shared__ int is_last;
@@ -545,8 +554,9 @@ __device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted)
 #ifdef TSDS_SCAN_TIMING
   if (threadIdx.x == 0) {
     const unsigned long long t3 = gtimer();
-    printf("scan timing: main %.1f us, last-CTA wait %.1f us, epilogue %.1f us, grid %d\n",
-           (F->pad1[1] - F->pad1[0]) * 1e-3, (F->pad1[2] - F->pad1[1]) * 1e-3, (t3 - F->pad1[2]) * 1e-3, gridDim.x);
+    printf("scan timing: main %.1f us, last-CTA wait %.1f us, epilogue %.1f us (first load %.1f us), grid %d\n",
+           (F->pad1[1] - F->pad1[0]) * 1e-3, (F->pad1[2] - F->pad1[1]) * 1e-3, (t3 - F->pad1[2]) * 1e-3,
+           (F->pad1[3] - F->pad1[2]) * 1e-3, gridDim.x);
     F->pad1[0] = ~0ull;
     F->pad1[1] = 0;
   }
