@@ -56,14 +56,12 @@ typedef struct tsds_ctx tsds_ctx;
 
 int tsds_version(void);
 const char *tsds_last_error(void);
-/* process-wide tuning knobs (no effect on results): "tma_min_bytes" (inputs
- * at least this large use the TMA bulk-copy scan; default: off (the LDG scan measured faster), env
- * TSDS_TMA_MIN_BYTES), "dyn_percent" (share of the LDG scan handed out
- * dynamically; default 0, env TSDS_DYN_PERCENT), "cta_bins_max_bytes"
- * (inputs up to this size with >= #SM bins use the CTA-per-bin scan;
- * default 128 MiB, env TSDS_CTA_BINS_MAX_BYTES), "lane_bins" (batched MinMax
- * with short bins: thread-per-bin kernel; 0 off, 1 auto, 2 whenever
- * eligible; env TSDS_LANE_BINS), "lttb_exact" (centroid
+/* process-wide tuning knobs (no effect on results): "dyn_percent" (share of
+ * the scan handed out dynamically; default 0, env TSDS_DYN_PERCENT),
+ * "cta_bins_max_bytes" (inputs up to this size with >= #SM bins use the
+ * CTA-per-bin scan; default 128 MiB, env TSDS_CTA_BINS_MAX_BYTES),
+ * "lane_bins" (batched MinMax with short bins: thread-per-bin kernel; 0 off,
+ * 1 auto, 2 whenever eligible; env TSDS_LANE_BINS), "lttb_exact" (centroid
  * summation of large-bucket LTTB: 0 auto = the reference's sequential order
  * for buckets <= 1024 points, a fixed tree above; 1 always sequential;
  * 2 always tree; env TSDS_LTTB_EXACT) */

@@ -22,7 +22,6 @@
 #include "tsds_lttb_large.cuh"
 #include "tsds_scan.cuh"
 #include "tsds_lanebins.cuh"
-#include "tsds_tma.cuh"
 
 using namespace tsds;
 
@@ -46,8 +45,9 @@ struct DevBuf {
 
 struct Misc {
   PipeFlags F;         // binning/scan flags (zero between pipelines)
-  int status_copy;     // status exported by the resetting scan
-  int pad[15];
+  int status_copy;     // status exported by the resetting scan (valid when ctx->status_live)
+  int mis_api_copy;    // its api-level "x is not uniform" verdict (MinMaxLTTB stage 2)
+  int pad[14];
   int64_t count;
   int64_t m2;
   int64_t pair[2];
@@ -61,7 +61,7 @@ struct tsds_ctx {
   bool own_stream = true;
   int sms = 148;
   std::mutex mu;
-  DevBuf y, x, xf64, part, bincnt, res, off, out, misc, cent, scratch, y2, x2, x2f64, full, out2, rctr, lscr;
+  DevBuf y, x, xf64, part, bincnt, res, off, out, misc, cent, scratch, y2, x2, x2f64, full, out2, lscr;
   int64_t lttb_rounds = 0;  // verification rounds of the last large-bucket LTTB
   int64_t lttb_dirty1 = 0;  // buckets whose guess was wrong in the first round
   int64_t lttb_pieces = 0;  // pieces evaluated exactly (all rounds, after pruning)
@@ -73,6 +73,7 @@ struct tsds_ctx {
   size_t h_cap = 0;
   bool dirty = false;
   bool flags_clean = false;  // Misc flags known to be zero on the device
+  bool status_live = false;  // a scan of the current call exports Misc.status_copy
   int64_t launches = 0;
   // profiling: CUDA events around every scan-kernel launch (bench roofline)
   bool profile = false;
@@ -138,11 +139,26 @@ int ensure_host(tsds_ctx* ctx, size_t bytes) {
   return TSDS_OK;
 }
 
+// Makes ctx's device current for one C-ABI call and restores the caller's
+// current device on return (torch and other libraries keep per-thread
+// device state that a call must not change).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 Misc* misc(tsds_ctx* ctx) { return (Misc*)ctx->misc.p; }
 
 int begin_call(tsds_ctx* ctx) {
-  CUDA_TRY(cudaSetDevice(ctx->device));
   RC_TRY(ensure(ctx, ctx->misc, sizeof(Misc), true));
+  ctx->status_live = false;
   if (ctx->dirty) {
     // a failed call may have left arrival counters set: re-zero them
     if (ctx->bincnt.p) CUDA_TRY(cudaMemsetAsync(ctx->bincnt.p, 0, ctx->bincnt.cap, ctx->stream));
@@ -159,7 +175,7 @@ int begin_call(tsds_ctx* ctx) {
 int dtype_ok(int dt) { return dt >= 0 && dt < DT_COUNT; }
 
 // tuning knobs: environment defaults, overridable with tsds_set_option
-int64_t g_dyn_percent = -1, g_tma_min_bytes = -1, g_cta_bins_max = -1, g_lane_bins = -1;
+int64_t g_dyn_percent = -1, g_cta_bins_max = -1, g_lane_bins = -1;
 
 // thread-per-bin batched kernel: 0 off, 1 auto (default), 2 whenever eligible
 int64_t lane_bins_mode() {
@@ -199,101 +215,12 @@ void prepare_bins(BinSpec& b, int64_t max_index) {
   }
 }
 
-// ------------------------------------------------------------ TMA scan launch
-int64_t tma_min_bytes() {
-  if (g_tma_min_bytes < 0) {
-    const char* e = getenv("TSDS_TMA_MIN_BYTES");
-    g_tma_min_bytes = e ? atoll(e) : INT64_MAX;  // opt-in: the LDG scan measured faster
-  }
-  return g_tma_min_bytes;
-}
-
-template <int DT, bool PROP>
-int launch_scan_tma_t(tsds_ctx* ctx, ScanArgs& A) {
-  using O = Ops<DT>;
-  constexpr int VEC = O::VEC;
-  constexpr int ES = 16 / VEC;
-  constexpr int64_t TE = TMA_TILE_BYTES / ES;
-  auto kern = tma_scan_kernel<DT, PROP>;
-  auto mkern = merge_kernel<DT, PROP>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM));
-    attr_set = true;
-  }
-  prepare_bins(A.bins, A.E1 + (int64_t)(A.g1 - A.g0) * 4 + 64);
-  A.shift = (int64_t)(((uintptr_t)A.y % 16) / ES);
-  const int64_t align = 32 * VEC;
-  A.vstart = ((A.E0 + A.shift) / align) * align;
-  const int64_t vend = std::max(A.E1 + A.shift, A.vstart + 1);
-  const int64_t ntiles = (vend - A.vstart + TE - 1) / TE;
-  A.che = TE;
-  A.n_static = ntiles;
-  A.dse = TE;
-  A.n_dyn = 0;
-  const int64_t G = std::max<int64_t>(1, std::min<int64_t>(ctx->sms, ntiles));
-  A.n_ranges = G;
-  A.range_len = (ntiles + G - 1) / G;
-  const int64_t cv_lo = (A.E0 + A.shift + VEC - 1) / VEC;
-  const int64_t cv_hi = (A.E1 + A.shift) / VEC;
-  const int64_t nbins = A.g1 - A.g0;
-  RC_TRY(ensure(ctx, ctx->part, (size_t)ntiles * 2 * sizeof(MinMaxCand)));
-  RC_TRY(ensure(ctx, ctx->bincnt, (size_t)nbins * sizeof(unsigned), true));
-  RC_TRY(ensure(ctx, ctx->res, (size_t)nbins * 2 * sizeof(int64_t)));
-  RC_TRY(ensure(ctx, ctx->rctr, (size_t)G * 8, true));
-  A.part = (MinMaxCand*)ctx->part.p;
-  A.bin_cnt = (unsigned*)ctx->bincnt.p;
-  A.res = (int64_t*)ctx->res.p;
-  A.flags = &misc(ctx)->F;
-  A.range_ctr = (unsigned long long*)ctx->rctr.p;
-  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-  if (ctx->profile) {
-    if (ctx->ev_free.empty()) {
-      CUDA_TRY(cudaEventCreate(&ev.first));
-      CUDA_TRY(cudaEventCreate(&ev.second));
-    } else {
-      ev = ctx->ev_free.back();
-      ctx->ev_free.pop_back();
-    }
-    CUDA_TRY(cudaEventRecord(ev.first, ctx->stream));
-  }
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = ctx->profile ? 0 : 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)G);
-  cfg.blockDim = dim3(TMA_THREADS);
-  cfg.dynamicSmemBytes = TMA_SMEM;
-  cfg.stream = ctx->stream;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A, cv_lo, cv_hi));
-  LAUNCH_CHECK();
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cudaLaunchConfig_t mcfg = {};
-  const int64_t mgrid = std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 4, (nbins + SCAN_WARPS - 1) / SCAN_WARPS));
-  mcfg.gridDim = dim3((unsigned)mgrid);
-  mcfg.blockDim = dim3(SCAN_WARPS * 32);
-  mcfg.stream = ctx->stream;
-  mcfg.attrs = attr;
-  mcfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&mcfg, mkern, A));
-  LAUNCH_CHECK();
-  if (ctx->profile) {
-    CUDA_TRY(cudaEventRecord(ev.second, ctx->stream));
-    ctx->ev_used.push_back(ev);
-  }
-  return TSDS_OK;
-}
-
 // ---------------------------------------------------------------- scan launch
 template <int DT, bool PROP>
 int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
   using O = Ops<DT>;
   constexpr int VEC = O::VEC;
   constexpr int ES = 16 / VEC;
-  if (!A.independent && (A.E1 - A.E0) * ES >= tma_min_bytes() && (uintptr_t)A.y % ES == 0)
-    return launch_scan_tma_t<DT, PROP>(ctx, A);
   auto kern = scan_kernel<DT, PROP, TSDS_UNROLL>;
   static int occ = 0;
   if (occ == 0) {
@@ -545,7 +472,7 @@ int fetch_result(tsds_ctx* ctx, const int64_t* dev, int64_t cap, int64_t* out, i
   CUDA_TRY(cudaMemcpyAsync(hs, &misc(ctx)->F.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaMemcpyAsync(hs + 1, &misc(ctx)->status_copy, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  if (hs[0] == 0) hs[0] = hs[1];
+  if (hs[0] == 0 && ctx->status_live) hs[0] = hs[1];
   if (hs[0] != 0) ctx->flags_clean = false;
   RC_TRY(finish_status(ctx, hs));
   int64_t m = h[0];
@@ -586,6 +513,7 @@ int run_minmax_m4(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y
       A.check_flags = 1;
       A.reset_flags = 1;
       A.status_out = &misc(ctx)->status_copy;
+      ctx->status_live = true;
     }
   }
   A.y = dy;
@@ -953,17 +881,24 @@ int run_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt
   if (A.check_flags) {
     A.reset_flags = 1;
     A.status_out = &misc(ctx)->status_copy;
+    ctx->status_live = true;
   }
   RC_TRY(launch_scan(ctx, ydt, nan_mode, A));
   // stage boundary: the candidate count decides stage 2
   RC_TRY(ensure_host(ctx, (size_t)(fcap + 2) * 8 + 64));
   int64_t* h = (int64_t*)ctx->h_pin;
   int* hs = (int*)(h + fcap + 1);
+  hs[0] = 0;
+  hs[1] = 1;
   CUDA_TRY(cudaMemcpyAsync(h, dfull, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(cudaMemcpyAsync(hs, &misc(ctx)->status_copy, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  if (ctx->status_live)
+    CUDA_TRY(cudaMemcpyAsync(hs, &misc(ctx)->status_copy, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   if (*hs) ctx->flags_clean = false;
   RC_TRY(finish_status(ctx, hs));
+  // device x that the stage-1 binning found uniform is dropped for stage 2
+  // too (api.py:19-28: the reference normalises x away before minmaxlttb)
+  if (xk && mem == TSDS_MEM_DEVICE && ctx->status_live && hs[1] == 0) xk = nullptr;
   const int64_t m = h[0];
   if (m <= n_out) return fetch_result(ctx, dfull, m, out, out_len);
   const int64_t* full = dfull + 1;
@@ -1033,8 +968,7 @@ int tsds_version(void) { return 100; }
 int tsds_set_option(const char* name, int64_t value) {
   if (!name) return set_err(TSDS_ERR_ARG, "option name is NULL");
   std::string n(name);
-  if (n == "tma_min_bytes") g_tma_min_bytes = std::max<int64_t>(0, value);
-  else if (n == "dyn_percent") g_dyn_percent = std::max<int64_t>(0, std::min<int64_t>(90, value));
+  if (n == "dyn_percent") g_dyn_percent = std::max<int64_t>(0, std::min<int64_t>(90, value));
   else if (n == "lane_bins") g_lane_bins = std::max<int64_t>(0, std::min<int64_t>(2, value));
   else if (n == "cta_bins_max_bytes") g_cta_bins_max = std::max<int64_t>(0, value);
   else if (n == "lttb_exact") g_lttb_exact = std::max<int64_t>(0, std::min<int64_t>(2, value));
@@ -1057,9 +991,12 @@ int tsds_ctx_create(int device, tsds_ctx** out) {
   *out = nullptr;
   tsds_ctx* ctx = new tsds_ctx();
   ctx->device = device;
-  cudaError_t e = cudaSetDevice(device);
+  int prev = -1;
+  cudaError_t e = cudaGetDevice(&prev);
+  if (e == cudaSuccess) e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+  if (prev >= 0 && prev != device) cudaSetDevice(prev);
   if (e != cudaSuccess) {
     delete ctx;
     return set_err(TSDS_ERR_CUDA, std::string("tsds_ctx_create: ") + cudaGetErrorString(e));
@@ -1070,11 +1007,11 @@ int tsds_ctx_create(int device, tsds_ctx** out) {
 
 void tsds_ctx_destroy(tsds_ctx* ctx) {
   if (!ctx) return;
-  cudaSetDevice(ctx->device);
+  DeviceGuard dg_(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->y, &ctx->x, &ctx->xf64, &ctx->part, &ctx->bincnt, &ctx->res, &ctx->off, &ctx->out,
                     &ctx->misc, &ctx->cent, &ctx->scratch, &ctx->y2, &ctx->x2, &ctx->x2f64, &ctx->full, &ctx->out2,
-                    &ctx->rctr, &ctx->lscr})
+                    &ctx->lscr})
     if (b->p) cudaFree(b->p);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
   if (ctx->h_lstat) cudaFreeHost(ctx->h_lstat);
@@ -1084,12 +1021,12 @@ void tsds_ctx_destroy(tsds_ctx* ctx) {
 
 int tsds_ctx_set_stream(tsds_ctx* ctx, void* s) {
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (s) {
     ctx->stream = (cudaStream_t)s;
     ctx->own_stream = false;
   } else {
-    cudaSetDevice(ctx->device);
     cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
     ctx->own_stream = true;
   }
@@ -1099,6 +1036,7 @@ int tsds_ctx_set_stream(tsds_ctx* ctx, void* s) {
 void* tsds_ctx_stream(tsds_ctx* ctx) { return (void*)ctx->stream; }
 
 int tsds_ctx_synchronize(tsds_ctx* ctx) {
+  DeviceGuard dg_(ctx->device);
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return TSDS_OK;
 }
@@ -1113,7 +1051,7 @@ int64_t tsds_ctx_stat(tsds_ctx* ctx, const char* name) {
                   n == "lttb_longest_chain";
   if (ctx->lstat_pending && lt) {
     std::lock_guard<std::mutex> lk(ctx->mu);
-    cudaSetDevice(ctx->device);
+    DeviceGuard dg_(ctx->device);
     if (cudaStreamSynchronize(ctx->stream) == cudaSuccess) {
       ctx->lttb_rounds = ctx->h_lstat[3];   // correction-chain steps
       ctx->lttb_dirty1 = ctx->h_lstat[2];   // |D|: buckets whose predecessor changed in round 1
@@ -1139,12 +1077,14 @@ int64_t tsds_ctx_stat(tsds_ctx* ctx, const char* name) {
 
 int tsds_ctx_profile(tsds_ctx* ctx, int enable) {
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   ctx->profile = enable != 0;
   return TSDS_OK;
 }
 
 int tsds_ctx_profile_read(tsds_ctx* ctx, double* total_ms, int64_t* count) {
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   double t = 0.0;
   for (auto& ev : ctx->ev_used) {
@@ -1164,6 +1104,7 @@ int tsds_downsample(tsds_ctx* ctx, int algo, const void* x, int xdt, const void*
   if (!ctx || !y || !out || !out_len || n < 1 || !dtype_ok(ydt) || (x && !xdtype_ok(xdt)))
     return set_err(TSDS_ERR_ARG, "tsds_downsample: invalid argument");
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   RC_TRY(begin_call(ctx));
   switch (algo) {
     case TSDS_MINMAX:
@@ -1201,6 +1142,7 @@ int tsds_downsample_async(tsds_ctx* ctx, int algo, const void* x, int xdt, const
   const int width = algo == TSDS_MINMAX ? 2 : 4;
   if (n_out < width || n_out % width) return set_err(TSDS_ERR_ARG, "invalid n_out");
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   RC_TRY(begin_call(ctx));
   if (n <= n_out) {
     iota_kernel<<<(unsigned)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, ctx->stream>>>(out_dev, n, count_dev);
@@ -1208,8 +1150,12 @@ int tsds_downsample_async(tsds_ctx* ctx, int algo, const void* x, int xdt, const
   } else {
     RC_TRY(run_minmax_m4(ctx, algo, x, xdt, y, ydt, n, n_out, nan_mode, TSDS_MEM_DEVICE, out_dev, count_dev));
   }
-  if (status_dev)
-    CUDA_TRY(cudaMemcpyAsync(status_dev, &misc(ctx)->status_copy, sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (status_dev) {
+    if (ctx->status_live)
+      CUDA_TRY(cudaMemcpyAsync(status_dev, &misc(ctx)->status_copy, sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
+    else
+      CUDA_TRY(cudaMemsetAsync(status_dev, 0, sizeof(int), ctx->stream));
+  }
   return TSDS_OK;
 }
 
@@ -1218,6 +1164,7 @@ int tsds_lttb_stage2(tsds_ctx* ctx, const void* x2, int xdt, const void* y2, int
   if (!ctx || !y2 || !full || !out || !out_len || m < 2 || n_out < 3 || !dtype_ok(ydt) || (x2 && !xdtype_ok(xdt)))
     return set_err(TSDS_ERR_ARG, "tsds_lttb_stage2: invalid argument");
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   if (m <= n_out) {
     memcpy(out, full, (size_t)m * 8);
     *out_len = m;
@@ -1256,19 +1203,26 @@ int tsds_downsample_bins_async(tsds_ctx* ctx, int algo, const void* y, int ydt, 
       (algo != TSDS_MINMAX && algo != TSDS_M4))
     return set_err(TSDS_ERR_ARG, "tsds_downsample_bins_async: invalid argument");
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   RC_TRY(begin_call(ctx));
-  // the shard's span: offsets are relative to y; read the two ends
-  int64_t ends[2];
-  CUDA_TRY(cudaMemcpyAsync(&ends[0], off, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(cudaMemcpyAsync(&ends[1], off + nb, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  // the shard's offsets (relative to y_dev) come back to the host once: the
+  // span, and whether they are monotone (x that violates its documented
+  // order gives overlapping bins, reduced independently like op_bins)
+  std::vector<int64_t> h(nb + 1);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), off, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  ScanArgs A = scan_args(y, BinSpec{1, off, 0, 0, 0}, 0, nb, ends[0], ends[1]);
-  A.independent = ends[1] < ends[0];
+  const bool mono = host_monotone(h);
+  int64_t lo = h.front(), hi = h.back();
+  for (int64_t v : h) {
+    lo = std::min(lo, v);
+    hi = std::max(hi, v);
+  }
+  ScanArgs A = scan_args(y, BinSpec{1, off, 0, 0, 0}, 0, nb, mono ? h.front() : lo, mono ? h.back() : hi);
+  A.independent = !mono;
   A.epi = algo == TSDS_MINMAX ? EPI_MINMAX : EPI_M4;
   A.out = out_dev;
   A.out_count = count_dev;
   A.idx_sub = -idx_base;
-  if (ends[1] < ends[0]) return set_err(TSDS_ERR_ARG, "non-monotone shard offsets");
   return launch_scan(ctx, ydt, nan_mode, A);
 }
 
@@ -1302,6 +1256,7 @@ int tsds_minmax_batched_async(tsds_ctx* ctx, const void* y, int ydt, int64_t S, 
   if (!ctx || !y || S < 1 || L < 1 || !dtype_ok(ydt) || n_out < 2 || n_out % 2)
     return set_err(TSDS_ERR_ARG, "tsds_minmax_batched_async: invalid argument");
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   RC_TRY(begin_call(ctx));
   if (L <= n_out) {
     iota_rows_kernel<<<(unsigned)std::min<int64_t>(4096, (S * L + 255) / 256), 256, 0, ctx->stream>>>(out_dev, S, L,
@@ -1317,6 +1272,7 @@ int tsds_minmax_batched(tsds_ctx* ctx, const void* y, int ydt, int64_t S, int64_
   if (!ctx || !y || !out || !counts || S < 1 || L < 1 || !dtype_ok(ydt) || n_out < 2 || n_out % 2)
     return set_err(TSDS_ERR_ARG, "tsds_minmax_batched: invalid argument");
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   RC_TRY(begin_call(ctx));
   if (L <= n_out) {
     for (int64_t s = 0; s < S; s++) {
@@ -1340,6 +1296,7 @@ int tsds_minmax_batched(tsds_ctx* ctx, const void* y, int ydt, int64_t S, int64_
 int tsds_argminmax(tsds_ctx* ctx, const void* y, int ydt, int64_t n, int nan_mode, int mem, int64_t* out2) {
   if (!ctx || !y || !out2 || n < 1 || !dtype_ok(ydt)) return set_err(TSDS_ERR_ARG, "tsds_argminmax: invalid argument");
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   RC_TRY(begin_call(ctx));
   const void* dy;
   RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
@@ -1359,6 +1316,7 @@ int tsds_argminmax(tsds_ctx* ctx, const void* y, int ydt, int64_t n, int nan_mod
 int tsds_op_is_uniform_spaced(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int32_t* flag_dev) {
   if (!ctx || !x || !flag_dev || !xdtype_ok(xdt)) return set_err(TSDS_ERR_ARG, "invalid argument");
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   RC_TRY(begin_call(ctx));
   RC_TRY(ensure(ctx, ctx->off, 16));
   RC_TRY(launch_binning(ctx, xdt, x, n, 1, 0, nullptr, 0, 0, 0, (int64_t*)ctx->off.p));
@@ -1374,13 +1332,14 @@ int tsds_op_is_uniform_spaced(tsds_ctx* ctx, const void* x, int xdt, int64_t n, 
 int tsds_op_equal_count_offsets(tsds_ctx* ctx, int64_t len, int64_t nb, int64_t* off_dev) {
   if (!ctx || !off_dev || nb < 1 || len < 0) return set_err(TSDS_ERR_ARG, "invalid bin count");
   std::lock_guard<std::mutex> lk(ctx->mu);
-  CUDA_TRY(cudaSetDevice(ctx->device));
+  DeviceGuard dg_(ctx->device);
   return launch_count_offsets(ctx, len, nb, 0, off_dev);
 }
 
 int tsds_op_equal_width_offsets(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int64_t nb, int64_t* off_dev) {
   if (!ctx || !off_dev || nb < 1 || !xdtype_ok(xdt) || (n > 0 && !x)) return set_err(TSDS_ERR_ARG, "invalid argument");
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   RC_TRY(begin_call(ctx));
   RC_TRY(launch_binning(ctx, xdt, x, n, nb, 0, nullptr, 0, 0, 1, off_dev));
   int hs = 0;
@@ -1394,6 +1353,7 @@ static int op_bins(tsds_ctx* ctx, int epi, const void* y, int ydt, const int64_t
   if (!ctx || !y || !off || !idx || !cnt || b1 < b0 || !dtype_ok(ydt)) return set_err(TSDS_ERR_ARG, "invalid argument");
   if (b1 == b0) return TSDS_OK;
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   RC_TRY(begin_call(ctx));
   // offsets may be non-monotone for arbitrary callers: E0/E1 from the host
   std::vector<int64_t> h(b1 - b0 + 1);
@@ -1422,6 +1382,7 @@ int tsds_op_lttb(tsds_ctx* ctx, const double* xf, const void* y, int ydt, int64_
   if (!ctx || !y || !off || !out_dev || !m_host || n < 2 || nb < 1 || !dtype_ok(ydt))
     return set_err(TSDS_ERR_ARG, "invalid argument");
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
   RC_TRY(begin_call(ctx));
   RC_TRY(ensure(ctx, ctx->out2, (size_t)(nb + 3) * 8));
   int64_t* d = (int64_t*)ctx->out2.p;

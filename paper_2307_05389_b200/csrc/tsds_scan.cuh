@@ -115,7 +115,7 @@ struct ScanArgs {
   int use_dyn_mode;    // take the bin mode from flags->mode (set by binning_kernel)
   int check_flags;     // honour flags->status (abort) and flags->nonmono
   int reset_flags;     // clear the binning flags at the end (pipeline consumer)
-  int* status_out;     // nullable: receives flags->status before the reset
+  int* status_out;     // nullable: int[2] receives {flags->status, flags->mis_api} before the reset
   int independent;     // host-known non-monotone offsets
   int cta_bins;        // small inputs: CTA per bin (its warps split the bin), no cross-CTA merges
   // epilogue
@@ -125,10 +125,6 @@ struct ScanArgs {
   int64_t idx_sub;     // subtracted from every output index
   int lttb_frame;      // 1: out[0]=0 and out[total+1]=n_frame-1 (MinMaxLTTB `full`)
   int64_t n_frame;
-  // TMA path (tsds_tma.cuh): per-CTA tile ranges claimed through counters
-  unsigned long long* range_ctr;  // [n_ranges], zero between launches
-  int64_t n_ranges;
-  int64_t range_len;   // tiles per home range
 };
 
 __device__ __forceinline__ int64_t chunk_of(const ScanArgs& A, int64_t i) {
@@ -155,7 +151,7 @@ __device__ __forceinline__ void chunk_range(const ScanArgs& A, int64_t w, int64_
 // ------------------------------------------------------------------------
 // one bin segment [a, c) reduced by a warp
 
-// vector sources: global memory (streaming loads) or a shared-memory tile
+// vector source: global memory (streaming loads)
 template <bool L1ALLOC>
 struct GlobalSrc {
   static constexpr bool SMEM = false;
@@ -164,22 +160,6 @@ struct GlobalSrc {
   __device__ __forceinline__ uint4 stream(const uint4* p, int j) const { return ldg_stream<L1ALLOC>(p + j); }
   __device__ __forceinline__ uint4 again(const uint4* p, int j) const { return __ldg(p + j); }
 };
-struct SmemSrc {
-  static constexpr bool SMEM = true;
-  uint32_t sv;  // shared-memory address of the tile copy; it starts at virtual vector v0
-  int64_t v0;
-  __device__ __forceinline__ const uint4* base(int64_t jb) const {
-    return reinterpret_cast<const uint4*>((uintptr_t)(sv + (uint32_t)(jb - v0) * 16u));
-  }
-  __device__ __forceinline__ uint4 stream(const uint4* p, int j) const {
-    uint4 r;
-    uint32_t a = (uint32_t)(uintptr_t)p + (uint32_t)j * 16u;
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
-    return r;
-  }
-  __device__ __forceinline__ uint4 again(const uint4* p, int j) const { return stream(p, j); }
-};
-
 // One warp reduces elements [a, c) of the series: full 16-byte vectors
 // through `src`, the (< VEC) unaligned head/tail elements with scalar loads.
 // Vector indices inside the loop are 32-bit offsets from the first full
@@ -562,7 +542,10 @@ __device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted)
   }
 #endif
   if (threadIdx.x == 0) {
-    if (A.status_out) *A.status_out = *(volatile int*)&F->status;
+    if (A.status_out) {  // {status, api-level "x not uniform"} before the reset
+      A.status_out[0] = *(volatile int*)&F->status;
+      A.status_out[1] = *(volatile int*)&F->mis_api;
+    }
     if (A.reset_flags) {
       F->mis_api = 0;
       F->mis_slice = 0;
@@ -573,8 +556,6 @@ __device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted)
     F->work_ctr = 0ull;
     F->scan_blocks_done = 0u;
   }
-  if (threadIdx.x == 0 && A.range_ctr)
-    for (int64_t c = 0; c < A.n_ranges; c++) A.range_ctr[c] = 0ull;
 }
 
 template <int DT, bool PROP, int U>
