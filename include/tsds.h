@@ -152,12 +152,26 @@ int tsds_op_equal_count_offsets(tsds_ctx *ctx, int64_t len, int64_t n_bins, int6
 int tsds_op_equal_width_offsets(tsds_ctx *ctx, const void *x, int x_dtype, int64_t n, int64_t n_bins,
                                 int64_t *off_dev);
 
+/* fill_width_offsets (_kernels.py:521-535): off_dev[k] = first i with
+ * float64(x[i]) >= x0 + (k*span)/n_bins, for k in [k0, k1) (the reference
+ * operator with caller-supplied x0/span, used by boundaries_parallel and
+ * by sharded binning with the global edge formula).  Asynchronous. */
+int tsds_op_fill_width_offsets(tsds_ctx *ctx, const void *x, int x_dtype, int64_t n, double x0, double span,
+                               int64_t n_bins, int64_t k0, int64_t k1, int64_t *off_dev);
+
 /* minmax_bins / m4_bins (_kernels.py:308-354): bins [b0, b1) of off_dev,
- * writing idx_dev[width*(b-b0) + t] and cnt_dev[b-b0] (width 2 / 4). */
+ * writing idx_dev[width*b + t] and cnt_dev[b] (width 2 / 4; absolute bin
+ * numbers, other slots untouched -- the reference layout). */
 int tsds_op_minmax_bins(tsds_ctx *ctx, const void *y, int y_dtype, const int64_t *off_dev, int64_t b0,
                         int64_t b1, int nan_mode, int64_t *idx_dev, int64_t *cnt_dev);
 int tsds_op_m4_bins(tsds_ctx *ctx, const void *y, int y_dtype, const int64_t *off_dev, int64_t b0, int64_t b1,
                     int nan_mode, int64_t *idx_dev, int64_t *cnt_dev);
+
+/* compact_bins (_kernels.py:359-369): out_dev = concatenation of
+ * idx_dev[width*b .. width*b+cnt_dev[b]) over b in [0, n_bins);
+ * *total_dev (int64) receives the count.  Asynchronous. */
+int tsds_op_compact_bins(tsds_ctx *ctx, const int64_t *idx_dev, const int64_t *cnt_dev, int width, int64_t n_bins,
+                         int64_t *out_dev, int64_t *total_dev);
 
 /* lttb_implicit / lttb_explicit (_kernels.py:375-480): x_f64 NULL for the
  * implicit kernel; off_dev int64[n_bins+1]; out_dev int64[n_bins+2];

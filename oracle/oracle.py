@@ -56,6 +56,10 @@ def lib():
         L.or_minmax_batched.argtypes = [vp, i32, i64, i64, i64, i32, i32, vp, vp]
         L.or_lttb_walk.argtypes = [vp, i32, vp, i32, i64, vp, i64, vp]
         L.or_lttb_walk.restype = i64
+        L.or_fill_width_offsets.argtypes = [vp, i32, i64, ctypes.c_double, ctypes.c_double, i64, i64, i64, vp]
+        L.or_bins_slots.argtypes = [vp, i32, vp, i64, i64, i32, i32, vp, vp]
+        L.or_compact_bins.argtypes = [vp, vp, i32, i64, vp]
+        L.or_compact_bins.restype = i64
         _lib = L
     return _lib
 
@@ -166,3 +170,31 @@ def stage2(x, y, full, n_out):
         off2 = equal_width(x2[1:-1], nb).astype(np.int64) + 1
         sel = lttb_walk(x2, y2, off2)
     return full[sel].astype(np.uint64)
+
+
+# --------------------------------------------------------------------------
+# operator level (the reference numba kernels' own signatures)
+
+
+def fill_width_offsets(x, x0, span, n_bins, k0, k1, out):
+    """_kernels.fill_width_offsets: out[k] for k in [k0, k1)."""
+    x = _x_view(x)
+    lib().or_fill_width_offsets(_ptr(x), DTYPE_CODES[x.dtype], x.shape[0], float(x0), float(span), int(n_bins),
+                                int(k0), int(k1), _ptr(out))
+
+
+def bins_slots(width, y, off, b0, b1, idx, cnt, nan=False):
+    """_kernels minmax_bins (width 2) / m4_bins (width 4) writing idx[width*b+t], cnt[b]."""
+    y = np.ascontiguousarray(y)
+    off = np.ascontiguousarray(off, dtype=np.int64)
+    lib().or_bins_slots(_ptr(y), DTYPE_CODES[y.dtype], _ptr(off), int(b0), int(b1), int(width), int(nan), _ptr(idx),
+                        _ptr(cnt))
+
+
+def compact_bins(idx, cnt, width):
+    """_kernels.compact_bins."""
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    cnt = np.ascontiguousarray(cnt, dtype=np.int64)
+    out = np.zeros(max(1, int(cnt.sum())), np.int64)
+    m = lib().or_compact_bins(_ptr(idx), _ptr(cnt), int(width), cnt.shape[0], _ptr(out))
+    return out[:m]

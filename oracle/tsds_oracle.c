@@ -348,6 +348,33 @@ int64_t or_lttb_walk(const void *x, int xdt, const void *y, int ydt, int64_t n,
 }
 
 /* ------------------------------------------------------------------------ */
+/* operator-level entry points (the numba kernels' own signatures), used to  */
+/* check the C-ABI operator layer of the product one kernel at a time.       */
+
+/* fill_width_offsets(x, x0, span, n_bins, k0, k1, out) (_kernels.py:521-535) */
+void or_fill_width_offsets(const void *x, int dt, int64_t n, double x0, double span,
+                           int64_t n_bins, int64_t k0, int64_t k1, int64_t *out) {
+    fill_width(x, dt, n, x0, span, n_bins, k0, k1, out);
+}
+
+/* minmax_bins / m4_bins(a, off, b0, b1, idx, cnt) (_kernels.py:308-354):
+ * idx[width*b + t], cnt[b] for b in [b0, b1), absolute bin numbers. */
+void or_bins_slots(const void *y, int dt, const int64_t *off, int64_t b0, int64_t b1,
+                   int width, int nan_mode, int64_t *idx, int64_t *cnt) {
+    bins_job j = {y, dt, off, b0, b1, width, nan_mode, idx, cnt};
+    bins_run(&j);
+}
+
+/* compact_bins(idx, cnt, width, total) (_kernels.py:359-369) */
+int64_t or_compact_bins(const int64_t *idx, const int64_t *cnt, int width, int64_t n_bins,
+                        int64_t *out) {
+    int64_t m = 0;
+    for (int64_t b = 0; b < n_bins; b++)
+        for (int64_t t = 0; t < cnt[b]; t++) out[m++] = idx[(int64_t)width * b + t];
+    return m;
+}
+
+/* ------------------------------------------------------------------------ */
 /* algorithms (algorithms.py) -- validation happens in the Python wrapper,   */
 /* x is already normalized (api.py:19-28).  Return value: the number of      */
 /* indices written to out, or -2 for "invalid index span".                   */

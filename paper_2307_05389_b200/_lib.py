@@ -48,6 +48,8 @@ EXPORTED = (
     "tsds_op_is_uniform_spaced",
     "tsds_op_equal_count_offsets",
     "tsds_op_equal_width_offsets",
+    "tsds_op_fill_width_offsets",
+    "tsds_op_compact_bins",
     "tsds_op_minmax_bins",
     "tsds_op_m4_bins",
     "tsds_op_lttb",
@@ -107,6 +109,9 @@ def load():
         L.tsds_op_is_uniform_spaced.argtypes = [vp, vp, i32, i64, vp]
         L.tsds_op_equal_count_offsets.argtypes = [vp, i64, i64, vp]
         L.tsds_op_equal_width_offsets.argtypes = [vp, vp, i32, i64, i64, vp]
+        L.tsds_op_fill_width_offsets.argtypes = [vp, vp, i32, i64, ctypes.c_double, ctypes.c_double, i64, i64, i64,
+                                                 vp]
+        L.tsds_op_compact_bins.argtypes = [vp, vp, vp, i32, i64, vp, vp]
         L.tsds_op_minmax_bins.argtypes = [vp, vp, i32, vp, i64, i64, i32, vp, vp]
         L.tsds_op_m4_bins.argtypes = [vp, vp, i32, vp, i64, i64, i32, vp, vp]
         L.tsds_op_lttb.argtypes = [vp, vp, vp, i32, i64, vp, i64, vp, p64]

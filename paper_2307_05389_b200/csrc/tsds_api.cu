@@ -1348,6 +1348,30 @@ int tsds_op_equal_width_offsets(tsds_ctx* ctx, const void* x, int xdt, int64_t n
   return finish_status(ctx, &hs);
 }
 
+int tsds_op_fill_width_offsets(tsds_ctx* ctx, const void* x, int xdt, int64_t n, double x0, double span,
+                               int64_t nb, int64_t k0, int64_t k1, int64_t* off_dev) {
+  if (!ctx || !off_dev || nb < 1 || k0 < 0 || k1 < k0 || !xdtype_ok(xdt) || (n > 0 && !x))
+    return set_err(TSDS_ERR_ARG, "invalid argument");
+  if (k1 == k0) return TSDS_OK;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
+  const unsigned grid = cap_grid((k1 - k0 + 7) / 8, (int64_t)ctx->sms * 8);
+  XDT_SWITCH(xdt, (fill_width_kernel<XD><<<grid, 256, 0, ctx->stream>>>(x, n, x0, span, nb, k0, k1, off_dev)));
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
+int tsds_op_compact_bins(tsds_ctx* ctx, const int64_t* idx_dev, const int64_t* cnt_dev, int width, int64_t nb,
+                         int64_t* out_dev, int64_t* total_dev) {
+  if (!ctx || !idx_dev || !cnt_dev || !out_dev || !total_dev || nb < 0 || width < 1)
+    return set_err(TSDS_ERR_ARG, "invalid argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
+  compact_slots_kernel<<<1, 1024, 0, ctx->stream>>>(idx_dev, cnt_dev, width, nb, out_dev, total_dev);
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
 static int op_bins(tsds_ctx* ctx, int epi, const void* y, int ydt, const int64_t* off, int64_t b0, int64_t b1,
                    int nan_mode, int64_t* idx, int64_t* cnt) {
   if (!ctx || !y || !off || !idx || !cnt || b1 < b0 || !dtype_ok(ydt)) return set_err(TSDS_ERR_ARG, "invalid argument");

@@ -352,4 +352,20 @@ __global__ inline void count_offsets_kernel(int64_t len, int64_t nb, int64_t add
   }
 }
 
+// fill_width_offsets(x, x0, span, n_bins, k0, k1, out) (_kernels.py:521-535):
+// out[k] = first i with float64(x[i]) >= x0 + (k*span)/n_bins for k in
+// [k0, k1); warp per edge, the reference's exact binary-search probe path.
+template <int XDT>
+__global__ void fill_width_kernel(const void* x, int64_t n, double x0, double span, int64_t nb, int64_t k0,
+                                  int64_t k1, int64_t* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k = k0 + w; k < k1; k += nw) {
+    const double e = __dadd_rn(x0, __ddiv_rn(__dmul_rn((double)k, span), (double)nb));
+    const int64_t v = lower_bound_exact<XDT>(x, n, e);
+    if (lane == 0) out[k] = v;
+  }
+}
+
 }  // namespace tsds

@@ -418,15 +418,51 @@ __device__ int64_t cta_compact(const ScanArgs& A, const BinSpec& B, int64_t ga, 
   return running;
 }
 
-// slot epilogue (reference writer layout idx[w*b + t], cnt[b])
+// slot epilogue: the reference writers' layout idx[w*b + t], cnt[b] with
+// absolute bin numbers b in [g0, g1) (_kernels.py:308-354); other slots are
+// left untouched like the reference's
 __device__ void cta_slots(const ScanArgs& A, const BinSpec& B) {
   const int width = A.epi == EPI_SLOTS_MINMAX ? 2 : 4;
   for (int64_t g = A.g0 + threadIdx.x; g < A.g1; g += blockDim.x) {
     int64_t v[4];
     int c = bin_emit(A, B, g, v);
-    for (int t = 0; t < c; t++) A.out[width * (g - A.g0) + t] = v[t] - A.idx_sub;
-    A.out_count[g - A.g0] = c;
+    for (int t = 0; t < c; t++) A.out[width * g + t] = v[t] - A.idx_sub;
+    A.out_count[g] = c;
   }
+}
+
+// compact_bins (_kernels.py:359-369): concatenates idx[width*b .. +cnt[b])
+// over b in bin order; one CTA, one block-wide exclusive scan per pass of
+// blockDim bins.  *total receives the count.
+__global__ void compact_slots_kernel(const int64_t* idx, const int64_t* cnt, int width, int64_t nb, int64_t* out,
+                                     int64_t* total) {
+  __shared__ int64_t warp_tot[32];
+  __shared__ int64_t running;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) running = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nb; base += blockDim.x) {
+    const int64_t b = base + tid;
+    const int64_t c = b < nb ? cnt[b] : 0;
+    int64_t incl = c;
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, incl, m);
+      if (lane >= m) incl += t;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    int64_t pos = running + incl - c, all = 0;
+    for (int w = 0; w < nw; w++) {
+      if (w < wid) pos += warp_tot[w];
+      all += warp_tot[w];
+    }
+    for (int64_t t = 0; t < c; t++) out[pos + t] = idx[(int64_t)width * b + t];
+    __syncthreads();
+    if (tid == 0) running += all;
+    __syncthreads();
+  }
+  if (tid == 0) *total = running;
 }
 
 // one chunk [cs, ce) walked bin segment by bin segment by a warp
@@ -507,7 +543,7 @@ __device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted)
   if (aborted) {
     if (threadIdx.x == 0) {
       if (A.epi == EPI_SLOTS_MINMAX || A.epi == EPI_SLOTS_M4) {
-        for (int64_t g = A.g0; g < A.g1; g++) A.out_count[g - A.g0] = 0;
+        for (int64_t g = A.g0; g < A.g1; g++) A.out_count[g] = 0;
       } else if (A.epi != EPI_PAIR && A.out_count) {
         *A.out_count = 0;
       }

@@ -100,42 +100,6 @@ def test_bench_table_schema():
 
 
 @pytest.mark.gpu
-def test_endpoint_roundtrips(tmp_path):
-    from paper_2307_05389_b200 import downsample
-
-    y = np.random.default_rng(0).random(1000)
-    code, dst = run_endpoint(tmp_path, le(y), ["--algo", "minmax", "--dtype", "f64", "--count", "1000", "--n-out", "10"])
-    assert code == 0 and np.array_equal(read_indices(dst), downsample("minmax", y, n_out=10))
-    rng = np.random.default_rng(1)
-    x = np.cumsum(rng.integers(1, 5, 400)).astype(np.int64)
-    y = rng.random(400, dtype=np.float32)
-    code, dst = run_endpoint(tmp_path, le(x) + le(y),
-                             ["--algo", "m4", "--dtype", "f32", "--x-dtype", "i64", "--count", "400", "--n-out", "8"])
-    assert code == 0 and np.array_equal(read_indices(dst), downsample("m4", x, y, n_out=8))
-    y = np.random.default_rng(2).random(512, np.float32).astype(np.float16)
-    code, dst = run_endpoint(tmp_path, le(y), ["--algo", "lttb", "--dtype", "f16", "--count", "512", "--n-out", "20"])
-    assert code == 0 and np.array_equal(read_indices(dst), downsample("lttb", y, n_out=20))
-    y = np.random.default_rng(3).random(5000)
-    code, dst = run_endpoint(tmp_path, le(y), ["--algo", "minmaxlttb", "--dtype", "f64", "--count", "5000",
-                                               "--n-out", "40", "--ratio", "3", "--parallel", "--workers", "2"])
-    assert code == 0
-    assert np.array_equal(read_indices(dst), downsample("minmaxlttb", y, n_out=40, minmax_ratio=3, parallel=True, workers=2))
-
-
-@pytest.mark.gpu
-def test_endpoint_over_real_pipes():
-    from paper_2307_05389_b200 import downsample
-
-    y = np.random.default_rng(4).random(2000, dtype=np.float32)
-    proc = subprocess.run([sys.executable, "-m", "paper_2307_05389_b200", "downsample", "--algo", "minmaxlttb",
-                           "--dtype", "f32", "--count", "2000", "--n-out", "16"],
-                          input=le(y), capture_output=True, timeout=300)
-    assert proc.returncode == 0, proc.stderr.decode()
-    got = np.frombuffer(proc.stdout, dtype=np.dtype(np.uint64).newbyteorder("<"))
-    assert np.array_equal(got, downsample("minmaxlttb", y, n_out=16))
-
-
-@pytest.mark.gpu
 def test_bench_csv_to_file(tmp_path, capsys):
     out = tmp_path / "rows.csv"
     assert main(["bench", "--dtypes", "f32", "--sizes", "600", "--n-out", "50", "--algos", "minmax",

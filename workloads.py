@@ -122,6 +122,98 @@ def config5(tag, S=C5_S, L=C5_L, out=None):
 
 
 # --------------------------------------------------------------------------
+# process-parallel generation of the large configs (same values, bit for
+# bit, as config4 / config5 above): numpy's generators and cumsum hold the
+# GIL for much of the work, so the chunks / series are produced by forked
+# workers writing into one shared anonymous mapping.
+
+_SHARED = {}
+
+
+def _shared_array(shape, dtype):
+    import mmap
+
+    dt = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dt.itemsize
+    mm = mmap.mmap(-1, max(nbytes, 1))
+    return np.frombuffer(mm, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+
+
+def _pool(procs):
+    import multiprocessing as mp
+
+    return mp.get_context("fork").Pool(procs)
+
+
+def _c4_last(args):
+    c, m = args
+    r = np.random.default_rng([4, c])
+    return float(np.cumsum(r.exponential(1.0, m))[-1]), float(np.cumsum(r.standard_normal(m))[-1])
+
+
+def _c4_fill(args):
+    c, s, m, xc, yc = args
+    x, y = _SHARED["c4"]
+    r = np.random.default_rng([4, c])
+    x[s : s + m] = np.cumsum(r.exponential(1.0, m)) + xc
+    y[s : s + m] = (np.cumsum(r.standard_normal(m)) + yc).astype(np.float32)
+    return c
+
+
+def config4_parallel(n=C4_N, chunk=1 << 26, procs=None):
+    """config4 with its chunks generated by `procs` processes.
+
+    Pass 1 finds each chunk's local cumsum end; the carries then follow
+    sequentially exactly as in config4 (xc <- fl(last + xc)); pass 2
+    regenerates every chunk with its carry.  Identical output to config4.
+    """
+    import os
+
+    procs = procs or os.cpu_count() or 1
+    spans = [(c, s, min(chunk, n - s)) for c, s in enumerate(range(0, n, chunk))]
+    x = _shared_array((n,), np.float64)
+    y = _shared_array((n,), np.float32)
+    _SHARED["c4"] = (x, y)
+    try:
+        with _pool(min(procs, len(spans))) as pool:
+            lasts = pool.map(_c4_last, [(c, m) for c, s, m in spans])
+            jobs, xc, yc = [], 0.0, 0.0
+            for (c, s, m), (lx, ly) in zip(spans, lasts):
+                jobs.append((c, s, m, xc, yc))
+                xc = float(np.float64(lx) + np.float64(xc))
+                yc = float(np.float64(ly) + np.float64(yc))
+            pool.map(_c4_fill, jobs)
+    finally:
+        _SHARED.pop("c4", None)
+    return x, y
+
+
+def _c5_fill(args):
+    tag, s0, s1, L = args
+    Y = _SHARED["c5"]
+    for s in range(s0, s1):
+        Y[s] = config5_series(tag, s, L)
+    return s1 - s0
+
+
+def config5_parallel(tag, S=C5_S, L=C5_L, procs=None):
+    """config5 (S x L batch) with the series generated by `procs` processes."""
+    import os
+
+    procs = procs or os.cpu_count() or 1
+    dt = {"i16": np.int16, "f16": np.float16, "u8": np.uint8}[tag]
+    Y = _shared_array((S, L), dt)
+    _SHARED["c5"] = Y
+    step = max(1, -(-S // (procs * 4)))
+    try:
+        with _pool(min(procs, S)) as pool:
+            pool.map(_c5_fill, [(tag, s, min(S, s + step), L) for s in range(0, S, step)])
+    finally:
+        _SHARED.pop("c5", None)
+    return Y
+
+
+# --------------------------------------------------------------------------
 # randomised parity instances (the reference sweep recipe)
 
 
