@@ -81,6 +81,8 @@ def _torch_dtype_map():
 
 def _as_device(obj):
     """DeviceSeries for CUDA arrays, None for host objects."""
+    if isinstance(obj, DeviceSeries):
+        return obj
     mod = type(obj).__module__
     if mod.startswith("torch"):
         import torch

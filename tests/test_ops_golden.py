@@ -7,6 +7,7 @@ libtsds.so (include/tsds.h), called directly with device pointers, do too;
 so do Downsampler.transform / fit_transform and the CLI endpoint's bytes.
 """
 
+import ctypes
 import json
 import os
 import subprocess
@@ -176,13 +177,13 @@ def test_c_abi_lttb_walk(gold):
         nb = off.shape[0] - 1
         xf = None if case["x"] is None else _dev(A[case["x"]].astype(np.float64))
         out = torch.full((nb + 2,), -3, dtype=torch.int64, device="cuda")
-        m = np.zeros(1, np.int64)
+        m = ctypes.c_int64(0)
         yd, od = _dev(y), _dev(off)
         rc = L.tsds_op_lttb(ctx.handle, None if xf is None else xf.data_ptr(), yd.data_ptr(), _code(y), y.shape[0],
-                            od.data_ptr(), nb, out.data_ptr(), m.ctypes.data)
+                            od.data_ptr(), nb, out.data_ptr(), ctypes.byref(m))
         _lib.check(rc, "lttb")
         want = A[case["want"]]
-        assert int(m[0]) == want.shape[0]
+        assert m.value == want.shape[0]
         assert np.array_equal(out[: want.shape[0]].cpu().numpy(), want), (y.dtype, case["x"] is None)
 
 
