@@ -1,30 +1,46 @@
 """Benchmark: downsample input GB/s (and points/s) vs HBM roofline, vs the CPU reference.
 
-Default workload (N=1): BASELINE config 2 -- M4Downsampler with x, 1e8 points
-(int64 x, float64 y with 0.01% NaN), n_out=4000 -- the config BASELINE.json's
-metric is quoted on that fits one GPU.
+One JSON line.  Its top level is the headline workload -- BASELINE config 4,
+MinMaxLTTB with x over 1e9 points (f64 x, f32 y, n_out 5000, ratio 4), the
+largest config and the one the metric's 1/2/4/8-GPU scaling refers to --
+and ``configs`` holds one entry per BASELINE config (C1, C2, C3 at n_out
+1000 and 10000, C4, C5 for i16 / u8 / f16), each with the same keys:
 
-  value      device-resident throughput: algorithmic input bytes (n * sizeof(y),
-             SURVEY.md 8(d)) / step time, K steps timed with CUDA events on
-             the library's stream; inputs (1.6 GB) exceed the 126 MB L2.
-  e2e        the same metric through the public API (ts.downsample) with
-             pinned HOST numpy inputs: y H2D + binning + scan + D2H of the
-             indices inside every timed step (x stays on the host: only the
-             few probes of the bin-edge searches read it).
-  roofline   the scan kernel (dominant): algorithmic bytes per launch / its
-             average CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
-  cpu_baseline  the oracle port (oracle/tsds_oracle.c, all host threads) on the
-             same workload, bounded sample.
+  value         device-resident throughput: algorithmic input bytes
+                (n * sizeof(y)) / step time.  A step is one
+                whole call of the C-ABI's asynchronous entry point on
+                HBM-resident inputs (binning, scan, compaction, LTTB stages;
+                MinMaxLTTB's stage 2 included, no host round trip), timed with
+                CUDA events on the library's stream, K steps after W warm-ups.
+                Inputs smaller than L2 (C1) get an L2 flush between steps
+                (a 256 MB write followed by a 256 MB read, outside the events).
+  roofline      the step's streaming kernel (the one pass over y): algorithmic
+                bytes per launch / its mean CUDA-event duration (second pass,
+                events around that kernel only) vs MEASURED_PEAKS.json hbm_gbs;
+                traffic from the committed ncu capture (profiles/).
+  e2e           the same metric through the public API (ts.downsample /
+                ts.minmax_batched) on the host numpy arrays the generator made
+                (pageable memory, the drop-in case): H2D of y, binning, kernels
+                and the index readback inside every timed step.
+  cpu_baseline  the oracle port (oracle/tsds_oracle.c: a C restatement of the
+                reference, pinned to its outputs by tests/test_oracle_golden.py)
+                on all host threads, same workload.
 
---impl reference times that CPU port alone (kind "port": the reference is
-Python/numba and cannot travel to the GPU box; the port is pinned to it by
-tests/test_oracle_golden.py).  Under torchrun (N>1) every rank processes its
-own config-2 series (weak scaling) and the indices are gathered to rank 0
-over NCCL; only rank 0 prints.
+Every config's result is checked against the reference's outputs
+(tests/golden/configs.npz) before it is timed.
+
+--impl reference prints the same line for the CPU port alone (kind "port":
+the reference is Python/numba and cannot travel to the GPU box).  Under
+torchrun (N>1) the sharded paths run: C4's MinMax preselection split by
+sub-bin ranges over the ranks (each rank holds only its shard of y in its
+HBM) with the candidates all-gathered over NCCL and the triangle stage on
+every rank, and C5's series partitioned across ranks -- strong scaling
+(the same total work at every N), time = max over ranks.
 """
 
 import argparse
 import ctypes
+import hashlib
 import json
 import os
 import statistics
@@ -40,50 +56,135 @@ sys.path.insert(0, ROOT)
 
 import workloads as W  # noqa: E402
 
-N_OUT = 4000
+METRIC = "downsample input GB/s"
+HEADLINE = "C4"
+L2_FLUSH = 256 << 20
+ALGO_CODE = {"minmax": 1, "m4": 2, "lttb": 3, "minmaxlttb": 4}
+DT_CODE = {np.dtype(np.float16): 0, np.dtype(np.float32): 1, np.dtype(np.float64): 2, np.dtype(np.int16): 4,
+           np.dtype(np.int64): 6, np.dtype(np.uint8): 7}
+
+# BASELINE.json configs; the config dicts are shared by both arms
+SPECS = {
+    "C1": dict(workload="config1: MinMaxDownsampler, y only, 1e7 f32 random walk with running-extreme ties, "
+                        "n_out=2000", algo="minmax", n=W.C1_N, n_out=2000, dtype="f32", golden="c1_minmax"),
+    "C2": dict(workload="config2: M4Downsampler with x, 1e8 f64 points (0.01% NaN), int64 jittered timestamps, "
+                        "n_out=4000", algo="m4", n=W.C2_N, n_out=4000, dtype="f64", golden="c2_m4"),
+    "C3_1000": dict(workload="config3: LTTBDownsampler, y only, 5e7 f64 Laplace walk with spikes, n_out=1000",
+                    algo="lttb", n=W.C3_N, n_out=1000, dtype="f64", golden="c3_lttb_1000"),
+    "C3_10000": dict(workload="config3: LTTBDownsampler, y only, 5e7 f64 Laplace walk with spikes, n_out=10000",
+                     algo="lttb", n=W.C3_N, n_out=10000, dtype="f64", golden="c3_lttb_10000"),
+    "C4": dict(workload="config4: MinMaxLTTBDownsampler with x, 1e9 points, f64 cumsum(Exp(1)) x, f32 random-walk "
+                        "y, n_out=5000, minmax_ratio=4", algo="minmaxlttb", n=W.C4_N, n_out=5000, ratio=4,
+               dtype="f32", golden="c4_minmaxlttb"),
+    "C5_i16": dict(workload="config5: batched MinMax, 4096 int16 series x 2e6 points, n_out=1000 per series",
+                   algo="minmax_batched", tag="i16", S=W.C5_S, L=W.C5_L, n_out=1000, dtype="i16"),
+    "C5_u8": dict(workload="config5: batched MinMax, 4096 uint8 series x 2e6 points, n_out=1000 per series",
+                  algo="minmax_batched", tag="u8", S=W.C5_S, L=W.C5_L, n_out=1000, dtype="u8"),
+    "C5_f16": dict(workload="config5: batched MinMax, 4096 float16 series x 2e6 points, n_out=1000 per series",
+                   algo="minmax_batched", tag="f16", S=W.C5_S, L=W.C5_L, n_out=1000, dtype="f16"),
+}
+ORDER = ["C1", "C2", "C3_1000", "C3_10000", "C4", "C5_i16", "C5_u8", "C5_f16"]
 
 
-def _peaks():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+def config_dict(key, world=1):
+    s = SPECS[key]
+    d = {"workload": s["workload"], "n_out": s["n_out"]}
+    if "S" in s:
+        d.update(series=s["S"], points_per_series=s["L"], n=s["S"] * s["L"])
+    else:
+        d["n"] = s["n"]
+    if "ratio" in s:
+        d["minmax_ratio"] = s["ratio"]
+    d["parallelism"] = "single GPU" if world == 1 else (
+        f"sharded x{world}: " + ("series partitioned across ranks" if "S" in s else
+                                 "MinMax preselection split by sub-bin ranges, candidates all-gathered over NCCL"))
+    return d
 
 
-def _traffic():
-    p = os.path.join(ROOT, "profiles", "ncu_scan_traffic.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            return json.load(f).get("traffic_bytes_per_launch")
-    return None
+def make_data(key, procs=None):
+    s = SPECS[key]
+    if key == "C1":
+        return None, W.config1()
+    if key == "C2":
+        return W.config2()
+    if key.startswith("C3"):
+        return None, W.config3()
+    if key == "C4":
+        return W.config4_parallel(procs=procs)
+    return None, W.config5_parallel(s["tag"], procs=procs)
+
+
+_DATA_CACHE = {}
+
+
+def data_for(key):
+    """Inputs shared by the two C3 entries (same series)."""
+    k = "C3" if key.startswith("C3") else key
+    if k not in _DATA_CACHE:
+        _DATA_CACHE.clear()
+        _DATA_CACHE[k] = make_data(key)
+    return _DATA_CACHE[k]
+
+
+def algorithmic_bytes(key, y):
+    return int(y.nbytes)  # n * sizeof(y): y read once (x probes, outputs < 0.2 %)
+
+
+def n_points(key, y):
+    return int(y.size)
+
+
+def golden_ok(key, got, counts=None):
+    g = np.load(os.path.join(ROOT, "tests", "golden", "configs.npz"))
+    s = SPECS[key]
+    if "tag" in s:
+        tag = s["tag"]
+        if not np.array_equal(counts, g[f"c5_{tag}_count"]):
+            return False
+        hs = np.array([int.from_bytes(hashlib.blake2b(np.ascontiguousarray(got[r, : counts[r]], dtype="<u8").tobytes(),
+                                                      digest_size=8).digest(), "little") for r in range(got.shape[0])],
+                      np.uint64)
+        return bool(np.array_equal(hs, g[f"c5_{tag}_hash"]))
+    return bool(np.array_equal(np.asarray(got, np.uint64), g[s["golden"]]))
+
+
+# ------------------------------------------------------------------ host info
+
+
+def host_info():
+    info = {"cores": os.cpu_count() or 1}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() == "Model name":
+                info["cpu_model"] = v.strip()
+            if k.strip() == "Socket(s)":
+                info["sockets"] = int(v.strip())
+    except Exception:
+        pass
+    return info
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons, sampled every 100 ms while open;
+    windows between mark() pairs select the samples taken under load."""
 
-    Q = (
-        "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-        "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
-    )
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.rows = []
-        self.marks = []
+        self.windows = []
         self.proc = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE,
-                stderr=subprocess.DEVNULL,
-                text=True,
-            )
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
         except FileNotFoundError:
             self.proc = None
         return self
@@ -94,8 +195,8 @@ class ClockSampler:
             if len(parts) == 6:
                 self.rows.append((time.perf_counter(), parts))
 
-    def mark(self):
-        self.marks.append(time.perf_counter())
+    def window(self, t0, t1):
+        self.windows.append((t0, t1 + 0.05))
 
     def __exit__(self, *a):
         if self.proc:
@@ -106,267 +207,319 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        window = "timed region"
-        rows = [r for t, r in self.rows if len(self.marks) >= 2 and self.marks[0] <= t <= self.marks[1] + 0.05]
+        rows = [r for t, r in self.rows if any(a <= t <= b for a, b in self.windows)]
         if not rows:
-            window = "1 s soak of identical steps + timed region"
-            rows = [r for t, r in self.rows]
-        self.rows = rows
-        if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        num = lambda v: v.replace(".", "").isdigit()  # noqa: E731
+        sm = [float(r[0]) for r in rows if num(r[0])]
+        mx = [float(r[1]) for r in rows if num(r[1])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {
-            "sm_mhz": statistics.median(sm) if sm else None,
-            "sm_max_mhz": max(mx) if mx else None,
-            "reasons": reasons,
-            "samples": len(self.rows),
-            "window": window,
-        }
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows),
+                "window": "timed regions + a 1 s soak of identical steps before each"}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _traffic(key):
+    p = os.path.join(ROOT, "profiles", "r02_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(key)
+    return None
 
 
 def _dist():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def cpu_reference(x, y, steps, warmup, threads):
-    """Time the oracle port (CPU) on the workload; returns seconds per call."""
+# ------------------------------------------------------------------ CPU port
+
+
+def cpu_call(key, x, y, threads):
     from oracle import oracle as O
 
+    s = SPECS[key]
+    if "tag" in s:
+        return O.minmax_batched(y, s["n_out"], threads=threads)
+    args = (y,) if x is None else (x, y)
+    return O.downsample(s["algo"], *args, n_out=s["n_out"], minmax_ratio=s.get("ratio", 4), threads=threads)
+
+
+def cpu_time(key, x, y, threads, steps, warmup, budget_s=6.0):
+    """Median seconds per call of the CPU port; steps capped so the timed
+    calls take about budget_s (reported)."""
     for _ in range(warmup):
-        O.downsample("m4", x, y, n_out=N_OUT, threads=threads)
+        cpu_call(key, x, y, threads)
     ts = []
+    t_start = time.perf_counter()
     for _ in range(steps):
         t0 = time.perf_counter()
-        O.downsample("m4", x, y, n_out=N_OUT, threads=threads)
+        cpu_call(key, x, y, threads)
         ts.append(time.perf_counter() - t0)
-    return statistics.median(ts), ts
+        if time.perf_counter() - t_start > budget_s and len(ts) >= 3:
+            break
+    return statistics.median(ts), len(ts)
 
 
-def run_reference(args):
-    ws, rank, local = _dist()
-    if rank != 0:
-        return
-    x, y = W.config2()
-    threads = os.cpu_count() or 1
-    steps = max(1, args.steps)
-    med, ts = cpu_reference(x, y, steps, max(1, min(args.warmup, 2)), threads)
-    gbs = y.nbytes / med / 1e9
-    line = {
-        "impl": "reference",
-        "metric": "downsample input GB/s (M4, config 2)",
-        "value": round(gbs, 3),
-        "unit": "GB/s",
-        "n_gpus": args.gpus,
-        "steps": steps,
-        "warmup": args.warmup,
-        "ms_per_step": round(med * 1e3, 3),
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic (workloads.config2, seeded)",
-        "config": {"workload": "config2: M4 with x, 1e8 f64 points (0.01% NaN), int64 x, n_out=4000", "n": y.shape[0]},
-        "points_per_s": round(y.shape[0] / med, 1),
-        "cpu_baseline": {
-            "value": round(gbs, 3),
-            "unit": "GB/s",
-            "cores": threads,
-            "kind": "port",
-            "sample": f"full config-2 series (1e8 points) per step, median of {steps}",
-        },
-        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+# ------------------------------------------------------------------ GPU arm
+
+
+class GpuRunner:
+    def __init__(self, dev):
+        import torch
+
+        from paper_2307_05389_b200 import _lib
+
+        self.torch = torch
+        self.dev = dev
+        self.L = _lib.load()
+        self.lib = _lib
+        _lib.set_default_device(dev)
+        self.ctx = _lib.context(dev)
+        self.stream = torch.cuda.Stream(dev)
+        torch.cuda.set_stream(self.stream)
+        self.ctx.set_stream(self.stream.cuda_stream)
+        self.flush_w = None
+
+    def flush_l2(self):
+        torch = self.torch
+        if self.flush_w is None:
+            self.flush_w = torch.empty(L2_FLUSH, dtype=torch.uint8, device=f"cuda:{self.dev}")
+            self.flush_r = torch.ones(L2_FLUSH // 4, dtype=torch.float32, device=f"cuda:{self.dev}")
+        self.flush_w.fill_(3)
+        self.flush_r.sum()  # evicts the written lines (write-backs happen here, not in the timed step)
+
+    def make_step(self, key, x, y):
+        """(step() enqueuing one async call, result() -> host result) on device-resident copies."""
+        torch, L, ctx = self.torch, self.L, self.ctx
+        s = SPECS[key]
+        d = f"cuda:{self.dev}"
+        yd = torch.from_numpy(np.ascontiguousarray(y)).to(d)
+        if "tag" in s:
+            S, Ln = y.shape
+            out = torch.empty(S * s["n_out"], dtype=torch.int64, device=d)
+            cnt = torch.zeros(S, dtype=torch.int64, device=d)
+
+            def step():
+                self.lib.check(L.tsds_minmax_batched_async(ctx.handle, yd.data_ptr(), DT_CODE[y.dtype], S, Ln,
+                                                           s["n_out"], 0, out.data_ptr(), cnt.data_ptr()), key)
+
+            def result():
+                c = cnt.cpu().numpy()
+                return out.view(S, s["n_out"]).cpu().numpy(), c
+
+            return step, result, (yd, out, cnt)
+        xd = None if x is None else torch.from_numpy(np.ascontiguousarray(x)).to(d)
+        out = torch.empty(s["n_out"], dtype=torch.int64, device=d)
+        cnt = torch.zeros(1, dtype=torch.int64, device=d)
+        st = torch.zeros(1, dtype=torch.int32, device=d)
+        n = y.shape[0]
+        xptr = None if xd is None else xd.data_ptr()
+        xdt = 0 if x is None else DT_CODE[x.dtype]
+
+        def step():
+            self.lib.check(L.tsds_downsample_async(ctx.handle, ALGO_CODE[s["algo"]], xptr, xdt, yd.data_ptr(),
+                                                   DT_CODE[y.dtype], n, s["n_out"], s.get("ratio", 4), 0,
+                                                   out.data_ptr(), cnt.data_ptr(), st.data_ptr()), key)
+
+        def result():
+            m = int(cnt.item())
+            assert int(st.item()) == 0
+            return out[:m].cpu().numpy(), None
+
+        return step, result, (xd, yd, out, cnt, st)
+
+    def time_steps(self, step, steps, flush):
+        """Sum of per-step CUDA-event durations (ms) on the library's stream."""
+        torch = self.torch
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        l0 = self.ctx.launches
+        for e0, e1 in ev:
+            if flush:
+                self.flush_l2()
+            e0.record(self.stream)
+            step()
+            e1.record(self.stream)
+        torch.cuda.synchronize(self.dev)
+        return sum(e0.elapsed_time(e1) for e0, e1 in ev), self.ctx.launches - l0
+
+    def kernel_ms(self, step, steps, flush):
+        """Mean duration of the streaming kernel (events around it only)."""
+        L = self.L
+        L.tsds_ctx_profile(self.ctx.handle, 1)
+        for _ in range(steps):
+            if flush:
+                self.flush_l2()
+            step()
+        tot, cnt = ctypes.c_double(0), ctypes.c_int64(0)
+        L.tsds_ctx_profile_read(self.ctx.handle, ctypes.byref(tot), ctypes.byref(cnt))
+        L.tsds_ctx_profile(self.ctx.handle, 0)
+        return tot.value / max(1, cnt.value), int(cnt.value) // max(1, steps)
+
+
+def e2e_call(key, x, y):
+    import paper_2307_05389_b200 as ts
+
+    s = SPECS[key]
+    if "tag" in s:
+        return ts.minmax_batched(y, s["n_out"])
+    args = (y,) if x is None else (x, y)
+    kw = {"minmax_ratio": s["ratio"]} if "ratio" in s else {}
+    return ts.downsample(s["algo"], *args, n_out=s["n_out"], **kw)
+
+
+def measure_config(key, runner, args, clk, cpu, peak, peak_kind):
+    x, y = data_for(key)
+    s = SPECS[key]
+    nbytes, npts = algorithmic_bytes(key, y), n_points(key, y)
+    step, result, keep = runner.make_step(key, x, y)
+    step()
+    got, counts = result()
+    assert golden_ok(key, got, counts), f"{key}: device result differs from the reference's golden output"
+    flush = nbytes < (126 << 20)
+    for _ in range(args.warmup):
+        step()
+    runner.torch.cuda.synchronize(runner.dev)
+    # ~1 s soak of identical steps so the clock sampler sees this workload under load
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < 1.0:
+        for _ in range(20):
+            step()
+        runner.torch.cuda.synchronize(runner.dev)
+    t1 = time.perf_counter()
+    ms, launches = runner.time_steps(step, args.steps, flush)
+    clk.window(t0, time.perf_counter())
+    del t1
+    ms_step = ms / args.steps
+    kms, kper = runner.kernel_ms(step, args.steps, flush)
+    gbs = nbytes / (ms_step * 1e-3) / 1e9
+    achieved = nbytes / (kms * 1e-3) / 1e9
+    entry = {
+        "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "ms_per_step": round(ms_step, 5),
+        "points_per_s": round(npts / (ms_step * 1e-3), 1), "algorithmic_bytes_per_step": nbytes,
+        "steps": args.steps, "warmup": args.warmup, "config": config_dict(key),
+        "l2": "flushed between steps (256 MB write + 256 MB read)" if flush else
+              f"inputs ({nbytes / 1e9:.2f} GB) larger than L2 (126 MB); no flush",
+        "parity": "equal to the reference's output (tests/golden/configs.npz)",
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": {"minmax": "scan_kernel<f32> (CTA-per-bin mode)",
+                                                "m4": "scan_kernel<f64>", "lttb": "lttb_sb_kernel<f64>",
+                                                "minmaxlttb": "scan_kernel<f32> (MinMax preselection)",
+                                                "minmax_batched": "lane_bins_kernel / scan_kernel"}[s["algo"]],
+                     "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "frac_of_step": round(gbs / peak, 4),
+                     "traffic": _traffic(key), "algorithmic_bytes_per_launch": nbytes,
+                     "avg_launch_ms": round(kms, 5), "launches_per_step": kper},
     }
-    print(json.dumps(line), flush=True)
+    del keep
+    runner.torch.cuda.empty_cache()
+    # ---- e2e through the public API, host (pageable) numpy inputs
+    e2e_call(key, x, y)
+    n_e2e = 3
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        r = e2e_call(key, x, y)
+    e2e_s = (time.perf_counter() - t0) / n_e2e
+    clk.window(t0, time.perf_counter())
+    if "tag" in s:
+        assert golden_ok(key, r[0], r[1]), f"{key}: e2e result differs"
+    else:
+        assert golden_ok(key, r), f"{key}: e2e result differs"
+    d2h = s["n_out"] * 8 * (s["S"] if "S" in s else 1) + 16
+    entry["e2e"] = {"value": round(nbytes / e2e_s / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": nbytes,
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_s * 1e3, 3),
+                    "path": "public API on pageable host numpy (H2D of y, binning, kernels, index readback)"}
+    if cpu is not None:
+        med, k = cpu_time(key, x, y, cpu["cores"], args.cpu_steps, 1)
+        entry["cpu_baseline"] = {"value": round(nbytes / med / 1e9, 3), "unit": "GB/s", "cores": cpu["cores"],
+                                 "kind": "port", "cpu_model": cpu.get("cpu_model"), "sockets": cpu.get("sockets"),
+                                 "sample": f"full config, median of {k} after 1 warm-up",
+                                 "ms_per_call": round(med * 1e3, 3)}
+    return entry
 
 
 def run_ours(args):
     import torch
 
     ws, rank, local = _dist()
-    dev = local if ws > 1 else 0
-    torch.cuda.set_device(dev)
     if ws > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-    import paper_2307_05389_b200 as ts
-    from paper_2307_05389_b200 import _lib
-
-    L = _lib.load()
-    _lib.set_default_device(dev)
-    ctx = _lib.context(dev)
-    # a dedicated (non-default) stream shared by libtsds and torch's events
-    stream = torch.cuda.Stream(dev)
-    torch.cuda.set_stream(stream)
-    ctx.set_stream(stream.cuda_stream)
-
-    # ---- data: every rank its own config-2 series (rank-shifted x keeps it monotone)
-    x_h, y_h = W.config2()
-    n = y_h.shape[0]
-    if rank:
-        x_h = x_h + np.int64(rank) * (x_h[-1] + 1000)
-    xd = torch.from_numpy(x_h).cuda(dev)
-    yd = torch.from_numpy(y_h).cuda(dev)
-    out = torch.empty(N_OUT, dtype=torch.int64, device=f"cuda:{dev}")
-    cnt = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
-    status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{dev}")
-
-    def step():
-        rc = L.tsds_downsample_async(
-            ctx.handle, 2, xd.data_ptr(), 6, yd.data_ptr(), 2, n, N_OUT, 0, out.data_ptr(), cnt.data_ptr(), status.data_ptr()
-        )
-        _lib.check(rc, "m4")
-
-    # correctness gate (the timed result must be the reference's)
-    step()
-    torch.cuda.synchronize()
-    got = out[: int(cnt.item())].cpu().numpy()
-    want = ts.downsample("m4", x_h, y_h, n_out=N_OUT).view(np.int64)
-    assert int(status.item()) == 0 and np.array_equal(got, want), "device-resident result differs from the API result"
-    if rank == 0:
-        from oracle import oracle as O
-
-        gold = O.downsample("m4", x_h[:2_000_000], y_h[:2_000_000], n_out=N_OUT, threads=os.cpu_count() or 1)
-        assert np.array_equal(ts.downsample("m4", x_h[:2_000_000], y_h[:2_000_000], n_out=N_OUT), gold)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-
-    # ---- timed region (device-resident)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(dev) as clk:
-        # untimed soak (~1 s of identical steps) so the clock sampler sees the
-        # part under load even when K steps take only milliseconds
-        t_soak = time.perf_counter()
-        while time.perf_counter() - t_soak < 1.0:
-            for _ in range(50):
-                step()
-            torch.cuda.synchronize()
-        clk.mark()
-        launches0 = ctx.launches
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        clk.mark()
-    launches = ctx.launches - launches0
-    ms = e0.elapsed_time(e1)
-    # second pass of K identical steps with CUDA events around every scan
-    # launch (events between kernels disable the programmatic-dependent-launch
-    # overlap, so this pass is only used for the per-kernel roofline)
-    L.tsds_ctx_profile(ctx.handle, 1)
-    for _ in range(args.steps):
-        step()
-    tot = ctypes.c_double(0)
-    kcount = ctypes.c_int64(0)
-    L.tsds_ctx_profile_read(ctx.handle, ctypes.byref(tot), ctypes.byref(kcount))
-    L.tsds_ctx_profile(ctx.handle, 0)
-    scan_ms = tot.value / max(1, kcount.value)
-    if ws > 1:
-        t = torch.tensor([ms], device=f"cuda:{dev}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-        # gather every rank's indices (the job's result) to all ranks
-        got = torch.zeros(ws * N_OUT, dtype=torch.int64, device=f"cuda:{dev}")
-        torch.distributed.all_gather_into_tensor(got, out)
-    ms_step = ms / args.steps
-    bytes_step = y_h.nbytes
-    gbs = ws * bytes_step / (ms_step * 1e-3) / 1e9
-
-    # ---- e2e through the public API with pinned host inputs
-    xp = torch.from_numpy(x_h).pin_memory().numpy()
-    yp = torch.from_numpy(y_h).pin_memory().numpy()
-    ts.downsample("m4", xp, yp, n_out=N_OUT)
-    e2e_steps = max(2, min(args.steps, 10))
-    if ws > 1:
-        torch.distributed.barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        r = ts.downsample("m4", xp, yp, n_out=N_OUT)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if ws > 1:
-        t = torch.tensor([e2e_s], device=f"cuda:{dev}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    assert np.array_equal(r.view(np.int64), want)
-    e2e_gbs = ws * bytes_step / e2e_s / 1e9
-
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        med, _ = cpu_reference(x_h, y_h, 3, 1, threads)
-        cpu = {
-            "value": round(bytes_step / med / 1e9, 3),
-            "unit": "GB/s",
-            "cores": threads,
-            "kind": "port",
-            "sample": "full config-2 series (1e8 points), median of 3 after 1 warm-up",
-        }
-
+        return run_ours_sharded(args)
+    runner = GpuRunner(0)
     peak, peak_kind = _peaks()
-    achieved = bytes_step / (scan_ms * 1e-3) / 1e9
+    cpu = None if args.no_cpu else host_info()
+    keys = [k for k in ORDER if k.split("_")[0] in args.configs]
+    entries = {}
+    with ClockSampler(0) as clk:
+        for key in keys:
+            entries[key] = measure_config(key, runner, args, clk, cpu, peak, peak_kind)
+            print(f"[bench] {key}: {entries[key]['value']} GB/s, step {entries[key]['ms_per_step']} ms, "
+                  f"kernel {entries[key]['roofline']['frac']} of peak, e2e {entries[key]['e2e']['value']} GB/s",
+                  file=sys.stderr, flush=True)
+    _DATA_CACHE.clear()
+    head = entries.get(HEADLINE) or entries[keys[0]]
     line = {
-        "metric": "downsample input GB/s (M4, config 2)",
-        "value": round(gbs, 3),
-        "unit": "GB/s",
-        "n_gpus": ws,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": round(ms_step, 4),
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic (workloads.config2, seeded; per-rank series under torchrun)",
-        "config": {
-            "workload": "config2: M4Downsampler with x, 1e8 f64 points (0.01% NaN), int64 x, n_out=4000",
-            "n_per_gpu": n,
-            "bins": N_OUT // 4,
-            "l2": "inputs (1.6 GB) larger than L2 (126 MB); no flush needed",
-            "parallelism": f"replica per GPU x{ws}" if ws > 1 else "single GPU",
-        },
-        "points_per_s": round(ws * n / (ms_step * 1e-3), 1),
-        "roofline": {
-            "bound": "hbm",
-            "kernel": "scan_kernel<f64> (fused binning-aware argmin/argmax + compaction)",
-            "achieved": round(achieved, 1),
-            "peak": peak,
-            "peak_kind": peak_kind,
-            "unit": "GB/s",
-            "frac": round(achieved / peak, 4),
-            "traffic": _traffic(),
-            "algorithmic_bytes_per_launch": bytes_step,
-            "avg_launch_ms": round(scan_ms, 5),
-        },
-        "clocks": clk.summary(),
-        "gpu_launches": int(launches),
-        "e2e": {
-            "value": round(e2e_gbs, 3),
-            "unit": "GB/s",
-            "h2d_bytes_per_step": int(y_h.nbytes + (N_OUT // 4 + 1) * 8),
-            "d2h_bytes_per_step": int((N_OUT + 1) * 8 + 4),
-            "ms_per_step": round(e2e_s * 1e3, 3),
-            "path": "ts.downsample('m4', x, y) on pinned numpy (host binning of x, y H2D, scan, indices D2H)",
-        },
+        "metric": METRIC, "value": head["value"], "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": SPECS[HEADLINE if HEADLINE in entries else keys[0]]["dtype"],
+        "data": "synthetic (workloads.py, seeded generators of BASELINE configs, SURVEY.md 8(d))",
+        "config": head["config"], "points_per_s": head["points_per_s"], "roofline": head["roofline"],
+        "clocks": clk.summary(), "gpu_launches": head["gpu_launches"], "e2e": head["e2e"],
+        "l2": head["l2"], "parity": head["parity"],
     }
-    if cpu:
-        line["cpu_baseline"] = cpu
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if ws > 1:
-        torch.distributed.destroy_process_group()
+    if "cpu_baseline" in head:
+        line["cpu_baseline"] = head["cpu_baseline"]
+    line["configs"] = entries
+    print(json.dumps(line), flush=True)
+    del torch
+
+
+def run_ours_sharded(args):
+    from paper_2307_05389_b200 import distributed as D
+
+    return D.bench_sharded(args, sys.modules[__name__])
+
+
+def run_reference(args):
+    ws, rank, local = _dist()
+    if rank != 0:
+        return
+    info = host_info()
+    keys = [k for k in ORDER if k.split("_")[0] in args.configs]
+    entries = {}
+    for key in keys:
+        x, y = data_for(key)
+        nbytes = algorithmic_bytes(key, y)
+        med, k = cpu_time(key, x, y, info["cores"], args.steps, args.warmup, budget_s=args.ref_budget)
+        gbs = nbytes / med / 1e9
+        entries[key] = {
+            "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "ms_per_step": round(med * 1e3, 3),
+            "points_per_s": round(n_points(key, y) / med, 1), "steps": k, "warmup": args.warmup,
+            "config": config_dict(key, ws),
+            "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": info["cores"], "kind": "port",
+                             "cpu_model": info.get("cpu_model"), "sockets": info.get("sockets"),
+                             "sample": f"full config per step, median of {k} after {args.warmup} warm-ups"},
+            "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(f"[bench ref] {key}: {entries[key]['value']} GB/s ({k} steps)", file=sys.stderr, flush=True)
+    _DATA_CACHE.clear()
+    head = entries.get(HEADLINE) or entries[keys[0]]
+    line = {"impl": "reference", "metric": METRIC, "value": head["value"], "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": head["steps"], "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": SPECS[HEADLINE if HEADLINE in entries else keys[0]]["dtype"],
+            "data": "synthetic (workloads.py, seeded generators of BASELINE configs, SURVEY.md 8(d))",
+            "config": head["config"], "points_per_s": head["points_per_s"], "cpu_baseline": head["cpu_baseline"],
+            "e2e": head["e2e"], "configs": entries}
+    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -375,10 +528,14 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--configs", default="C1,C2,C3,C4,C5", help="subset of C1..C5 (C4 is the headline)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-steps", type=int, default=5)
+    ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of timed CPU calls per config (reference arm)")
     args = ap.parse_args()
-    if args.warmup < 3 and args.impl == "ours":
-        args.warmup = 3
+    args.configs = [c.strip().upper() for c in args.configs.split(",") if c.strip()]
+    if args.impl == "ours":
+        args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -79,9 +79,11 @@ int64_t tsds_ctx_launches(tsds_ctx *ctx);
 /* counters: "launches", "lttb_rounds" (verification rounds of the last
  * large-bucket LTTB); -1 for an unknown name */
 int64_t tsds_ctx_stat(tsds_ctx *ctx, const char *name);
-/* measurement hooks: record CUDA events around every argmin/argmax scan
- * launch; _read synchronises, returns their summed duration and count, and
- * clears the record */
+/* measurement hooks: record CUDA events around every launch of the call's
+ * streaming kernel (the one pass over y: the argmin/argmax scan, the
+ * thread-per-bin batched kernel, or the LTTB summary pass); programmatic
+ * dependent launch is off for them while enabled.  _read synchronises,
+ * returns their summed duration and count, and clears the record */
 int tsds_ctx_profile(tsds_ctx *ctx, int enable);
 int tsds_ctx_profile_read(tsds_ctx *ctx, double *total_ms, int64_t *count);
 
@@ -97,13 +99,17 @@ int tsds_downsample(tsds_ctx *ctx, int algo, const void *x, int x_dtype, const v
                     int64_t n, int64_t n_out, int64_t minmax_ratio, int nan_mode, int mem, int64_t *out,
                     int64_t *out_len);
 
-/* Asynchronous device-resident variant for MinMax / M4 (no host sync, no
- * copies): x, y, out_dev (int64[n_out]) and count_dev (int64) are device
- * pointers; *status_dev (int32) receives TSDS_ERR_SPAN if the x span is
- * invalid.  Enqueued on ctx's stream. */
+/* Asynchronous device-resident variant of tsds_downsample for all four
+ * algorithms: x, y, out_dev (int64[n_out]) and count_dev (int64) are device
+ * pointers on ctx's device; *status_dev (int32, nullable) receives
+ * TSDS_ERR_SPAN if the x span is invalid (then *count_dev is not a result).
+ * Everything is enqueued on ctx's stream without a host round trip --
+ * MinMaxLTTB included (stage 2 reads the candidate count on the device) --
+ * except MinMaxLTTB with minmax_ratio above ~30, whose stage 2 is sized on
+ * the host (one synchronisation).  CUDA-graph capturable otherwise. */
 int tsds_downsample_async(tsds_ctx *ctx, int algo, const void *x, int x_dtype, const void *y, int y_dtype,
-                          int64_t n, int64_t n_out, int nan_mode, int64_t *out_dev, int64_t *count_dev,
-                          int32_t *status_dev);
+                          int64_t n, int64_t n_out, int64_t minmax_ratio, int nan_mode, int64_t *out_dev,
+                          int64_t *count_dev, int32_t *status_dev);
 
 /* One shard of a sharded MinMax / M4 (multi-GPU): the bins
  * [b0, b1) of a larger series, i.e. _run_bins' per-thread bin chunk

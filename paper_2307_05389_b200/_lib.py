@@ -100,7 +100,7 @@ def load():
         L.tsds_ctx_profile.argtypes = [vp, i32]
         L.tsds_ctx_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), p64]
         L.tsds_downsample.argtypes = [vp, i32, vp, i32, vp, i32, i64, i64, i64, i32, i32, vp, p64]
-        L.tsds_downsample_async.argtypes = [vp, i32, vp, i32, vp, i32, i64, i64, i32, vp, vp, vp]
+        L.tsds_downsample_async.argtypes = [vp, i32, vp, i32, vp, i32, i64, i64, i64, i32, vp, vp, vp]
         L.tsds_downsample_bins_async.argtypes = [vp, i32, vp, i32, vp, i64, i64, i32, vp, vp]
         L.tsds_lttb_stage2.argtypes = [vp, vp, i32, vp, i32, vp, i64, i64, vp, p64]
         L.tsds_minmax_batched.argtypes =[vp, vp, i32, i64, i64, i64, i32, i32, vp, vp]

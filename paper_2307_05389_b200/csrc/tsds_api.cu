@@ -414,12 +414,14 @@ ScanArgs scan_args(const void* y, BinSpec bins, int64_t g0, int64_t g1, int64_t 
 
 // one fused binning launch (uniform checks + edges + verdict); flags land in Misc.F
 int launch_binning(tsds_ctx* ctx, int xdt, const void* x, int64_t n, int64_t nb, int64_t add, const void* xapi,
-                   int64_t napi, int uniform_first, int materialize, int64_t* off) {
+                   int64_t napi, int uniform_first, int materialize, int64_t* off, const int64_t* n_dev = nullptr,
+                   int64_t n_sub = 0, int64_t skip_le = 0, const int* force_count = nullptr) {
   const int cta_edges = (nb - 1) * BIN_THREADS <= (int64_t)ctx->sms * 2048 ? 1 : 0;
   const int64_t edge_blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 16,
       cta_edges ? nb - 1 : (nb + BIN_THREADS / 32 - 1) / (BIN_THREADS / 32)));
   const int64_t piece_blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms, (std::max(n, napi) + 511) / 512));
-  BinJob J{x, n, nb, add, xapi, napi, uniform_first, materialize, cta_edges, piece_blocks, off, &misc(ctx)->F};
+  BinJob J{x,  n,   nb,          add, xapi, napi,  uniform_first, materialize, cta_edges, piece_blocks,
+           off, &misc(ctx)->F, n_dev, n_sub, skip_le, force_count};
   unsigned grid = (unsigned)(piece_blocks + edge_blocks);
   XDT_SWITCH(xdt, (binning_kernel<XD><<<grid, BIN_THREADS, 0, ctx->stream>>>(J)));
   LAUNCH_CHECK();
@@ -549,7 +551,7 @@ int lttb_exact_mode() {
 }
 
 int run_lttb_walk_small(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
-                        const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev, bool have_cent = false);
+                        const int64_t* off, int64_t nb, const int64_t* map, int64_t* idx_out, int64_t* cnt_out);
 
 int ensure_lstat(tsds_ctx* ctx) {
   if (!ctx->h_lstat) CUDA_TRY(cudaMallocHost(&ctx->h_lstat, 128));
@@ -634,7 +636,7 @@ static inline unsigned cap_grid(int64_t want, int64_t cap) {
 // no host round trip; consecutive kernels are chained with programmatic
 // dependent launch.
 int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
-                   const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev) {
+                   const int64_t* off, int64_t nb, const int64_t* map, int64_t* idx_out, int64_t* cnt_out) {
   if (nb >= ((int64_t)1 << 24))  // work-list entries pack the bucket rank into 24 bits
     return set_err(TSDS_ERR_ARG, "large-bucket LTTB supports fewer than 2^24 buckets");
   RC_TRY(ensure(ctx, ctx->cent, (size_t)std::max<int64_t>(nb, 1) * sizeof(double2)));
@@ -690,12 +692,13 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   const int exact = mode == 1 ? 1 : (mode == 2 ? 0 : (avg <= 1024 ? 1 : 0));
   const int vec_ok = ((uintptr_t)y & 15) == 0 ? 1 : 0;
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-  RC_TRY(prof_mark(ctx, ev, false));
   CUDA_TRY(cudaMemsetAsync(counts, 0, zero_bytes, ctx->stream));
-  // ---- 1. sub-block summaries (the one streaming pass over y)
+  // ---- 1. sub-block summaries (the one streaming pass over y; profiled)
+  RC_TRY(prof_mark(ctx, ev, false));
   YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_sb_kernel<YD>,
                                     one_wave(ctx, lttb_sb_kernel<YD>, LTTB_SB_WARPS * 32, LTTB_SB_SMEM),
                                     LTTB_SB_WARPS * 32, LTTB_SB_SMEM, xf, drop, y, n, vec_ok, A)));
+  RC_TRY(prof_mark(ctx, ev, true));
   // ---- 2. guess + round-1 plan (cooperative)
   const int64_t cap = 32768;
   YDT_SWITCH(ydt, ({
@@ -717,8 +720,7 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
                                     (const int64_t*)counts, A, (const int64_t*)ext, picks, (const int32_t*)list_a,
                                     lock, ctr, vec_ok)));
   RC_TRY(launch_pdl(ctx, lttb_emit_kernel, cap_grid((nb + 257) / 256, 1024), 256, 0, (const int64_t*)picks,
-                    (const int64_t*)counts, n, map, out_dev + 1, out_dev));
-  RC_TRY(prof_mark(ctx, ev, true));
+                    (const int64_t*)counts, n, map, idx_out, cnt_out));
   RC_TRY(ensure_lstat(ctx));
   CUDA_TRY(cudaMemcpyAsync(ctx->h_lstat, ctr, 32 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->lstat_pending = true;
@@ -726,21 +728,24 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
 }
 
 int run_lttb_walk(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
-                  const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev) {
+                  const int64_t* off, int64_t nb, const int64_t* map, int64_t* idx_out, int64_t* cnt_out) {
   const int64_t avg = (n - 2) / std::max<int64_t>(nb, 1);
-  if (avg > SMALL_MAX / 2) return run_lttb_large(ctx, xf, drop, y, ydt, n, off, nb, map, out_dev);
-  return run_lttb_walk_small(ctx, xf, drop, y, ydt, n, off, nb, map, out_dev);
+  if (avg > SMALL_MAX / 2) return run_lttb_large(ctx, xf, drop, y, ydt, n, off, nb, map, idx_out, cnt_out);
+  return run_lttb_walk_small(ctx, xf, drop, y, ydt, n, off, nb, map, idx_out, cnt_out);
 }
 
+// Small-bucket walk (centroids + single-CTA walk).  n_dev (nullable): the
+// series length lives on the device (MinMaxLTTB stage 2: the candidate
+// count); n is then its upper bound and both kernels are no-ops when
+// *n_dev <= skip_le.
 int run_lttb_walk_small(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
-                        const int64_t* off, int64_t nb, const int64_t* map, int64_t* out_dev, bool have_cent) {
+                        const int64_t* off, int64_t nb, const int64_t* map, int64_t* idx_out, int64_t* cnt_out,
+                        const int64_t* n_dev, int64_t skip_le) {
   RC_TRY(ensure(ctx, ctx->cent, (size_t)std::max<int64_t>(nb, 1) * sizeof(double2)));
   double2* cent = (double2*)ctx->cent.p;
-  if (!have_cent) {
-    unsigned gc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 16, (nb + 7) / 8));
-    YDT_SWITCH(ydt, (lttb_centroid_kernel<YD><<<gc, 256, 0, ctx->stream>>>(xf, drop, y, off, nb, cent)));
-    LAUNCH_CHECK();
-  }
+  unsigned gc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 16, (nb + 7) / 8));
+  YDT_SWITCH(ydt, (lttb_centroid_kernel<YD><<<gc, 256, 0, ctx->stream>>>(xf, drop, y, off, nb, cent, n_dev, skip_le)));
+  LAUNCH_CHECK();
   // scratch for the small-bucket (jump) strategy when buckets are small on average
   LttbScratch S{nullptr, nullptr, nullptr};
   int levels = 1;
@@ -759,9 +764,14 @@ int run_lttb_walk_small(tsds_ctx* ctx, const double* xf, const int* drop, const 
     nodes_cap = n;
   }
   YDT_SWITCH(ydt, (lttb_walk_kernel<YD><<<1, LTTB_THREADS, 0, ctx->stream>>>(
-                      xf, drop, y, n, off, nb, cent, map, out_dev + 1, out_dev, S, nodes_cap, levels)));
+                      xf, drop, y, n, off, nb, cent, map, idx_out, cnt_out, S, nodes_cap, levels, n_dev, skip_le)));
   LAUNCH_CHECK();
   return TSDS_OK;
+}
+
+int run_lttb_walk_small(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
+                        const int64_t* off, int64_t nb, const int64_t* map, int64_t* idx_out, int64_t* cnt_out) {
+  return run_lttb_walk_small(ctx, xf, drop, y, ydt, n, off, nb, map, idx_out, cnt_out, nullptr, 0);
 }
 
 int to_f64(tsds_ctx* ctx, const void* x, int xdt, int64_t n, DevBuf& buf, const double** xf) {
@@ -821,19 +831,22 @@ int interior_bins(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int64_t nb, 
   return TSDS_OK;
 }
 
-int run_lttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, int64_t n, int64_t n_out, int mem,
-             int64_t* out, int64_t* out_len) {
+// LTTB (algorithms.py:184-208) enqueued into (idx_out, cnt_out) on the
+// device.  No host round trip: a failed device binning (non-finite span)
+// leaves empty bins behind, so the walk runs over nothing and the status
+// word reports the error.
+int enqueue_lttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, int64_t n, int64_t n_out, int mem,
+                 int64_t* idx_out, int64_t* cnt_out) {
   const int64_t nb = n_out - 2;
   BinSpec bins;
   ScanArgs guards = scan_args(nullptr, BinSpec{}, 0, 0, 0, 0);
   const void* xk;
   RC_TRY(interior_bins(ctx, x, xdt, n, nb, mem, &bins, &guards, &xk, 1));
-  const int64_t* off;
   if (bins.mode == 0 && !guards.use_dyn_mode) {
     RC_TRY(ensure(ctx, ctx->off, (size_t)(nb + 1) * 8));
     RC_TRY(launch_count_offsets(ctx, n - 2, nb, 1, (int64_t*)ctx->off.p));
   }
-  off = (const int64_t*)ctx->off.p;
+  const int64_t* off = (const int64_t*)ctx->off.p;
   const void* dy;
   RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
   const double* xf = nullptr;
@@ -842,27 +855,25 @@ int run_lttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, int6
     const void* dx;
     RC_TRY(stage_input(ctx, ctx->x, xk, (size_t)n * dtype_size(xdt), mem, &dx));
     RC_TRY(to_f64(ctx, dx, xdt, n, ctx->xf64, &xf));
-    if (mem == TSDS_MEM_DEVICE) drop = &misc(ctx)->F.mis_api;
+    if (mem == TSDS_MEM_DEVICE) drop = &misc(ctx)->F.mis_api;  // api-level uniform verdict, read by the walk
   }
-  RC_TRY(ensure(ctx, ctx->out, (size_t)(n_out + 2) * 8));
-  int64_t* dout = (int64_t*)ctx->out.p;
-  // the walk never runs on a failed binning: status is checked at fetch;
-  // guard by skipping the walk when the host already knows (host path), and
-  // on the device path the walk reads offsets that the width kernel wrote
-  // (on error they are stale but in-bounds only if monotone) -> sync first.
-  if (mem == TSDS_MEM_DEVICE && x) {
-    int hs = 0;
-    CUDA_TRY(cudaMemcpyAsync(&hs, &misc(ctx)->F.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    if (hs) ctx->flags_clean = false;
-    RC_TRY(finish_status(ctx, &hs));
-  }
-  RC_TRY(run_lttb_walk(ctx, xf, drop, dy, ydt, n, off, nb, nullptr, dout));
-  return fetch_result(ctx, dout, n_out, out, out_len);
+  return run_lttb_walk(ctx, xf, drop, dy, ydt, n, off, nb, nullptr, idx_out, cnt_out);
 }
 
-int run_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, int64_t n, int64_t n_out,
-                   int64_t ratio, int nan_mode, int mem, int64_t* out, int64_t* out_len) {
+// MinMaxLTTB (algorithms.py:211-255) enqueued into (idx_out, cnt_out).
+// Stage 1: the MinMax preselection scan writes `full` = [0] + picks + [n-1]
+// and its count m into ctx->full = [m, full...].  Stage 2 (the triangle
+// walk over the candidates) then runs
+//   * device inputs, buckets of <= SMALL_MAX/2 candidates on average
+//     (minmax_ratio <= ~30): entirely on the device -- every stage-2 kernel
+//     reads m itself, m <= n_out returns `full` (stage2_finish_kernel), and
+//     the api-level uniform verdict of x is read on the device; no host sync;
+//   * host x: m and `full` come back to the host, x[full] is gathered and
+//     binned there (x never crosses PCIe); otherwise (large ratios) the
+//     walk is sized on the host from m.
+// *synced tells the caller whether a host round trip happened.
+int enqueue_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, int64_t n, int64_t n_out,
+                       int64_t ratio, int nan_mode, int mem, int64_t* idx_out, int64_t* cnt_out) {
   const int64_t nsub = (n_out - 2) * ((ratio + 1) / 2);
   ScanArgs A = scan_args(nullptr, BinSpec{}, 0, nsub, 1, n - 1);
   const void* xk;
@@ -884,7 +895,48 @@ int run_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt
     ctx->status_live = true;
   }
   RC_TRY(launch_scan(ctx, ydt, nan_mode, A));
-  // stage boundary: the candidate count decides stage 2
+  const int64_t* full = dfull + 1;
+  const int64_t nb2 = n_out - 2;
+  const int es_y = dtype_size(ydt);
+  RC_TRY(ensure(ctx, ctx->off, (size_t)(nb2 + 1) * 8));
+  int64_t* off2 = (int64_t*)ctx->off.p;
+
+  const bool device_stage2 = (mem == TSDS_MEM_DEVICE || !xk) && (fcap - 2) / std::max<int64_t>(nb2, 1) <= SMALL_MAX / 2 &&
+                             fcap <= ((int64_t)1 << 24);
+  if (device_stage2) {
+    RC_TRY(ensure(ctx, ctx->y2, (size_t)fcap * es_y));
+    RC_TRY(ensure(ctx, ctx->x2f64, (size_t)fcap * 8));
+    const int es_x = xk ? dtype_size(xdt) : 8;
+    if (xk) RC_TRY(ensure(ctx, ctx->x2, (size_t)fcap * es_x));
+    const unsigned g = cap_grid((fcap + 255) / 256, (int64_t)ctx->sms * 8);
+    const int* api_nonuniform = ctx->status_live ? &misc(ctx)->mis_api_copy : nullptr;
+    double* x2f = (double*)ctx->x2f64.p;
+    if (xk) {
+      XDT_SWITCH(xdt, (stage2_inputs_kernel<XD><<<g, 256, 0, ctx->stream>>>(dfull, n_out, dy, es_y, ctx->y2.p, xk,
+                                                                             ctx->x2.p, x2f, api_nonuniform)));
+    } else {
+      stage2_inputs_kernel<-1><<<g, 256, 0, ctx->stream>>>(dfull, n_out, dy, es_y, ctx->y2.p, nullptr, nullptr, x2f,
+                                                            nullptr);
+    }
+    LAUNCH_CHECK();
+    if (xk) {
+      // equal-width bins over x2[1:m-1] (algorithms.py:246-250), or the
+      // equal-count formula when the whole x was found uniform
+      RC_TRY(launch_binning(ctx, xdt, (const char*)ctx->x2.p + es_x, fcap - 2, nb2, 1, nullptr, 0, 0, 1, off2, dfull,
+                            2, n_out, api_nonuniform));
+    } else {
+      const unsigned gc = cap_grid((nb2 + 256) / 256, (int64_t)ctx->sms * 4);
+      count_offsets_kernel<<<gc, 256, 0, ctx->stream>>>(0, nb2, 1, off2, dfull, 2, n_out);
+      LAUNCH_CHECK();
+    }
+    RC_TRY(run_lttb_walk_small(ctx, x2f, nullptr, ctx->y2.p, ydt, fcap, off2, nb2, full, idx_out, cnt_out, dfull,
+                               n_out));
+    stage2_finish_kernel<<<cap_grid((fcap + 255) / 256, 64), 256, 0, ctx->stream>>>(dfull, n_out, idx_out, cnt_out);
+    LAUNCH_CHECK();
+    return TSDS_OK;
+  }
+
+  // stage boundary on the host: the candidate count decides stage 2
   RC_TRY(ensure_host(ctx, (size_t)(fcap + 2) * 8 + 64));
   int64_t* h = (int64_t*)ctx->h_pin;
   int* hs = (int*)(h + fcap + 1);
@@ -900,14 +952,13 @@ int run_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt
   // too (api.py:19-28: the reference normalises x away before minmaxlttb)
   if (xk && mem == TSDS_MEM_DEVICE && ctx->status_live && hs[1] == 0) xk = nullptr;
   const int64_t m = h[0];
-  if (m <= n_out) return fetch_result(ctx, dfull, m, out, out_len);
-  const int64_t* full = dfull + 1;
-  const int64_t nb2 = n_out - 2;
+  if (m <= n_out) {
+    CUDA_TRY(cudaMemcpyAsync(idx_out, full, (size_t)m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(cnt_out, dfull, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    return TSDS_OK;
+  }
   RC_TRY(gather(ctx, dy, ydt, full, m, ctx->y2));
   const double* x2f = nullptr;
-  int64_t* off2;
-  RC_TRY(ensure(ctx, ctx->off, (size_t)(nb2 + 1) * 8));
-  off2 = (int64_t*)ctx->off.p;
   if (!xk) {
     // candidate positions stand in for x (algorithms.py:244-250)
     RC_TRY(to_f64(ctx, full, DT_I64, m, ctx->x2f64, &x2f));
@@ -932,15 +983,8 @@ int run_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt
     const int es = dtype_size(xdt);
     RC_TRY(launch_binning(ctx, xdt, (const char*)ctx->x2.p + es, m - 2, nb2, 1, nullptr, 0, 0, 1, off2));
     RC_TRY(to_f64(ctx, ctx->x2.p, xdt, m, ctx->x2f64, &x2f));
-    int hs2 = 0;
-    CUDA_TRY(cudaMemcpyAsync(&hs2, &misc(ctx)->F.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    RC_TRY(finish_status(ctx, &hs2));
   }
-  RC_TRY(ensure(ctx, ctx->out, (size_t)(n_out + 2) * 8));
-  int64_t* dout = (int64_t*)ctx->out.p;
-  RC_TRY(run_lttb_walk(ctx, x2f, nullptr, ctx->y2.p, ydt, m, off2, nb2, full, dout));
-  return fetch_result(ctx, dout, n_out, out, out_len);
+  return run_lttb_walk(ctx, x2f, nullptr, ctx->y2.p, ydt, m, off2, nb2, full, idx_out, cnt_out);
 }
 
 __global__ void iota_rows_kernel(int64_t* out, int64_t S, int64_t L, int64_t n_out, int64_t* counts) {
@@ -1099,62 +1143,88 @@ int tsds_ctx_profile_read(tsds_ctx* ctx, double* total_ms, int64_t* count) {
   return TSDS_OK;
 }
 
-int tsds_downsample(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y, int ydt, int64_t n, int64_t n_out,
-                    int64_t ratio, int nan_mode, int mem, int64_t* out, int64_t* out_len) {
-  if (!ctx || !y || !out || !out_len || n < 1 || !dtype_ok(ydt) || (x && !xdtype_ok(xdt)))
-    return set_err(TSDS_ERR_ARG, "tsds_downsample: invalid argument");
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  DeviceGuard dg_(ctx->device);
-  RC_TRY(begin_call(ctx));
+// whole algorithm call enqueued into (idx_out, cnt_out) on ctx's stream
+// (validation of n_out / ratio already done by the caller)
+static int enqueue_algo(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y, int ydt, int64_t n,
+                        int64_t n_out, int64_t ratio, int nan_mode, int mem, int64_t* idx_out, int64_t* cnt_out) {
+  auto identity_dev = [&](int64_t len) -> int {
+    iota_kernel<<<(unsigned)std::min<int64_t>(1024, (len + 255) / 256), 256, 0, ctx->stream>>>(idx_out, len, cnt_out);
+    LAUNCH_CHECK();
+    return TSDS_OK;
+  };
   switch (algo) {
     case TSDS_MINMAX:
-    case TSDS_M4: {
-      const int width = algo == TSDS_MINMAX ? 2 : 4;
-      if (n_out < width || n_out % width) return set_err(TSDS_ERR_ARG, "invalid n_out");
-      if (n <= n_out) return identity(ctx, n, out, out_len);
-      RC_TRY(ensure(ctx, ctx->out, (size_t)(n_out + 1) * 8));
-      int64_t* d = (int64_t*)ctx->out.p;
-      RC_TRY(run_minmax_m4(ctx, algo, x, xdt, y, ydt, n, n_out, nan_mode, mem, d + 1, d));
-      return fetch_result(ctx, d, n_out, out, out_len);
-    }
+    case TSDS_M4:
+      if (n <= n_out) return identity_dev(n);
+      return run_minmax_m4(ctx, algo, x, xdt, y, ydt, n, n_out, nan_mode, mem, idx_out, cnt_out);
     case TSDS_LTTB:
-      if (n_out < 3) return set_err(TSDS_ERR_ARG, "n_out too small for LTTB");
-      if (n <= n_out) return identity(ctx, n, out, out_len);
-      return run_lttb(ctx, x, xdt, y, ydt, n, n_out, mem, out, out_len);
+      if (n <= n_out) return identity_dev(n);
+      return enqueue_lttb(ctx, x, xdt, y, ydt, n, n_out, mem, idx_out, cnt_out);
     case TSDS_MINMAXLTTB:
-      if (n_out < 3) return set_err(TSDS_ERR_ARG, "n_out too small for LTTB");
-      if (ratio < 1) return set_err(TSDS_ERR_ARG, "invalid ratio");
-      if (n <= n_out * ratio) {
-        if (n <= n_out) return identity(ctx, n, out, out_len);
-        return run_lttb(ctx, x, xdt, y, ydt, n, n_out, mem, out, out_len);
-      }
-      return run_minmaxlttb(ctx, x, xdt, y, ydt, n, n_out, ratio, nan_mode, mem, out, out_len);
+      if (n <= n_out) return identity_dev(n);
+      if (n <= n_out * ratio) return enqueue_lttb(ctx, x, xdt, y, ydt, n, n_out, mem, idx_out, cnt_out);
+      return enqueue_minmaxlttb(ctx, x, xdt, y, ydt, n, n_out, ratio, nan_mode, mem, idx_out, cnt_out);
     default:
       return set_err(TSDS_ERR_ARG, "unknown algorithm");
   }
 }
 
-int tsds_downsample_async(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y, int ydt, int64_t n,
-                          int64_t n_out, int nan_mode, int64_t* out_dev, int64_t* count_dev, int32_t* status_dev) {
-  if (!ctx || !y || !out_dev || !count_dev || n < 1 || !dtype_ok(ydt) || (x && !xdtype_ok(xdt)) ||
-      (algo != TSDS_MINMAX && algo != TSDS_M4))
-    return set_err(TSDS_ERR_ARG, "tsds_downsample_async: invalid argument");
-  const int width = algo == TSDS_MINMAX ? 2 : 4;
-  if (n_out < width || n_out % width) return set_err(TSDS_ERR_ARG, "invalid n_out");
+static int check_algo_args(int algo, int64_t n_out, int64_t ratio) {
+  switch (algo) {
+    case TSDS_MINMAX:
+    case TSDS_M4: {
+      const int width = algo == TSDS_MINMAX ? 2 : 4;
+      if (n_out < width || n_out % width) return set_err(TSDS_ERR_ARG, "invalid n_out");
+      return TSDS_OK;
+    }
+    case TSDS_LTTB:
+      if (n_out < 3) return set_err(TSDS_ERR_ARG, "n_out too small for LTTB");
+      return TSDS_OK;
+    case TSDS_MINMAXLTTB:
+      if (n_out < 3) return set_err(TSDS_ERR_ARG, "n_out too small for LTTB");
+      if (ratio < 1) return set_err(TSDS_ERR_ARG, "invalid ratio");
+      return TSDS_OK;
+    default:
+      return set_err(TSDS_ERR_ARG, "unknown algorithm");
+  }
+}
+
+int tsds_downsample(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y, int ydt, int64_t n, int64_t n_out,
+                    int64_t ratio, int nan_mode, int mem, int64_t* out, int64_t* out_len) {
+  if (!ctx || !y || !out || !out_len || n < 1 || !dtype_ok(ydt) || (x && !xdtype_ok(xdt)))
+    return set_err(TSDS_ERR_ARG, "tsds_downsample: invalid argument");
+  RC_TRY(check_algo_args(algo, n_out, ratio));
+  if (n <= n_out) {  // identity (algorithms.py:31-32), no device work
+    for (int64_t i = 0; i < n; i++) out[i] = i;
+    *out_len = n;
+    return TSDS_OK;
+  }
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard dg_(ctx->device);
   RC_TRY(begin_call(ctx));
-  if (n <= n_out) {
-    iota_kernel<<<(unsigned)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, ctx->stream>>>(out_dev, n, count_dev);
-    LAUNCH_CHECK();
-  } else {
-    RC_TRY(run_minmax_m4(ctx, algo, x, xdt, y, ydt, n, n_out, nan_mode, TSDS_MEM_DEVICE, out_dev, count_dev));
-  }
+  RC_TRY(ensure(ctx, ctx->out, (size_t)(n_out + 2) * 8));
+  int64_t* d = (int64_t*)ctx->out.p;
+  RC_TRY(enqueue_algo(ctx, algo, x, xdt, y, ydt, n, n_out, ratio, nan_mode, mem, d + 1, d));
+  return fetch_result(ctx, d, n_out, out, out_len);
+}
+
+int tsds_downsample_async(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y, int ydt, int64_t n,
+                          int64_t n_out, int64_t ratio, int nan_mode, int64_t* out_dev, int64_t* count_dev,
+                          int32_t* status_dev) {
+  if (!ctx || !y || !out_dev || !count_dev || n < 1 || !dtype_ok(ydt) || (x && !xdtype_ok(xdt)))
+    return set_err(TSDS_ERR_ARG, "tsds_downsample_async: invalid argument");
+  RC_TRY(check_algo_args(algo, n_out, ratio));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
+  RC_TRY(begin_call(ctx));
+  RC_TRY(enqueue_algo(ctx, algo, x, xdt, y, ydt, n, n_out, ratio, nan_mode, TSDS_MEM_DEVICE, out_dev, count_dev));
   if (status_dev) {
+    // the binning status of this call: exported by a resetting scan, or
+    // still in the flags (LTTB walks and stage-2 binning do not reset them)
     if (ctx->status_live)
       CUDA_TRY(cudaMemcpyAsync(status_dev, &misc(ctx)->status_copy, sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
     else
-      CUDA_TRY(cudaMemsetAsync(status_dev, 0, sizeof(int), ctx->stream));
+      CUDA_TRY(cudaMemcpyAsync(status_dev, &misc(ctx)->F.status, sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
   }
   return TSDS_OK;
 }
@@ -1193,7 +1263,7 @@ int tsds_lttb_stage2(tsds_ctx* ctx, const void* x2, int xdt, const void* y2, int
   RC_TRY(ensure(ctx, ctx->out, (size_t)(n_out + 2) * 8));
   int64_t* dout = (int64_t*)ctx->out.p;
   RC_TRY(run_lttb_walk(ctx, x2f, nullptr, ctx->y2.p, ydt, m, (const int64_t*)ctx->off.p, nb2,
-                       (const int64_t*)ctx->full.p, dout));
+                       (const int64_t*)ctx->full.p, dout + 1, dout));
   return fetch_result(ctx, dout, n_out, out, out_len);
 }
 
@@ -1410,7 +1480,7 @@ int tsds_op_lttb(tsds_ctx* ctx, const double* xf, const void* y, int ydt, int64_
   RC_TRY(begin_call(ctx));
   RC_TRY(ensure(ctx, ctx->out2, (size_t)(nb + 3) * 8));
   int64_t* d = (int64_t*)ctx->out2.p;
-  RC_TRY(run_lttb_walk(ctx, xf, nullptr, y, ydt, n, off, nb, nullptr, d));
+  RC_TRY(run_lttb_walk(ctx, xf, nullptr, y, ydt, n, off, nb, nullptr, d + 1, d));
   int64_t m = 0;
   CUDA_TRY(cudaMemcpyAsync(&m, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));

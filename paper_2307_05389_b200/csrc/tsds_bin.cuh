@@ -251,6 +251,14 @@ struct BinJob {
   int64_t n_uniform;  // blocks [0, n_uniform) check uniform spacing, the rest search edges
   int64_t* off;       // [nb+1]
   PipeFlags* F;
+  // device-sized inputs (MinMaxLTTB stage 2, no host round trip): when
+  // n_dev is set, n = *n_dev - n_sub and the whole launch is a no-op if
+  // *n_dev <= skip_le (the candidate set is returned as is); when
+  // force_count is set and *force_count == 0 (whole x uniform: dropped at
+  // the api level) the verdict is the equal-count formula.
+  const int64_t* n_dev;
+  int64_t n_sub, skip_le;
+  const int* force_count;
 };
 
 template <int XDT>
@@ -260,12 +268,21 @@ __global__ void binning_kernel(const BinJob J) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t n = J.n, nb = J.nb;
+  int64_t n = J.n;
+  const int64_t nb = J.nb;
+  if (J.n_dev) {
+    const int64_t m = *J.n_dev;
+    if (m <= J.skip_le) return;
+    n = m - J.n_sub;
+  }
+  const bool forced = J.force_count && *J.force_count == 0;
 
   // Blocks [0, n_uniform) run the uniform-spacing checks while the other
   // blocks search the edges speculatively (valid whenever the verdict turns
   // out to be "edges"); both roles proceed concurrently.
-  if ((int64_t)blockIdx.x < J.n_uniform) {
+  if (forced) {
+    // equal-count verdict known up front: nothing to check or search
+  } else if ((int64_t)blockIdx.x < J.n_uniform) {
     uniform_pieces<XDT>(J.x, n, &F->mis_slice, blockIdx.x, J.n_uniform);
     if (J.xapi) uniform_pieces<XDT>(J.xapi, J.napi, &F->mis_api, blockIdx.x, J.n_uniform);
   } else if (n > 0) {
@@ -306,7 +323,7 @@ __global__ void binning_kernel(const BinJob J) {
     const bool api_uniform = J.xapi && *(volatile int*)&F->mis_api == 0;
     const bool sl_uniform = *(volatile int*)&F->mis_slice == 0;
     int mode;  // 0 formula, 1 zeros, 2 zero span, 3 edges, 4 error
-    if (api_uniform || (J.uniform_first && sl_uniform)) {
+    if (forced || api_uniform || (J.uniform_first && sl_uniform)) {
       mode = 0;
     } else if (n == 0) {
       mode = 1;
@@ -328,7 +345,10 @@ __global__ void binning_kernel(const BinJob J) {
         unsigned __int128 p = (unsigned __int128)(uint64_t)k * (uint64_t)n;
         J.off[k] = (int64_t)(p / (uint64_t)nb) + J.add;
       }
-  } else if (mode == 1 || mode == 2) {
+  } else if (mode == 1 || mode == 2 || mode == 4) {
+    // mode 4 ("invalid index span"): empty bins, so consumers that are
+    // already enqueued (the LTTB walk) run over nothing; the status word
+    // reports the error to the caller
     for (int64_t k = threadIdx.x; k <= nb; k += blockDim.x)
       J.off[k] = (mode == 2 && k == nb ? n : 0) + J.add;
   } else if (mode == 3) {
@@ -344,8 +364,17 @@ __global__ void binning_kernel(const BinJob J) {
   }
 }
 
-// equal-count offsets (materialised; used by the operator-level C-ABI)
-__global__ inline void count_offsets_kernel(int64_t len, int64_t nb, int64_t add, int64_t* off) {
+// equal-count offsets (materialised; used by the operator-level C-ABI).
+// len_dev (nullable): device-sized length len = *len_dev - len_sub, no-op
+// when *len_dev <= skip_le (MinMaxLTTB stage 2 on the device).
+__global__ inline void count_offsets_kernel(int64_t len, int64_t nb, int64_t add, int64_t* off,
+                                            const int64_t* len_dev = nullptr, int64_t len_sub = 0,
+                                            int64_t skip_le = 0) {
+  if (len_dev) {
+    const int64_t m = *len_dev;
+    if (m <= skip_le) return;
+    len = m - len_sub;
+  }
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= nb; k += (int64_t)gridDim.x * blockDim.x) {
     unsigned __int128 p = (unsigned __int128)(uint64_t)k * (uint64_t)len;
     off[k] = (int64_t)(p / (uint64_t)nb) + add;

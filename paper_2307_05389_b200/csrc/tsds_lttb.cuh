@@ -120,11 +120,15 @@ __device__ __forceinline__ void lttb_centroid_phase(const double* xin, const int
     }
   }
 }
+// m_dev (nullable): MinMaxLTTB stage 2 on the device -- no-op when the
+// candidate count *m_dev <= skip_le (the candidates are the answer)
 template <int YDT>
 __global__ void lttb_centroid_kernel(const double* xin, const int* drop, const void* y,
-                                     const int64_t* off, int64_t nb, double2* cent) {
+                                     const int64_t* off, int64_t nb, double2* cent,
+                                     const int64_t* m_dev = nullptr, int64_t skip_le = 0) {
   pdl_launch_dependents();
   pdl_wait();
+  if (m_dev && *m_dev <= skip_le) return;
   lttb_centroid_phase<YDT>(xin, drop, y, off, nb, cent);
 }
 
@@ -180,7 +184,13 @@ template <int YDT>
 __global__ void __launch_bounds__(LTTB_THREADS)
 lttb_walk_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
                  const double2* cent, const int64_t* map, int64_t* out, int64_t* m_out,
-                 LttbScratch S, int64_t scratch_nodes, int jump_levels) {
+                 LttbScratch S, int64_t scratch_nodes, int jump_levels,
+                 const int64_t* n_dev = nullptr, int64_t skip_le = 0) {
+  if (n_dev) {  // device-sized series (MinMaxLTTB stage 2): n = candidate count
+    const int64_t m = *n_dev;
+    if (m <= skip_le) return;
+    n = m;
+  }
   const double* x = eff_x(xin, drop);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   __shared__ int64_t s_i64[32];
@@ -321,6 +331,49 @@ lttb_walk_kernel(const double* xin, const int* drop, const void* y, int64_t n, c
 }
 
 // ---- gathers / conversions used by the MinMaxLTTB stage 2
+
+// Stage-2 inputs without a host round trip (algorithms.py:243-254), from
+// the stage-1 output dfull = [m, full[0..m)]: y2 = y[full] and, with x,
+// x2 = x[full] (raw, for the stage-2 binning); x2f = float64(x2), or the
+// candidate positions themselves when there is no x or the api-level check
+// found x uniform (*api_nonuniform == 0: dropped, api.py:19-28).  No-op
+// when m <= n_out (stage2_finish_kernel returns `full`).
+template <int XDT>
+__global__ void stage2_inputs_kernel(const int64_t* dfull, int64_t n_out, const void* y, int yes, void* y2,
+                                     const void* x, void* x2, double* x2f, const int* api_nonuniform) {
+  const int64_t m = dfull[0];
+  if (m <= n_out) return;
+  const int64_t* full = dfull + 1;
+  const bool use_x = x && !(api_nonuniform && *api_nonuniform == 0);
+  using XT_ = typename YT<XDT < 0 ? DT_I64 : XDT>::T;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = __ldg(full + i);
+    switch (yes) {
+      case 1: ((uint8_t*)y2)[i] = ((const uint8_t*)y)[j]; break;
+      case 2: ((uint16_t*)y2)[i] = ((const uint16_t*)y)[j]; break;
+      case 4: ((uint32_t*)y2)[i] = ((const uint32_t*)y)[j]; break;
+      default: ((uint64_t*)y2)[i] = ((const uint64_t*)y)[j]; break;
+    }
+    if constexpr (XDT >= 0) {
+      if (x) {
+        const XT_ v = __ldg((const XT_*)x + j);
+        ((XT_*)x2)[i] = v;
+        x2f[i] = use_x ? ycv<XDT>(v) : (double)j;
+        continue;
+      }
+    }
+    x2f[i] = (double)j;
+  }
+}
+
+// m <= n_out: the candidates are the result (algorithms.py:241-242)
+__global__ void stage2_finish_kernel(const int64_t* dfull, int64_t n_out, int64_t* out, int64_t* count) {
+  const int64_t m = dfull[0];
+  if (m > n_out) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = dfull[1 + i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = m;
+}
 
 template <int DT>
 __global__ void gather_kernel(const void* src, const int64_t* idx, int64_t m, void* dst) {

@@ -103,7 +103,7 @@ def test_stale_status_is_not_reported(ts):
     out = torch.zeros(100, dtype=torch.int64, device="cuda")
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
-    rc = L.tsds_downsample_async(ctx.handle, 1, xbad.data_ptr(), 2, y.data_ptr(), 1, 10_000, 100, 0, out.data_ptr(),
+    rc = L.tsds_downsample_async(ctx.handle, 1, xbad.data_ptr(), 2, y.data_ptr(), 1, 10_000, 100, 4, 0, out.data_ptr(),
                                  cnt.data_ptr(), st.data_ptr())
     assert rc == 0
     ctx.synchronize()
@@ -112,7 +112,7 @@ def test_stale_status_is_not_reported(ts):
     # later valid calls without device binning
     assert ts.downsample("minmax", yh, n_out=100).shape[0] > 0
     assert ts.downsample("lttb", yh, n_out=100).shape[0] == 100
-    rc = L.tsds_downsample_async(ctx.handle, 1, None, 0, y.data_ptr(), 1, 10_000, 100, 0, out.data_ptr(),
+    rc = L.tsds_downsample_async(ctx.handle, 1, None, 0, y.data_ptr(), 1, 10_000, 100, 4, 0, out.data_ptr(),
                                  cnt.data_ptr(), st.data_ptr())
     assert rc == 0
     ctx.synchronize()
@@ -126,3 +126,58 @@ def test_calls_restore_callers_current_device(ts):
     y = W.random_series("f32", 50_000, 5)
     ts.downsample("minmax", y, n_out=100)
     assert torch.cuda.current_device() == 0
+
+
+def test_async_api_all_algorithms_equal_sync(ts, oracle):
+    """tsds_downsample_async (device pointers, no host round trip) for every
+    algorithm, including MinMaxLTTB's on-device stage 2 with and without x,
+    uniform x, m <= n_out (candidates returned) and a large ratio (host-sized
+    stage 2), against the oracle."""
+    import torch
+
+    from paper_2307_05389_b200 import _lib
+
+    L = _lib.load()
+    ctx = _lib.context(0)
+    rng = np.random.default_rng(5)
+    n = 300_000
+    y = np.cumsum(rng.standard_normal(n)).astype(np.float32)
+    xs = {
+        "none": None,
+        "exp": np.cumsum(rng.exponential(1.0, n)),
+        "gaps": np.cumsum(rng.integers(1, 4, n) * np.where(rng.random(n) < 0.001, 5000, 1)).astype(np.int64),
+        "uniform": np.arange(n, dtype=np.int64) * 5 + 3,
+    }
+    yd = torch.from_numpy(y).cuda()
+    algos = [("minmax", 1, 2000, 4), ("m4", 2, 2000, 4), ("lttb", 3, 1000, 4), ("minmaxlttb", 4, 1000, 4),
+             ("minmaxlttb", 4, 500, 60), ("minmaxlttb", 4, 5000, 40), ("minmaxlttb", 4, 200, 1)]
+    for xname, x in xs.items():
+        xd = None if x is None else torch.from_numpy(x).cuda()
+        for algo, code, n_out, ratio in algos:
+            out = torch.full((n_out,), -1, dtype=torch.int64, device="cuda")
+            cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+            st = torch.full((1,), 7, dtype=torch.int32, device="cuda")
+            rc = L.tsds_downsample_async(ctx.handle, code, None if xd is None else xd.data_ptr(),
+                                         0 if x is None else (2 if x.dtype == np.float64 else 6), yd.data_ptr(), 1, n,
+                                         n_out, ratio, 0, out.data_ptr(), cnt.data_ptr(), st.data_ptr())
+            _lib.check(rc, algo)
+            ctx.synchronize()
+            args = (y,) if x is None else (x, y)
+            want = oracle.downsample(algo, *args, n_out=n_out, minmax_ratio=ratio)
+            assert int(st.item()) == 0
+            m = int(cnt.item())
+            assert np.array_equal(out[:m].cpu().numpy(), want.astype(np.int64)), (xname, algo, n_out, ratio)
+
+
+def test_lttb_device_x_invalid_span_raises(ts):
+    import torch
+
+    y = torch.from_numpy(W.random_series("f64", 50_000, 8)).cuda()
+    x = np.cumsum(np.ones(50_000))
+    x[-2] = np.inf  # interior slice x[1:-1] ends at +inf
+    with pytest.raises(ValueError, match="invalid index span"):
+        ts.downsample("lttb", torch.from_numpy(x).cuda(), y, n_out=500)
+    with pytest.raises(ValueError, match="invalid index span"):
+        ts.downsample("minmaxlttb", torch.from_numpy(x).cuda(), y, n_out=500)
+    # the context stays usable
+    assert ts.downsample("lttb", y, n_out=500).shape[0] == 500
