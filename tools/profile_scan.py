@@ -41,7 +41,7 @@ def main():
         st = torch.zeros(1, dtype=torch.int32, device=dev)
         for _ in range(steps):
             rc = L.tsds_downsample_async(
-                ctx.handle, algo, None if xd is None else xd.data_ptr(), xdt, yd.data_ptr(), ydt, y.shape[0], n_out, 0,
+                ctx.handle, algo, None if xd is None else xd.data_ptr(), xdt, yd.data_ptr(), ydt, y.shape[0], n_out, 4, 0,
                 out.data_ptr(), cnt.data_ptr(), st.data_ptr(),
             )
             _lib.check(rc)

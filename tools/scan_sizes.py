@@ -30,7 +30,7 @@ def main():
         y = torch.from_numpy(np.random.default_rng(0).standard_normal(n).astype(np.float32)).cuda()
 
         def step():
-            _lib.check(L.tsds_downsample_async(ctx.handle, 1, None, 0, y.data_ptr(), 1, n, 2000, 0,
+            _lib.check(L.tsds_downsample_async(ctx.handle, 1, None, 0, y.data_ptr(), 1, n, 2000, 4, 0,
                                                out.data_ptr(), cnt.data_ptr(), sts.data_ptr()))
 
         for _ in range(5):
