@@ -111,23 +111,62 @@ int tsds_downsample_async(tsds_ctx *ctx, int algo, const void *x, int x_dtype, c
                           int64_t n, int64_t n_out, int64_t minmax_ratio, int nan_mode, int64_t *out_dev,
                           int64_t *count_dev, int32_t *status_dev);
 
-/* One shard of a sharded MinMax / M4 (multi-GPU): the bins
- * [b0, b1) of a larger series, i.e. _run_bins' per-thread bin chunk
- * (algorithms.py:88-98) on one device.  y_dev holds the shard's elements;
- * off_dev[0..n_bins] are the shard's bin offsets relative to y_dev;
- * idx_base is added to every emitted index (the shard's global start).
- * out_dev: int64[width*n_bins] (compacted, ascending), count_dev: int64. */
-int tsds_downsample_bins_async(tsds_ctx *ctx, int algo, const void *y_dev, int y_dtype, const int64_t *off_dev,
-                               int64_t n_bins, int64_t idx_base, int nan_mode, int64_t *out_dev,
-                               int64_t *count_dev);
+/* ---------------------------------------------------------------------------
+ * Sharded path (multi-GPU).  The reference's only parallel
+ * strategy hands contiguous bin chunks to workers and concatenates their
+ * outputs in bin order (_run_bins, algorithms.py:82-100); here the workers
+ * are ranks, one GPU each, every rank holding only its shard of y (and of x)
+ * in HBM.  Each rank writes one fixed-size RECORD
+ *     rec[0] = count, rec[1 + f*cap + i] = field f of entry i (i < count)
+ * the records are all-gathered (tsds_comm_allgather) and concatenated in
+ * rank order (tsds_records_concat) -- bin order, hence bit-identical to the
+ * single-GPU result.  All calls are asynchronous on ctx's stream.
+ * ------------------------------------------------------------------------ */
 
-/* MinMaxLTTB stage 2 (algorithms.py:235-255) on gathered candidates, for
- * the sharded path: full[0..m) are the candidate positions ([0] + per-bin
- * picks + [n-1]), y2 = y[full] and x2 = x[full] (x2 NULL when the series
- * has no x: positions stand in for x and the bins are equal-count).  Host
- * pointers; out int64[n_out] receives original indices. */
-int tsds_lttb_stage2(tsds_ctx *ctx, const void *x2, int x_dtype, const void *y2, int y_dtype, const int64_t *full,
-                     int64_t m, int64_t n_out, int64_t *out, int64_t *out_len);
+/* MinMax / M4 over bins [0, n_bins) of a shard: y_dev holds the shard,
+ * off_dev[0..n_bins] its bin offsets relative to y_dev, [span_begin,
+ * span_end) the element span they cover, monotone = offsets non-decreasing
+ * (else bins are reduced independently); idx_base is added to every index.
+ * rec_dev: record with one field, cap = width*n_bins. */
+int tsds_shard_bins_async(tsds_ctx *ctx, int algo, const void *y_dev, int y_dtype, const int64_t *off_dev,
+                          int64_t n_bins, int64_t idx_base, int64_t span_begin, int64_t span_end, int monotone,
+                          int nan_mode, int64_t *rec_dev);
+
+/* MinMaxLTTB preselection of a shard (algorithms.py:226-240): the MinMax
+ * picks of its sub-bins plus the frame points it owns (frame_first = 0 on
+ * the first rank, frame_last = n-1 on the last, else -1), each with the raw
+ * bits of its x (x_dev NULL: 0) and y value -- three fields (global index,
+ * x bits, y bits), cap >= 2*n_bins + 2. */
+int tsds_shard_preselect_async(tsds_ctx *ctx, const void *y_dev, int y_dtype, const void *x_dev, int x_dtype,
+                               const int64_t *off_dev, int64_t n_bins, int64_t idx_base, int64_t span_begin,
+                               int64_t span_end, int monotone, int nan_mode, int64_t frame_first, int64_t frame_last,
+                               int64_t cap, int64_t *rec_dev);
+
+/* Concatenate nranks records (back to back, stride 1 + nfields*cap; nranks
+ * <= 256) in rank order: field f -> out_dev + f*ld_out, total -> *count_dev. */
+int tsds_records_concat(tsds_ctx *ctx, const int64_t *recv_dev, int nranks, int64_t cap, int nfields,
+                        int64_t *out_dev, int64_t ld_out, int64_t *count_dev);
+
+/* MinMaxLTTB stage 2 (algorithms.py:241-255) on gathered candidates, on the
+ * device: cand_dev = [m, full[0..cap)] (full = global indices incl. the
+ * frame points, ascending), xbits_dev / ybits_dev their raw x / y bits
+ * (xbits NULL: no x or x dropped as uniform -- positions stand in, bins are
+ * equal-count).  m <= n_out returns full.  out_dev int64[n_out]. */
+int tsds_lttb_stage2_async(tsds_ctx *ctx, int64_t *cand_dev, int64_t cap, const int64_t *xbits_dev, int x_dtype,
+                           const int64_t *ybits_dev, int y_dtype, int64_t n_out, int64_t *out_dev,
+                           int64_t *count_dev);
+
+/* Communicator: NCCL, loaded at run time (libtsds
+ * does not link it), bound to ctx's device and stream.  Rank 0 makes the
+ * 128-byte id, the caller distributes it out of band (e.g. over
+ * torch.distributed), every rank calls tsds_comm_init with it. */
+typedef struct tsds_comm tsds_comm;
+#define TSDS_COMM_ID_BYTES 128
+int tsds_comm_unique_id(void *id);
+int tsds_comm_init(tsds_ctx *ctx, int nranks, int rank, const void *id, tsds_comm **out);
+void tsds_comm_destroy(tsds_comm *comm);
+/* ncclAllGather of `bytes` per rank: recv_dev[r*bytes ...] = rank r's send_dev */
+int tsds_comm_allgather(tsds_comm *comm, const void *send_dev, void *recv_dev, int64_t bytes);
 
 /* Batched MinMax (extension; the reference has no batch API):
  * row s of y[n_series][len] gives out[s*n_out ...] and counts[s]; row s

@@ -40,8 +40,14 @@ EXPORTED = (
     "tsds_ctx_profile_read",
     "tsds_downsample",
     "tsds_downsample_async",
-    "tsds_downsample_bins_async",
-    "tsds_lttb_stage2",
+    "tsds_shard_bins_async",
+    "tsds_shard_preselect_async",
+    "tsds_records_concat",
+    "tsds_lttb_stage2_async",
+    "tsds_comm_unique_id",
+    "tsds_comm_init",
+    "tsds_comm_destroy",
+    "tsds_comm_allgather",
     "tsds_minmax_batched",
     "tsds_minmax_batched_async",
     "tsds_argminmax",
@@ -101,8 +107,16 @@ def load():
         L.tsds_ctx_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), p64]
         L.tsds_downsample.argtypes = [vp, i32, vp, i32, vp, i32, i64, i64, i64, i32, i32, vp, p64]
         L.tsds_downsample_async.argtypes = [vp, i32, vp, i32, vp, i32, i64, i64, i64, i32, vp, vp, vp]
-        L.tsds_downsample_bins_async.argtypes = [vp, i32, vp, i32, vp, i64, i64, i32, vp, vp]
-        L.tsds_lttb_stage2.argtypes = [vp, vp, i32, vp, i32, vp, i64, i64, vp, p64]
+        L.tsds_shard_bins_async.argtypes = [vp, i32, vp, i32, vp, i64, i64, i64, i64, i32, i32, vp]
+        L.tsds_shard_preselect_async.argtypes = [vp, vp, i32, vp, i32, vp, i64, i64, i64, i64, i32, i32, i64, i64, i64,
+                                                 vp]
+        L.tsds_records_concat.argtypes = [vp, vp, i32, i64, i32, vp, i64, vp]
+        L.tsds_lttb_stage2_async.argtypes = [vp, vp, i64, vp, i32, vp, i32, i64, vp, vp]
+        L.tsds_comm_unique_id.argtypes = [vp]
+        L.tsds_comm_init.argtypes = [vp, i32, i32, vp, ctypes.POINTER(vp)]
+        L.tsds_comm_destroy.argtypes = [vp]
+        L.tsds_comm_destroy.restype = None
+        L.tsds_comm_allgather.argtypes = [vp, vp, vp, i64]
         L.tsds_minmax_batched.argtypes =[vp, vp, i32, i64, i64, i64, i32, i32, vp, vp]
         L.tsds_minmax_batched_async.argtypes = [vp, vp, i32, i64, i64, i64, i32, vp, vp]
         L.tsds_argminmax.argtypes = [vp, vp, i32, i64, i32, i32, vp]

@@ -22,6 +22,8 @@
 #include "tsds_lttb_large.cuh"
 #include "tsds_scan.cuh"
 #include "tsds_lanebins.cuh"
+#include "tsds_nccl.h"
+#include "tsds_shard.cuh"
 
 using namespace tsds;
 
@@ -831,6 +833,41 @@ int interior_bins(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int64_t nb, 
   return TSDS_OK;
 }
 
+// MinMaxLTTB stage 2 is sized on the device when its buckets are small on
+// average (the single-CTA walk's jump tables): minmax_ratio up to ~30
+bool stage2_on_device(int64_t fcap, int64_t n_out) {
+  return (fcap - 2) / std::max<int64_t>(n_out - 2, 1) <= SMALL_MAX / 2 && fcap <= ((int64_t)1 << 24);
+}
+
+// MinMaxLTTB stage 2 (algorithms.py:243-255) on the device from dfull =
+// [m, full[0..m)] and the candidates' values y2 (ydt) / x2 (xdt, or NULL:
+// positions) already gathered, x2f = float64 x of every candidate.  m is
+// read by the kernels (m <= n_out: `full` is the result); api_nonuniform
+// (nullable) == 0 means the whole x was uniform, so the bins are the
+// equal-count formula.  No host round trip.
+int enqueue_stage2_dev(tsds_ctx* ctx, int64_t* dfull, int64_t fcap, const void* y2, int ydt, const void* x2, int xdt,
+                       const double* x2f, const int* api_nonuniform, int64_t n_out, int64_t* idx_out,
+                       int64_t* cnt_out) {
+  const int64_t nb2 = n_out - 2;
+  RC_TRY(ensure(ctx, ctx->off, (size_t)(nb2 + 1) * 8));
+  int64_t* off2 = (int64_t*)ctx->off.p;
+  if (x2) {
+    // equal-width bins over x2[1:m-1] (algorithms.py:246-250), or the
+    // equal-count formula when the whole x was found uniform
+    const int es_x = dtype_size(xdt);
+    RC_TRY(launch_binning(ctx, xdt, (const char*)x2 + es_x, fcap - 2, nb2, 1, nullptr, 0, 0, 1, off2, dfull, 2,
+                          n_out, api_nonuniform));
+  } else {
+    const unsigned gc = cap_grid((nb2 + 256) / 256, (int64_t)ctx->sms * 4);
+    count_offsets_kernel<<<gc, 256, 0, ctx->stream>>>(0, nb2, 1, off2, dfull, 2, n_out);
+    LAUNCH_CHECK();
+  }
+  RC_TRY(run_lttb_walk_small(ctx, x2f, nullptr, y2, ydt, fcap, off2, nb2, dfull + 1, idx_out, cnt_out, dfull, n_out));
+  stage2_finish_kernel<<<cap_grid((fcap + 255) / 256, 64), 256, 0, ctx->stream>>>(dfull, n_out, idx_out, cnt_out);
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
 // LTTB (algorithms.py:184-208) enqueued into (idx_out, cnt_out) on the
 // device.  No host round trip: a failed device binning (non-finite span)
 // leaves empty bins behind, so the walk runs over nothing and the status
@@ -898,11 +935,8 @@ int enqueue_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int
   const int64_t* full = dfull + 1;
   const int64_t nb2 = n_out - 2;
   const int es_y = dtype_size(ydt);
-  RC_TRY(ensure(ctx, ctx->off, (size_t)(nb2 + 1) * 8));
-  int64_t* off2 = (int64_t*)ctx->off.p;
 
-  const bool device_stage2 = (mem == TSDS_MEM_DEVICE || !xk) && (fcap - 2) / std::max<int64_t>(nb2, 1) <= SMALL_MAX / 2 &&
-                             fcap <= ((int64_t)1 << 24);
+  const bool device_stage2 = (mem == TSDS_MEM_DEVICE || !xk) && stage2_on_device(fcap, n_out);
   if (device_stage2) {
     RC_TRY(ensure(ctx, ctx->y2, (size_t)fcap * es_y));
     RC_TRY(ensure(ctx, ctx->x2f64, (size_t)fcap * 8));
@@ -919,21 +953,8 @@ int enqueue_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int
                                                             nullptr);
     }
     LAUNCH_CHECK();
-    if (xk) {
-      // equal-width bins over x2[1:m-1] (algorithms.py:246-250), or the
-      // equal-count formula when the whole x was found uniform
-      RC_TRY(launch_binning(ctx, xdt, (const char*)ctx->x2.p + es_x, fcap - 2, nb2, 1, nullptr, 0, 0, 1, off2, dfull,
-                            2, n_out, api_nonuniform));
-    } else {
-      const unsigned gc = cap_grid((nb2 + 256) / 256, (int64_t)ctx->sms * 4);
-      count_offsets_kernel<<<gc, 256, 0, ctx->stream>>>(0, nb2, 1, off2, dfull, 2, n_out);
-      LAUNCH_CHECK();
-    }
-    RC_TRY(run_lttb_walk_small(ctx, x2f, nullptr, ctx->y2.p, ydt, fcap, off2, nb2, full, idx_out, cnt_out, dfull,
-                               n_out));
-    stage2_finish_kernel<<<cap_grid((fcap + 255) / 256, 64), 256, 0, ctx->stream>>>(dfull, n_out, idx_out, cnt_out);
-    LAUNCH_CHECK();
-    return TSDS_OK;
+    return enqueue_stage2_dev(ctx, dfull, fcap, ctx->y2.p, ydt, xk ? ctx->x2.p : nullptr, xdt, x2f, api_nonuniform,
+                              n_out, idx_out, cnt_out);
   }
 
   // stage boundary on the host: the candidate count decides stage 2
@@ -957,6 +978,8 @@ int enqueue_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int
     CUDA_TRY(cudaMemcpyAsync(cnt_out, dfull, 8, cudaMemcpyDeviceToDevice, ctx->stream));
     return TSDS_OK;
   }
+  RC_TRY(ensure(ctx, ctx->off, (size_t)(nb2 + 1) * 8));
+  int64_t* off2 = (int64_t*)ctx->off.p;
   RC_TRY(gather(ctx, dy, ydt, full, m, ctx->y2));
   const double* x2f = nullptr;
   if (!xk) {
@@ -1229,71 +1252,151 @@ int tsds_downsample_async(tsds_ctx* ctx, int algo, const void* x, int xdt, const
   return TSDS_OK;
 }
 
-int tsds_lttb_stage2(tsds_ctx* ctx, const void* x2, int xdt, const void* y2, int ydt, const int64_t* full, int64_t m,
-                     int64_t n_out, int64_t* out, int64_t* out_len) {
-  if (!ctx || !y2 || !full || !out || !out_len || m < 2 || n_out < 3 || !dtype_ok(ydt) || (x2 && !xdtype_ok(xdt)))
-    return set_err(TSDS_ERR_ARG, "tsds_lttb_stage2: invalid argument");
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  DeviceGuard dg_(ctx->device);
-  if (m <= n_out) {
-    memcpy(out, full, (size_t)m * 8);
-    *out_len = m;
-    return TSDS_OK;
-  }
-  RC_TRY(begin_call(ctx));
-  const int64_t nb2 = n_out - 2;
-  std::vector<int64_t> o2(nb2 + 1);
-  if (!x2) {
-    for (int64_t k = 0; k <= nb2; k++) o2[k] = (int64_t)((unsigned __int128)k * (uint64_t)(m - 2) / (uint64_t)nb2) + 1;
-  } else {
-    int rc = tsds_host_equal_width_offsets((const char*)x2 + dtype_size(xdt), xdt, m - 2, nb2, o2.data());
-    if (rc == TSDS_ERR_SPAN) return set_err(rc, "invalid index span");
-    for (auto& v : o2) v += 1;
-  }
-  RC_TRY(upload(ctx, ctx->off, o2.data(), o2.size() * 8));
-  RC_TRY(upload(ctx, ctx->full, full, (size_t)m * 8));
-  RC_TRY(upload(ctx, ctx->y2, y2, (size_t)m * dtype_size(ydt)));
-  const double* x2f = nullptr;
-  if (!x2) {
-    RC_TRY(to_f64(ctx, ctx->full.p, DT_I64, m, ctx->x2f64, &x2f));
-  } else {
-    RC_TRY(upload(ctx, ctx->x2, x2, (size_t)m * dtype_size(xdt)));
-    RC_TRY(to_f64(ctx, ctx->x2.p, xdt, m, ctx->x2f64, &x2f));
-  }
-  RC_TRY(ensure(ctx, ctx->out, (size_t)(n_out + 2) * 8));
-  int64_t* dout = (int64_t*)ctx->out.p;
-  RC_TRY(run_lttb_walk(ctx, x2f, nullptr, ctx->y2.p, ydt, m, (const int64_t*)ctx->off.p, nb2,
-                       (const int64_t*)ctx->full.p, dout + 1, dout));
-  return fetch_result(ctx, dout, n_out, out, out_len);
-}
+// ------------------------------------------------------------------ sharding
 
-int tsds_downsample_bins_async(tsds_ctx* ctx, int algo, const void* y, int ydt, const int64_t* off, int64_t nb,
-                               int64_t idx_base, int nan_mode, int64_t* out_dev, int64_t* count_dev) {
-  if (!ctx || !y || !off || !out_dev || !count_dev || nb < 1 || !dtype_ok(ydt) ||
+int tsds_shard_bins_async(tsds_ctx* ctx, int algo, const void* y, int ydt, const int64_t* off, int64_t nb,
+                          int64_t idx_base, int64_t span_begin, int64_t span_end, int monotone, int nan_mode,
+                          int64_t* rec_dev) {
+  if (!ctx || !y || !off || !rec_dev || nb < 1 || !dtype_ok(ydt) || span_end < span_begin ||
       (algo != TSDS_MINMAX && algo != TSDS_M4))
-    return set_err(TSDS_ERR_ARG, "tsds_downsample_bins_async: invalid argument");
+    return set_err(TSDS_ERR_ARG, "tsds_shard_bins_async: invalid argument");
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard dg_(ctx->device);
   RC_TRY(begin_call(ctx));
-  // the shard's offsets (relative to y_dev) come back to the host once: the
-  // span, and whether they are monotone (x that violates its documented
-  // order gives overlapping bins, reduced independently like op_bins)
-  std::vector<int64_t> h(nb + 1);
-  CUDA_TRY(cudaMemcpyAsync(h.data(), off, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  const bool mono = host_monotone(h);
-  int64_t lo = h.front(), hi = h.back();
-  for (int64_t v : h) {
-    lo = std::min(lo, v);
-    hi = std::max(hi, v);
-  }
-  ScanArgs A = scan_args(y, BinSpec{1, off, 0, 0, 0}, 0, nb, mono ? h.front() : lo, mono ? h.back() : hi);
-  A.independent = !mono;
+  ScanArgs A = scan_args(y, BinSpec{1, off, 0, 0, 0}, 0, nb, span_begin, span_end);
+  A.independent = monotone ? 0 : 1;
   A.epi = algo == TSDS_MINMAX ? EPI_MINMAX : EPI_M4;
-  A.out = out_dev;
-  A.out_count = count_dev;
+  A.out = rec_dev + 1;
+  A.out_count = rec_dev;
   A.idx_sub = -idx_base;
   return launch_scan(ctx, ydt, nan_mode, A);
+}
+
+int tsds_shard_preselect_async(tsds_ctx* ctx, const void* y, int ydt, const void* x, int xdt, const int64_t* off,
+                               int64_t nb, int64_t idx_base, int64_t span_begin, int64_t span_end, int monotone,
+                               int nan_mode, int64_t frame_first, int64_t frame_last, int64_t cap, int64_t* rec_dev) {
+  if (!ctx || !y || !off || !rec_dev || nb < 0 || !dtype_ok(ydt) || (x && !xdtype_ok(xdt)) ||
+      span_end < span_begin || cap < 2 * nb + 2)
+    return set_err(TSDS_ERR_ARG, "tsds_shard_preselect_async: invalid argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
+  RC_TRY(begin_call(ctx));
+  RC_TRY(ensure(ctx, ctx->full, (size_t)(2 * nb + 2) * 8));
+  int64_t* tmp = (int64_t*)ctx->full.p;  // [c, global indices...]
+  if (nb > 0) {
+    ScanArgs A = scan_args(y, BinSpec{1, off, 0, 0, 0}, 0, nb, span_begin, span_end);
+    A.independent = monotone ? 0 : 1;
+    A.epi = EPI_MINMAX;
+    A.out = tmp + 1;
+    A.out_count = tmp;
+    A.idx_sub = -idx_base;
+    RC_TRY(launch_scan(ctx, ydt, nan_mode, A));
+  } else {
+    CUDA_TRY(cudaMemsetAsync(tmp, 0, 8, ctx->stream));
+  }
+  const unsigned g = cap_grid((2 * nb + 2 + 255) / 256, (int64_t)ctx->sms * 4);
+  preselect_pack_kernel<<<g, 256, 0, ctx->stream>>>(tmp, cap, y, dtype_size(ydt), x, x ? dtype_size(xdt) : 8,
+                                                     idx_base, frame_first, frame_last, rec_dev);
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
+int tsds_records_concat(tsds_ctx* ctx, const int64_t* recv_dev, int nranks, int64_t cap, int nfields,
+                        int64_t* out_dev, int64_t ld_out, int64_t* count_dev) {
+  if (!ctx || !recv_dev || !out_dev || !count_dev || nranks < 1 || nranks > 256 || cap < 0 || nfields < 1 ||
+      (nfields > 1 && ld_out < (int64_t)nranks * cap))
+    return set_err(TSDS_ERR_ARG, "tsds_records_concat: invalid argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
+  const unsigned g = cap_grid(((int64_t)nranks * cap + 255) / 256, (int64_t)ctx->sms * 4);
+  records_concat_kernel<<<g, 256, 0, ctx->stream>>>(recv_dev, nranks, cap, nfields, out_dev, ld_out, count_dev);
+  LAUNCH_CHECK();
+  return TSDS_OK;
+}
+
+int tsds_lttb_stage2_async(tsds_ctx* ctx, int64_t* cand_dev, int64_t cap, const int64_t* xbits_dev, int xdt,
+                           const int64_t* ybits_dev, int ydt, int64_t n_out, int64_t* out_dev, int64_t* count_dev) {
+  if (!ctx || !cand_dev || !ybits_dev || !out_dev || !count_dev || cap < 2 || n_out < 3 || !dtype_ok(ydt) ||
+      (xbits_dev && !xdtype_ok(xdt)))
+    return set_err(TSDS_ERR_ARG, "tsds_lttb_stage2_async: invalid argument");
+  if (!stage2_on_device(cap, n_out))
+    return set_err(TSDS_ERR_ARG, "tsds_lttb_stage2_async: candidate buckets too large for the device walk");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
+  RC_TRY(begin_call(ctx));
+  const int yes = dtype_size(ydt);
+  RC_TRY(ensure(ctx, ctx->y2, (size_t)cap * yes));
+  RC_TRY(ensure(ctx, ctx->x2f64, (size_t)cap * 8));
+  if (xbits_dev) RC_TRY(ensure(ctx, ctx->x2, (size_t)cap * dtype_size(xdt)));
+  double* x2f = (double*)ctx->x2f64.p;
+  const unsigned g = cap_grid((cap + 255) / 256, (int64_t)ctx->sms * 8);
+  if (xbits_dev) {
+    XDT_SWITCH(xdt, (stage2_unpack_kernel<XD><<<g, 256, 0, ctx->stream>>>(cand_dev, n_out, xbits_dev, ybits_dev, yes,
+                                                                           ctx->y2.p, ctx->x2.p, x2f)));
+  } else {
+    stage2_unpack_kernel<-1><<<g, 256, 0, ctx->stream>>>(cand_dev, n_out, nullptr, ybits_dev, yes, ctx->y2.p, nullptr,
+                                                          x2f);
+  }
+  LAUNCH_CHECK();
+  return enqueue_stage2_dev(ctx, cand_dev, cap, ctx->y2.p, ydt, xbits_dev ? ctx->x2.p : nullptr, xdt, x2f, nullptr,
+                            n_out, out_dev, count_dev);
+}
+
+// communicator: NCCL (bound at run time, tsds_nccl.cpp) on ctx's device and stream
+struct tsds_comm {
+  tsds_ctx* ctx = nullptr;
+  ncclComm_t comm = nullptr;
+  int nranks = 0, rank = 0;
+};
+
+int tsds_comm_unique_id(void* id) {
+  if (!id) return set_err(TSDS_ERR_ARG, "tsds_comm_unique_id: NULL");
+  std::string err;
+  if (!tsds_nccl::available(&err)) return set_err(TSDS_ERR_CUDA, err);
+  ncclUniqueId u;
+  ncclResult_t r = tsds_nccl::get_unique_id(&u);
+  if (r != ncclSuccess) return set_err(TSDS_ERR_CUDA, "ncclGetUniqueId: " + tsds_nccl::error_string(r));
+  memcpy(id, &u, sizeof(u));
+  return TSDS_OK;
+}
+
+int tsds_comm_init(tsds_ctx* ctx, int nranks, int rank, const void* id, tsds_comm** out) {
+  if (!ctx || !id || !out || nranks < 1 || rank < 0 || rank >= nranks)
+    return set_err(TSDS_ERR_ARG, "tsds_comm_init: invalid argument");
+  *out = nullptr;
+  std::string err;
+  if (!tsds_nccl::available(&err)) return set_err(TSDS_ERR_CUDA, err);
+  DeviceGuard dg_(ctx->device);
+  ncclUniqueId u;
+  memcpy(&u, id, sizeof(u));
+  tsds_comm* c = new tsds_comm();
+  c->ctx = ctx;
+  c->nranks = nranks;
+  c->rank = rank;
+  ncclResult_t r = tsds_nccl::comm_init_rank(&c->comm, nranks, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return set_err(TSDS_ERR_CUDA, "ncclCommInitRank: " + tsds_nccl::error_string(r));
+  }
+  *out = c;
+  return TSDS_OK;
+}
+
+void tsds_comm_destroy(tsds_comm* c) {
+  if (!c) return;
+  DeviceGuard dg_(c->ctx->device);
+  if (c->comm) tsds_nccl::comm_destroy(c->comm);
+  delete c;
+}
+
+int tsds_comm_allgather(tsds_comm* c, const void* send_dev, void* recv_dev, int64_t bytes) {
+  if (!c || !send_dev || !recv_dev || bytes < 0) return set_err(TSDS_ERR_ARG, "tsds_comm_allgather: invalid argument");
+  tsds_ctx* ctx = c->ctx;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
+  ncclResult_t r = tsds_nccl::all_gather_bytes(send_dev, recv_dev, (size_t)bytes, c->comm, ctx->stream);
+  if (r != ncclSuccess) return set_err(TSDS_ERR_CUDA, "ncclAllGather: " + tsds_nccl::error_string(r));
+  return TSDS_OK;
 }
 
 static int batched_enqueue(tsds_ctx* ctx, const void* dy, int ydt, int64_t S, int64_t L, int64_t n_out, int nan_mode,
