@@ -24,6 +24,7 @@
 #include "tsds_lanebins.cuh"
 #include "tsds_nccl.h"
 #include "tsds_shard.cuh"
+#include "tsds_staging.h"
 
 using namespace tsds;
 
@@ -73,6 +74,7 @@ struct tsds_ctx {
   bool lstat_pending = false;
   void* h_pin = nullptr;
   size_t h_cap = 0;
+  StagingRing ring;  // pageable host inputs (tsds_staging.h)
   bool dirty = false;
   bool flags_clean = false;  // Misc flags known to be zero on the device
   bool status_live = false;  // a scan of the current call exports Misc.status_copy
@@ -445,8 +447,15 @@ bool host_monotone(const std::vector<int64_t>& off) {
   return true;
 }
 
+// host -> device copy of a host array into a context buffer: pinned or small
+// inputs are DMA'd directly, large pageable ones through the staging ring
 int upload(tsds_ctx* ctx, DevBuf& b, const void* h, size_t bytes) {
   RC_TRY(ensure(ctx, b, bytes));
+  constexpr size_t kStageMin = 8u << 20;
+  if (bytes >= kStageMin && !host_is_pinned(h)) {
+    CUDA_TRY(ctx->ring.upload(b.p, h, bytes, ctx->stream));
+    return TSDS_OK;
+  }
   CUDA_TRY(cudaMemcpyAsync(b.p, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
   return TSDS_OK;
 }
@@ -1082,6 +1091,7 @@ void tsds_ctx_destroy(tsds_ctx* ctx) {
     if (b->p) cudaFree(b->p);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
   if (ctx->h_lstat) cudaFreeHost(ctx->h_lstat);
+  ctx->ring.release();
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
