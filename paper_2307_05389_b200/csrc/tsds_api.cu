@@ -5,7 +5,8 @@
 //   [x on device]  binning_kernel (uniform checks + exact edge searches) -PDL-> scan
 //   [x on host]    tsds_host_* binning (only y crosses PCIe)
 //   scan_kernel (fused argminmax + segmented merge + compaction)
-//   LTTB: lttb_centroid_kernel -> lttb_walk_kernel (single CTA)
+//   LTTB: small buckets lttb_next_kernel -> lttb_path_kernel; large buckets
+//         the summary / guess / verify chain of tsds_lttb_large.cuh
 // Everything is enqueued on the context's stream; host syncs happen only to
 // return variable-length results (and once between MinMaxLTTB's stages).
 #include <algorithm>
@@ -50,7 +51,8 @@ struct Misc {
   PipeFlags F;         // binning/scan flags (zero between pipelines)
   int status_copy;     // status exported by the resetting scan (valid when ctx->status_live)
   int mis_api_copy;    // its api-level "x is not uniform" verdict (MinMaxLTTB stage 2)
-  int pad[14];
+  int lttb_maxb;       // largest bucket of the small-bucket walk (reset by lttb_path_kernel)
+  int pad[13];
   int64_t count;
   int64_t m2;
   int64_t pair[2];
@@ -752,30 +754,36 @@ int run_lttb_walk(tsds_ctx* ctx, const double* xf, const int* drop, const void* 
 int run_lttb_walk_small(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
                         const int64_t* off, int64_t nb, const int64_t* map, int64_t* idx_out, int64_t* cnt_out,
                         const int64_t* n_dev, int64_t skip_le) {
-  RC_TRY(ensure(ctx, ctx->cent, (size_t)std::max<int64_t>(nb, 1) * sizeof(double2)));
-  double2* cent = (double2*)ctx->cent.p;
-  unsigned gc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 16, (nb + 7) / 8));
-  YDT_SWITCH(ydt, (lttb_centroid_kernel<YD><<<gc, 256, 0, ctx->stream>>>(xf, drop, y, off, nb, cent, n_dev, skip_le)));
-  LAUNCH_CHECK();
-  // scratch for the small-bucket (jump) strategy when buckets are small on average
+  // scratch: next() of every point (level 0), lifting levels for the global fallback
   LttbScratch S{nullptr, nullptr, nullptr};
   int levels = 1;
   while (((int64_t)1 << levels) <= nb + 1) levels++;
   int64_t nodes_cap = 0;
   const int64_t avg = (n - 2) / std::max<int64_t>(nb, 1);
-  if (avg <= SMALL_MAX / 2 && n <= ((int64_t)1 << 24)) {
-    size_t bytes = (size_t)(nb + 1) * 4 + (size_t)n * 4 + (size_t)levels * n * 4 + 64;
-    RC_TRY(ensure(ctx, ctx->scratch, bytes));
-    char* p = (char*)ctx->scratch.p;
-    S.firstne = (int32_t*)p;
-    p += ((nb + 1) * 4 + 15) & ~15;
-    S.bk = (int32_t*)p;
-    p += (n * 4 + 15) & ~15;
-    S.jump = (int32_t*)p;
+  if (n > ((int64_t)1 << 30)) return set_err(TSDS_ERR_ARG, "small-bucket LTTB: series too long");
+  const bool lift_ok = avg <= SMALL_MAX / 2 && n <= ((int64_t)1 << 24);
+  size_t bytes = (size_t)n * 4 + 64 + (lift_ok ? (size_t)levels * n * 4 : 0);
+  RC_TRY(ensure(ctx, ctx->scratch, bytes));
+  int32_t* jump0 = (int32_t*)ctx->scratch.p;
+  if (lift_ok) {
+    S.jump = jump0 + ((n + 15) & ~(int64_t)15);
     nodes_cap = n;
   }
-  YDT_SWITCH(ydt, (lttb_walk_kernel<YD><<<1, LTTB_THREADS, 0, ctx->stream>>>(
-                      xf, drop, y, n, off, nb, cent, map, idx_out, cnt_out, S, nodes_cap, levels, n_dev, skip_le)));
+  int* maxb = &misc(ctx)->lttb_maxb;
+  const unsigned gn = cap_grid((nb + 1 + 7) / 8, (int64_t)ctx->sms * 16);
+  YDT_SWITCH(ydt, (lttb_next_kernel<YD><<<gn, 256, 0, ctx->stream>>>(xf, drop, y, n, off, nb, jump0, maxb, n_dev,
+                                                                      skip_le)));
+  LAUNCH_CHECK();
+  // the segment path keeps next() in shared memory when it fits
+  const int64_t words = lttb_path_words(n, nb);
+  const size_t smem = words * 4 <= (size_t)200 * 1024 ? (size_t)words * 4 : 0;
+  YDT_SWITCH(ydt, ({
+               auto kp = lttb_path_kernel<YD>;
+               if (smem > 48 * 1024) cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+               kp<<<1, LTTB_THREADS, smem, ctx->stream>>>(xf, drop, y, n, off, nb, jump0, maxb, map, idx_out,
+                                                          cnt_out, S, nodes_cap, levels, (int64_t)(smem / 4), n_dev,
+                                                          skip_le);
+             }));
   LAUNCH_CHECK();
   return TSDS_OK;
 }
@@ -871,10 +879,8 @@ int enqueue_stage2_dev(tsds_ctx* ctx, int64_t* dfull, int64_t fcap, const void* 
     count_offsets_kernel<<<gc, 256, 0, ctx->stream>>>(0, nb2, 1, off2, dfull, 2, n_out);
     LAUNCH_CHECK();
   }
-  RC_TRY(run_lttb_walk_small(ctx, x2f, nullptr, y2, ydt, fcap, off2, nb2, dfull + 1, idx_out, cnt_out, dfull, n_out));
-  stage2_finish_kernel<<<cap_grid((fcap + 255) / 256, 64), 256, 0, ctx->stream>>>(dfull, n_out, idx_out, cnt_out);
-  LAUNCH_CHECK();
-  return TSDS_OK;
+  // the path kernel also returns `full` itself when m <= n_out
+  return run_lttb_walk_small(ctx, x2f, nullptr, y2, ydt, fcap, off2, nb2, dfull + 1, idx_out, cnt_out, dfull, n_out);
 }
 
 // LTTB (algorithms.py:184-208) enqueued into (idx_out, cnt_out) on the
@@ -912,7 +918,7 @@ int enqueue_lttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, 
 // walk over the candidates) then runs
 //   * device inputs, buckets of <= SMALL_MAX/2 candidates on average
 //     (minmax_ratio <= ~30): entirely on the device -- every stage-2 kernel
-//     reads m itself, m <= n_out returns `full` (stage2_finish_kernel), and
+//     reads m itself, m <= n_out returns `full` (lttb_path_kernel), and
 //     the api-level uniform verdict of x is read on the device; no host sync;
 //   * host x: m and `full` come back to the host, x[full] is gathered and
 //     binned there (x never crosses PCIe); otherwise (large ratios) the

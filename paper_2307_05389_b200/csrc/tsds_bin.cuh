@@ -342,8 +342,12 @@ __global__ void binning_kernel(const BinJob J) {
   if (mode == 0) {
     if (J.materialize)
       for (int64_t k = threadIdx.x; k <= nb; k += blockDim.x) {
-        unsigned __int128 p = (unsigned __int128)(uint64_t)k * (uint64_t)n;
-        J.off[k] = (int64_t)(p / (uint64_t)nb) + J.add;
+        if (n < ((int64_t)1 << 31) && nb < ((int64_t)1 << 31)) {
+          J.off[k] = (int64_t)((uint64_t)k * (uint64_t)n / (uint64_t)nb) + J.add;  // no 128-bit division needed
+        } else {
+          unsigned __int128 p = (unsigned __int128)(uint64_t)k * (uint64_t)n;
+          J.off[k] = (int64_t)(p / (uint64_t)nb) + J.add;
+        }
       }
   } else if (mode == 1 || mode == 2 || mode == 4) {
     // mode 4 ("invalid index span"): empty bins, so consumers that are
@@ -357,9 +361,25 @@ __global__ void binning_kernel(const BinJob J) {
       J.off[nb] = n + J.add;
     }
     __syncthreads();
+    // monotone check: each thread a contiguous run of offsets, loaded 16 at
+    // a time (independent L2 loads in flight instead of one round trip per
+    // pair: 9,996 edges took ~40 us one by one)
     bool bad = false;
-    for (int64_t k = threadIdx.x; k < nb; k += blockDim.x)
-      bad |= ld_cg_i64(J.off + k + 1) < ld_cg_i64(J.off + k);
+    const int64_t per = (nb + blockDim.x - 1) / blockDim.x;
+    const int64_t a = (int64_t)threadIdx.x * per, b = a + per < nb ? a + per : nb;  // pairs (k, k+1), k in [a, b)
+    if (a < b) {
+      int64_t prev = __ldcg(J.off + a);
+      for (int64_t k = a + 1; k <= b; k += 16) {
+        int64_t v[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) v[u] = k + u <= b ? __ldcg(J.off + k + u) : INT64_MAX;
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+          bad |= v[u] < prev;
+          prev = v[u];
+        }
+      }
+    }
     if (__syncthreads_or(bad) && threadIdx.x == 0) F->nonmono = 1;
   }
 }

@@ -9,12 +9,10 @@
 // SURVEY.md hard part 2) and the centroid sums keep the reference's
 // sequential order, so every pick is bit-identical to the reference.
 //
-// Two walk strategies inside one single-CTA kernel (chosen on the device):
-//   * small buckets (max bucket <= SMALL_MAX, e.g. MinMaxLTTB stage 2):
-//     every node p computes next(p) = its pick in the next non-empty bucket
-//     in parallel, then the path 0 -> next -> ... is recovered with binary
-//     lifting (jump tables), i.e. no sequential chain at all;
-//   * large buckets: a block-wide first-max reduction per bucket.
+// Small buckets (average <= SMALL_MAX/2, e.g. MinMaxLTTB stage 2) run as
+// two launches: every point's transition next(p) in parallel, then one CTA
+// recovers the path 0 -> next -> ... (lttb_next_kernel / lttb_path_kernel
+// below).  Large buckets use tsds_lttb_large.cuh.
 #pragma once
 
 #include "tsds_common.cuh"
@@ -120,16 +118,28 @@ __device__ __forceinline__ void lttb_centroid_phase(const double* xin, const int
     }
   }
 }
-// m_dev (nullable): MinMaxLTTB stage 2 on the device -- no-op when the
-// candidate count *m_dev <= skip_le (the candidates are the answer)
+// Centroid of points [s, e) in the reference's sequential summation order
+// (_kernels.py:398-408): lanes fetch 32 consecutive points, every lane
+// replays the sequential f64 sum through shuffles; uniform across the warp.
 template <int YDT>
-__global__ void lttb_centroid_kernel(const double* xin, const int* drop, const void* y,
-                                     const int64_t* off, int64_t nb, double2* cent,
-                                     const int64_t* m_dev = nullptr, int64_t skip_le = 0) {
-  pdl_launch_dependents();
-  pdl_wait();
-  if (m_dev && *m_dev <= skip_le) return;
-  lttb_centroid_phase<YDT>(xin, drop, y, off, nb, cent);
+__device__ __forceinline__ double2 warp_centroid(const double* x, const void* y, int64_t s, int64_t e) {
+  const int lane = threadIdx.x & 31;
+  double sx = 0.0, sy = 0.0;
+  for (int64_t b = s; b < e; b += 32) {
+    const int64_t i = b + lane;
+    double vx = 0.0, vy = 0.0;
+    if (i < e) {
+      vx = xd(x, i);
+      vy = yd<YDT>(y, i);
+    }
+    const int cnt = (int)((e - b) < 32 ? (e - b) : 32);
+    for (int t = 0; t < cnt; t++) {
+      sx = __dadd_rn(sx, __shfl_sync(0xffffffffu, vx, t));
+      sy = __dadd_rn(sy, __shfl_sync(0xffffffffu, vy, t));
+    }
+  }
+  const double cw = (double)(e - s);
+  return make_double2(__ddiv_rn(sx, cw), __ddiv_rn(sy, cw));
 }
 
 struct AreaCand {
@@ -180,119 +190,240 @@ __device__ __forceinline__ void centroid_for(const double* x, const void* y, con
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small-bucket walk in two launches.
+//
+// (1) lttb_next_kernel, warp per bucket k (k = -1: the frame point 0): for
+//     every point p of bucket k, next(p) = the reference's pick in the next
+//     non-empty bucket k2 with a = p and c = centroid of bucket k2+1 (or the
+//     last point) -- i.e. the walk's transition function, all of it in
+//     parallel.  It also records the largest bucket size.
+// (2) lttb_path_kernel, one CTA: the walk is the path 0 -> next -> ... ; it
+//     visits one point per non-empty bucket.  With next() in shared memory
+//     the path is recovered in three short phases over segments of S path
+//     positions (S ~ sqrt(#buckets)): every candidate entry point of every
+//     segment is walked S steps (parallel), the segment entries are chained
+//     (one thread, #segments steps), every segment is re-walked from its
+//     entry writing the picks (parallel) -- ~3*sqrt(L) dependent shared
+//     memory lookups instead of L dependent global ones.  Larger inputs fall
+//     back to binary lifting in global memory, buckets > SMALL_MAX to a
+//     block-wide reduction per bucket.  Picks are the reference's (the same
+//     pick_in / tri_area arithmetic), only the schedule differs.
+
 template <int YDT>
-__global__ void __launch_bounds__(LTTB_THREADS)
-lttb_walk_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
-                 const double2* cent, const int64_t* map, int64_t* out, int64_t* m_out,
-                 LttbScratch S, int64_t scratch_nodes, int jump_levels,
-                 const int64_t* n_dev = nullptr, int64_t skip_le = 0) {
-  if (n_dev) {  // device-sized series (MinMaxLTTB stage 2): n = candidate count
+__global__ void __launch_bounds__(256) lttb_next_kernel(const double* xin, const int* drop, const void* y,
+                                                        int64_t n, const int64_t* off, int64_t nb,
+                                                        int32_t* jump0, int* maxb, const int64_t* n_dev,
+                                                        int64_t skip_le) {
+  pdl_launch_dependents();
+  pdl_wait();
+  if (n_dev) {
     const int64_t m = *n_dev;
     if (m <= skip_le) return;
     n = m;
   }
   const double* x = eff_x(xin, drop);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  __shared__ int64_t s_i64[32];
-  __shared__ AreaCand s_c[32];
-  __shared__ int64_t s_max, s_cnt;
-
-  // ---- max bucket size and non-empty count
-  int64_t mx = 0, ne = 0;
-  for (int64_t k = tid; k < nb; k += LTTB_THREADS) {
-    int64_t w = __ldg(off + k + 1) - __ldg(off + k);
-    mx = w > mx ? w : mx;
-    ne += w > 0;
-  }
-  for (int m = 16; m >= 1; m >>= 1) {
-    int64_t o = __shfl_xor_sync(0xffffffffu, mx, m);
-    mx = o > mx ? o : mx;
-    ne += __shfl_xor_sync(0xffffffffu, ne, m);
-  }
-  if (lane == 0) { s_i64[wid] = mx; s_c[wid].i = ne; }
-  __syncthreads();
-  if (tid == 0) {
-    int64_t a = 0, b = 0;
-    for (int w = 0; w < LTTB_THREADS / 32; w++) { a = s_i64[w] > a ? s_i64[w] : a; b += s_c[w].i; }
-    s_max = a;
-    s_cnt = b;
-  }
-  __syncthreads();
-  const int64_t L = s_cnt;
-  const bool small = s_max <= SMALL_MAX && n <= scratch_nodes && (((int64_t)1 << jump_levels) > L);
-
-  if (small) {
-    // ---- firstne[k] = smallest non-empty bucket >= k (nb if none): block suffix scan
-    const int64_t ch = (nb + 1 + LTTB_THREADS - 1) / LTTB_THREADS;
-    const int64_t k0 = tid * ch, k1 = (k0 + ch) < (nb + 1) ? (k0 + ch) : (nb + 1);
-    int32_t loc = (int32_t)nb;
-    for (int64_t k = k1 - 1; k >= k0; k--)
-      if (k < nb && __ldg(off + k + 1) > __ldg(off + k)) loc = (int32_t)k;
-    __shared__ int32_t suf[LTTB_THREADS];
-    suf[tid] = loc;
-    __syncthreads();
-    for (int d = 1; d < LTTB_THREADS; d <<= 1) {
-      int32_t v = (tid + d < LTTB_THREADS) ? suf[tid + d] : (int32_t)nb;
-      __syncthreads();
-      suf[tid] = min(suf[tid], v);
-      __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k = gw - 1; k < nb; k += nw) {
+    int64_t s = 0, e = 1;
+    if (k >= 0) {
+      s = __ldg(off + k);
+      e = __ldg(off + k + 1);
+      if (e <= s) continue;
+      if (lane == 0) atomicMax(maxb, (int)((e - s) < 0x7fffffff ? (e - s) : 0x7fffffff));
     }
-    int32_t run = (tid + 1 < LTTB_THREADS) ? suf[tid + 1] : (int32_t)nb;
-    for (int64_t k = k1 - 1; k >= k0; k--) {
-      if (k < nb && __ldg(off + k + 1) > __ldg(off + k)) run = (int32_t)k;
-      S.firstne[k] = run;
-    }
-    // bucket of each interior point
-    for (int64_t k = tid; k < nb; k += LTTB_THREADS)
-      for (int64_t i = __ldg(off + k); i < __ldg(off + k + 1); i++) S.bk[i] = (int32_t)k;
-    __syncthreads();
-    // ---- next(p) for node 0 and every bucketed point; END = n-1 (self loop)
-    for (int64_t p = tid; p < n; p += LTTB_THREADS) {
-      int32_t nx;
-      int64_t kp;
-      bool node = true;
-      if (p == 0) kp = -1;
-      else if (p == n - 1) node = false;
-      else if (p < __ldg(off + 0) || p >= __ldg(off + nb)) node = false;
-      if (!node) {
-        nx = (int32_t)(n - 1);
-      } else {
-        if (p != 0) kp = S.bk[p];
-        int64_t k2 = S.firstne[kp + 1];
-        if (k2 >= nb) {
-          nx = (int32_t)(n - 1);
-        } else {
-          double cx, cy;
-          centroid_for<YDT>(x, y, off, nb, cent, k2, n, cx, cy);
-          nx = (int32_t)pick_in<YDT>(x, y, __ldg(off + k2), __ldg(off + k2 + 1), xd(x, p), yd<YDT>(y, p), cx, cy);
-        }
+    int64_t k2 = k + 1;  // next non-empty bucket (32 buckets per ballot)
+    while (k2 < nb) {
+      const int64_t kk = k2 + lane;
+      const bool ne = kk < nb && __ldg(off + kk + 1) > __ldg(off + kk);
+      const unsigned bal = __ballot_sync(0xffffffffu, ne);
+      if (bal) {
+        k2 += __ffs(bal) - 1;
+        break;
       }
-      S.jump[p] = nx;
+      k2 += 32;
+    }
+    if (k2 >= nb) {
+      for (int64_t p = s + lane; p < e; p += 32) jump0[p] = (int32_t)(n - 1);
+      continue;
+    }
+    const int64_t s2 = __ldg(off + k2), e2 = __ldg(off + k2 + 1);
+    double cx, cy;
+    if (k2 == nb - 1 || __ldg(off + k2 + 2) <= e2) {
+      cx = xd(x, n - 1);
+      cy = yd<YDT>(y, n - 1);
+    } else {
+      const double2 c = warp_centroid<YDT>(x, y, e2, __ldg(off + k2 + 2));
+      cx = c.x;
+      cy = c.y;
+    }
+    for (int64_t p = s + lane; p < e; p += 32)
+      jump0[p] = (int32_t)pick_in<YDT>(x, y, s2, e2, xd(x, p), yd<YDT>(y, p), cx, cy);
+  }
+  if (gw == 0 && lane == 0) jump0[n - 1] = (int32_t)(n - 1);
+}
+
+constexpr int PATH_SEG_CAND = SMALL_MAX;  // entry candidates per segment (max bucket size of the smem path)
+
+// shared-memory words the segment path needs for n points and nb buckets
+// (J[n], ne[<=nb], per segment PATH_SEG_CAND exits + entry + start)
+__host__ __device__ inline int64_t lttb_path_words(int64_t n, int64_t nb) {
+  // segments of S >= ceil(sqrt(L+1)) positions over L+1 <= nb+1 positions
+  int64_t r = 1;
+  while (r * r < nb + 1) r++;
+  return n + nb + 1 + (r + 1) * (PATH_SEG_CAND + 2);
+}
+
+template <int YDT>
+__global__ void __launch_bounds__(LTTB_THREADS)
+lttb_path_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
+                 int32_t* jump0, int* maxb, const int64_t* map, int64_t* out, int64_t* m_out,
+                 LttbScratch S, int64_t scratch_nodes, int jump_levels, int64_t smem_words, const int64_t* n_dev,
+                 int64_t skip_le) {
+  pdl_wait();
+  if (n_dev) {
+    const int64_t m = *n_dev;
+    if (m <= skip_le) {  // MinMaxLTTB: m <= n_out candidates are the result (algorithms.py:241-242)
+      for (int64_t i = threadIdx.x; i < m; i += blockDim.x) out[i] = __ldg(map + i);
+      if (threadIdx.x == 0) *m_out = m;
+      return;
+    }
+    n = m;
+  }
+  extern __shared__ int32_t sm[];
+  const double* x = eff_x(xin, drop);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  __shared__ int32_t s_wsum[LTTB_THREADS / 32];
+  __shared__ int64_t s_L;
+  __shared__ int s_mb;
+  if (tid == 0) s_mb = *maxb;
+
+  // ---- L = number of non-empty buckets; ne[j] = j-th non-empty bucket (if it fits in smem)
+  const int64_t ch = (nb + LTTB_THREADS - 1) / LTTB_THREADS;
+  const int64_t k0 = (int64_t)tid * ch, k1 = (k0 + ch) < nb ? (k0 + ch) : nb;
+  int32_t cnt = 0;
+  for (int64_t k = k0; k < k1; k++) cnt += __ldg(off + k + 1) > __ldg(off + k);
+  int32_t incl = cnt;
+  for (int d = 1; d < 32; d <<= 1) {
+    const int32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += t;
+  }
+  if (lane == 31) s_wsum[wid] = incl;
+  __syncthreads();
+  int32_t before = incl - cnt, total = 0;
+  for (int w = 0; w < LTTB_THREADS / 32; w++) {
+    if (w < wid) before += s_wsum[w];
+    total += s_wsum[w];
+  }
+  if (tid == 0) s_L = total;
+  const int64_t L = total;
+  const int mb = s_mb;
+  const int64_t Sg = [&] {  // segment length in path positions
+    int64_t q = 8;
+    while (q * q < L + 1) q++;
+    return q;
+  }();
+  const int64_t nseg = (L + 1 + Sg - 1) / Sg;
+  int32_t* J = sm;                 // [n]
+  int32_t* ne = sm + n;            // [L + 1] (reused for the path: positions 0..L)
+  int32_t* E = ne + L + 1;         // [nseg * PATH_SEG_CAND] segment exits per entry candidate
+  int32_t* ent = E + nseg * PATH_SEG_CAND;  // [nseg] entries; start[nseg] follows
+  int32_t* st = ent + nseg;
+  const bool smem_path = mb <= PATH_SEG_CAND && n + L + 1 + nseg * (PATH_SEG_CAND + 2) <= smem_words;
+
+  if (smem_path) {
+    for (int64_t p = tid; p < n; p += LTTB_THREADS) J[p] = __ldcg(jump0 + p);
+    int32_t j = before;
+    for (int64_t k = k0; k < k1; k++)
+      if (__ldg(off + k + 1) > __ldg(off + k)) ne[j++] = (int32_t)k;
+    __syncthreads();
+    // phase 1: every entry candidate of segments 0..nseg-2 walked Sg steps;
+    // candidates 0..7 of every segment in one pass (buckets are small), the
+    // rest only when some bucket is larger
+    for (int pass = 0; pass < (mb > 8 ? 2 : 1); pass++) {
+      const int c0 = pass == 0 ? 0 : 8, cw = pass == 0 ? 8 : PATH_SEG_CAND - 8;
+      for (int64_t t = tid; t < (nseg - 1) * cw; t += LTTB_THREADS) {
+        const int64_t sg = t / cw, c = c0 + (t - sg * cw);
+        const int64_t P = sg * Sg;  // entry position
+        int64_t q0, q1;
+        if (P == 0) {
+          q0 = 0;
+          q1 = 1;
+        } else {
+          q0 = __ldg(off + ne[P - 1]);
+          q1 = __ldg(off + ne[P - 1] + 1);
+        }
+        if (c == 0) st[sg] = (int32_t)q0;
+        if (q0 + c >= q1) continue;
+        int32_t p = (int32_t)(q0 + c);
+        for (int64_t i = 0; i < Sg; i++) p = J[p];
+        E[sg * PATH_SEG_CAND + c] = p;
+      }
     }
     __syncthreads();
+    // phase 2: chain the segment entries
+    if (tid == 0) {
+      int32_t cur = 0;
+      for (int64_t sg = 0; sg < nseg; sg++) {
+        ent[sg] = cur;
+        if (sg + 1 < nseg) cur = E[sg * PATH_SEG_CAND + (cur - st[sg])];
+      }
+    }
+    __syncthreads();
+    // phase 3: re-walk every segment from its entry; the path (positions
+    // 0..L) overwrites ne[], which is no longer needed
+    int32_t* path = ne;
+    for (int64_t sg = tid; sg < nseg; sg += LTTB_THREADS) {
+      int32_t p = ent[sg];
+      const int64_t end = (sg + 1) * Sg < L + 1 ? (sg + 1) * Sg : L + 1;
+      for (int64_t pos = sg * Sg; pos < end; pos++) {
+        path[pos] = p;
+        p = J[p];
+      }
+    }
+    __syncthreads();
+    for (int64_t pos = tid; pos <= L; pos += LTTB_THREADS) {
+      const int32_t p = path[pos];
+      out[pos] = map ? __ldg(map + p) : p;
+    }
+    if (tid == 0) {
+      out[L + 1] = map ? __ldg(map + n - 1) : n - 1;
+      *m_out = L + 2;
+      *maxb = 0;
+    }
+    return;
+  }
+
+  const bool lift = mb <= SMALL_MAX && n <= scratch_nodes && (((int64_t)1 << jump_levels) > L);
+  if (lift) {
+    // binary lifting over next() in global memory (level 0 = jump0)
     for (int t = 1; t < jump_levels; t++) {
-      const int32_t* J = S.jump + (int64_t)(t - 1) * n;
+      const int32_t* Jp = t == 1 ? jump0 : S.jump + (int64_t)(t - 1) * n;
       int32_t* J2 = S.jump + (int64_t)t * n;
-      for (int64_t p = tid; p < n; p += LTTB_THREADS) J2[p] = J[J[p]];
+      for (int64_t p = tid; p < n; p += LTTB_THREADS) J2[p] = __ldcg(Jp + __ldcg(Jp + p));
       __syncthreads();
     }
-    // ---- path: out[j] = next^j(0), j = 1..L
     for (int64_t j = 1 + tid; j <= L; j += LTTB_THREADS) {
       int64_t p = 0;
       for (int t = 0; t < jump_levels; t++)
-        if ((j >> t) & 1) p = S.jump[(int64_t)t * n + p];
+        if ((j >> t) & 1) p = __ldcg((t == 0 ? jump0 : S.jump + (int64_t)t * n) + p);
       out[j] = map ? __ldg(map + p) : p;
     }
     if (tid == 0) {
       out[0] = map ? __ldg(map + 0) : 0;
       out[L + 1] = map ? __ldg(map + n - 1) : n - 1;
       *m_out = L + 2;
+      *maxb = 0;
     }
     return;
   }
 
-  // ---- large buckets: block-wide reduction per bucket
+  // ---- large buckets: block-wide reduction per bucket (sequential over buckets)
   __shared__ double s_ax, s_ay;
+  __shared__ double2 s_cent;
+  __shared__ AreaCand s_c[32];
   if (tid == 0) { s_ax = xd(x, 0); s_ay = yd<YDT>(y, 0); }
   __syncthreads();
   int64_t m = 1;
@@ -300,7 +431,18 @@ lttb_walk_kernel(const double* xin, const int* drop, const void* y, int64_t n, c
     int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
     if (e <= s) continue;
     double cx, cy;
-    centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
+    if (k == nb - 1 || __ldg(off + k + 2) <= e) {
+      cx = xd(x, n - 1);
+      cy = yd<YDT>(y, n - 1);
+    } else {
+      if (wid == 0) {
+        const double2 c = warp_centroid<YDT>(x, y, e, __ldg(off + k + 2));
+        if (lane == 0) s_cent = c;
+      }
+      __syncthreads();
+      cx = s_cent.x;
+      cy = s_cent.y;
+    }
     const double ax = s_ax, ay = s_ay;
     AreaCand best{-1.0, IDX_NONE};
     for (int64_t i = s + tid; i < e; i += LTTB_THREADS) {
@@ -327,6 +469,7 @@ lttb_walk_kernel(const double* xin, const int* drop, const void* y, int64_t n, c
     out[0] = map ? __ldg(map + 0) : 0;
     out[m] = map ? __ldg(map + n - 1) : n - 1;
     *m_out = m + 1;
+    *maxb = 0;
   }
 }
 
@@ -337,7 +480,7 @@ lttb_walk_kernel(const double* xin, const int* drop, const void* y, int64_t n, c
 // x2 = x[full] (raw, for the stage-2 binning); x2f = float64(x2), or the
 // candidate positions themselves when there is no x or the api-level check
 // found x uniform (*api_nonuniform == 0: dropped, api.py:19-28).  No-op
-// when m <= n_out (stage2_finish_kernel returns `full`).
+// when m <= n_out (lttb_path_kernel returns `full`).
 template <int XDT>
 __global__ void stage2_inputs_kernel(const int64_t* dfull, int64_t n_out, const void* y, int yes, void* y2,
                                      const void* x, void* x2, double* x2f, const int* api_nonuniform) {
@@ -366,14 +509,6 @@ __global__ void stage2_inputs_kernel(const int64_t* dfull, int64_t n_out, const 
   }
 }
 
-// m <= n_out: the candidates are the result (algorithms.py:241-242)
-__global__ void stage2_finish_kernel(const int64_t* dfull, int64_t n_out, int64_t* out, int64_t* count) {
-  const int64_t m = dfull[0];
-  if (m > n_out) return;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = dfull[1 + i];
-  if (blockIdx.x == 0 && threadIdx.x == 0) *count = m;
-}
 
 template <int DT>
 __global__ void gather_kernel(const void* src, const int64_t* idx, int64_t m, void* dst) {
