@@ -228,6 +228,53 @@ __device__ int64_t lower_bound_fast_cta(const void* x, int64_t n, double e, doub
   return lower_bound_exact_cta<XDT>(x, n, e);
 }
 
+// Warp-wide version for many edges (one warp per edge): interpolated guess
+// and two secant steps (each one broadcast load), a 32-element window around
+// the estimate (one coalesced load), r = window start + #elements < e, then
+// the reference's binary-search path to r verified in one round (lane l
+// checks level l; top levels are shared by all edges and hit in L2).  Four
+// dependent rounds and ~20 distinct sectors per edge, instead of six rounds
+// of 31 speculative probes; exact fallback when the window misses or x is
+// not monotone along the path.
+template <int XDT>
+__device__ int64_t lower_bound_fast_warp(const void* x, int64_t n, double e, double x0, double span) {
+  const int lane = threadIdx.x & 31;
+  if (n < 64 || n >= ((int64_t)1 << 32)) return lower_bound_exact<XDT>(x, n, e);
+  double t = __ddiv_rn(__dsub_rn(e, x0), span);
+  t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+  int64_t g = (int64_t)(t * (double)(n - 1));
+  const double slope = span / (double)(n - 1);
+#pragma unroll
+  for (int it = 0; it < 2; it++) {
+    const double d = (e - xf64<XDT>(x, g)) / slope;
+    if (!(d == d) || fabs(d) >= (double)n) break;
+    int64_t g2 = g + (int64_t)d;
+    g = g2 < 0 ? 0 : (g2 > n - 1 ? n - 1 : g2);
+  }
+  int64_t ws = g - 16;
+  if (ws > n - 32) ws = n - 32;
+  if (ws < 0) ws = 0;
+  const bool pred = xf64<XDT>(x, ws + lane) < e;
+  const unsigned bal = __ballot_sync(0xffffffffu, pred);
+  // bracket: x[ws] < e (or ws == 0) and x[ws+31] >= e (or the window ends at n)
+  bool ok = (ws == 0 || (bal & 1u)) && (ws + 32 == n || !(bal >> 31));
+  const int64_t r = ws + __popc(bal);
+  if (ok) {
+    // lane l checks probe l of the reference's search path ending at r
+    int64_t lo = 0, hi = n, mid = -1;
+    for (int l = 0; l <= lane && lo < hi; l++) {
+      mid = (lo + hi) >> 1;
+      if (l == lane) break;
+      if (mid < r) lo = mid + 1; else hi = mid;
+    }
+    bool bad = false;
+    if (lo < hi && mid >= 0) bad = (xf64<XDT>(x, mid) < e) != (mid < r);
+    ok = __ballot_sync(0xffffffffu, bad) == 0u;
+  }
+  if (ok) return r;
+  return lower_bound_exact<XDT>(x, n, e);
+}
+
 // One launch computes the bins of x[0..n) (binning.py:43-82 semantics):
 //   * uniform-spacing checks of the binned slice and (optionally) of the
 //     whole x for the api-level normalisation (api.py:19-28);
@@ -300,7 +347,7 @@ __global__ void binning_kernel(const BinJob J) {
         const int64_t w0 = eb * (blockDim.x >> 5) + (threadIdx.x >> 5);
         for (int64_t k = 1 + w0; k < nb; k += neb * (blockDim.x >> 5)) {
           double e = __dadd_rn(x0, __ddiv_rn(__dmul_rn((double)k, span), (double)nb));
-          int64_t v = lower_bound_exact<XDT>(J.x, n, e);
+          int64_t v = lower_bound_fast_warp<XDT>(J.x, n, e, x0, span);
           if (lane == 0) J.off[k] = v + J.add;
         }
       }
