@@ -451,7 +451,7 @@ def run_ours(args):
     import torch
 
     ws, rank, local = _dist()
-    if ws > 1:
+    if ws > 1 or args.sharded:
         return run_ours_sharded(args)
     runner = GpuRunner(0)
     peak, peak_kind = _peaks()
@@ -482,10 +482,166 @@ def run_ours(args):
     del torch
 
 
+# ------------------------------------------------------------ sharded (N GPUs)
+
+
+def _shared_c4(rank, world):
+    """C4 host arrays generated once (rank 0) and mapped by every rank from
+    /dev/shm (12 GB of host RAM in total, not per rank)."""
+    import torch.distributed as dist
+
+    tag = os.environ.get("MASTER_PORT", "0")
+    paths = [f"/dev/shm/tsds_bench_c4_{tag}_{k}.bin" for k in ("x", "y")]
+    if rank == 0:
+        x, y = W.config4_parallel()
+        for a, p in zip((x, y), paths):
+            a.tofile(p)
+        del x, y
+    if world > 1:
+        dist.barrier()
+    x = np.memmap(paths[0], dtype=np.float64, mode="r")
+    y = np.memmap(paths[1], dtype=np.float32, mode="r")
+    return x, y, paths
+
+
 def run_ours_sharded(args):
+    """C4 (MinMax preselection sharded by sub-bin ranges, candidates
+    all-gathered over NCCL, stage 2 on every rank) and C5 (series
+    partitioned), strong scaling; time = max over ranks of K device-timed steps."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2307_05389_b200 import _lib
     from paper_2307_05389_b200 import distributed as D
 
-    return D.bench_sharded(args, sys.modules[__name__])
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    be = D.GpuBackend(local)
+    stream = torch.cuda.ExternalStream(be.ctx.stream, device=torch.device("cuda", local))
+    ex = D.NcclExchange(be.ctx)
+    peak, peak_kind = _peaks()
+    entries = {}
+    g = np.load(os.path.join(ROOT, "tests", "golden", "configs.npz"))
+
+    def timed(step, nbytes):
+        for _ in range(args.warmup):
+            step()
+        be.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = be.ctx.launches
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        be.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item()) / args.steps
+        return ms, ws * nbytes / (ms * 1e-3) / 1e9, (be.ctx.launches - l0) // args.steps
+
+    def e2e_time(fn):
+        fn()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            r = fn()
+        dt = (time.perf_counter() - t0) / 3
+        t = torch.tensor([dt], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), r
+
+    def entry(key, ms, gbs, launches, nbytes_total, e2e_s, n_points):
+        return {
+            "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "ms_per_step": round(ms, 5),
+            "points_per_s": round(n_points / (ms * 1e-3), 1), "steps": args.steps, "warmup": args.warmup,
+            "config": config_dict(key, ws), "gpu_launches_per_step_rank0": int(launches),
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak * ws, "peak_kind":
+                         f"{peak_kind} x {ws} GPUs", "unit": "GB/s", "frac": round(gbs / (peak * ws), 4),
+                         "traffic": None, "note": "whole sharded step (incl. NCCL all-gather) vs aggregate HBM"},
+            "parity": "equal to the reference's output (tests/golden/configs.npz) on every rank",
+            "e2e": {"value": round(nbytes_total / e2e_s / 1e9, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": int(nbytes_total // ws), "d2h_bytes_per_step": 8 * 5000,
+                    "ms_per_step": round(e2e_s * 1e3, 3),
+                    "path": "per rank: its shard of the pageable host arrays through the library (staging ring), "
+                            "sharded step, result to host"},
+        }
+
+    clk = ClockSampler(local).__enter__()
+    if "C4" in args.configs:
+        x, y, paths = _shared_c4(rank, ws)
+        s = SPECS["C4"]
+        plan = D.make_plan("minmaxlttb", x, y.shape[0], s["n_out"], s["ratio"], ws)
+        ss = D.ShardedSeries.from_host(plan, rank, x, y, ex, be)
+        ss.step()
+        assert np.array_equal(ss.result(), g["c4_minmaxlttb"]), "C4 sharded result differs from the reference"
+        t_a = time.perf_counter()
+        ms, gbs, launches = timed(ss.step, y.nbytes // ws)
+        clk.window(t_a, time.perf_counter())
+        del ss
+        torch.cuda.empty_cache()
+        e2e_s, r = e2e_time(lambda: D.sharded_downsample("minmaxlttb", x, y, n_out=s["n_out"],
+                                                         minmax_ratio=s["ratio"], backend=be, exchange=ex))
+        assert np.array_equal(r, g["c4_minmaxlttb"])
+        entries["C4"] = entry("C4", ms, gbs, launches, y.nbytes, e2e_s, y.shape[0])
+        del x, y
+        dist.barrier()
+        if rank == 0:
+            for p in paths:
+                os.unlink(p)
+    for key in ("C5_i16", "C5_u8", "C5_f16"):
+        if "C5" not in args.configs:
+            break
+        s = SPECS[key]
+        s0, s1 = D.shard_ranges(s["S"], ws)[rank]
+        Y = W.config5_parallel(s["tag"], rows=(s0, s1))
+        rows = torch.from_numpy(Y).to(f"cuda:{local}")
+        b = D.ShardedBatch(s["S"], s["L"], s["n_out"], rank, ws, rows, DT_CODE[Y.dtype], ex, be)
+        b.step()
+        idx, cnt = b.result()
+        assert golden_ok(key, idx, cnt), f"{key} sharded result differs from the reference"
+        nbytes_total = s["S"] * s["L"] * Y.dtype.itemsize
+        t_a = time.perf_counter()
+        ms, gbs, launches = timed(b.step, nbytes_total // ws)
+        clk.window(t_a, time.perf_counter())
+        del b, rows
+        torch.cuda.empty_cache()
+
+        def e2e_c5():
+            import paper_2307_05389_b200 as ts
+
+            li, lc = ts.minmax_batched(Y, s["n_out"])  # this rank's rows, pageable host -> staging ring
+            rws = -(-s["S"] // ws)
+            blk = np.zeros(rws * (s["n_out"] + 1), np.int64)  # ShardedBatch's block layout [counts | idx]
+            blk[: s1 - s0] = lc
+            blk[rws : rws + (s1 - s0) * s["n_out"]] = li.view(np.int64).reshape(-1)
+            send = torch.from_numpy(blk).to(f"cuda:{local}")
+            recv = torch.empty(ws * blk.shape[0], dtype=torch.int64, device=f"cuda:{local}")
+            torch.cuda.synchronize(local)
+            ex.allgather(send, recv)
+            be.synchronize()
+            return recv.cpu()
+
+        e2e_s, _ = e2e_time(e2e_c5)
+        entries[key] = entry(key, ms, gbs, launches, nbytes_total, e2e_s, s["S"] * s["L"])
+        del Y
+    clk.__exit__(None, None, None)
+    head = entries.get("C4") or next(iter(entries.values()))
+    line = {
+        "metric": METRIC, "value": head["value"], "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (workloads.py, seeded generators of BASELINE configs, SURVEY.md 8(d))",
+        "config": head["config"], "points_per_s": head["points_per_s"], "roofline": head["roofline"],
+        "gpu_launches": head["gpu_launches_per_step_rank0"] * args.steps, "e2e": head["e2e"],
+        "parity": head["parity"], "clocks": clk.summary(), "configs": entries,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ex.close()
+    dist.destroy_process_group()
 
 
 def run_reference(args):
@@ -530,6 +686,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--configs", default="C1,C2,C3,C4,C5", help="subset of C1..C5 (C4 is the headline)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--sharded", action="store_true", help="run the sharded (multi-GPU) path even at N=1")
     ap.add_argument("--cpu-steps", type=int, default=5)
     ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of timed CPU calls per config (reference arm)")
     args = ap.parse_args()

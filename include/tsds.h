@@ -156,6 +156,13 @@ int tsds_lttb_stage2_async(tsds_ctx *ctx, int64_t *cand_dev, int64_t cap, const 
                            const int64_t *ybits_dev, int y_dtype, int64_t n_out, int64_t *out_dev,
                            int64_t *count_dev);
 
+/* Host -> device copy on ctx's stream for callers that keep data resident
+ * (e.g. a rank uploading its shard): pinned sources are DMA'd directly,
+ * pageable ones (numpy) go through the context's staging ring of pinned
+ * slots filled by parallel host threads.  When the call returns the source
+ * may be reused; the data is on the device when the stream reaches it. */
+int tsds_upload(tsds_ctx *ctx, void *dst_dev, const void *src_host, int64_t bytes);
+
 /* Communicator: NCCL, loaded at run time (libtsds
  * does not link it), bound to ctx's device and stream.  Rank 0 makes the
  * 128-byte id, the caller distributes it out of band (e.g. over

@@ -44,6 +44,7 @@ EXPORTED = (
     "tsds_shard_preselect_async",
     "tsds_records_concat",
     "tsds_lttb_stage2_async",
+    "tsds_upload",
     "tsds_comm_unique_id",
     "tsds_comm_init",
     "tsds_comm_destroy",
@@ -112,6 +113,7 @@ def load():
                                                  vp]
         L.tsds_records_concat.argtypes = [vp, vp, i32, i64, i32, vp, i64, vp]
         L.tsds_lttb_stage2_async.argtypes = [vp, vp, i64, vp, i32, vp, i32, i64, vp, vp]
+        L.tsds_upload.argtypes = [vp, vp, vp, i64]
         L.tsds_comm_unique_id.argtypes = [vp]
         L.tsds_comm_init.argtypes = [vp, i32, i32, vp, ctypes.POINTER(vp)]
         L.tsds_comm_destroy.argtypes = [vp]
@@ -193,6 +195,13 @@ class Context:
     @property
     def launches(self):
         return int(load().tsds_ctx_launches(self.handle))
+
+
+def upload(ctx, dst_tensor, src_array):
+    """Copy a contiguous host array into a device tensor on ctx's stream
+    (staging ring for pageable memory); synchronises before returning."""
+    check(load().tsds_upload(ctx.handle, dst_tensor.data_ptr(), src_array.ctypes.data, src_array.nbytes), "upload")
+    ctx.synchronize()
 
 
 def context(device=None):

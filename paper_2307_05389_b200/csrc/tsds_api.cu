@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -497,6 +498,29 @@ int fetch_result(tsds_ctx* ctx, const int64_t* dev, int64_t cap, int64_t* out, i
   return TSDS_OK;
 }
 
+// Host binning of host-resident x (the uniform check of the whole x and the
+// equal-width offsets of the slice xs[0..ns), + add) on a helper thread, so
+// it runs while the caller streams y through the staging ring.
+struct HostBins {
+  std::vector<int64_t> off;
+  int rc = TSDS_OK;
+  bool uniform = false;
+  std::thread th;
+  void start(const void* x, int xdt, int64_t n, const void* xs, int64_t ns, int64_t nb, int64_t add) {
+    th = std::thread([=] {
+      uniform = tsds_host_is_uniform_spaced(x, xdt, n) != 0;  // api.py:26-28
+      if (uniform) return;
+      off.resize(nb + 1);
+      rc = tsds_host_equal_width_offsets(xs, xdt, ns, nb, off.data());
+      for (auto& v : off) v += add;
+    });
+  }
+  void join() {
+    if (th.joinable()) th.join();
+  }
+  ~HostBins() { join(); }
+};
+
 // ----------------------------------------------------------------- MinMax / M4
 int run_minmax_m4(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y, int ydt, int64_t n, int64_t n_out,
                   int nan_mode, int mem, int64_t* out_dev, int64_t* count_dev) {
@@ -504,20 +528,20 @@ int run_minmax_m4(tsds_ctx* ctx, int algo, const void* x, int xdt, const void* y
   const int64_t nb = n_out / width;
   BinSpec bins{0, nullptr, n, nb, 0};
   ScanArgs A = scan_args(nullptr, bins, 0, nb, 0, n);
-  // host y: enqueue its (asynchronous, pinned) upload first so that the host
-  // binning of x below overlaps the transfer
+  // host x: its bins are computed on a helper thread while y streams to the device
+  HostBins hb;
+  if (x && mem == TSDS_MEM_HOST) hb.start(x, xdt, n, x, n, nb, 0);
   const void* dy;
   RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
   if (x) {
     if (mem == TSDS_MEM_HOST) {
-      if (!tsds_host_is_uniform_spaced(x, xdt, n)) {
-        std::vector<int64_t> off(nb + 1);
-        int rc = tsds_host_equal_width_offsets(x, xdt, n, nb, off.data());
-        if (rc == TSDS_ERR_SPAN) return set_err(rc, "invalid index span");
-        RC_TRY(upload(ctx, ctx->off, off.data(), off.size() * 8));
+      hb.join();
+      if (!hb.uniform) {
+        if (hb.rc == TSDS_ERR_SPAN) return set_err(hb.rc, "invalid index span");
+        RC_TRY(upload(ctx, ctx->off, hb.off.data(), hb.off.size() * 8));
         A.bins.mode = 1;
         A.bins.off = (const int64_t*)ctx->off.p;
-        A.independent = !host_monotone(off);
+        A.independent = !host_monotone(hb.off);
       }
     } else {
       RC_TRY(ensure(ctx, ctx->off, (size_t)(nb + 1) * 8));
@@ -822,21 +846,20 @@ int gather(tsds_ctx* ctx, const void* src, int dt, const int64_t* idx, int64_t m
 
 // interior offsets (algorithms.py:66-79): bins over 1..n-2 (+1).  Fills
 // either a formula BinSpec or ctx->off.  x_eff is NULL when x was dropped.
+// host x: `hb` was started on (x, slice x[1:n-1], nb, +1) before y's upload
 int interior_bins(tsds_ctx* ctx, const void* x, int xdt, int64_t n, int64_t nb, int mem, BinSpec* bins,
-                  ScanArgs* guards, const void** x_keep, int materialize) {
+                  ScanArgs* guards, const void** x_keep, int materialize, HostBins* hb) {
   *bins = BinSpec{0, nullptr, n - 2, nb, 1};
   *x_keep = nullptr;
   if (!x) return TSDS_OK;
   const int es = dtype_size(xdt);
   if (mem == TSDS_MEM_HOST) {
-    if (tsds_host_is_uniform_spaced(x, xdt, n)) return TSDS_OK;  // api.py:26-28
-    std::vector<int64_t> off(nb + 1);
-    int rc = tsds_host_equal_width_offsets((const char*)x + es, xdt, n - 2, nb, off.data());
-    if (rc == TSDS_ERR_SPAN) return set_err(rc, "invalid index span");
-    for (auto& v : off) v += 1;
-    RC_TRY(upload(ctx, ctx->off, off.data(), off.size() * 8));
+    hb->join();
+    if (hb->uniform) return TSDS_OK;  // api.py:26-28
+    if (hb->rc == TSDS_ERR_SPAN) return set_err(hb->rc, "invalid index span");
+    RC_TRY(upload(ctx, ctx->off, hb->off.data(), hb->off.size() * 8));
     *bins = BinSpec{1, (const int64_t*)ctx->off.p, 0, 0, 0};
-    guards->independent = !host_monotone(off);
+    guards->independent = !host_monotone(hb->off);
     *x_keep = x;
     return TSDS_OK;
   }
@@ -893,14 +916,16 @@ int enqueue_lttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, 
   BinSpec bins;
   ScanArgs guards = scan_args(nullptr, BinSpec{}, 0, 0, 0, 0);
   const void* xk;
-  RC_TRY(interior_bins(ctx, x, xdt, n, nb, mem, &bins, &guards, &xk, 1));
+  HostBins hb;
+  if (x && mem == TSDS_MEM_HOST) hb.start(x, xdt, n, (const char*)x + dtype_size(xdt), n - 2, nb, 1);
+  const void* dy;
+  RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
+  RC_TRY(interior_bins(ctx, x, xdt, n, nb, mem, &bins, &guards, &xk, 1, &hb));
   if (bins.mode == 0 && !guards.use_dyn_mode) {
     RC_TRY(ensure(ctx, ctx->off, (size_t)(nb + 1) * 8));
     RC_TRY(launch_count_offsets(ctx, n - 2, nb, 1, (int64_t*)ctx->off.p));
   }
   const int64_t* off = (const int64_t*)ctx->off.p;
-  const void* dy;
-  RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
   const double* xf = nullptr;
   const int* drop = nullptr;
   if (xk) {
@@ -929,9 +954,11 @@ int enqueue_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int
   const int64_t nsub = (n_out - 2) * ((ratio + 1) / 2);
   ScanArgs A = scan_args(nullptr, BinSpec{}, 0, nsub, 1, n - 1);
   const void* xk;
-  RC_TRY(interior_bins(ctx, x, xdt, n, nsub, mem, &A.bins, &A, &xk, 0));
+  HostBins hb;
+  if (x && mem == TSDS_MEM_HOST) hb.start(x, xdt, n, (const char*)x + dtype_size(xdt), n - 2, nsub, 1);
   const void* dy;
   RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
+  RC_TRY(interior_bins(ctx, x, xdt, n, nsub, mem, &A.bins, &A, &xk, 0, &hb));
   const int64_t fcap = 2 * nsub + 2;
   RC_TRY(ensure(ctx, ctx->full, (size_t)(fcap + 1) * 8));
   int64_t* dfull = (int64_t*)ctx->full.p;
@@ -1008,7 +1035,13 @@ int enqueue_minmaxlttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     const int es = dtype_size(xdt);
     std::vector<char> x2((size_t)m * es);
-    for (int64_t i = 0; i < m; i++) memcpy(&x2[(size_t)i * es], (const char*)xk + (size_t)hfull[i] * es, es);
+    // ~2*nsub random reads over the whole x: latency-bound, spread over the host pool
+    const int parts = (int)std::min<int64_t>(HostPool::get().size(), std::max<int64_t>(1, m / 1024));
+    const int64_t per = (m + parts - 1) / parts;
+    HostPool::get().run(parts, [&](int t) {
+      for (int64_t i = t * per; i < std::min<int64_t>(m, (t + 1) * per); i++)
+        memcpy(&x2[(size_t)i * es], (const char*)xk + (size_t)hfull[i] * es, es);
+    });
     std::vector<int64_t> o2(nb2 + 1);
     int rc = tsds_host_equal_width_offsets(x2.data() + es, xdt, m - 2, nb2, o2.data());
     if (rc == TSDS_ERR_SPAN) return set_err(rc, "invalid index span");
@@ -1364,6 +1397,19 @@ struct tsds_comm {
   ncclComm_t comm = nullptr;
   int nranks = 0, rank = 0;
 };
+
+int tsds_upload(tsds_ctx* ctx, void* dst_dev, const void* src_host, int64_t bytes) {
+  if (!ctx || (bytes > 0 && (!dst_dev || !src_host)) || bytes < 0) return set_err(TSDS_ERR_ARG, "tsds_upload: invalid argument");
+  if (bytes == 0) return TSDS_OK;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard dg_(ctx->device);
+  if ((size_t)bytes >= ((size_t)8 << 20) && !host_is_pinned(src_host)) {
+    CUDA_TRY(ctx->ring.upload(dst_dev, src_host, (size_t)bytes, ctx->stream));
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(dst_dev, src_host, (size_t)bytes, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  return TSDS_OK;
+}
 
 int tsds_comm_unique_id(void* id) {
   if (!id) return set_err(TSDS_ERR_ARG, "tsds_comm_unique_id: NULL");

@@ -209,8 +209,11 @@ struct StagingRing {
       const char* e = getenv("TSDS_STAGING_PARTS");
       return e ? std::max(1, atoi(e)) : std::max(1, HostPool::get().size() * 3 / 4);
     }();
-    for (size_t off = 0; off < bytes; off += slot_bytes) {
-      const size_t len = std::min(slot_bytes, bytes - off);
+    // chunks of bytes/8 (4 MB .. slot) so that even small inputs overlap the
+    // host copy of chunk k+1 with the DMA of chunk k
+    const size_t chunk = std::min(slot_bytes, std::max<size_t>((size_t)4 << 20, (bytes / 8 + 4095) & ~(size_t)4095));
+    for (size_t off = 0; off < bytes; off += chunk) {
+      const size_t len = std::min(chunk, bytes - off);
       const int s = next;
       next = (next + 1) % NS;
       if (busy[s] && (e = cudaEventSynchronize(ev[s])) != cudaSuccess) return e;

@@ -71,6 +71,16 @@ def is_uniform(x):
     return bool(_lib.load().tsds_host_is_uniform_spaced(x.ctypes.data, CODE[x.dtype], x.shape[0]))
 
 
+def _torch_dtype(dt):
+    import torch
+
+    return {np.dtype(np.float16): torch.float16, np.dtype(np.float32): torch.float32,
+            np.dtype(np.float64): torch.float64, np.dtype(np.int8): torch.int8, np.dtype(np.int16): torch.int16,
+            np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64, np.dtype(np.uint8): torch.uint8,
+            np.dtype(np.uint16): torch.uint16, np.dtype(np.uint32): torch.uint32,
+            np.dtype(np.uint64): torch.uint64}[np.dtype(dt)]
+
+
 # ---------------------------------------------------------------------------- plan
 
 
@@ -339,10 +349,17 @@ class ShardedSeries:
         e0, e1 = plan.spans[rank] if plan.spans else (0, 0)
         dev = getattr(backend, "torch_device", None) or torch.device("cuda", backend.device if device is None
                                                                       else device)
-        ys = torch.from_numpy(np.ascontiguousarray(y[e0:e1])).to(dev)
-        xs = None
-        if plan.x_used and x is not None:
-            xs = torch.from_numpy(np.ascontiguousarray(x[e0:e1])).to(dev)
+        def put(a):
+            a = a[e0:e1]
+            if dev.type != "cuda":  # CPU test doubles
+                return torch.from_numpy(np.ascontiguousarray(a))
+            t = torch.empty(a.shape[0], dtype=_torch_dtype(a.dtype), device=dev)
+            if a.shape[0]:
+                _lib.upload(backend.ctx, t, np.ascontiguousarray(a))
+            return t
+
+        ys = put(y)
+        xs = put(x) if plan.x_used and x is not None else None
         dts = (CODE[y.dtype], CODE[x.dtype] if x is not None else 0)
         return cls(plan, rank, ys, xs, exchange, backend, nan, dts)
 

@@ -188,26 +188,28 @@ def config4_parallel(n=C4_N, chunk=1 << 26, procs=None):
     return x, y
 
 
-def _c5_fill(args):
-    tag, s0, s1, L = args
+def _c5_fill_rows(args):
+    tag, s0, s1, L, base = args
     Y = _SHARED["c5"]
     for s in range(s0, s1):
-        Y[s] = config5_series(tag, s, L)
+        Y[s - base] = config5_series(tag, s, L)
     return s1 - s0
 
 
-def config5_parallel(tag, S=C5_S, L=C5_L, procs=None):
-    """config5 (S x L batch) with the series generated by `procs` processes."""
+def config5_parallel(tag, S=C5_S, L=C5_L, procs=None, rows=None):
+    """config5 (S x L batch) with the series generated by `procs` processes;
+    rows=(s0, s1) generates only those series (a rank's shard)."""
     import os
 
     procs = procs or os.cpu_count() or 1
     dt = {"i16": np.int16, "f16": np.float16, "u8": np.uint8}[tag]
-    Y = _shared_array((S, L), dt)
+    s0, s1 = rows if rows is not None else (0, S)
+    Y = _shared_array((s1 - s0, L), dt)
     _SHARED["c5"] = Y
-    step = max(1, -(-S // (procs * 4)))
+    step = max(1, -(-(s1 - s0) // (procs * 4)))
     try:
-        with _pool(min(procs, S)) as pool:
-            pool.map(_c5_fill, [(tag, s, min(S, s + step), L) for s in range(0, S, step)])
+        with _pool(max(1, min(procs, s1 - s0))) as pool:
+            pool.map(_c5_fill_rows, [(tag, s, min(s1, s + step), L, s0) for s in range(s0, s1, step)])
     finally:
         _SHARED.pop("c5", None)
     return Y
