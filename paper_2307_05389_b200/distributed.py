@@ -318,10 +318,14 @@ class ShardedSeries:
     indices, identical on every rank and equal to the single-GPU call.
     """
 
-    def __init__(self, plan, rank, y_shard, x_shard=None, exchange=None, backend=None, nan=False, dtypes=None):
+    def __init__(self, plan, rank, y_shard, x_shard=None, exchange=None, backend=None, nan=False, dtypes=None,
+                 x_host=None):
         import torch
 
         self.plan, self.rank, self.nan = plan, rank, nan
+        # MinMaxLTTB with x kept on the host: the ~2*n_bins candidates' x bits are
+        # gathered there after the scan instead of shipping the whole x shard
+        self.x_host = x_host if plan.x_used and x_shard is None else None
         self.backend = backend
         self.exchange = exchange
         self.y = y_shard
@@ -340,8 +344,10 @@ class ShardedSeries:
             torch.cuda.synchronize(dev)
 
     @classmethod
-    def from_host(cls, plan, rank, x, y, exchange=None, backend=None, device=None, nan=False):
-        """Upload only this rank's element span of y (and x) to its GPU."""
+    def from_host(cls, plan, rank, x, y, exchange=None, backend=None, device=None, nan=False, x_on_device=True):
+        """Upload only this rank's element span of y (and of x, unless
+        x_on_device=False: then only the candidates' x values are read from
+        the host array, once per step) to its GPU."""
         import torch
 
         y = as_value_series(y)
@@ -359,13 +365,28 @@ class ShardedSeries:
             return t
 
         ys = put(y)
-        xs = put(x) if plan.x_used and x is not None else None
+        xs = put(x) if plan.x_used and x is not None and x_on_device else None
         dts = (CODE[y.dtype], CODE[x.dtype] if x is not None else 0)
-        return cls(plan, rank, ys, xs, exchange, backend, nan, dts)
+        return cls(plan, rank, ys, xs, exchange, backend, nan, dts, x_host=None if x_on_device else x)
+
+    def _fill_x_bits(self):
+        import torch
+
+        self.backend.synchronize()
+        cap = self.plan.cap
+        cnt = int(self.rec[0].item())
+        idx = self.rec[1 : 1 + cnt].cpu().numpy()
+        v = np.ascontiguousarray(self.x_host[idx])
+        bits = v.view({1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}[v.dtype.itemsize]).astype(np.uint64)
+        self.rec[1 + cap : 1 + cap + cnt].copy_(torch.from_numpy(bits.view(np.int64)))
+        if self.rec.is_cuda:
+            torch.cuda.synchronize(self.rec.device)
 
     def step(self):
         p = self.plan
         self.backend.shard_record(p, self.rank, self.y, self.ydt, self.x, self.xdt, self.off, self.rec, self.nan)
+        if self.x_host is not None and p.algo == "minmaxlttb":
+            self._fill_x_bits()
         self.exchange.allgather(self.rec, self.recv)
         ld = p.world * p.cap
         if p.algo in WIDTH:
@@ -410,7 +431,7 @@ def sharded_downsample(algo, *args, n_out, minmax_ratio=4, nan=False, group=None
         backend = GpuBackend(rank if device is None else device)
     if exchange is None:
         exchange = default_exchange(backend.ctx, group)
-    s = ShardedSeries.from_host(plan, rank, x, y, exchange, backend, nan=nan)
+    s = ShardedSeries.from_host(plan, rank, x, y, exchange, backend, nan=nan, x_on_device=False)
     s.step()
     return s.result()
 
