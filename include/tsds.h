@@ -61,7 +61,10 @@ const char *tsds_last_error(void);
  * "cta_bins_max_bytes" (inputs up to this size with >= #SM bins use the
  * CTA-per-bin scan; default 128 MiB, env TSDS_CTA_BINS_MAX_BYTES),
  * "lane_bins" (batched MinMax with short bins: thread-per-bin kernel; 0 off,
- * 1 auto, 2 whenever eligible; env TSDS_LANE_BINS), "lttb_exact" (centroid
+ * 1 auto, 2 whenever eligible; env TSDS_LANE_BINS), "atomic_bins" (scans of
+ * <= 32-bit values with >= #SM bins merge bin segments with 64-bit atomics
+ * and compact in a dependent one-CTA kernel; 0 off, 1 auto, 2 whenever
+ * eligible; env TSDS_ATOMIC_BINS), "lttb_exact" (centroid
  * summation of large-bucket LTTB: 0 auto = the reference's sequential order
  * for buckets <= 1024 points, a fixed tree above; 1 always sequential;
  * 2 always tree; env TSDS_LTTB_EXACT) */

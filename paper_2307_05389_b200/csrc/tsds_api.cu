@@ -67,7 +67,8 @@ struct tsds_ctx {
   bool own_stream = true;
   int sms = 148;
   std::mutex mu;
-  DevBuf y, x, xf64, part, bincnt, res, off, out, misc, cent, scratch, y2, x2, x2f64, full, out2, lscr;
+  DevBuf y, x, xf64, part, bincnt, res, off, out, misc, cent, scratch, y2, x2, x2f64, full, out2, lscr, amm;
+  bool amm_dirty = false;  // atomic-mode bin words need re-initialising (after a failed call)
   int64_t lttb_rounds = 0;  // verification rounds of the last large-bucket LTTB
   int64_t lttb_dirty1 = 0;  // buckets whose guess was wrong in the first round
   int64_t lttb_pieces = 0;  // pieces evaluated exactly (all rounds, after pruning)
@@ -169,6 +170,7 @@ int begin_call(tsds_ctx* ctx) {
   if (ctx->dirty) {
     // a failed call may have left arrival counters set: re-zero them
     if (ctx->bincnt.p) CUDA_TRY(cudaMemsetAsync(ctx->bincnt.p, 0, ctx->bincnt.cap, ctx->stream));
+    ctx->amm_dirty = true;
     ctx->dirty = false;
     ctx->flags_clean = false;
   }
@@ -191,6 +193,15 @@ int64_t lane_bins_mode() {
     g_lane_bins = e ? std::max(0, std::min(2, atoi(e))) : 1;
   }
   return g_lane_bins;
+}
+
+int64_t g_atomic_bins = -1;
+int64_t atomic_bins_mode() {
+  if (g_atomic_bins < 0) {
+    const char* e = getenv("TSDS_ATOMIC_BINS");
+    g_atomic_bins = e ? std::max(0, std::min(2, atoi(e))) : 1;
+  }
+  return g_atomic_bins;
 }
 
 // CTA-per-bin scan for inputs up to this many bytes (latency-bound sizes)
@@ -265,9 +276,28 @@ int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
   }
   const int64_t nchunks = A.n_static + A.n_dyn;
   const int64_t nbins = A.g1 - A.g0;
+  // atomic merge mode: keys of <= 32 bits and 32-bit indices, enough bins
+  // that no bin word is contended, a compacting epilogue (TSDS option
+  // atomic_bins: 0 off, 1 auto, 2 whenever eligible)
+  const int64_t am_mode = atomic_bins_mode();
+  const bool am_ok = ES <= 4 && !A.independent && A.E1 < ((int64_t)1 << 32) - 2 && A.epi != EPI_PAIR && nbins >= 1 &&
+                     nbins <= ((int64_t)1 << 16);
+  A.atomic_mode = am_ok && (am_mode == 2 || (am_mode == 1 && nbins >= (int64_t)ctx->sms)) ? 1 : 0;
   // small inputs split into many bins: CTA per bin (TSDS option cta_bins_max_bytes)
-  A.cta_bins = !A.independent && tv * ES <= cta_bins_max_bytes() && nbins >= (int64_t)ctx->sms &&
+  A.cta_bins = !A.atomic_mode && !A.independent && tv * ES <= cta_bins_max_bytes() && nbins >= (int64_t)ctx->sms &&
                tv / std::max<int64_t>(nbins, 1) >= 256 / ES;
+  if (A.atomic_mode) {
+    // [amin | amax] per bin, kept at (~0, 0) between launches by the finish kernel
+    if (ctx->amm.cap < (size_t)nbins * 16 || ctx->amm_dirty) {
+      RC_TRY(ensure(ctx, ctx->amm, (size_t)std::max<int64_t>(nbins, 4096) * 16));
+      const size_t half = ctx->amm.cap / 16 * 8;
+      CUDA_TRY(cudaMemsetAsync(ctx->amm.p, 0xff, half, ctx->stream));
+      CUDA_TRY(cudaMemsetAsync((char*)ctx->amm.p + half, 0, half, ctx->stream));
+      ctx->amm_dirty = false;
+    }
+    A.amin = (unsigned long long*)ctx->amm.p;
+    A.amax = (unsigned long long*)((char*)ctx->amm.p + ctx->amm.cap / 16 * 8);
+  }
   RC_TRY(ensure(ctx, ctx->part, (size_t)nchunks * 2 * sizeof(MinMaxCand)));
   RC_TRY(ensure(ctx, ctx->bincnt, (size_t)nbins * sizeof(unsigned), true));
   RC_TRY(ensure(ctx, ctx->res, (size_t)nbins * 2 * sizeof(int64_t)));
@@ -305,6 +335,19 @@ int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
   if (ctx->profile) {
     CUDA_TRY(cudaEventRecord(ev.second, ctx->stream));
     ctx->ev_used.push_back(ev);
+  }
+  if (A.atomic_mode) {
+    cudaLaunchConfig_t fc = {};
+    fc.gridDim = dim3(1);
+    fc.blockDim = dim3(1024);
+    fc.stream = ctx->stream;
+    cudaLaunchAttribute fa[1];
+    fa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    fa[0].val.programmaticStreamSerializationAllowed = 1;
+    fc.attrs = fa;
+    fc.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&fc, atomic_finish_kernel<DT, PROP>, A));
+    LAUNCH_CHECK();
   }
   return TSDS_OK;
 }
@@ -1085,6 +1128,7 @@ int tsds_set_option(const char* name, int64_t value) {
   std::string n(name);
   if (n == "dyn_percent") g_dyn_percent = std::max<int64_t>(0, std::min<int64_t>(90, value));
   else if (n == "lane_bins") g_lane_bins = std::max<int64_t>(0, std::min<int64_t>(2, value));
+  else if (n == "atomic_bins") g_atomic_bins = std::max<int64_t>(0, std::min<int64_t>(2, value));
   else if (n == "cta_bins_max_bytes") g_cta_bins_max = std::max<int64_t>(0, value);
   else if (n == "lttb_exact") g_lttb_exact = std::max<int64_t>(0, std::min<int64_t>(2, value));
   else return set_err(TSDS_ERR_ARG, "unknown option " + n);
@@ -1126,7 +1170,7 @@ void tsds_ctx_destroy(tsds_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->y, &ctx->x, &ctx->xf64, &ctx->part, &ctx->bincnt, &ctx->res, &ctx->off, &ctx->out,
                     &ctx->misc, &ctx->cent, &ctx->scratch, &ctx->y2, &ctx->x2, &ctx->x2f64, &ctx->full, &ctx->out2,
-                    &ctx->lscr})
+                    &ctx->lscr, &ctx->amm})
     if (b->p) cudaFree(b->p);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
   if (ctx->h_lstat) cudaFreeHost(ctx->h_lstat);

@@ -125,7 +125,25 @@ struct ScanArgs {
   int64_t idx_sub;     // subtracted from every output index
   int lttb_frame;      // 1: out[0]=0 and out[total+1]=n_frame-1 (MinMaxLTTB `full`)
   int64_t n_frame;
+  // atomic merge mode (keys of <= 32 bits, indices < 2^32): every bin
+  // segment merges into per-bin packed (key << 32 | index) words with 64-bit
+  // atomicMin / atomicMax; no arrival counters, no last-CTA ticket --
+  // atomic_finish_kernel (PDL-launched) turns them into picks and compacts
+  int atomic_mode;
+  unsigned long long* amin;  // [g1-g0], ~0 between launches
+  unsigned long long* amax;  // [g1-g0], 0 between launches
 };
+
+// packed (key, index) words whose unsigned order is the merge order:
+// min -> (key, index) ascending; max -> key ascending, index descending
+__device__ __forceinline__ unsigned long long pack_min(const Cand& c) {
+  const uint64_t k = c.key > 0xffffffffull ? 0xffffffffull : c.key;
+  return (k << 32) | (uint64_t)(uint32_t)c.idx;
+}
+__device__ __forceinline__ unsigned long long pack_max(const Cand& c) {
+  const uint64_t k = c.key > 0xffffffffull ? 0xffffffffull : c.key;
+  return (k << 32) | (uint64_t)(0xffffffffu - (uint32_t)c.idx);
+}
 
 __device__ __forceinline__ int64_t chunk_of(const ScanArgs& A, int64_t i) {
   int64_t v = i + A.shift - A.vstart;
@@ -480,7 +498,12 @@ __device__ __forceinline__ void process_chunk(const ScanArgs& A, const BinSpec& 
     int64_t se = e < ce ? e : ce;
     MinMaxCand r = seg_reduce<DT, PROP, U>(A, pos, se);
     bool before = s < cs, after = e > ce;
-    if (!before && !after) {
+    if (A.atomic_mode) {
+      if (lane == 0 && r.mn.idx != IDX_NONE) {
+        atomicMin(A.amin + (g - A.g0), pack_min(r.mn));
+        atomicMax(A.amax + (g - A.g0), pack_max(r.mx));
+      }
+    } else if (!before && !after) {
       if (lane == 0) finalize<DT, PROP>(A, B, g, r);
     } else {
       unsigned old = 0;
@@ -611,9 +634,10 @@ scan_kernel(const ScanArgs A) {
   if (A.use_dyn_mode) B.mode = *(volatile int*)&F->mode;
   const bool aborted = A.check_flags && *(volatile int*)&F->status;
   const bool indep = A.independent || (A.check_flags && *(volatile int*)&F->nonmono);
+  if (A.atomic_mode) pdl_launch_dependents();  // atomic_finish_kernel may start waiting
 
 #ifndef TSDS_NO_CTA_BINS
-  if (!aborted && A.cta_bins) {
+  if (!aborted && A.cta_bins && !A.atomic_mode) {
     // CTA per bin: every warp reduces a contiguous eighth of the bin, the
     // partials merge in shared memory (lexicographic (key, index) merges,
     // so the first occurrence wins in any order); one round trip per bin
@@ -668,7 +692,75 @@ scan_kernel(const ScanArgs A) {
     }
   }
 
+  if (A.atomic_mode) return;  // atomic_finish_kernel: picks, compaction, flag resets
   scan_epilogue(A, B, aborted);
+}
+
+// Atomic-mode epilogue, one CTA launched as the scan's programmatic
+// dependent: per bin the merged (key, index) words become the picks (the
+// reference's NaN-first-slot rule applied) and are reset for
+// the next launch; then the usual compaction / slot epilogue and the
+// pipeline-flag resets of scan_epilogue.
+template <int DT, bool PROP>
+__global__ void __launch_bounds__(1024) atomic_finish_kernel(const ScanArgs A) {
+  pdl_wait();
+  PipeFlags* F = A.flags;
+  BinSpec B = A.bins;
+  if (A.use_dyn_mode) B.mode = *(volatile int*)&F->mode;
+  const bool aborted = A.check_flags && *(volatile int*)&F->status;
+  const bool indep = A.independent || (A.check_flags && *(volatile int*)&F->nonmono);
+  for (int64_t g = A.g0 + threadIdx.x; g < A.g1; g += blockDim.x) {
+    const unsigned long long am = __ldcg(A.amin + (g - A.g0)), ax = __ldcg(A.amax + (g - A.g0));
+    A.amin[g - A.g0] = ~0ull;
+    A.amax[g - A.g0] = 0ull;
+    if (aborted || indep) continue;  // indep: the scan's per-bin path already wrote res
+    const int64_t s = bin_off(B, g), e = bin_off(B, g + 1);
+    if (e <= s) continue;
+    int64_t lo = (int64_t)(uint32_t)am, hi = (int64_t)(0xffffffffu - (uint32_t)ax);
+    if constexpr (!PROP && Ops<DT>::IEEE) {
+      if (elem_is_nan<DT>(A.y, s)) { lo = s; hi = s; }
+    }
+    int64_t* o = A.res + 2 * (g - A.g0);
+    o[0] = lo;
+    o[1] = hi;
+  }
+  __syncthreads();
+  if (aborted) {
+    if (threadIdx.x == 0) {
+      if (A.epi == EPI_SLOTS_MINMAX || A.epi == EPI_SLOTS_M4) {
+        for (int64_t g = A.g0; g < A.g1; g++) A.out_count[g] = 0;
+      } else if (A.epi != EPI_PAIR && A.out_count) {
+        *A.out_count = 0;
+      }
+    }
+  } else if (A.epi == EPI_SLOTS_MINMAX || A.epi == EPI_SLOTS_M4) {
+    cta_slots(A, B);
+  } else if (A.out && A.epi != EPI_PAIR) {
+    int64_t* out = A.out + (A.lttb_frame ? 1 : 0);
+    int64_t tot = cta_compact(A, B, A.g0, A.g1, out, A.idx_sub);
+    if (threadIdx.x == 0) {
+      if (A.lttb_frame) {
+        A.out[0] = 0;
+        A.out[tot + 1] = A.n_frame - 1;
+        tot += 2;
+      }
+      *A.out_count = tot;
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (A.status_out) {
+      A.status_out[0] = *(volatile int*)&F->status;
+      A.status_out[1] = *(volatile int*)&F->mis_api;
+    }
+    if (A.reset_flags) {
+      F->mis_api = 0;
+      F->mis_slice = 0;
+      F->status = 0;
+      F->nonmono = 0;
+      F->mode = 0;
+    }
+    F->work_ctr = 0ull;
+  }
 }
 
 // batched compaction: one CTA per series (bins [s*nb, (s+1)*nb))

@@ -296,3 +296,43 @@ def test_lttb_large_vector_paths(ts, oracle):
     assert ts.downsample("lttb", big, n_out=60_000).tolist() == oracle.downsample("lttb", big, n_out=60_000).tolist()
     yd = torch.from_numpy(base).cuda()[1:]
     assert ts.downsample("lttb", yd, n_out=1000).tolist() == oracle.downsample("lttb", base[1:], n_out=1000).tolist()
+
+
+@pytest.mark.parametrize("mode", [0, 2])
+def test_atomic_bin_merge_mode(ts, oracle, mode):
+    """Atomic merge mode (64-bit packed (key, index) atomics + dependent
+    compaction kernel) forced on (2) and off (0): every <= 32-bit dtype,
+    ties, NaN in first slots, NaN-propagating, device x with non-monotone
+    offsets, the slot writers and MinMaxLTTB preselection."""
+    import torch
+
+    from paper_2307_05389_b200 import _lib
+
+    L = _lib.load()
+    rng = np.random.default_rng(41)
+    try:
+        L.tsds_set_option(b"atomic_bins", mode)
+        for tag in ("f32", "f16", "i8", "u8", "i16", "u16", "i32", "u32"):
+            y = W.random_series(tag, 250_003, int(rng.integers(1 << 30)), ties=True)
+            if tag in ("f32", "f16"):
+                y[rng.integers(0, y.size, 200)] = np.nan
+                y[[0, 1250, 2500]] = np.nan
+            x = np.cumsum(rng.integers(1, 9, y.size)).astype(np.int64)
+            for algo, n_out in (("minmax", 2000), ("m4", 400), ("minmax", 6), ("minmaxlttb", 300)):
+                want = oracle.downsample(algo, y, n_out=n_out)
+                assert ts.downsample(algo, y, n_out=n_out).tolist() == want.tolist(), (tag, algo, n_out)
+                want = oracle.downsample(algo, x, y, n_out=n_out)
+                assert ts.downsample(algo, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(),
+                                     n_out=n_out).tolist() == want.tolist(), (tag, algo, n_out, "dev x")
+            if tag in ("f32", "f16"):
+                got = ts.downsample("nanm4", y, n_out=2000).tolist()
+                assert got == oracle.downsample("m4", y, n_out=2000, nan=True).tolist(), (tag, "nanm4")
+        # non-monotone device x: independent bins
+        y = W.random_series("f32", 100_000, 3, ties=True)
+        x = np.cumsum(rng.integers(1, 9, y.size)).astype(np.int64)
+        x[50_000:50_100] = x[50_000:50_100][::-1]
+        want = oracle.downsample("minmax", x, y, n_out=1000)
+        assert ts.downsample("minmax", torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(),
+                             n_out=1000).tolist() == want.tolist()
+    finally:
+        L.tsds_set_option(b"atomic_bins", 1)

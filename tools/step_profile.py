@@ -21,6 +21,7 @@ def main():
     ap.add_argument("config")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--flush", default="auto", choices=["auto", "none", "write"])
     a = ap.parse_args()
     r = B.GpuRunner(0)
     x, y = B.data_for(a.config)
@@ -28,8 +29,10 @@ def main():
     for _ in range(a.warmup):
         step()
     r.torch.cuda.synchronize()
-    flush = B.algorithmic_bytes(a.config, y) < (126 << 20)
+    flush = B.algorithmic_bytes(a.config, y) < (126 << 20) if a.flush == "auto" else a.flush != "none"
     ms, launches = r.time_steps(step, a.steps, flush)
+    kms, kper = r.kernel_ms(step, a.steps, flush)
+    print(f"  streaming kernel {kms * 1e3:.1f} us x {kper}/step", flush=True)
     print(f"{a.config}: {ms / a.steps:.4f} ms/step, {launches / a.steps:.1f} launches/step", flush=True)
     del keep
 
