@@ -13,7 +13,8 @@ and ``configs`` holds one entry per BASELINE config (C1, C2, C3 at n_out
                 MinMaxLTTB's stage 2 included, no host round trip), timed with
                 CUDA events on the library's stream, K steps after W warm-ups.
                 Inputs smaller than L2 (C1) get an L2 flush between steps
-                (a 256 MB write, 2x the L2, outside the events).
+                (a 256 MB write, 2x the L2, then a 256 MB read so that
+                the L2 holds clean lines; both outside the events).
   roofline      the step's streaming kernel (the one pass over y): algorithmic
                 bytes per launch / its mean CUDA-event duration (second pass,
                 events around that kernel only) vs MEASURED_PEAKS.json hbm_gbs;
@@ -291,11 +292,15 @@ class GpuRunner:
         self.flush_w = None
 
     def flush_l2(self):
-        """Write a buffer of 2x the L2 capacity (the timing rule's flush)."""
+        """Write a buffer of 2x the L2 capacity (the timing rule's flush), then
+        read a second one: the write alone leaves the L2 full of dirty lines
+        whose write-back would be charged to the timed kernel's reads."""
         torch = self.torch
         if self.flush_w is None:
             self.flush_w = torch.empty(L2_FLUSH, dtype=torch.uint8, device=f"cuda:{self.dev}")
+            self.flush_r = torch.zeros(L2_FLUSH // 4, dtype=torch.int32, device=f"cuda:{self.dev}")
         self.flush_w.fill_(3)
+        self.flush_r.max()
 
     def make_step(self, key, x, y):
         """(step() enqueuing one async call, result() -> host result) on device-resident copies."""
@@ -406,7 +411,7 @@ def measure_config(key, runner, args, clk, cpu, peak, peak_kind):
         "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "ms_per_step": round(ms_step, 5),
         "points_per_s": round(npts / (ms_step * 1e-3), 1), "algorithmic_bytes_per_step": nbytes,
         "steps": args.steps, "warmup": args.warmup, "config": config_dict(key),
-        "l2": "flushed between steps (256 MB write, 2x L2)" if flush else
+        "l2": "flushed between steps (256 MB write + 256 MB read, 2x L2 each)" if flush else
               f"inputs ({nbytes / 1e9:.2f} GB) larger than L2 (126 MB); no flush",
         "parity": "equal to the reference's output (tests/golden/configs.npz)",
         "gpu_launches": int(launches),

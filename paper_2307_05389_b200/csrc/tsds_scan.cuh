@@ -135,14 +135,23 @@ struct ScanArgs {
 };
 
 // packed (key, index) words whose unsigned order is the merge order:
-// min -> (key, index) ascending; max -> key ascending, index descending
-__device__ __forceinline__ unsigned long long pack_min(const Cand& c) {
-  const uint64_t k = c.key > 0xffffffffull ? 0xffffffffull : c.key;
-  return (k << 32) | (uint64_t)(uint32_t)c.idx;
+// min -> (key, index) ascending; max -> key ascending, index descending.
+// key32: the candidate's 64-bit key narrowed to an order-preserving 32-bit
+// one (int32 keys are sign-extended with the top bit flipped: their low word
+// with bit 31 flipped keeps the order; every other <= 32-bit dtype already
+// has keys below 2^32, the NaN-propagating sentinels 0 / 2^64-1 clamp)
+template <int DT>
+__device__ __forceinline__ uint64_t key32(uint64_t key) {
+  if constexpr (DT == DT_I32) return (uint64_t)((uint32_t)key ^ 0x80000000u);
+  else return key > 0xffffffffull ? 0xffffffffull : key;
 }
+template <int DT>
+__device__ __forceinline__ unsigned long long pack_min(const Cand& c) {
+  return (key32<DT>(c.key) << 32) | (uint64_t)(uint32_t)c.idx;
+}
+template <int DT>
 __device__ __forceinline__ unsigned long long pack_max(const Cand& c) {
-  const uint64_t k = c.key > 0xffffffffull ? 0xffffffffull : c.key;
-  return (k << 32) | (uint64_t)(0xffffffffu - (uint32_t)c.idx);
+  return (key32<DT>(c.key) << 32) | (uint64_t)(0xffffffffu - (uint32_t)c.idx);
 }
 
 __device__ __forceinline__ int64_t chunk_of(const ScanArgs& A, int64_t i) {
@@ -500,8 +509,8 @@ __device__ __forceinline__ void process_chunk(const ScanArgs& A, const BinSpec& 
     bool before = s < cs, after = e > ce;
     if (A.atomic_mode) {
       if (lane == 0 && r.mn.idx != IDX_NONE) {
-        atomicMin(A.amin + (g - A.g0), pack_min(r.mn));
-        atomicMax(A.amax + (g - A.g0), pack_max(r.mx));
+        atomicMin(A.amin + (g - A.g0), pack_min<DT>(r.mn));
+        atomicMax(A.amax + (g - A.g0), pack_max<DT>(r.mx));
       }
     } else if (!before && !after) {
       if (lane == 0) finalize<DT, PROP>(A, B, g, r);

@@ -1,26 +1,25 @@
 #!/bin/bash
-# Round-end evidence (run under gpurun, 1 GPU).  Outputs land in gpurun_out/;
-# tools/summarize_ncu.py and tools/lttb_table.py turn them into profiles/<tag>_*.
-TAG=${1:-r01}
-python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
-python tools/configs_time.py > gpurun_out/${TAG}_configs.md 2> gpurun_out/${TAG}_configs.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-    --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu \
-    > gpurun_out/${TAG}_ncu_launches.log 2>&1
-python tools/profile_scan.py c2 3 > gpurun_out/${TAG}_plain_c2.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s 1 -c 1 \
-    -o gpurun_out/${TAG}_scan_c2 -f python tools/profile_scan.py c2 3 > gpurun_out/${TAG}_ncu_full.log 2>&1
-for n in 1000 10000; do
-  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-      --cache-control none --csv --log-file gpurun_out/${TAG}_lttb_launches_$n.csv \
-      python tools/profile_lttb.py $n 2 > gpurun_out/${TAG}_ncu_lttb_$n.log 2>&1
+# Round evidence (run under gpurun, 1 GPU): for every bench config a plain run, an ncu
+# launch list (per-launch duration + DRAM bytes) and one `ncu --set full` capture of the
+# config's streaming kernel; tools/summarize_round.py turns them into profiles/<tag>_*.
+# usage: bash tools/profile_round.sh r02 [configs...]
+TAG=${1:-r02}; shift
+KEYS=${@:-C1 C2 C3_1000 C3_10000 C4 C5_i16 C5_u8 C5_f16}
+mkdir -p gpurun_out
+declare -A KREGEX=( [C1]=scan_kernel [C2]=scan_kernel [C3_1000]=lttb_sb_kernel [C3_10000]=lttb_guess_kernel
+                    [C4]=scan_kernel [C5_i16]=scan_kernel [C5_u8]=lane_bins_kernel [C5_f16]=lane_bins_kernel )
+for K in $KEYS; do
+  python tools/step_profile.py $K --steps 5 --warmup 3 > gpurun_out/${TAG}_plain_$K.log 2>&1 || { echo "plain $K failed"; continue; }
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+      --log-file gpurun_out/${TAG}_launches_$K.csv python tools/step_profile.py $K --steps 2 --warmup 1 --flush none \
+      > gpurun_out/${TAG}_ncu_launches_$K.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:${KREGEX[$K]} -s 2 -c 1 \
+      -o gpurun_out/${TAG}_full_$K -f python tools/step_profile.py $K --steps 2 --warmup 1 --flush none \
+      > gpurun_out/${TAG}_ncu_full_$K.log 2>&1
+  echo "$K: $(tail -1 gpurun_out/${TAG}_plain_$K.log)"
 done
-ncu --set full --clock-control none --import-source on -k regex:lttb_sb_kernel -s 1 -c 1 \
-    -o gpurun_out/${TAG}_lttb_sb -f python tools/profile_lttb.py 1000 2 > gpurun_out/${TAG}_ncu_lttb_sb.log 2>&1
-
-# summarise on the box (ncu -i), keep the summaries, drop the large reports
-mkdir -p gpurun_out/prof_${TAG}
-PROF_DIR=gpurun_out/prof_${TAG} python tools/summarize_ncu.py ${TAG} > /dev/null 2>&1
-ncu -i gpurun_out/${TAG}_lttb_sb.ncu-rep --page details --csv > gpurun_out/prof_${TAG}/${TAG}_lttb_sb_details.csv 2>/dev/null
-rm -f gpurun_out/*.ncu-rep
-echo summarised
+python tools/summarize_round.py $TAG --on-box > gpurun_out/${TAG}_summarize.log 2>&1
+# keep the reports small enough to travel: drop the big ones
+du -sh gpurun_out/*.ncu-rep 2>/dev/null | tail -20
+find gpurun_out -name '*.ncu-rep' -size +6M -delete
+echo profiled
