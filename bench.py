@@ -426,8 +426,17 @@ def measure_config(key, runner, args, clk, cpu, peak, peak_kind):
     }
     del keep
     runner.torch.cuda.empty_cache()
-    # ---- e2e through the public API, host (pageable) numpy inputs
+    # ---- e2e through the public API, host numpy inputs.  Call 1 sees fresh pageable arrays
+    # (staging ring); the library's pin-on-reuse cache (pinning.py) page-locks an array the
+    # second time it is passed, so the timed steady-state calls are DMA'd from pinned memory.
+    from paper_2307_05389_b200 import pinning
+
+    t0 = time.perf_counter()
     e2e_call(key, x, y)
+    first_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    e2e_call(key, x, y)
+    second_s = time.perf_counter() - t0
     n_e2e = 3
     t0 = time.perf_counter()
     for _ in range(n_e2e):
@@ -439,9 +448,17 @@ def measure_config(key, runner, args, clk, cpu, peak, peak_kind):
     else:
         assert golden_ok(key, r), f"{key}: e2e result differs"
     d2h = s["n_out"] * 8 * (s["S"] if "S" in s else 1) + 16
+    pinned = pinning.pinned_bytes() > 0
     entry["e2e"] = {"value": round(nbytes / e2e_s / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": nbytes,
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_s * 1e3, 3),
-                    "path": "public API on pageable host numpy (H2D of y, binning, kernels, index readback)"}
+                    "path": "public API on host numpy (H2D of y, binning, kernels, index readback every step); "
+                            "steady state of repeated calls on the same arrays"
+                            + (": y page-locked in place by the pin-on-reuse cache on its 2nd call" if pinned else
+                               " (input below the pin threshold: direct pageable copy)"),
+                    "first_call": {"value": round(nbytes / first_s / 1e9, 3), "ms": round(first_s * 1e3, 3),
+                                   "path": "fresh pageable arrays through the staging ring"},
+                    "second_call_ms": round(second_s * 1e3, 3), "host_input_pinned": bool(pinned)}
+    pinning.release_all()
     if cpu is not None:
         med, k = cpu_time(key, x, y, cpu["cores"], args.cpu_steps, 1)
         entry["cpu_baseline"] = {"value": round(nbytes / med / 1e9, 3), "unit": "GB/s", "cores": cpu["cores"],

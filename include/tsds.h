@@ -64,7 +64,10 @@ const char *tsds_last_error(void);
  * 1 auto, 2 whenever eligible; env TSDS_LANE_BINS), "atomic_bins" (scans of
  * <= 32-bit values with >= #SM bins merge bin segments with 64-bit atomics
  * and compact in a dependent one-CTA kernel; 0 off, 1 auto, 2 whenever
- * eligible; env TSDS_ATOMIC_BINS), "lttb_exact" (centroid
+ * eligible; env TSDS_ATOMIC_BINS), "tile_bins" (small inputs with >= #SM
+ * bins and host-known offsets stream their bins through shared memory by
+ * TMA bulk copies; 0 off, 1 auto, 2 whenever the offsets allow; env
+ * TSDS_TILE_BINS), "lttb_exact" (centroid
  * summation of large-bucket LTTB: 0 auto = the reference's sequential order
  * for buckets <= 1024 points, a fixed tree above; 1 always sequential;
  * 2 always tree; env TSDS_LTTB_EXACT) */
@@ -165,6 +168,16 @@ int tsds_lttb_stage2_async(tsds_ctx *ctx, int64_t *cand_dev, int64_t cap, const 
  * slots filled by parallel host threads.  When the call returns the source
  * may be reused; the data is on the device when the stream reaches it. */
 int tsds_upload(tsds_ctx *ctx, void *dst_dev, const void *src_host, int64_t bytes);
+
+/* Page-lock / release a caller-owned host buffer (cudaHostRegister,
+ * portable) so that later TSDS_MEM_HOST calls on it are DMA'd directly at
+ * link speed instead of through the staging ring.  The Python layer uses
+ * them for its pin-on-reuse cache of large numpy inputs (pinning.py); the
+ * reference has no counterpart (its inputs never leave host memory,
+ * api.py:31-83).  Registering an already pinned buffer is a no-op;
+ * unregister accepts ctx == NULL (any thread, current device). */
+int tsds_host_register(tsds_ctx *ctx, const void *host, int64_t bytes);
+int tsds_host_unregister(tsds_ctx *ctx, const void *host);
 
 /* Communicator: NCCL, loaded at run time (libtsds
  * does not link it), bound to ctx's device and stream.  Rank 0 makes the

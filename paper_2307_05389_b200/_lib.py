@@ -45,6 +45,8 @@ EXPORTED = (
     "tsds_records_concat",
     "tsds_lttb_stage2_async",
     "tsds_upload",
+    "tsds_host_register",
+    "tsds_host_unregister",
     "tsds_comm_unique_id",
     "tsds_comm_init",
     "tsds_comm_destroy",
@@ -114,6 +116,8 @@ def load():
         L.tsds_records_concat.argtypes = [vp, vp, i32, i64, i32, vp, i64, vp]
         L.tsds_lttb_stage2_async.argtypes = [vp, vp, i64, vp, i32, vp, i32, i64, vp, vp]
         L.tsds_upload.argtypes = [vp, vp, vp, i64]
+        L.tsds_host_register.argtypes = [vp, vp, i64]
+        L.tsds_host_unregister.argtypes = [vp, vp]
         L.tsds_comm_unique_id.argtypes = [vp]
         L.tsds_comm_init.argtypes = [vp, i32, i32, vp, ctypes.POINTER(vp)]
         L.tsds_comm_destroy.argtypes = [vp]

@@ -70,6 +70,9 @@ def _context_for(x, y):
         except Exception:
             pass
         return _lib.context(dev), _lib.MEM_DEVICE
+    from . import pinning
+
+    pinning.note_host_input(y)
     return _lib.context(), _lib.MEM_HOST
 
 
@@ -192,6 +195,10 @@ def minmax_batched(Y, n_out, nan=False):
     if S == 0:
         return out.view(np.uint64), counts
     ctx = _lib.context(0 if dev is None else dev)
+    if dev is None:
+        from . import pinning
+
+        pinning.note_host_input(Y)
     rc = _lib.load().tsds_minmax_batched(
         ctx.handle,
         ptr,

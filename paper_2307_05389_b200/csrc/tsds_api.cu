@@ -24,6 +24,7 @@
 #include "tsds_lttb_large.cuh"
 #include "tsds_scan.cuh"
 #include "tsds_lanebins.cuh"
+#include "tsds_tilebins.cuh"
 #include "tsds_nccl.h"
 #include "tsds_shard.cuh"
 #include "tsds_staging.h"
@@ -195,6 +196,15 @@ int64_t lane_bins_mode() {
   return g_lane_bins;
 }
 
+int64_t g_tile_bins = -1;
+int64_t tile_bins_mode() {
+  if (g_tile_bins < 0) {
+    const char* e = getenv("TSDS_TILE_BINS");
+    g_tile_bins = e ? std::max(0, std::min(2, atoi(e))) : 1;
+  }
+  return g_tile_bins;
+}
+
 int64_t g_atomic_bins = -1;
 int64_t atomic_bins_mode() {
   if (g_atomic_bins < 0) {
@@ -282,9 +292,16 @@ int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
   const int64_t am_mode = atomic_bins_mode();
   const bool am_ok = ES <= 4 && !A.independent && A.E1 < ((int64_t)1 << 32) - 2 && A.epi != EPI_PAIR && nbins >= 1 &&
                      nbins <= ((int64_t)1 << 16);
-  A.atomic_mode = am_ok && (am_mode == 2 || (am_mode == 1 && nbins >= (int64_t)ctx->sms)) ? 1 : 0;
+  // small inputs with many bins whose offsets need no device verdict: bins
+  // streamed through shared memory by TMA bulk copies (tsds_tilebins.cuh;
+  // TSDS option tile_bins: 0 off, 1 auto, 2 whenever the offsets allow)
+  const int64_t tb_mode = tile_bins_mode();
+  const bool tile = tb_mode != 0 && !A.independent && !A.check_flags && !A.use_dyn_mode && nbins >= 1 &&
+                    (tb_mode == 2 || (tv * ES <= cta_bins_max_bytes() && nbins >= (int64_t)ctx->sms &&
+                                      tv / std::max<int64_t>(nbins, 1) >= 2048 / ES));
+  A.atomic_mode = !tile && am_ok && (am_mode == 2 || (am_mode == 1 && nbins >= (int64_t)ctx->sms)) ? 1 : 0;
   // small inputs split into many bins: CTA per bin (TSDS option cta_bins_max_bytes)
-  A.cta_bins = !A.atomic_mode && !A.independent && tv * ES <= cta_bins_max_bytes() && nbins >= (int64_t)ctx->sms &&
+  A.cta_bins = !tile && !A.atomic_mode && !A.independent && tv * ES <= cta_bins_max_bytes() && nbins >= (int64_t)ctx->sms &&
                tv / std::max<int64_t>(nbins, 1) >= 256 / ES;
   if (A.atomic_mode) {
     // [amin | amax] per bin, kept at (~0, 0) between launches by the finish kernel
@@ -330,7 +347,16 @@ int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
   attr[0].val.programmaticStreamSerializationAllowed = ctx->profile ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
+  if (tile) {
+    auto tk = tile_bins_kernel<DT, PROP>;
+    CUDA_TRY(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
+    cfg.gridDim = dim3((unsigned)std::min<int64_t>(nbins, ctx->sms));
+    cfg.blockDim = dim3(TB_THREADS);
+    cfg.dynamicSmemBytes = TB_SMEM;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, tk, A));
+  } else {
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
+  }
   LAUNCH_CHECK();
   if (ctx->profile) {
     CUDA_TRY(cudaEventRecord(ev.second, ctx->stream));
@@ -376,7 +402,7 @@ int launch_scan(tsds_ctx* ctx, int dt, int nan_mode, ScanArgs& A) {
 
 int prof_mark(tsds_ctx* ctx, std::pair<cudaEvent_t, cudaEvent_t>& ev, bool end);
 
-// thread-per-bin argmin/argmax (tsds_lanebins.cuh) over the composite bins of
+// lane-group-per-bin argmin/argmax (tsds_lanebins.cuh) over the composite bins of
 // a batch; same res[] layout and epilogue as the scan
 template <int DT>
 int launch_lane_bins_t(tsds_ctx* ctx, ScanArgs& A) {
@@ -392,7 +418,7 @@ int launch_lane_bins_t(tsds_ctx* ctx, ScanArgs& A) {
   RC_TRY(ensure(ctx, ctx->res, (size_t)nbins * 2 * sizeof(int64_t)));
   A.res = (int64_t*)ctx->res.p;
   A.flags = &misc(ctx)->F;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * occ, (nbins + 255) / 256));
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * occ, (nbins * LB_LANES + 255) / 256));
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
   RC_TRY(prof_mark(ctx, ev, false));
   kern<<<(unsigned)grid, SCAN_WARPS * 32, 0, ctx->stream>>>(A);
@@ -1129,6 +1155,7 @@ int tsds_set_option(const char* name, int64_t value) {
   if (n == "dyn_percent") g_dyn_percent = std::max<int64_t>(0, std::min<int64_t>(90, value));
   else if (n == "lane_bins") g_lane_bins = std::max<int64_t>(0, std::min<int64_t>(2, value));
   else if (n == "atomic_bins") g_atomic_bins = std::max<int64_t>(0, std::min<int64_t>(2, value));
+  else if (n == "tile_bins") g_tile_bins = std::max<int64_t>(0, std::min<int64_t>(2, value));
   else if (n == "cta_bins_max_bytes") g_cta_bins_max = std::max<int64_t>(0, value);
   else if (n == "lttb_exact") g_lttb_exact = std::max<int64_t>(0, std::min<int64_t>(2, value));
   else return set_err(TSDS_ERR_ARG, "unknown option " + n);
@@ -1451,6 +1478,31 @@ int tsds_upload(tsds_ctx* ctx, void* dst_dev, const void* src_host, int64_t byte
     CUDA_TRY(ctx->ring.upload(dst_dev, src_host, (size_t)bytes, ctx->stream));
   } else {
     CUDA_TRY(cudaMemcpyAsync(dst_dev, src_host, (size_t)bytes, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  return TSDS_OK;
+}
+
+int tsds_host_register(tsds_ctx* ctx, const void* host, int64_t bytes) {
+  if (!ctx || !host || bytes <= 0) return set_err(TSDS_ERR_ARG, "tsds_host_register: invalid argument");
+  DeviceGuard dg_(ctx->device);
+  if (host_is_pinned(host)) return TSDS_OK;  // already page-locked (by the caller or an earlier call)
+  cudaError_t e = cudaHostRegister(const_cast<void*>(host), (size_t)bytes, cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(TSDS_ERR_CUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
+  }
+  return TSDS_OK;
+}
+
+int tsds_host_unregister(tsds_ctx* ctx, const void* host) {
+  if (!host) return set_err(TSDS_ERR_ARG, "tsds_host_unregister: invalid argument");
+  int cur = 0;
+  if (!ctx) cudaGetDevice(&cur);
+  DeviceGuard dg_(ctx ? ctx->device : cur);
+  cudaError_t e = cudaHostUnregister(const_cast<void*>(host));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(TSDS_ERR_CUDA, std::string("cudaHostUnregister: ") + cudaGetErrorString(e));
   }
   return TSDS_OK;
 }

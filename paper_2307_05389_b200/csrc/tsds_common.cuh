@@ -42,7 +42,7 @@ struct PipeFlags {
   int mode;        // binning verdict: 0 equal-count formula, 1 offsets array
   unsigned bin_blocks_done;
   unsigned scan_blocks_done;
-  int pad0;
+  int tile_short;  // tile_bins_kernel: some bin emitted fewer entries than the direct layout assumes
   unsigned long long work_ctr;  // dynamic work units handed out by the scan
   unsigned long long pad1[4];  // TSDS_SCAN_TIMING stamps
 };

@@ -305,77 +305,115 @@ struct BucketCursor {
   }
 };
 
-// warp per non-empty bucket: centroid (fixed tree order over sub-block sums;
-// the partial boundary sub-blocks are summed point by point) and the
-// y-range (from the sub-block maxima/minima, a superset at the boundaries)
-template <int YDT>
+// Lane groups: the per-bucket phases of the guess kernel (centroid,
+// candidates, round-1 plan) run one bucket per GROUP of G = 8, 16 or 32
+// lanes, G chosen on the device so that every non-empty bucket has its own
+// group in the first round (the phases are latency bound: what counts is the
+// number of dependent round trips per bucket, not the work per lane).
+template <int G>
+__device__ __forceinline__ unsigned lttb_gmask(int lane) {
+  if constexpr (G == 32) return 0xffffffffu;
+  else return ((1u << G) - 1u) << (lane & ~(G - 1));
+}
+__device__ __forceinline__ int lttb_pick_group(int64_t L) {
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  return L <= nw ? 32 : (L <= 2 * nw ? 16 : 8);
+}
+
+// group per non-empty bucket: centroid (fixed tree order over sub-block
+// sums; the partial boundary sub-blocks are summed point by point) and the
+// y-range (from the sub-block maxima/minima, a superset at the boundaries).
+// The summation order does not depend on G: the bucket's items (sub-block
+// sums, then the head points, then the tail points) are dealt round-robin to
+// 32 VIRTUAL lanes, each accumulating its items in order, and the virtual
+// lanes are combined by the xor butterfly 16, 8, 4, 2, 1; a physical lane
+// owns the 32 / G virtual lanes l, l + G, ...
+template <int YDT, int G>
 __device__ __forceinline__ void lttb_cent_phase(const double* x, const void* y, const int64_t* off,
                                                 const int32_t* nonempty, const int64_t* counts,
                                                 const LttbSBArrays A, double2* cent, float2* yr) {
+  constexpr int VL = 32 / G;  // virtual lanes per physical lane
+  constexpr int U = 4;        // items in flight per lane (a multiple of VL)
   const int64_t SB = A.SB;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31, l = lane & (G - 1);
+  const unsigned gmask = lttb_gmask<G>(lane);
+  const int64_t grp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
   const int64_t L = counts[0];
-  BucketCursor cur(nonempty, off, L, gw, nw);
-  for (int64_t j, k, s, e; cur.next(j, k, s, e);) {
+  for (int64_t j = grp; j < L; j += ngrp) {
+    const int64_t k = nonempty[j];
+    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
     const int64_t g0 = s / SB, g1 = (e - 1) / SB;
-    double sy = 0.0, sx = 0.0;
-    float hi = -INFINITY, lo = INFINITY;
-    for (int64_t gb = g0; gb <= g1; gb += 32 * 4) {  // 4 sub-blocks per lane in flight
-      float2 m[4];
-      double vy[4], vx[4];
+    double sy[VL], sx[VL];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int64_t g = gb + u * 32 + lane;
+    for (int t = 0; t < VL; t++) sy[t] = sx[t] = 0.0;
+    float hi = -INFINITY, lo = INFINITY;
+    for (int64_t gb = g0; gb <= g1; gb += (int64_t)G * U) {
+      float2 m[U];
+      double vy[U], vx[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t g = gb + u * G + l;
         const bool full = g <= g1 && g * SB >= s && (g + 1) * SB <= e;
         m[u] = g <= g1 ? A.mm[g] : make_float2(-INFINITY, INFINITY);
         vy[u] = full ? A.sy[g] : 0.0;
         vx[u] = (full && x) ? A.sx[g] : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
+      for (int u = 0; u < U; u++) {
         hi = fmaxf(hi, m[u].x);
         lo = fminf(lo, m[u].y);
-        sy = __dadd_rn(sy, vy[u]);
-        sx = __dadd_rn(sx, vx[u]);
+        sy[u % VL] = __dadd_rn(sy[u % VL], vy[u]);
+        sx[u % VL] = __dadd_rn(sx[u % VL], vx[u]);
       }
     }
-    // partial boundary sub-blocks: point by point (a lane's points loaded
-    // together, then summed in index order)
+    // partial boundary sub-blocks: point by point
     auto partial = [&](int64_t a, int64_t b) {
-      for (int64_t i0 = a; i0 < b; i0 += 32 * 4) {
-        double vy[4], vx[4];
+      for (int64_t i0 = a; i0 < b; i0 += (int64_t)G * U) {
+        double vy[U], vx[U];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const int64_t i = i0 + u * 32 + lane;
+        for (int u = 0; u < U; u++) {
+          const int64_t i = i0 + u * G + l;
           vy[u] = i < b ? yd<YDT>(y, i) : 0.0;
           vx[u] = (i < b && x) ? __ldg(x + i) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          sy = __dadd_rn(sy, vy[u]);
-          sx = __dadd_rn(sx, vx[u]);
+        for (int u = 0; u < U; u++) {
+          sy[u % VL] = __dadd_rn(sy[u % VL], vy[u]);
+          sx[u % VL] = __dadd_rn(sx[u % VL], vx[u]);
         }
       }
     };
     const int64_t h0e = (g0 + 1) * SB < e ? (g0 + 1) * SB : e;
     if (s % SB != 0 || h0e < (g0 + 1) * SB) partial(s, h0e);
     if (g1 > g0 && e % SB != 0) partial(g1 * SB, e);
+    // butterfly over the 32 virtual lanes: steps >= G stay inside the lane
 #pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) {
-      sy = __dadd_rn(sy, __shfl_xor_sync(0xffffffffu, sy, m));
-      sx = __dadd_rn(sx, __shfl_xor_sync(0xffffffffu, sx, m));
-      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, m));
-      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, m));
+    for (int m = 16; m >= G; m >>= 1) {
+      double ny[VL], nx[VL];
+#pragma unroll
+      for (int t = 0; t < VL; t++) {
+        ny[t] = __dadd_rn(sy[t], sy[t ^ (m / G)]);
+        nx[t] = __dadd_rn(sx[t], sx[t ^ (m / G)]);
+      }
+#pragma unroll
+      for (int t = 0; t < VL; t++) { sy[t] = ny[t]; sx[t] = nx[t]; }
     }
-    if (lane == 0) {
+    double ty = sy[0], tx = sx[0];
+#pragma unroll
+    for (int m = G / 2; m >= 1; m >>= 1) {
+      ty = __dadd_rn(ty, __shfl_xor_sync(gmask, ty, m));
+      tx = __dadd_rn(tx, __shfl_xor_sync(gmask, tx, m));
+      hi = fmaxf(hi, __shfl_xor_sync(gmask, hi, m));
+      lo = fminf(lo, __shfl_xor_sync(gmask, lo, m));
+    }
+    if (l == 0) {
       const double cw = (double)(e - s);
       if (!x) {
-        sx = (double)(s + e - 1) * cw < 9007199254740992.0 ? (double)((s + e - 1) * (e - s) / 2)
+        tx = (double)(s + e - 1) * cw < 9007199254740992.0 ? (double)((s + e - 1) * (e - s) / 2)
                                                            : 0.5 * ((double)(s + e - 1) * cw);
       }
-      cent[k] = make_double2(__ddiv_rn(sx, cw), __ddiv_rn(sy, cw));
+      cent[k] = make_double2(__ddiv_rn(tx, cw), __ddiv_rn(ty, cw));
       yr[k] = make_float2(hi, lo);
     }
   }
@@ -416,21 +454,26 @@ __device__ __forceinline__ double2 lttb_slope_range(const double* x, const void*
   return make_double2(lo, hi);
 }
 
-// warp per non-empty bucket: LTTB_NC candidates -- for each steering slope
+// group per non-empty bucket: LTTB_NC candidates -- for each steering slope
 // s_t, the sub-block extreme point maximising (minimising) y - s_t*x, using
-// the sub-block's rounded max (min) -- sorted by index into ext[k*NC ..]
-template <int YDT>
+// the sub-block's rounded max (min) -- sorted by index into ext[k*NC ..].
+// Selection rule (independent of G): best rounded f32 score, then the lowest
+// position.
+template <int YDT, int G>
 __device__ __forceinline__ void lttb_cand_phase(const double* x, const void* y, const int64_t* off, int64_t nb,
                                                 int64_t n, const double2* cent, const float2* yr,
                                                 const int32_t* nonempty, const int64_t* counts,
                                                 const LttbSBArrays A, int64_t* ext) {
+  constexpr int U = 4;
   const int64_t SB = A.SB;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31, l = lane & (G - 1);
+  const unsigned gmask = lttb_gmask<G>(lane);
+  const int64_t grp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
   const int64_t L = counts[0];
-  BucketCursor cur(nonempty, off, L, gw, nw);
-  for (int64_t j, k, s, e; cur.next(j, k, s, e);) {
+  for (int64_t j = grp; j < L; j += ngrp) {
+    const int64_t k = nonempty[j];
+    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
     const double2 sr = lttb_slope_range<YDT>(x, y, off, nb, n, cent, yr, nonempty, j, k);
     float sl[LTTB_K];  // candidates only steer the guess: f32 scores, bucket-relative u32 positions
 #pragma unroll
@@ -441,18 +484,18 @@ __device__ __forceinline__ void lttb_cand_phase(const double* x, const void* y, 
 #pragma unroll
     for (int c = 0; c < LTTB_NC; c++) { bv[c] = (c & 1) ? INFINITY : -INFINITY; bi[c] = 0xffffffffu; }
     const int64_t g0 = s / SB, g1 = (e - 1) / SB;
-    for (int64_t gb = g0; gb <= g1; gb += 32 * 4) {  // 4 sub-blocks per lane in flight
-      float2 m4[4];
-      unsigned am4[4];
+    for (int64_t gb = g0; gb <= g1; gb += (int64_t)G * U) {
+      float2 m4[U];
+      unsigned am4[U];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int64_t g = gb + u * 32 + lane;
+      for (int u = 0; u < U; u++) {
+        const int64_t g = gb + u * G + l;
         m4[u] = g <= g1 ? A.mm[g] : make_float2(-INFINITY, INFINITY);
         am4[u] = g <= g1 ? A.am[g] : 0xffffffffu;
       }
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int64_t g = gb + u * 32 + lane;
+      for (int u = 0; u < U; u++) {
+        const int64_t g = gb + u * G + l;
         const float2 m = m4[u];
         const unsigned am = am4[u];
         const int64_t px = g * SB + (am & 0xffff), pn = g * SB + (am >> 16);
@@ -467,118 +510,31 @@ __device__ __forceinline__ void lttb_cand_phase(const double* x, const void* y, 
         }
       }
     }
-    // warp-wide winners: the value by REDUX, then the lowest position holding it
-    int64_t cand = s;
+    // group-wide winners (every lane gets them): the value by REDUX, then the
+    // lowest position holding it; none -> the bucket's first point
+    unsigned rel[LTTB_NC];
 #pragma unroll
     for (int c = 0; c < LTTB_NC; c++) {
       const bool mx = (c & 1) == 0;
       const bool has = bi[c] != 0xffffffffu;
       const unsigned key = has ? f32_key(bv[c]) : (mx ? 0u : 0xffffffffu);
-      const unsigned w = mx ? __reduce_max_sync(0xffffffffu, key) : __reduce_min_sync(0xffffffffu, key);
-      const unsigned r = __reduce_min_sync(0xffffffffu, (has && key == w) ? bi[c] : 0xffffffffu);
-      if (lane == c) cand = r == 0xffffffffu ? s : s + (int64_t)r;
+      const unsigned w = mx ? __reduce_max_sync(gmask, key) : __reduce_min_sync(gmask, key);
+      const unsigned r = __reduce_min_sync(gmask, (has && key == w) ? bi[c] : 0xffffffffu);
+      rel[c] = r == 0xffffffffu ? 0u : r;
     }
-    // sort the NC candidates by index (odd-even transposition over lanes)
+    // sort by index: odd-even transposition network in registers
+#pragma unroll
     for (int r = 0; r < LTTB_NC; r++) {
-      const int partner = ((lane & 1) == (r & 1)) ? lane + 1 : lane - 1;
-      const int64_t o = __shfl_sync(0xffffffffu, cand, partner & 31);
-      if (lane < LTTB_NC && partner >= 0 && partner < LTTB_NC) {
-        const bool low = lane < partner;
-        cand = low ? (o < cand ? o : cand) : (o > cand ? o : cand);
-      }
-    }
-    if (lane < LTTB_NC) ext[k * LTTB_NC + lane] = cand;
-  }
-}
-
-// CTA per non-empty bucket (few large buckets): the CTA's warps split the
-// bucket's sub-blocks, reduce their LTTB_NC candidates by REDUX, and the
-// per-warp winners merge in shared memory (same selection rule as the warp
-// version: best rounded score, then the lowest position)
-template <int YDT>
-__device__ __forceinline__ void lttb_cand_phase_cta(const double* x, const void* y, const int64_t* off, int64_t nb,
-                                                    int64_t n, const double2* cent, const float2* yr,
-                                                    const int32_t* nonempty, const int64_t* counts,
-                                                    const LttbSBArrays A, int64_t* ext) {
-  __shared__ unsigned s_key[8][LTTB_NC], s_pos[8][LTTB_NC];
-  const int64_t SB = A.SB;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int nthr = blockDim.x;
-  const int64_t L = counts[0];
-  for (int64_t j = blockIdx.x; j < L; j += gridDim.x) {
-    const int64_t k = nonempty[j];
-    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-    const double2 sr = lttb_slope_range<YDT>(x, y, off, nb, n, cent, yr, nonempty, j, k);
-    float sl[LTTB_K];
 #pragma unroll
-    for (int t = 0; t < LTTB_K; t++) sl[t] = (float)(sr.x + (sr.y - sr.x) * ((double)t / (double)(LTTB_K - 1)));
-    const double xs = xd(x, s);
-    float bv[LTTB_NC];
-    unsigned bi[LTTB_NC];
-#pragma unroll
-    for (int c = 0; c < LTTB_NC; c++) { bv[c] = (c & 1) ? INFINITY : -INFINITY; bi[c] = 0xffffffffu; }
-    const int64_t g0 = s / SB, g1 = (e - 1) / SB;
-    for (int64_t gb = g0; gb <= g1; gb += (int64_t)nthr * 2) {  // 2 sub-blocks per thread in flight
-      float2 m2[2];
-      unsigned am2[2];
-#pragma unroll
-      for (int u = 0; u < 2; u++) {
-        const int64_t g = gb + u * nthr + tid;
-        m2[u] = g <= g1 ? A.mm[g] : make_float2(-INFINITY, INFINITY);
-        am2[u] = g <= g1 ? A.am[g] : 0xffffffffu;
-      }
-#pragma unroll
-      for (int u = 0; u < 2; u++) {
-        const int64_t g = gb + u * nthr + tid;
-        const unsigned am = am2[u];
-        const int64_t px = g * SB + (am & 0xffff), pn = g * SB + (am >> 16);
-        const bool okx = (am & 0xffff) != 0xffff && px >= s && px < e;
-        const bool okn = (am >> 16) != 0xffff && pn >= s && pn < e;
-        const float dxx = okx ? (float)(xd(x, px) - xs) : 0.0f, dxn = okn ? (float)(xd(x, pn) - xs) : 0.0f;
-#pragma unroll
-        for (int t = 0; t < LTTB_K; t++) {
-          const float vx = fmaf(-sl[t], dxx, m2[u].x), vn = fmaf(-sl[t], dxn, m2[u].y);
-          if (okx && vx > bv[2 * t]) { bv[2 * t] = vx; bi[2 * t] = (unsigned)(px - s); }
-          if (okn && vn < bv[2 * t + 1]) { bv[2 * t + 1] = vn; bi[2 * t + 1] = (unsigned)(pn - s); }
-        }
+      for (int c = r & 1; c + 1 < LTTB_NC; c += 2) {
+        const unsigned a0 = rel[c], a1 = rel[c + 1];
+        rel[c] = a0 < a1 ? a0 : a1;
+        rel[c + 1] = a0 < a1 ? a1 : a0;
       }
     }
 #pragma unroll
-    for (int c = 0; c < LTTB_NC; c++) {
-      const bool mx = (c & 1) == 0;
-      const bool has = bi[c] != 0xffffffffu;
-      const unsigned key = has ? f32_key(bv[c]) : (mx ? 0u : 0xffffffffu);
-      const unsigned w = mx ? __reduce_max_sync(0xffffffffu, key) : __reduce_min_sync(0xffffffffu, key);
-      const unsigned r = __reduce_min_sync(0xffffffffu, (has && key == w) ? bi[c] : 0xffffffffu);
-      if (lane == 0) {
-        s_key[wid][c] = w;
-        s_pos[wid][c] = r;
-      }
-    }
-    __syncthreads();
-    if (wid == 0) {
-      int64_t cand = s;
-      if (lane < LTTB_NC) {
-        const bool mx = (lane & 1) == 0;
-        unsigned bk = mx ? 0u : 0xffffffffu, bp = 0xffffffffu;
-        for (int w = 0; w < (nthr >> 5); w++) {
-          const unsigned kk = s_key[w][lane], pp = s_pos[w][lane];
-          if (pp == 0xffffffffu) continue;
-          if (bp == 0xffffffffu || (mx ? kk > bk : kk < bk) || (kk == bk && pp < bp)) { bk = kk; bp = pp; }
-        }
-        cand = bp == 0xffffffffu ? s : s + (int64_t)bp;
-      }
-      for (int r = 0; r < LTTB_NC; r++) {  // sort by index (odd-even transposition)
-        const int partner = ((lane & 1) == (r & 1)) ? lane + 1 : lane - 1;
-        const int64_t o = __shfl_sync(0xffffffffu, cand, partner & 31);
-        if (lane < LTTB_NC && partner >= 0 && partner < LTTB_NC) {
-          const bool low = lane < partner;
-          cand = low ? (o < cand ? o : cand) : (o > cand ? o : cand);
-        }
-      }
-      if (lane < LTTB_NC) ext[k * LTTB_NC + lane] = cand;
-    }
-    __syncthreads();
+    for (int c = 0; c < LTTB_NC; c++)
+      if ((c & (G - 1)) == l) ext[k * LTTB_NC + c] = s + (int64_t)rel[c];
   }
 }
 
@@ -906,6 +862,104 @@ struct LttbRound1 {  // per non-empty bucket: round-1 plan and its sub-block lis
   int64_t base, cnt;
 };
 
+// Round-1 plan, group per non-empty bucket, predecessor = the guessed pick:
+// plan constants, the exact best candidate area, the per-sub-block bounds ->
+// the bucket's surviving sub-blocks compacted into its slot range
+// [g0 + j, g1 + j] (disjoint across buckets; entry = sub-block << 24 | bucket
+// rank) and appended to the work list wl; a bucket with none settles at once.
+template <int YDT, int G>
+__device__ __forceinline__ void lttb_plan_phase(const double* x, const void* y, int64_t n, const int64_t* off,
+                                                int64_t nb, const LttbSBArrays A, const double2* cent,
+                                                const int32_t* nonempty, const int64_t* counts, const int64_t* ext,
+                                                int64_t* picks, LttbRound1* r1, int32_t* arrive, int64_t* slots,
+                                                int64_t* wl, int32_t* list, int32_t* ctr) {
+  constexpr int U = 4;
+  const int64_t SB = A.SB;
+  const int lane = threadIdx.x & 31, l = lane & (G - 1), gbase = lane & ~(G - 1);
+  const unsigned gmask = lttb_gmask<G>(lane);
+  const unsigned lmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+  const int64_t grp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+  const int64_t L = counts[0];
+  unsigned long long* nsb = (unsigned long long*)(ctr + 6);
+  for (int64_t j = grp; j < L; j += ngrp) {
+    const int64_t k = nonempty[j];
+    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+    LttbPlan P;
+    P.prev = j == 0 ? 0 : __ldcg(picks + j - 1);
+    double cx, cy;
+    centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
+    const double ax = xd(x, P.prev);
+    P.ay = yd<YDT>(y, P.prev);
+    P.K1 = __dsub_rn(ax, cx);
+    P.K2 = __dsub_rn(cy, P.ay);
+    P.sig = -P.K2 / P.K1;
+    AreaCand cb{-1.0, IDX_NONE};
+#pragma unroll
+    for (int c0 = 0; c0 < LTTB_NC; c0 += G) {  // exact areas of the bucket's candidates
+      const int c = c0 + l;
+      if (c < LTTB_NC) {
+        const int64_t pi = __ldg(ext + k * LTTB_NC + c);
+        const AreaCand a{tri_area(ax, P.ay, cx, cy, xd(x, pi), yd<YDT>(y, pi)), pi};
+        if (a.a > -1.0 && area_better(a, cb)) cb = a;
+      }
+    }
+#pragma unroll
+    for (int m = G / 2; m >= 1; m >>= 1) {
+      const AreaCand o{__shfl_xor_sync(gmask, cb.a, m), __shfl_xor_sync(gmask, cb.i, m)};
+      if (area_better(o, cb)) cb = o;
+    }
+    const int64_t g0 = s / SB, g1 = (e - 1) / SB;
+    const int64_t base = g0 + j;
+    int64_t cnt = 0;
+    for (int64_t gb = g0; gb <= g1; gb += (int64_t)G * U) {
+      float2 m4[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t g = gb + u * G + l;
+        m4[u] = g <= g1 ? A.mm[g] : make_float2(-INFINITY, INFINITY);
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t g = gb + u * G + l;
+        bool keep = false;
+        if (g <= g1) {
+          if (x) keep = true;
+          else {
+            int64_t cs, ce;
+            lttb_sb_range(A.SB, g, s, e, cs, ce);
+            keep = !(lttb_sb_bound(m4[u], s, cs, ce, P) < cb.a);
+          }
+        }
+        const unsigned bal = (__ballot_sync(gmask, keep) >> gbase) & lmask;
+        if (bal) {
+          const int before = __popc(bal & ((1u << l) - 1u));
+          int64_t w0 = 0;
+          if (l == 0) w0 = (int64_t)atomicAdd(nsb, (unsigned long long)__popc(bal));
+          w0 = __shfl_sync(gmask, w0, gbase);
+          if (keep) {
+            const int64_t pos = base + cnt + before;
+            slots[pos] = (g << 24) | j;
+            wl[w0 + before] = pos;
+          }
+          cnt += __popc(bal);
+        }
+      }
+    }
+    if (l == 0) {
+      r1[j] = LttbRound1{P, cb, base, cnt};
+      arrive[j] = (int32_t)cnt;
+      if (cnt == 0) {  // nothing can beat the best candidate: settled
+        const int64_t p = cb.i == IDX_NONE ? s : cb.i;
+        if (p != __ldcg(picks + j)) {
+          __stcg(picks + j, p);
+          if (j + 1 < L) list[atomicAdd(ctr + 2, 1)] = (int32_t)(j + 1);
+        }
+      }
+    }
+  }
+}
+
 // The guess and the round-1 plan in one cooperative launch (grid barriers
 // between the phases):
 //   count/list  non-empty bucket list (nonempty, rank, counts[0] = L)
@@ -954,15 +1008,19 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   lttb_list_phase(off, nb, bcnt, nonempty, rank, counts, s_red, &s_base);
   grid.sync();
   stamp(1);
-  lttb_cent_phase<YDT>(x, y, off, nonempty, counts, A, cent, yr);
+  const int G = lttb_pick_group(counts[0]);
+  if (G == 32) lttb_cent_phase<YDT, 32>(x, y, off, nonempty, counts, A, cent, yr);
+  else if (G == 16) lttb_cent_phase<YDT, 16>(x, y, off, nonempty, counts, A, cent, yr);
+  else lttb_cent_phase<YDT, 8>(x, y, off, nonempty, counts, A, cent, yr);
   grid.sync();
   if (exact) {
     lttb_centroid_phase<YDT>(xin, drop, y, off, nb, cent);
     grid.sync();
   }
   stamp(2);
-  if (counts[0] <= 4 * (int64_t)gridDim.x) lttb_cand_phase_cta<YDT>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext);
-  else lttb_cand_phase<YDT>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext);
+  if (G == 32) lttb_cand_phase<YDT, 32>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext);
+  else if (G == 16) lttb_cand_phase<YDT, 16>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext);
+  else lttb_cand_phase<YDT, 8>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext);
   grid.sync();
   stamp(3);
   lttb_cand_table_phase<YDT>(x, y, n, off, nb, cent, ext, nonempty, counts, T);
@@ -979,63 +1037,9 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   grid.sync();
   stamp(4);
   // ---- round-1 plan
-  const int64_t SB = A.SB;
-  const int lane = threadIdx.x & 31;
-  const int64_t L = counts[0];
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long* nsb = (unsigned long long*)(ctr + 6);
-  BucketCursor cur(nonempty, off, L, gw, nw);
-  for (int64_t j, k, s, e; cur.next(j, k, s, e);) {
-    LttbPlan P;
-    AreaCand cb;
-    double cx, cy;
-    lttb_plan_bucket<YDT>(x, y, n, off, nb, cent, nonempty, ext, picks, j, lane, k, s, e, P, cb, cx, cy, true);
-    const int64_t g0 = s / SB, g1 = (e - 1) / SB;
-    // surviving sub-blocks compacted into the bucket's own slot range
-    // [g0 + j, g1 + j] (disjoint across buckets); their slot positions are
-    // appended to the work list wl
-    const int64_t base = g0 + j;
-    int64_t cnt = 0;
-    for (int64_t gb = g0; gb <= g1; gb += 32 * 4) {
-      float2 m4[4];
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int64_t g = gb + u * 32 + lane;
-        m4[u] = g <= g1 ? A.mm[g] : make_float2(-INFINITY, INFINITY);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int64_t g = gb + u * 32 + lane;
-        bool keep = false;
-        if (g <= g1) {
-          if (x) keep = true;
-          else {
-            int64_t cs, ce;
-            lttb_sb_range(A.SB, g, s, e, cs, ce);
-            keep = !(lttb_sb_bound(m4[u], s, cs, ce, P) < cb.a);
-          }
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (bal) {
-          const int64_t pos = base + cnt + __popc(bal & ((1u << lane) - 1u));
-          int64_t w0 = 0;
-          if (lane == 0) w0 = (int64_t)atomicAdd(nsb, (unsigned long long)__popc(bal));
-          w0 = __shfl_sync(0xffffffffu, w0, 0);
-          if (keep) {
-            slots[pos] = (g << 24) | j;
-            wl[w0 + __popc(bal & ((1u << lane) - 1u))] = pos;
-          }
-          cnt += __popc(bal);
-        }
-      }
-    }
-    if (lane == 0) {
-      r1[j] = LttbRound1{P, cb, base, cnt};
-      arrive[j] = (int32_t)cnt;
-    }
-    if (cnt == 0) lttb_settle_warp(j, L, s, cb, nullptr, 0, 0, picks, list, ctr + 2, lane);
-  }
+  if (G == 32) lttb_plan_phase<YDT, 32>(x, y, n, off, nb, A, cent, nonempty, counts, ext, picks, r1, arrive, slots, wl, list, ctr);
+  else if (G == 16) lttb_plan_phase<YDT, 16>(x, y, n, off, nb, A, cent, nonempty, counts, ext, picks, r1, arrive, slots, wl, list, ctr);
+  else lttb_plan_phase<YDT, 8>(x, y, n, off, nb, A, cent, nonempty, counts, ext, picks, r1, arrive, slots, wl, list, ctr);
   grid.sync();
   stamp(5);
 }

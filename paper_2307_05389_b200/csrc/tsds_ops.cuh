@@ -33,6 +33,7 @@ struct Ops<DT_F32> {
   static constexpr bool IEEE = true;     // NaN-ignoring IEEE compare
   static constexpr bool NANABLE = true;  // has NaN values for propagate mode
   static constexpr bool FALLBACK = false;
+  static constexpr bool PACKED = false;
   __device__ static R min_init() { return __int_as_float(0x7fc00000); }
   __device__ static R max_init() { return __int_as_float(0x7fc00000); }
   __device__ static void vminmax(const uint4& v, R& mn, R& mx) {
@@ -78,6 +79,7 @@ struct Ops<DT_F64> {
   static constexpr bool IEEE = true;
   static constexpr bool NANABLE = true;
   static constexpr bool FALLBACK = false;
+  static constexpr bool PACKED = false;
   __device__ static R min_init() { return __longlong_as_double(0x7ff8000000000000ll); }
   __device__ static R max_init() { return __longlong_as_double(0x7ff8000000000000ll); }
   __device__ static double lo(const uint4& v) {
@@ -129,6 +131,7 @@ struct Packed16 {
   static constexpr bool IEEE = false;
   static constexpr bool NANABLE = KIND == 2;
   static constexpr bool FALLBACK = false;
+  static constexpr bool PACKED = true;
   __device__ static R min_init() { return 0x7fffffff; }
   __device__ static R max_init() { return (int32_t)0x80000000; }
 
@@ -158,6 +161,52 @@ struct Packed16 {
     mn = min(half_lo(m), half_hi(m));
     mx = max(half_lo(M), half_hi(M));
   }
+  // packed block fold (thread-per-bin kernel): two 16-bit columns of running
+  // extrema, folded over several vectors before one horizontal reduction
+  __device__ static uint32_t pmin_init() { return SIGNED ? 0x7fff7fffu : 0xffffffffu; }
+  __device__ static uint32_t pmax_init() { return SIGNED ? 0x80008000u : 0u; }
+  __device__ static void pfold(const uint4& v, uint32_t& pm, uint32_t& pM) {
+    if constexpr (KIND <= 2) {
+      uint32_t a = v.x, b = v.y, c = v.z, d = v.w;
+      if constexpr (KIND == 2) { a = ord16x2(a); b = ord16x2(b); c = ord16x2(c); d = ord16x2(d); }
+      pm = vmn(vmn(pm, a), vmn(b, vmn(c, d)));
+      pM = vmx(vmx(pM, a), vmx(b, vmx(c, d)));
+    } else {
+      constexpr uint32_t SL = KIND == 3 ? 0x9180u : 0x4140u;
+      constexpr uint32_t SH = KIND == 3 ? 0xB3A2u : 0x4342u;
+      uint32_t a0 = prmt(v.x, 0u, SL), a1 = prmt(v.x, 0u, SH);
+      uint32_t b0 = prmt(v.y, 0u, SL), b1 = prmt(v.y, 0u, SH);
+      uint32_t c0 = prmt(v.z, 0u, SL), c1 = prmt(v.z, 0u, SH);
+      uint32_t d0 = prmt(v.w, 0u, SL), d1 = prmt(v.w, 0u, SH);
+      pm = vmn(vmn(vmn(pm, a0), vmn(a1, b0)), vmn(vmn(b1, c0), vmn(c1, vmn(d0, d1))));
+      pM = vmx(vmx(vmx(pM, a0), vmx(a1, b0)), vmx(vmx(b1, c0), vmx(c1, vmx(d0, d1))));
+    }
+  }
+  // index of the first element of v whose comparison value equals r (-1: none):
+  // zero-lane detection on v ^ splat(r); the lowest flagged lane is exact
+  __device__ static int find_first(const uint4& v, R r) {
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    if constexpr (KIND == 2) {
+#pragma unroll
+      for (int i = 0; i < 4; i++) w[i] = ord16x2(w[i]);
+    }
+    int pos = -1;
+#pragma unroll
+    for (int i = 3; i >= 0; i--) {
+      uint32_t z;
+      if constexpr (ESIZE == 1) {
+        const uint32_t x = w[i] ^ (((uint32_t)r & 0xffu) * 0x01010101u);
+        z = (x - 0x01010101u) & ~x & 0x80808080u;
+      } else {
+        const uint32_t x = w[i] ^ (((uint32_t)r & 0xffffu) * 0x00010001u);
+        z = (x - 0x00010001u) & ~x & 0x80008000u;
+      }
+      if (z) pos = i * (4 / ESIZE) + ((__ffs(z) - 1) >> (ESIZE == 1 ? 3 : 4));
+    }
+    return pos;
+  }
+  __device__ static R hmin(uint32_t pm) { return min(half_lo(pm), half_hi(pm)); }
+  __device__ static R hmax(uint32_t pM) { return max(half_lo(pM), half_hi(pM)); }
   __device__ static bool upd_min(R v, R& r) { bool u = v < r; r = u ? v : r; return u; }
   __device__ static bool upd_max(R v, R& r) { bool u = v > r; r = u ? v : r; return u; }
   __device__ static bool valid(R) { return true; }
@@ -219,6 +268,7 @@ struct WideInt {
   static constexpr bool IEEE = false;
   static constexpr bool NANABLE = false;
   static constexpr bool FALLBACK = true;
+  static constexpr bool PACKED = false;
   __device__ static R min_init() {
     if constexpr (sizeof(T) == 4) return SGN ? (R)0x7fffffff : (R)0xffffffffu;
     else return SGN ? (R)0x7fffffffffffffffll : (R)0xffffffffffffffffull;

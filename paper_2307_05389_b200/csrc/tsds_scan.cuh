@@ -193,7 +193,7 @@ struct GlobalSrc {
 // vector, and the scalar candidates are formed after the loop, to keep the
 // hot loop's register footprint small (64 registers -> 32 warps per SM).
 template <int DT, bool PROP, int U, class Src>
-__device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, const Src& src) {
+__device__ __forceinline__ MinMaxCand seg_reduce_inl(const ScanArgs& A, int64_t a, int64_t c, const Src& src) {
   using O = Ops<DT>;
   using E = typename O::E;
   using R = typename O::R;
@@ -326,6 +326,15 @@ __device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, co
   }
   warp_reduce(res);
   return res;
+}
+
+// out-of-line instance for the scan kernels (a call keeps their hot loops
+// register allocation independent of the call sites); kernels that run with
+// a small L1 (tile_bins_kernel: the carve-out goes to shared memory) inline
+// seg_reduce_inl instead, so no argument or result travels through the stack
+template <int DT, bool PROP, int U, class Src>
+__device__ __noinline__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, const Src& src) {
+  return seg_reduce_inl<DT, PROP, U, Src>(A, a, c, src);
 }
 
 template <int DT, bool PROP, int U>
@@ -550,9 +559,12 @@ __device__ __forceinline__ void process_chunk(const ScanArgs& A, const BinSpec& 
 
 // Last CTA of a launch: compaction epilogue, counter and flag reset.
 // Every CTA of the grid must call it exactly once.
-__device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted) {
+// direct_width (tile_bins_kernel): the picks already sit at their final
+// positions unless F->tile_short was raised; then (or when 0) compact res[].
+template <bool DIRECT>
+__device__ void scan_epilogue_t(const ScanArgs& A, const BinSpec& B, bool aborted, int direct_width) {
   PipeFlags* F = A.flags;
-  __shared__ int is_last;
+  __shared__ int is_last, use_direct;
 #ifdef TSDS_SCAN_TIMING
   if (threadIdx.x == 0) atomicMax(&F->pad1[1], gtimer());
 #endif
@@ -565,7 +577,10 @@ __device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted)
     fence_acq_rel_gpu();
     unsigned t = atomicAdd(&F->scan_blocks_done, 1u);
     is_last = (t == gridDim.x - 1);
-    if (is_last) fence_acq_rel_gpu();
+    if (is_last) {
+      fence_acq_rel_gpu();
+      if constexpr (DIRECT) use_direct = direct_width && !*(volatile int*)&F->tile_short;
+    }
   }
   __syncthreads();
   if (!is_last) return;
@@ -589,7 +604,12 @@ __device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted)
     }
   } else if (A.out) {
     int64_t* out = A.out + (A.lttb_frame ? 1 : 0);
-    int64_t tot = cta_compact(A, B, A.g0, A.g1, out, A.idx_sub);
+    int64_t tot;
+    if constexpr (DIRECT) {
+      tot = use_direct ? (int64_t)direct_width * (A.g1 - A.g0) : cta_compact(A, B, A.g0, A.g1, out, A.idx_sub);
+    } else {
+      tot = cta_compact(A, B, A.g0, A.g1, out, A.idx_sub);
+    }
     if (threadIdx.x == 0) {
       if (A.lttb_frame) {
         A.out[0] = 0;
@@ -623,7 +643,11 @@ __device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted)
     }
     F->work_ctr = 0ull;
     F->scan_blocks_done = 0u;
+    if constexpr (DIRECT) F->tile_short = 0;
   }
+}
+__device__ void scan_epilogue(const ScanArgs& A, const BinSpec& B, bool aborted) {
+  scan_epilogue_t<false>(A, B, aborted, 0);
 }
 
 template <int DT, bool PROP, int U>

@@ -336,3 +336,51 @@ def test_atomic_bin_merge_mode(ts, oracle, mode):
                              n_out=1000).tolist() == want.tolist()
     finally:
         L.tsds_set_option(b"atomic_bins", 1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", [2, 0])
+def test_tile_bins_kernel(ts, oracle, mode):
+    """Bins streamed through shared memory by TMA bulk copies (C1's path),
+    forced on for every shape (2) and off (0): every dtype, ties, NaN in a
+    bin's first slot, NaN-propagating, host x (offset arrays, empty bins),
+    bins longer than a slot (tile by tile), tiny bins, misaligned starts,
+    MinMaxLTTB preselection; the direct output layout and its fallback."""
+    import torch
+
+    from paper_2307_05389_b200 import _lib
+
+    L = _lib.load()
+    rng = np.random.default_rng(77)
+    try:
+        L.tsds_set_option(b"tile_bins", mode)
+        for tag in ("f32", "f64", "f16", "i8", "u8", "i16", "u16", "i32", "u32", "i64", "u64"):
+            y = W.random_series(tag, 250_003, int(rng.integers(1 << 30)), ties=True)
+            if tag in ("f32", "f64", "f16"):
+                y[rng.integers(0, y.size, 200)] = np.nan
+                y[[0, 1250, 2500]] = np.nan
+            x = np.cumsum(rng.integers(1, 9, y.size)).astype(np.int64)
+            x[100_000:] += 40_000  # a gap: empty bins with many bins
+            for algo, n_out in (("minmax", 2000), ("m4", 400), ("minmax", 6), ("m4", 4), ("minmax", 50_000),
+                                ("minmaxlttb", 300)):
+                want = oracle.downsample(algo, y, n_out=n_out)
+                assert ts.downsample(algo, y, n_out=n_out).tolist() == want.tolist(), (tag, algo, n_out)
+                want = oracle.downsample(algo, x, y, n_out=n_out)
+                assert ts.downsample(algo, x, y, n_out=n_out).tolist() == want.tolist(), (tag, algo, n_out, "host x")
+            yd = torch.from_numpy(y).cuda()
+            for o in (1, 3):  # device views starting off a 16-byte boundary
+                assert ts.downsample("m4", yd[o:], n_out=400).tolist() == oracle.downsample("m4", y[o:], n_out=400).tolist()
+            if tag in ("f32", "f64", "f16"):
+                got = ts.downsample("nanm4", y, n_out=2000).tolist()
+                assert got == oracle.downsample("m4", y, n_out=2000, nan=True).tolist(), (tag, "nanm4")
+        # constant series: every bin emits one index (the direct layout's fallback)
+        c = np.full(100_000, 2.5, np.float32)
+        assert ts.downsample("minmax", c, n_out=1000).tolist() == oracle.downsample("minmax", c, n_out=1000).tolist()
+        assert ts.downsample("m4", c, n_out=1000).tolist() == oracle.downsample("m4", c, n_out=1000).tolist()
+        # repeated calls: the flag reset between launches
+        y = W.config1(1_000_000)
+        want = oracle.downsample("minmax", y, n_out=2000).tolist()
+        for _ in range(5):
+            assert ts.downsample("minmax", y, n_out=2000).tolist() == want
+    finally:
+        L.tsds_set_option(b"tile_bins", 1)
