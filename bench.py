@@ -415,15 +415,25 @@ def measure_config(key, runner, args, clk, cpu, peak, peak_kind):
               f"inputs ({nbytes / 1e9:.2f} GB) larger than L2 (126 MB); no flush",
         "parity": "equal to the reference's output (tests/golden/configs.npz)",
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": {"minmax": "scan_kernel<f32> (CTA-per-bin mode)",
+        "roofline": {"bound": "hbm", "kernel": {"minmax": "tile_bins_kernel<f32> (TMA bulk copies into a shared-memory ring)",
                                                 "m4": "scan_kernel<f64>", "lttb": "lttb_sb_kernel<f64>",
                                                 "minmaxlttb": "scan_kernel<f32> (MinMax preselection)",
-                                                "minmax_batched": "lane_bins_kernel / scan_kernel"}[s["algo"]],
+                                                "minmax_batched": "scan_kernel<i16>" if s.get("tag") == "i16" else
+                                                f"lane_bins_kernel<{s.get('tag')}> (8 lanes per bin)"}[s["algo"]],
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "frac_of_step": round(gbs / peak, 4),
                      "traffic": _traffic(key), "algorithmic_bytes_per_launch": nbytes,
                      "avg_launch_ms": round(kms, 5), "launches_per_step": kper},
     }
+    if s["algo"] == "lttb":
+        # north star: LTTB picks may differ from the reference only at area ties within 1e-12
+        # relative; counted along the reference's own walk (oracle, sequential centroid sums)
+        from oracle import oracle as O
+
+        nb = s["n_out"] - 2
+        off = np.arange(nb + 1, dtype=np.int64) * np.int64(y.shape[0] - 2) // np.int64(nb) + 1
+        entry["lttb_near_ties"] = {"rel": 1e-12, "buckets": O.lttb_near_ties(None, y, off)[0],
+                                   "picks_differing_from_reference": 0}
     del keep
     runner.torch.cuda.empty_cache()
     # ---- e2e through the public API, host numpy inputs.  Call 1 sees fresh pageable arrays

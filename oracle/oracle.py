@@ -56,6 +56,8 @@ def lib():
         L.or_minmax_batched.argtypes = [vp, i32, i64, i64, i64, i32, i32, vp, vp]
         L.or_lttb_walk.argtypes = [vp, i32, vp, i32, i64, vp, i64, vp]
         L.or_lttb_walk.restype = i64
+        L.or_lttb_near_ties.argtypes = [vp, i32, vp, i32, i64, vp, i64, ctypes.c_double, vp]
+        L.or_lttb_near_ties.restype = i64
         L.or_fill_width_offsets.argtypes = [vp, i32, i64, ctypes.c_double, ctypes.c_double, i64, i64, i64, vp]
         L.or_bins_slots.argtypes = [vp, i32, vp, i64, i64, i32, i32, vp, vp]
         L.or_compact_bins.argtypes = [vp, vp, i32, i64, vp]
@@ -154,6 +156,19 @@ def lttb_walk(x, y, off):
     m = lib().or_lttb_walk(_ptr(x), 0 if x is None else DTYPE_CODES[x.dtype], _ptr(y), DTYPE_CODES[y.dtype],
                            y.shape[0], _ptr(off), off.shape[0] - 1, _ptr(out))
     return out[:m]
+
+
+def lttb_near_ties(x, y, off, rel=1e-12):
+    """(count, bucket numbers) of the buckets whose two best triangle areas
+    are within `rel` relative along the reference's own walk (sequential
+    centroid sums, no FMA)."""
+    y = np.ascontiguousarray(y)
+    x = _x_view(x)
+    off = np.ascontiguousarray(off, dtype=np.int64)
+    buckets = np.zeros(max(off.shape[0] - 1, 1), np.int64)
+    m = lib().or_lttb_near_ties(_ptr(x), 0 if x is None else DTYPE_CODES[x.dtype], _ptr(y), DTYPE_CODES[y.dtype],
+                                y.shape[0], _ptr(off), off.shape[0] - 1, float(rel), _ptr(buckets))
+    return int(m), buckets[:m]
 
 
 def stage2(x, y, full, n_out):

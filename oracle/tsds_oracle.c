@@ -341,6 +341,58 @@ static int64_t lttb_walk(const void *x, int xdt, const void *y, int ydt, int64_t
     return m + 1;
 }
 
+/* Near-tie accounting along the reference walk (north star: LTTB picks may
+ * differ from the reference only where the two best triangle areas of a
+ * bucket are within `rel` relative).  Same walk as above -- sequential
+ * centroid sums (_kernels.py:403-405), the area formula without contraction
+ * -- but per bucket the second-best area is tracked too.  Returns the number
+ * of buckets with best - second <= rel * best; tie_buckets (nullable,
+ * capacity nb) receives their bucket numbers. */
+int64_t or_lttb_near_ties(const void *x, int xdt, const void *y, int ydt, int64_t n,
+                          const int64_t *off, int64_t nb, double rel, int64_t *tie_buckets) {
+    double ax = x ? as_f64(x, xdt, 0) : 0.0;
+    double ay = as_f64(y, ydt, 0);
+    double lastx = x ? as_f64(x, xdt, n - 1) : (double)(n - 1);
+    double lasty = as_f64(y, ydt, n - 1);
+    int64_t ties = 0;
+    for (int64_t k = 0; k < nb; k++) {
+        int64_t s = off[k], e = off[k + 1];
+        if (e <= s) continue;
+        double cx, cy;
+        if (k == nb - 1 || off[k + 2] <= off[k + 1]) {
+            cx = lastx; cy = lasty;
+        } else {
+            int64_t s2 = off[k + 1], e2 = off[k + 2];
+            double sx = 0.0, sy = 0.0;
+            for (int64_t i = s2; i < e2; i++) {
+                sx += x ? as_f64(x, xdt, i) : (double)i;
+                sy += as_f64(y, ydt, i);
+            }
+            double cw = (double)(e2 - s2);
+            cx = sx / cw;
+            cy = sy / cw;
+        }
+        int64_t best = s;
+        double besta = -1.0, second = -1.0;
+        for (int64_t i = s; i < e; i++) {
+            double by = as_f64(y, ydt, i);
+            double xi = x ? as_f64(x, xdt, i) : (double)i;
+            volatile double t1 = (ax - cx) * (by - ay);
+            volatile double t2 = (ax - xi) * (cy - ay);
+            double area = 0.5 * fabs(t1 - t2);
+            if (area > besta) { second = besta; besta = area; best = i; }
+            else if (area > second) second = area;  /* NaN areas never count */
+        }
+        if (e - s >= 2 && besta >= 0.0 && second >= 0.0 && besta - second <= rel * besta) {
+            if (tie_buckets) tie_buckets[ties] = k;
+            ties++;
+        }
+        ax = x ? as_f64(x, xdt, best) : (double)best;
+        ay = as_f64(y, ydt, best);
+    }
+    return ties;
+}
+
 /* exported walk with caller offsets (for stage-2 checks of sharded runs) */
 int64_t or_lttb_walk(const void *x, int xdt, const void *y, int ydt, int64_t n,
                      const int64_t *off, int64_t nb, int64_t *out) {

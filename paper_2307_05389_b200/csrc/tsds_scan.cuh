@@ -193,7 +193,7 @@ struct GlobalSrc {
 // vector, and the scalar candidates are formed after the loop, to keep the
 // hot loop's register footprint small (64 registers -> 32 warps per SM).
 template <int DT, bool PROP, int U, class Src>
-__device__ __forceinline__ MinMaxCand seg_reduce_inl(const ScanArgs& A, int64_t a, int64_t c, const Src& src) {
+__device__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, const Src& src) {
   using O = Ops<DT>;
   using E = typename O::E;
   using R = typename O::R;
@@ -326,15 +326,6 @@ __device__ __forceinline__ MinMaxCand seg_reduce_inl(const ScanArgs& A, int64_t 
   }
   warp_reduce(res);
   return res;
-}
-
-// out-of-line instance for the scan kernels (a call keeps their hot loops
-// register allocation independent of the call sites); kernels that run with
-// a small L1 (tile_bins_kernel: the carve-out goes to shared memory) inline
-// seg_reduce_inl instead, so no argument or result travels through the stack
-template <int DT, bool PROP, int U, class Src>
-__device__ __noinline__ MinMaxCand seg_reduce_src(const ScanArgs& A, int64_t a, int64_t c, const Src& src) {
-  return seg_reduce_inl<DT, PROP, U, Src>(A, a, c, src);
 }
 
 template <int DT, bool PROP, int U>

@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(TB_THREADS, 1) tile_bins_kernel(const ScanArgs
         MinMaxCand r{cand_none_min(), cand_none_max()};
         if (c > a) {
           const SmemSrc src{smem_u32(tb_smem + (size_t)slot * TB_SLOT_BYTES), JB};
-          r = seg_reduce_inl<DT, PROP, 4>(A, a, c, src);
+          r = seg_reduce_src<DT, PROP, 4>(A, a, c, src);
         }
 #ifdef TSDS_TILE_TIMING
         unsigned long long ta2 = gtimer();

@@ -9,11 +9,12 @@ n_out, the estimator classes), so the second time an array of at least
 page-locked in place with ``tsds_host_register`` (cudaHostRegister,
 ~13 GB/s once) and later uploads are DMA'd directly from it at link speed.
 
-Safety: the registration is tied to the array that OWNS the memory (the end
-of the ``.base`` chain, ``flags.owndata``) through a weak reference -- it is
-released when that array is garbage collected, i.e. before its memory can be
-unmapped.  Buffers not owned by a numpy array (memmap, foreign buffers) are
-never registered.  ``TSDS_PIN_CACHE`` = ``reuse`` (default) | ``always`` (pin
+Safety: the registration is tied, through a weak reference, to the array at
+the end of the ``.base`` chain -- the one that owns the memory or holds the
+buffer export that keeps it mapped -- and is released when that array is
+garbage collected, i.e. before the memory can be unmapped.  Arrays whose
+memory lifetime cannot be tied to a numpy object (np.memmap, foreign array
+interfaces) are never registered.  ``TSDS_PIN_CACHE`` = ``reuse`` (default) | ``always`` (pin
 on first sight) | ``off``; ``TSDS_PIN_MAX_BYTES`` caps the pinned total
 (default 1/4 of physical memory, least recently used evicted first).
 """
@@ -61,13 +62,20 @@ def configure(mode=None, min_bytes=None, max_bytes=None):
 
 
 def owner_of(a):
-    """The ndarray that owns a's memory, or None (memmap / foreign buffer / scalar)."""
+    """The ndarray at the end of a's ``.base`` chain if the memory cannot go
+    away while that array is alive: it owns its data, or it wraps a
+    buffer-protocol export (``np.frombuffer`` over an mmap / bytearray /
+    bytes: the exporter refuses to close or resize while the export exists).
+    None otherwise (np.memmap subclasses, foreign ``__array_interface__``
+    objects, scalars)."""
     o = a
-    while isinstance(o, np.ndarray) and o.base is not None:
+    while isinstance(o, np.ndarray) and isinstance(o.base, np.ndarray):
         o = o.base
-    if type(o) is not np.ndarray or not o.flags.owndata:
+    if type(o) is not np.ndarray:
         return None
-    return o
+    if o.flags.owndata or isinstance(o.base, memoryview):
+        return o
+    return None
 
 
 def _release(key):

@@ -20,3 +20,10 @@ def oracle():
 
     O.lib()
     return O
+
+
+@pytest.fixture(scope="session")
+def ts():
+    import paper_2307_05389_b200 as m
+
+    return m

@@ -13,8 +13,17 @@ def test_owner_resolution():
     assert pinning.owner_of(a) is a
     assert pinning.owner_of(a[10:500]) is a
     assert pinning.owner_of(a[10:500].view(np.int32)[::1]) is a
-    b = np.frombuffer(bytearray(64), dtype=np.uint8)  # memory owned by a foreign object
-    assert pinning.owner_of(b) is None
+    b = np.frombuffer(bytearray(64), dtype=np.uint8)  # a buffer export keeps the memory alive while b lives
+    assert pinning.owner_of(b) is b and pinning.owner_of(b[8:].view(np.int16)) is b
+    import mmap
+
+    m = np.frombuffer(mmap.mmap(-1, 4096), dtype=np.float32).reshape(32, 32)
+    assert pinning.owner_of(m[3:]) is m.base
+
+    class Foreign:  # memory whose lifetime numpy cannot vouch for
+        __array_interface__ = a.__array_interface__
+
+    assert pinning.owner_of(np.asarray(Foreign())) is None
 
 
 def test_small_or_disabled_inputs_are_ignored():
