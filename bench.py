@@ -545,6 +545,15 @@ def run_ours_sharded(args):
     from paper_2307_05389_b200 import _lib
     from paper_2307_05389_b200 import distributed as D
 
+    if "RANK" not in os.environ:  # --sharded without torchrun: a world of one
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        for k, v in (("RANK", "0"), ("LOCAL_RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_ADDR", "127.0.0.1"),
+                     ("MASTER_PORT", str(port))):
+            os.environ.setdefault(k, v)
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
     if not dist.is_initialized():

@@ -13,6 +13,26 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Checked build (make ../libtsds_checked.so VFLAGS=-DTSDS_CHECKED): bounds
+// and protocol assertions of our own inside the kernels -- compute-sanitizer
+// is not available on the GPU pool.  A failed check prints its location and
+// traps (the launch fails with an error the host reports).
+#ifdef TSDS_CHECKED
+#include <cstdio>
+#define TSDS_CHECK(cond)                                                                                   \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("TSDS_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, blockIdx.x, \
+             threadIdx.x);                                                                                 \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define TSDS_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace tsds {
 
 enum DType : int {

@@ -117,6 +117,7 @@ lane_bins_kernel(const ScanArgs A) {
       };
       auto vec_of = [&](int t) {
         const int v = l + LG * t;
+        TSDS_CHECK(t >= 0 && last >= 0);
         return v < last ? v : last;
       };
       auto load_clamped = [&](uint4 (&c)[LB_V], int t) {
@@ -128,6 +129,7 @@ lane_bins_kernel(const ScanArgs A) {
       auto reload = [&](uint4 (&c)[LB_V], int tt) {
         if (tt >= T) return;
         if ((tt + LB_V) * LG <= nv) {
+          TSDS_CHECK(l + LG * (tt + LB_V - 1) < nv);
           const uint4* q = p + (l + LG * tt);
 #pragma unroll
           for (int u = 0; u < LB_V; u++) c[u] = ldg_stream<true>(q + u * LG);
@@ -181,6 +183,8 @@ lane_bins_kernel(const ScanArgs A) {
       merge_min(res.mn, a);
       merge_max(res.mx, b);
     }
+    TSDS_CHECK(res.mn.idx == IDX_NONE || (res.mn.idx >= s && res.mn.idx < e));
+    TSDS_CHECK(res.mx.idx == IDX_NONE || (res.mx.idx >= s && res.mx.idx < e));
     if (l == 0) finalize<DT, false>(A, B, g, res);
   }
   scan_epilogue(A, B, false);

@@ -939,6 +939,7 @@ __device__ __forceinline__ void lttb_plan_phase(const double* x, const void* y, 
           w0 = __shfl_sync(gmask, w0, gbase);
           if (keep) {
             const int64_t pos = base + cnt + before;
+            TSDS_CHECK(pos >= g0 + j && pos <= g1 + j);  // inside the bucket's own slot range
             slots[pos] = (g << 24) | j;
             wl[w0 + before] = pos;
           }
@@ -1067,6 +1068,7 @@ lttb_eval_kernel(const double* xin, const int* drop, const void* y, int64_t n, c
     const int64_t pos = __ldcg(wl + t);
     const int64_t ent = __ldcg(slots + pos);
     const int64_t g = ent >> 24, j = ent & 0xffffff;
+    TSDS_CHECK(j >= 0 && j < L && g >= 0 && g * A.SB < n);
     const int64_t k = nonempty[j];
     const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
     const LttbPlan P = r1[j].P;
@@ -1226,6 +1228,7 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
         for (int w = 0; w < LTTB_CH_THREADS / 32; w++)
           if (area_better(sW[w], b)) b = sW[w];
         const int64_t pk = b.i == IDX_NONE ? s : b.i;
+        TSDS_CHECK(pk >= s && pk < e);
         int go = 0;
         lttb_lock(lock + j);
         const int64_t cur = j == 0 ? 0 : lttb_ld_relaxed(picks + j - 1);

@@ -341,6 +341,9 @@ __device__ __forceinline__ MinMaxCand seg_reduce(const ScanArgs& A, int64_t a, i
 template <int DT, bool PROP>
 __device__ __forceinline__ void finalize(const ScanArgs& A, const BinSpec& B, int64_t g, const MinMaxCand& r) {
   int64_t lo = r.mn.idx, hi = r.mx.idx;
+  TSDS_CHECK(g >= A.g0 && g < A.g1);
+  TSDS_CHECK(lo == IDX_NONE || (lo >= A.E0 && lo < A.E1));
+  TSDS_CHECK(hi == IDX_NONE || (hi >= A.E0 && hi < A.E1));
   if constexpr (!PROP && Ops<DT>::IEEE) {
     int64_t s = bin_off(B, g);
     if (elem_is_nan<DT>(A.y, s)) { lo = s; hi = s; }
@@ -437,7 +440,10 @@ __device__ int64_t cta_compact(const ScanArgs& A, const BinSpec& B, int64_t ga, 
     }
 #pragma unroll
     for (int r = 0; r < PB; r++)
-      for (int t = 0; t < c[r]; t++) out[pos++] = v[r][t] - sub;
+      for (int t = 0; t < c[r]; t++) {
+        TSDS_CHECK(pos >= 0 && pos < 4 * (gb - ga));
+        out[pos++] = v[r][t] - sub;
+      }
     __syncthreads();
     if (tid == 0) running += all;
     __syncthreads();
@@ -505,6 +511,7 @@ __device__ __forceinline__ void process_chunk(const ScanArgs& A, const BinSpec& 
     int64_t s = bin_off(B, g), e = bin_off(B, g + 1);
     if (e <= pos) { g++; continue; }
     int64_t se = e < ce ? e : ce;
+    TSDS_CHECK(g >= A.g0 && g < A.g1 && pos >= A.E0 && se <= A.E1 && pos < se);
     MinMaxCand r = seg_reduce<DT, PROP, U>(A, pos, se);
     bool before = s < cs, after = e > ce;
     if (A.atomic_mode) {
@@ -522,6 +529,7 @@ __device__ __forceinline__ void process_chunk(const ScanArgs& A, const BinSpec& 
         slot->mx = r.mx;
         fence_acq_rel_gpu();
         old = atomicAdd(A.bin_cnt + (g - A.g0), 1u);
+        TSDS_CHECK((int64_t)old <= chunk_of(A, e - 1) - chunk_of(A, s));  // arrival counter never overshoots
         if ((int64_t)old == chunk_of(A, e - 1) - chunk_of(A, s)) fence_acq_rel_gpu();
       }
       old = __shfl_sync(0xffffffffu, old, 0);

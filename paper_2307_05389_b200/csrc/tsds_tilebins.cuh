@@ -9,9 +9,9 @@
 // and a control warp keeps TB_SLOTS bins in flight with cp.async.bulk
 // (SASS UBLKCP) completing on mbarriers -- ~150 KB in flight per SM with no
 // per-lane address generation and no registers held by loads in flight.
-// The CTA's 16 reducer warps reduce a landed bin out of shared memory (the
-// locate re-read is a shared-memory read); the control warp merges their
-// partials and finalises the bin while they are on the next one.  Bins longer than a slot are walked tile by tile.
+// Four groups of four reducer warps each reduce a landed bin out of shared
+// memory (four bins at once; the locate re-read is a shared-memory read);
+// the control warp merges their partials and finalises the bins in order.  Bins longer than a slot are walked tile by tile.
 //
 // Output without a compaction pass: every bin's picks are also written
 // straight to their final position assuming every earlier bin emitted the
@@ -29,7 +29,7 @@ namespace tsds {
 
 constexpr int TB_SLOTS = 4;
 constexpr int TB_SLOT_BYTES = 48 * 1024;
-constexpr size_t TB_SMEM = (size_t)TB_SLOTS * TB_SLOT_BYTES + 128;
+constexpr size_t TB_SMEM = (size_t)TB_SLOTS * TB_SLOT_BYTES + 8 * (size_t)(TB_SLOTS * 5) + 64;  // ring + mbarriers
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -128,26 +128,27 @@ struct TileCursor {
   }
 };
 
-constexpr int TB_WARPS = 16;                    // reducer warps
+constexpr int TB_GW = 4;                         // reducer warps per group
+constexpr int TB_WARPS = TB_SLOTS * TB_GW;       // reducer warps: one group per slot
 constexpr int TB_THREADS = (TB_WARPS + 1) * 32;  // + one control warp (producer, merges, finalisation)
 constexpr int TB_TAB = 512;                      // bins per table pass
 
-// named barriers (ids 1..4; id 0 is __syncthreads)
-__device__ __forceinline__ void nbar_sync(int id) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(TB_THREADS) : "memory");
-}
-__device__ __forceinline__ void nbar_arrive(int id) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(TB_THREADS) : "memory");
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Roles: warps 0..TB_WARPS-1 reduce a landed tile out of shared memory (an
-// even share of its vectors each) and hand their partials to the control
-// warp through part_s[buf] (buf = tile parity): barrier A(buf) -- reducers
-// arrive, control waits -- says "partials written, slot no longer read";
-// barrier B(buf) -- control arrives, reducers wait two tiles later -- says
-// "partials consumed".  The control warp refills the released slot, merges
-// the partials with shuffles, finalises the bin and writes its output while
-// the reducers are already on the next tile.
+// Roles.  Tile number `it` of the CTA's sequence lands in slot it % TB_SLOTS
+// and is reduced by reducer GROUP it % TB_SLOTS (TB_GW warps, an even share
+// of the tile's vectors each): a warp's reduction is a chain of ~600
+// dependent instructions whatever the tile size, so the groups work on
+// TB_SLOTS different bins at once instead of all warps on one.  A group
+// hands its partials to the control warp through part_s[group][b] (b = the
+// group's iteration parity) and two mbarriers: A(group, b) -- the group's
+// warps arrive, control waits -- "partials written, slot no longer read";
+// B(group, b) -- control arrives, the group waits two iterations later --
+// "partials consumed".  The control warp takes the tiles in order: refills
+// the released slot, merges the partials with shuffles, finalises the bin
+// and writes its output while the groups are already on their next tiles.
 template <int DT, bool PROP>
 __global__ void __launch_bounds__(TB_THREADS, 1) tile_bins_kernel(const ScanArgs A) {
   using O = Ops<DT>;
@@ -155,15 +156,21 @@ __global__ void __launch_bounds__(TB_THREADS, 1) tile_bins_kernel(const ScanArgs
   constexpr int VEC = O::VEC;
   constexpr int64_t TE = TB_SLOT_BYTES / (int64_t)sizeof(E) - VEC;  // elements per tile
   extern __shared__ __align__(128) uint8_t tb_smem[];
-  __shared__ MinMaxCand part_s[2][TB_WARPS];
+  __shared__ MinMaxCand part_s[TB_SLOTS][2][TB_GW];
   __shared__ int64_t tab_s[TB_TAB], tab_e[TB_TAB];
   __shared__ int s_short;  // some bin of this CTA emits fewer than the full width
-  __shared__ int nan_s[2];  // the bin's first element is NaN (probed by reducer warp 0 on the bin's first tile)
+  __shared__ int nan_s[TB_SLOTS][2];  // the bin's first element is NaN (probed by the group's first warp on the bin's first tile)
   uint64_t* full = reinterpret_cast<uint64_t*>(tb_smem + (size_t)TB_SLOTS * TB_SLOT_BYTES);
+  uint64_t* abar = full + TB_SLOTS;      // A(group, b) at abar[group * 2 + b]
+  uint64_t* bbar = abar + 2 * TB_SLOTS;  // B(group, b)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const bool ctrl = wid == TB_WARPS;
   if (tid == 0) {
     for (int i = 0; i < TB_SLOTS; i++) mbar_init(&full[i], 1);
+    for (int i = 0; i < 2 * TB_SLOTS; i++) {
+      mbar_init(&abar[i], TB_GW);
+      mbar_init(&bbar[i], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_short = 0;
   }
@@ -174,12 +181,8 @@ __global__ void __launch_bounds__(TB_THREADS, 1) tile_bins_kernel(const ScanArgs
   const int width = (A.epi == EPI_MINMAX || A.epi == EPI_SLOTS_MINMAX) ? 2 : 4;
   const bool direct = A.out && (A.epi == EPI_MINMAX || A.epi == EPI_M4);
   const int64_t nb_cta = A.g0 + blockIdx.x < A.g1 ? (A.g1 - A.g0 - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  int slot = 0, it = 0;
-  uint32_t parity = 0;
+  int it = 0;     // tile number in the CTA's sequence (continues across table passes)
   int pslot = 0;  // control lane 0: next slot to fill
-#ifdef TSDS_TILE_TIMING
-  unsigned long long tt0 = gtimer(), t_wait = 0, t_red = 0, t_first = 0, t_seg = 0, t_bw = 0, t_ca = 0, t_cr = 0;
-#endif
   for (int64_t base = 0; base < nb_cta; base += TB_TAB) {
     const int cnt = (int)(nb_cta - base < TB_TAB ? nb_cta - base : TB_TAB);
     if (tid < cnt) {  // the bin table of this pass, one bin per thread
@@ -198,6 +201,8 @@ __global__ void __launch_bounds__(TB_THREADS, 1) tile_bins_kernel(const ScanArgs
       auto issue = [&](int sl) {
         const int64_t jb = (pc.ta + A.shift + VEC - 1) / VEC, je = (pc.tb(TE) + A.shift) / VEC;
         const uint32_t bytes = je > jb ? (uint32_t)(je - jb) * 16u : 0u;
+        TSDS_CHECK(bytes <= (uint32_t)TB_SLOT_BYTES && sl >= 0 && sl < TB_SLOTS);
+        TSDS_CHECK(pc.ta >= A.E0 && pc.tb(TE) <= A.E1);
         mbar_arrive_expect_tx(&full[sl], bytes);
         if (bytes) bulk_g2s(tb_smem + (size_t)sl * TB_SLOT_BYTES, yvirt + jb, bytes, &full[sl]);
       };
@@ -212,17 +217,10 @@ __global__ void __launch_bounds__(TB_THREADS, 1) tile_bins_kernel(const ScanArgs
       MinMaxCand acc{cand_none_min(), cand_none_max()};  // lane 0: the bin's running result over its tiles
       bool nan0 = false;
       for (; !cc.done(); cc.next(tab_s, tab_e, TE), it++) {
-        const int buf = it & 1;
-#ifdef TSDS_TILE_TIMING
-        unsigned long long tc0 = gtimer();
-#endif
-        nbar_sync(1 + buf);  // A(buf): partials written, the slot is no longer read
-#ifdef TSDS_TILE_TIMING
-        unsigned long long tc1 = gtimer();
-        t_ca += tc1 - tc0;
-#endif
+        const int grp = it % TB_SLOTS, m_it = it / TB_SLOTS, buf = m_it & 1;
+        mbar_wait(&abar[grp * 2 + buf], (uint32_t)(m_it >> 1) & 1u);  // A: partials written, slot no longer read
         if constexpr (!PROP && O::IEEE) {  // the NaN-first-slot rule (A.3)
-          if (lane == 0 && cc.ta == cc.s) nan0 = nan_s[buf] != 0;
+          if (lane == 0 && cc.ta == cc.s) nan0 = nan_s[grp][buf] != 0;
         }
         if (lane == 0 && !pc.done()) {  // refill the slot just released
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -231,10 +229,11 @@ __global__ void __launch_bounds__(TB_THREADS, 1) tile_bins_kernel(const ScanArgs
           pc.next(tab_s, tab_e, TE);
         }
         MinMaxCand m{cand_none_min(), cand_none_max()};
-        if (lane < TB_WARPS) m = part_s[buf][lane];
-        nbar_arrive(3 + buf);  // B(buf): partials consumed
+        if (lane < TB_GW) m = part_s[grp][buf][lane];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bbar[grp * 2 + buf]);  // B: partials consumed
 #pragma unroll
-        for (int d = TB_WARPS / 2; d >= 1; d >>= 1) {
+        for (int d = TB_GW / 2; d >= 1; d >>= 1) {
           const Cand x = shfl_cand(m.mn, d), z = shfl_cand(m.mx, d);
           merge_min(m.mn, x);
           merge_max(m.mx, z);
@@ -245,6 +244,7 @@ __global__ void __launch_bounds__(TB_THREADS, 1) tile_bins_kernel(const ScanArgs
           if (cc.last_tile(TE)) {
             const int64_t g = A.g0 + blockIdx.x + (base + cc.i) * gridDim.x, bs = cc.s, be = cc.e;
             const int64_t lo = nan0 ? bs : acc.mn.idx, hi = nan0 ? bs : acc.mx.idx;
+            TSDS_CHECK(g >= A.g0 && g < A.g1 && lo >= bs && lo < be && hi >= bs && hi < be);
             int64_t* o = A.res + 2 * (g - A.g0);
             o[0] = lo;
             o[1] = hi;
@@ -270,86 +270,57 @@ __global__ void __launch_bounds__(TB_THREADS, 1) tile_bins_kernel(const ScanArgs
             nan0 = false;
           }
         }
-#ifdef TSDS_TILE_TIMING
-        t_cr += gtimer() - tc1;
-#endif
       }
-#ifdef TSDS_TILE_TIMING
-      if (lane == 0 && blockIdx.x == 0) printf("control: A-wait %.1f us, rest %.1f us\n", t_ca * 1e-3, t_cr * 1e-3);
-#endif
     } else {
       // -------------------------------------------------------------- reducers
+      const int grp = wid / TB_GW, wg = wid % TB_GW;  // the group's slot, the warp's share of its tiles
       for (; !cc.done(); cc.next(tab_s, tab_e, TE), it++) {
-        const int buf = it & 1;
+        if (it % TB_SLOTS != grp) continue;
+        const int m_it = it / TB_SLOTS, buf = m_it & 1;
         const int64_t ta = cc.ta, tb = cc.tb(TE);
-#ifdef TSDS_TILE_TIMING
-        unsigned long long ta0 = gtimer();
-#endif
-        mbar_wait(&full[slot], parity);
-#ifdef TSDS_TILE_TIMING
-        unsigned long long ta1 = gtimer();
-        t_wait += ta1 - ta0;
-        if (it == 0) t_first = ta1 - tt0;
-#endif
-        // the tile's full vectors split evenly over the warps at vector
+        mbar_wait(&full[grp], (uint32_t)m_it & 1u);
+        // the tile's full vectors split evenly over the group's warps at vector
         // boundaries: only the tile's own head / tail are scalar (global) loads
         const int64_t JB = (ta + A.shift + VEC - 1) / VEC, JE = (tb + A.shift) / VEC;
         const int64_t nvt = JE > JB ? JE - JB : 0;
         int64_t a, c;
         if (nvt == 0) {
           a = ta;
-          c = wid == 0 ? tb : ta;
+          c = wg == 0 ? tb : ta;
         } else {
-          a = wid == 0 ? ta : (JB + nvt * wid / TB_WARPS) * VEC - A.shift;
-          c = wid == TB_WARPS - 1 ? tb : (JB + nvt * (wid + 1) / TB_WARPS) * VEC - A.shift;
+          a = wg == 0 ? ta : (JB + nvt * wg / TB_GW) * VEC - A.shift;
+          c = wg == TB_GW - 1 ? tb : (JB + nvt * (wg + 1) / TB_GW) * VEC - A.shift;
         }
+        TSDS_CHECK(a >= ta && c <= tb && a <= c);
+        TSDS_CHECK(nvt * 16 <= TB_SLOT_BYTES);
         MinMaxCand r{cand_none_min(), cand_none_max()};
         if (c > a) {
-          const SmemSrc src{smem_u32(tb_smem + (size_t)slot * TB_SLOT_BYTES), JB};
-          r = seg_reduce_src<DT, PROP, 4>(A, a, c, src);
+          const SmemSrc src{smem_u32(tb_smem + (size_t)grp * TB_SLOT_BYTES), JB};
+          r = seg_reduce_src<DT, PROP, 8>(A, a, c, src);
         }
-#ifdef TSDS_TILE_TIMING
-        unsigned long long ta2 = gtimer();
-        t_seg += ta2 - ta1;
-#endif
         bool nanp = false;
         if constexpr (!PROP && O::IEEE) {  // the bin's first element: out of the tile's copy when it lies in a full vector
-          if (wid == 0 && lane == 0 && ta == cc.s) {
+          if (wg == 0 && lane == 0 && ta == cc.s) {
             const int64_t rel = ta + A.shift - JB * VEC;
             if (rel >= 0 && nvt > 0)
-              nanp = smem_elem_is_nan<DT>(smem_u32(tb_smem + (size_t)slot * TB_SLOT_BYTES) + (uint32_t)(rel * sizeof(E)));
+              nanp = smem_elem_is_nan<DT>(smem_u32(tb_smem + (size_t)grp * TB_SLOT_BYTES) + (uint32_t)(rel * sizeof(E)));
             else
               nanp = elem_is_nan<DT>(A.y, ta);
           }
         }
-#ifdef TSDS_TILE_TIMING
-        unsigned long long ta3 = gtimer();
-#endif
-        if (it >= 2) nbar_sync(3 + buf);  // B(buf): the control warp consumed the partials of tile it - 2
-#ifdef TSDS_TILE_TIMING
-        t_bw += gtimer() - ta3;
-#endif
-        if (lane == 0) part_s[buf][wid] = r;
-        if constexpr (!PROP && O::IEEE) {
-          if (wid == 0 && lane == 0) nan_s[buf] = nanp ? 1 : 0;
+        if (m_it >= 2) mbar_wait(&bbar[grp * 2 + buf], (uint32_t)((m_it >> 1) - 1) & 1u);  // B: partials of m_it - 2 consumed
+        if (lane == 0) {
+          part_s[grp][buf][wg] = r;
+          if constexpr (!PROP && O::IEEE) {
+            if (wg == 0) nan_s[grp][buf] = nanp ? 1 : 0;
+          }
         }
-        nbar_arrive(1 + buf);  // A(buf); the barrier orders the shared-memory writes above for its waiter
-#ifdef TSDS_TILE_TIMING
-        t_red += gtimer() - ta1;
-#endif
-        if (++slot == TB_SLOTS) {
-          slot = 0;
-          parity ^= 1u;
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&abar[grp * 2 + buf]);  // A (release): the writes above are visible to its waiter
       }
     }
     __syncthreads();  // the table is rewritten by the next pass
   }
-#ifdef TSDS_TILE_TIMING
-  if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
-    printf("tile timing cta %d: tiles %d, first data %.1f us, wait %.1f, reduce %.1f (seg %.1f, B-wait %.1f), loop total %.1f us\n",
-           blockIdx.x, it, t_first * 1e-3, t_wait * 1e-3, t_red * 1e-3, t_seg * 1e-3, t_bw * 1e-3, (gtimer() - tt0) * 1e-3);
-#endif
   if (direct && tid == 0 && s_short) atomicOr((int*)&A.flags->tile_short, 1);
   scan_epilogue_t<true>(A, B, false, direct ? width : 0);
 }

@@ -5,7 +5,7 @@ slots (csrc/tsds_staging.h), which costs host-DRAM bandwidth (read + write +
 DMA read) and tops out below the PCIe rate.  Downsampling is typically
 called again and again on the same array (interactive zooming, different
 n_out, the estimator classes), so the second time an array of at least
-``TSDS_PIN_MIN_BYTES`` (default 64 MiB) is seen, its owner's buffer is
+``TSDS_PIN_MIN_BYTES`` (default 8 MiB, the staging ring's own threshold) is seen, its owner's buffer is
 page-locked in place with ``tsds_host_register`` (cudaHostRegister,
 ~13 GB/s once) and later uploads are DMA'd directly from it at link speed.
 
@@ -37,7 +37,7 @@ def _default_cap():
 
 
 _mode = os.environ.get("TSDS_PIN_CACHE", "reuse").lower()
-_min_bytes = int(os.environ.get("TSDS_PIN_MIN_BYTES", 64 << 20))
+_min_bytes = int(os.environ.get("TSDS_PIN_MIN_BYTES", 8 << 20))
 _max_bytes = int(os.environ.get("TSDS_PIN_MAX_BYTES", _default_cap()))
 _lock = threading.Lock()
 _seen = {}  # id(owner) -> sightings (negative: registration failed, do not retry)
