@@ -509,8 +509,8 @@ def run_ours(args):
     if "cpu_baseline" in head:
         line["cpu_baseline"] = head["cpu_baseline"]
     line["configs"] = entries
-    print(json.dumps(line), flush=True)
     del torch
+    return line
 
 
 # ------------------------------------------------------------ sharded (N GPUs)
@@ -584,6 +584,7 @@ def run_ours_sharded(args):
 
     def e2e_time(fn):
         fn()
+        fn()  # the second call on an array page-locks it (pinning.py); steady state from the third
         dist.barrier()
         t0 = time.perf_counter()
         for _ in range(3):
@@ -678,10 +679,9 @@ def run_ours_sharded(args):
         "gpu_launches": head["gpu_launches_per_step_rank0"] * args.steps, "e2e": head["e2e"],
         "parity": head["parity"], "clocks": clk.summary(), "configs": entries,
     }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
     ex.close()
     dist.destroy_process_group()
+    return line if rank == 0 else None
 
 
 def run_reference(args):
@@ -715,7 +715,23 @@ def run_reference(args):
             "data": "synthetic (workloads.py, seeded generators of BASELINE configs, SURVEY.md 8(d))",
             "config": head["config"], "points_per_s": head["points_per_s"], "cpu_baseline": head["cpu_baseline"],
             "e2e": head["e2e"], "configs": entries}
-    print(json.dumps(line), flush=True)
+    return line
+
+
+class _StdoutToStderr:
+    """Library chatter on fd 1 (e.g. NCCL's version banner) must not precede
+    the JSON line: everything written to stdout while open goes to stderr."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
 
 
 def main():
@@ -733,10 +749,10 @@ def main():
     args.configs = [c.strip().upper() for c in args.configs.split(",") if c.strip()]
     if args.impl == "ours":
         args.warmup = max(3, args.warmup)
-    if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_ours(args)
+    with _StdoutToStderr():
+        line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -742,7 +742,8 @@ static inline unsigned cap_grid(int64_t want, int64_t cap) {
 // no host round trip; consecutive kernels are chained with programmatic
 // dependent launch.
 int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
-                   const int64_t* off, int64_t nb, const int64_t* map, int64_t* idx_out, int64_t* cnt_out) {
+                   const int64_t* off, int64_t nb, const int64_t* map, int64_t* idx_out, int64_t* cnt_out,
+                   int64_t fill_len, int64_t fill_add) {
   if (nb >= ((int64_t)1 << 24))  // work-list entries pack the bucket rank into 24 bits
     return set_err(TSDS_ERR_ARG, "large-bucket LTTB supports fewer than 2^24 buckets");
   RC_TRY(ensure(ctx, ctx->cent, (size_t)std::max<int64_t>(nb, 1) * sizeof(double2)));
@@ -811,9 +812,9 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
                auto kg = lttb_guess_kernel<YD>;
                cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(cap + 16));
                const unsigned gg = std::min<unsigned>(one_wave(ctx, kg, 256, (size_t)(cap + 16)), (unsigned)nbl);
-               RC_TRY(launch_coop(ctx, kg, gg, 256, (size_t)(cap + 16), xf, drop, y, n, off, nb, A, cent, yr, bcnt,
-                                  nonempty, rank, counts, ext, T, C, entry, picks, r1, arrive, slots, wl, list_a, ctr,
-                                  exact, cap));
+               RC_TRY(launch_coop(ctx, kg, gg, 256, (size_t)(cap + 16), xf, drop, y, n, (int64_t*)off, nb, A, cent, yr,
+                                  bcnt, nonempty, rank, counts, ext, T, C, entry, picks, r1, arrive, slots, wl, list_a,
+                                  ctr, exact, cap, fill_len, fill_add));
              }));
   // ---- 3. round-1 evaluation, 4. correction chains, 5. output
   YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_eval_kernel<YD>, one_wave(ctx, lttb_eval_kernel<YD>, 256), 256, 0, xf,
@@ -833,10 +834,21 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   return TSDS_OK;
 }
 
+// fill_len > 0: `off` (int64[nb + 1], writable) still has to be filled with the
+// equal-count offsets floor(k * fill_len / nb) + fill_add; the large-bucket
+// path does it inside its first kernel, the small-bucket path with a launch.
 int run_lttb_walk(tsds_ctx* ctx, const double* xf, const int* drop, const void* y, int ydt, int64_t n,
-                  const int64_t* off, int64_t nb, const int64_t* map, int64_t* idx_out, int64_t* cnt_out) {
+                  const int64_t* off, int64_t nb, const int64_t* map, int64_t* idx_out, int64_t* cnt_out,
+                  int64_t fill_len = 0, int64_t fill_add = 0) {
   const int64_t avg = (n - 2) / std::max<int64_t>(nb, 1);
-  if (avg > SMALL_MAX / 2) return run_lttb_large(ctx, xf, drop, y, ydt, n, off, nb, map, idx_out, cnt_out);
+  if (avg > SMALL_MAX / 2) {
+    if (fill_len > 0 && fill_len < nb) {  // some empty buckets: materialise, then the general list phases
+      RC_TRY(launch_count_offsets(ctx, fill_len, nb, fill_add, (int64_t*)off));
+      fill_len = 0;
+    }
+    return run_lttb_large(ctx, xf, drop, y, ydt, n, off, nb, map, idx_out, cnt_out, fill_len, fill_add);
+  }
+  if (fill_len > 0) RC_TRY(launch_count_offsets(ctx, fill_len, nb, fill_add, (int64_t*)off));
   return run_lttb_walk_small(ctx, xf, drop, y, ydt, n, off, nb, map, idx_out, cnt_out);
 }
 
@@ -990,9 +1002,10 @@ int enqueue_lttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, 
   const void* dy;
   RC_TRY(stage_input(ctx, ctx->y, y, (size_t)n * dtype_size(ydt), mem, &dy));
   RC_TRY(interior_bins(ctx, x, xdt, n, nb, mem, &bins, &guards, &xk, 1, &hb));
-  if (bins.mode == 0 && !guards.use_dyn_mode) {
+  int64_t fill_len = 0;
+  if (bins.mode == 0 && !guards.use_dyn_mode) {  // equal-count offsets: filled by the walk's first kernel
     RC_TRY(ensure(ctx, ctx->off, (size_t)(nb + 1) * 8));
-    RC_TRY(launch_count_offsets(ctx, n - 2, nb, 1, (int64_t*)ctx->off.p));
+    fill_len = n - 2;
   }
   const int64_t* off = (const int64_t*)ctx->off.p;
   const double* xf = nullptr;
@@ -1003,7 +1016,7 @@ int enqueue_lttb(tsds_ctx* ctx, const void* x, int xdt, const void* y, int ydt, 
     RC_TRY(to_f64(ctx, dx, xdt, n, ctx->xf64, &xf));
     if (mem == TSDS_MEM_DEVICE) drop = &misc(ctx)->F.mis_api;  // api-level uniform verdict, read by the walk
   }
-  return run_lttb_walk(ctx, xf, drop, dy, ydt, n, off, nb, nullptr, idx_out, cnt_out);
+  return run_lttb_walk(ctx, xf, drop, dy, ydt, n, off, nb, nullptr, idx_out, cnt_out, fill_len, 1);
 }
 
 // MinMaxLTTB (algorithms.py:211-255) enqueued into (idx_out, cnt_out).

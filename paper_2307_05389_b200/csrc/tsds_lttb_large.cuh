@@ -980,13 +980,14 @@ __device__ __forceinline__ void lttb_plan_phase(const double* x, const void* y, 
 // ctr: [2] |D|, [6..7] sub-blocks listed (int64).
 template <int YDT>
 __global__ void __launch_bounds__(256, 3)
-lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, const int64_t* off, int64_t nb,
+lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, int64_t* off_w, int64_t nb,
                   const LttbSBArrays A, double2* cent, float2* yr, int32_t* bcnt, int32_t* nonempty, int32_t* rank,
                   int64_t* counts, int64_t* ext, uint8_t* T, uint8_t* C, uint8_t* entry, int64_t* picks,
                   LttbRound1* r1, int32_t* arrive, int64_t* slots, int64_t* wl, int32_t* list, int32_t* ctr,
-                  int exact, int64_t cap) {
+                  int exact, int64_t cap, int64_t fill_len, int64_t fill_add) {
   pdl_launch_dependents();
   pdl_wait();
+  const int64_t* off = off_w;
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ uint8_t lttb_dsm[];
@@ -1004,10 +1005,26 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
     }
   };
   stamp(0);
-  lttb_count_phase(off, nb, bcnt, s_red);
-  grid.sync();
-  lttb_list_phase(off, nb, bcnt, nonempty, rank, counts, s_red, &s_base);
-  grid.sync();
+  if (fill_len >= nb) {
+    // equal-count buckets over fill_len >= nb points (binning.py:27-40): the
+    // offsets are written here (no separate launch) and every bucket is
+    // non-empty, so the list is the identity -- one barrier instead of two
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= nb; k += (int64_t)gridDim.x * blockDim.x) {
+      const unsigned __int128 p128 = (unsigned __int128)(uint64_t)k * (uint64_t)fill_len;
+      off_w[k] = (int64_t)(p128 / (uint64_t)nb) + fill_add;
+      if (k < nb) {
+        nonempty[k] = (int32_t)k;
+        rank[k] = (int32_t)k;
+      }
+      if (k == 0) counts[0] = nb;
+    }
+    grid.sync();
+  } else {
+    lttb_count_phase(off, nb, bcnt, s_red);
+    grid.sync();
+    lttb_list_phase(off, nb, bcnt, nonempty, rank, counts, s_red, &s_base);
+    grid.sync();
+  }
   stamp(1);
   const int G = lttb_pick_group(counts[0]);
   if (G == 32) lttb_cent_phase<YDT, 32>(x, y, off, nonempty, counts, A, cent, yr);
