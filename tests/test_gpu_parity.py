@@ -361,8 +361,9 @@ def test_tile_bins_kernel(ts, oracle, mode):
                 y[[0, 1250, 2500]] = np.nan
             x = np.cumsum(rng.integers(1, 9, y.size)).astype(np.int64)
             x[100_000:] += 40_000  # a gap: empty bins with many bins
+            # ... ("minmax", 200_000): > 512 bins per CTA, i.e. several passes over the CTA's bin table
             for algo, n_out in (("minmax", 2000), ("m4", 400), ("minmax", 6), ("m4", 4), ("minmax", 50_000),
-                                ("minmaxlttb", 300)):
+                                ("minmax", 200_000), ("minmaxlttb", 300)):
                 want = oracle.downsample(algo, y, n_out=n_out)
                 assert ts.downsample(algo, y, n_out=n_out).tolist() == want.tolist(), (tag, algo, n_out)
                 want = oracle.downsample(algo, x, y, n_out=n_out)
