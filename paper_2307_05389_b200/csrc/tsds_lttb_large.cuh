@@ -1062,6 +1062,115 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   stamp(5);
 }
 
+// lane-group versions of lttb_eval_sb / lttb_settle_warp (round-1 evaluation:
+// several work-list entries per warp at once when there are more entries
+// than warps)
+template <int G>
+__device__ __forceinline__ AreaCand group_area_max(AreaCand c, unsigned gmask) {
+#pragma unroll
+  for (int m = G / 2; m >= 1; m >>= 1) {
+    const AreaCand o{__shfl_xor_sync(gmask, c.a, m), __shfl_xor_sync(gmask, c.i, m)};
+    if (area_better(o, c)) c = o;
+  }
+  return c;
+}
+
+template <int YDT, int G>
+__device__ __forceinline__ AreaCand lttb_eval_sb_g(const double* x, const void* y, int vec_ok, int64_t cs, int64_t ce,
+                                                   const LttbPlan& P, double cx, double cy, int l, unsigned gmask) {
+  constexpr int EPV = SBG<YDT>::EPV;
+  AreaCand best{-1.0, IDX_NONE};
+  if (x || !vec_ok) {
+    const double ax = xd(x, P.prev);
+    for (int64_t i = cs + l; i < ce; i += G) {
+      const AreaCand a{tri_area(ax, P.ay, cx, cy, xd(x, i), yd<YDT>(y, i)), i};
+      if (area_better(a, best)) best = a;
+    }
+    return group_area_max<G>(best, gmask);
+  }
+  const int64_t v0 = cs / EPV, v1 = (ce + EPV - 1) / EPV;  // vectors overlapping [cs, ce)
+  const uint4* yv = (const uint4*)y;
+  for (int64_t vb = v0; vb < v1; vb += G * 4) {
+    uint4 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int64_t v = vb + u * G + l;
+      if (v < v1) q[u] = __ldg(yv + v);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int64_t v = vb + u * G + l;
+      if (v < v1) {
+        const int64_t i0 = v * EPV;
+        const double dA = (double)(P.prev - i0);
+#pragma unroll
+        for (int e = 0; e < EPV; e++) {
+          const double a = lttb_varea<YDT>(q[u], e, dA, P.ay, P.K1, P.K2);
+          // first max in index order: a lane's vectors ascend, ties across lanes resolve by index below
+          if (i0 + e >= cs && i0 + e < ce && a > best.a) best = AreaCand{a, i0 + e};
+        }
+      }
+    }
+  }
+  return group_area_max<G>(best, gmask);
+}
+
+template <int G>
+__device__ __forceinline__ void lttb_settle_g(int64_t j, int64_t L, int64_t s, const AreaCand& cbj,
+                                              const AreaCand* part, int64_t base, int64_t cnt, int64_t* picks,
+                                              int32_t* list, int32_t* dcnt, int l, unsigned gmask) {
+  AreaCand best = l == 0 ? cbj : AreaCand{-1.0, IDX_NONE};
+  for (int64_t t = l; t < cnt; t += G) {
+    const AreaCand a{__ldcg(&part[base + t].a), __ldcg(&part[base + t].i)};
+    if (area_better(a, best)) best = a;
+  }
+  best = group_area_max<G>(best, gmask);
+  if (l == 0) {
+    const int64_t p = best.i == IDX_NONE ? s : best.i;
+    if (p != __ldcg(picks + j)) {
+      __stcg(picks + j, p);
+      if (j + 1 < L) list[atomicAdd(dcnt, 1)] = (int32_t)(j + 1);
+    }
+  }
+}
+
+// one round-1 work-list pass with G lanes per entry
+template <int YDT, int G>
+__device__ __forceinline__ void lttb_eval_pass(const double* x, const void* y, int64_t n, const int64_t* off,
+                                               int64_t nb, const LttbSBArrays& A, const double2* cent,
+                                               const int32_t* nonempty, int64_t L, int64_t np, const LttbRound1* r1,
+                                               int32_t* arrive, AreaCand* part, const int64_t* slots,
+                                               const int64_t* wl, int64_t* picks, int32_t* list, int32_t* ctr,
+                                               int vec_ok) {
+  const int lane = threadIdx.x & 31, l = lane & (G - 1), gbase = lane & ~(G - 1);
+  const unsigned gmask = lttb_gmask<G>(lane);
+  const int64_t grp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t t = grp; t < np; t += ngrp) {
+    const int64_t pos = __ldcg(wl + t);
+    const int64_t ent = __ldcg(slots + pos);
+    const int64_t g = ent >> 24, j = ent & 0xffffff;
+    TSDS_CHECK(j >= 0 && j < L && g >= 0 && g * A.SB < n);
+    const int64_t k = nonempty[j];
+    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+    const LttbPlan P = r1[j].P;
+    double cx = 0.0, cy = 0.0;
+    if (x || !vec_ok) centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
+    int64_t cs, ce;
+    lttb_sb_range(A.SB, g, s, e, cs, ce);
+    const AreaCand a = lttb_eval_sb_g<YDT, G>(x, y, vec_ok, cs, ce, P, cx, cy, l, gmask);
+    int last = 0;
+    if (l == 0) {
+      part[pos] = a;
+      __threadfence();
+      last = atomicSub(arrive + j, 1) == 1;
+      if (last) __threadfence();
+    }
+    if (__shfl_sync(gmask, last, gbase))
+      lttb_settle_g<G>(j, L, s, r1[j].cb, part, r1[j].base, r1[j].cnt, picks, list, ctr + 2, l, gmask);
+  }
+}
+
 // Round-1 evaluation, warp per work-list entry (a sub-block slot): exact
 // first max with the guessed predecessor into part[slot]; the warp completing a bucket's last
 // sub-block settles it.  Afterwards every bucket not in D satisfies
@@ -1081,29 +1190,13 @@ lttb_eval_kernel(const double* xin, const int* drop, const void* y, int64_t n, c
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t np = (int64_t)__ldcg((const unsigned long long*)(ctr + 6));
-  for (int64_t t = gw; t < np; t += nw) {
-    const int64_t pos = __ldcg(wl + t);
-    const int64_t ent = __ldcg(slots + pos);
-    const int64_t g = ent >> 24, j = ent & 0xffffff;
-    TSDS_CHECK(j >= 0 && j < L && g >= 0 && g * A.SB < n);
-    const int64_t k = nonempty[j];
-    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
-    const LttbPlan P = r1[j].P;
-    double cx = 0.0, cy = 0.0;
-    if (x || !vec_ok) centroid_for<YDT>(x, y, off, nb, cent, k, n, cx, cy);
-    int64_t cs, ce;
-    lttb_sb_range(A.SB, g, s, e, cs, ce);
-    const AreaCand a = lttb_eval_sb<YDT>(x, y, vec_ok, A, g, cs, ce, P, cx, cy, lane);
-    int last = 0;
-    if (lane == 0) {
-      part[pos] = a;
-      __threadfence();
-      last = atomicSub(arrive + j, 1) == 1;
-      if (last) __threadfence();
-    }
-    if (__shfl_sync(0xffffffffu, last, 0))
-      lttb_settle_warp(j, L, s, r1[j].cb, part, r1[j].base, r1[j].cnt, picks, list, ctr + 2, lane);
-  }
+  // lane groups sized so that every work-list entry is taken in the first round
+  if (np <= nw)
+    lttb_eval_pass<YDT, 32>(x, y, n, off, nb, A, cent, nonempty, L, np, r1, arrive, part, slots, wl, picks, list, ctr, vec_ok);
+  else if (np <= 2 * nw)
+    lttb_eval_pass<YDT, 16>(x, y, n, off, nb, A, cent, nonempty, L, np, r1, arrive, part, slots, wl, picks, list, ctr, vec_ok);
+  else
+    lttb_eval_pass<YDT, 8>(x, y, n, off, nb, A, cent, nonempty, L, np, r1, arrive, part, slots, wl, picks, list, ctr, vec_ok);
 }
 
 __device__ __forceinline__ void lttb_lock(int32_t* l) {
