@@ -1242,6 +1242,8 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   __shared__ int64_t sk[3];  // k, s, e
   __shared__ int64_t sq[NSQ];
   __shared__ int sn, sgo;
+  __shared__ int64_t s_prev;  // the pick this chain just stored into picks[j - 1] (valid when the chain continued)
+  __shared__ int s_have_prev;
   // static data of the chain's next bucket, prefetched while the current
   // bucket is being settled (everything but the predecessor is known)
   __shared__ int64_t pf_j, pf_k[3], pf_ci[LTTB_NC];
@@ -1252,10 +1254,17 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   for (int64_t t = blockIdx.x; t < nD; t += gridDim.x) {
     int64_t j = __ldcg(list + t);
     int clen = 0;  // steps of this chain (stat: longest chain, ctr[10])
-    if (tid == 0) pf_j = pf_mmj = -1;
+    if (tid == 0) {
+      pf_j = pf_mmj = -1;
+      s_have_prev = 0;
+    }
     __syncthreads();
     for (;;) {
       clen++;
+      // bucket j's lock is taken by a second thread while the plan and the
+      // evaluation run (its round trip leaves the critical path); thread 0
+      // validates, stores and releases at the end of the step
+      if (tid == 32) lttb_lock(lock + j);
       if (wid == 0) {
         int64_t k, s, e;
         LttbPlan P;
@@ -1267,7 +1276,9 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
           e = pf_k[2];
           cx = pf_c[0];
           cy = pf_c[1];
-          P.prev = j == 0 ? 0 : __ldcg(picks + j - 1);
+          // the chain's own previous store, if any (a concurrent change of
+          // picks[j - 1] is caught by the validation under the lock)
+          P.prev = j == 0 ? 0 : (s_have_prev ? s_prev : __ldcg(picks + j - 1));
           const double ax = xd(x, P.prev);
           P.ay = yd<YDT>(y, P.prev);
           P.K1 = __dsub_rn(ax, cx);
@@ -1339,8 +1350,7 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
           if (area_better(sW[w], b)) b = sW[w];
         const int64_t pk = b.i == IDX_NONE ? s : b.i;
         TSDS_CHECK(pk >= s && pk < e);
-        int go = 0;
-        lttb_lock(lock + j);
+        int go = 0;  // (the lock was acquired by thread 32 at the start of the step)
         const int64_t cur = j == 0 ? 0 : lttb_ld_relaxed(picks + j - 1);
         if (cur == P.prev && pk != lttb_ld_relaxed(picks + j)) {
           asm volatile("st.relaxed.gpu.b64 [%0], %1;" ::"l"(picks + j), "l"(pk) : "memory");
@@ -1348,6 +1358,8 @@ lttb_chain_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
         }
         lttb_unlock(lock + j);
         sgo = go;
+        s_prev = pk;
+        s_have_prev = go;
       } else if (wid > 0 && j + 1 < L) {
         // meanwhile warps 1.. prefetch bucket j+1 (used only if the chain goes on)
         const int64_t jn = j + 1;

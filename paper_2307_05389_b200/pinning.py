@@ -83,6 +83,8 @@ def _release(key):
     if ent is None:
         return
     ptr = ent[0]
+    if ptr is None:  # already unregistered by the owner's finalizer
+        return
     try:
         _lib.load().tsds_host_unregister(None, ptr)
         stats["released"] += 1
@@ -90,22 +92,52 @@ def _release(key):
         pass
 
 
+_pending = []  # owners collected while the lock was held (a finalizer can run inside any allocation)
+
+
+def _forget(key):
+    _seen.pop(key, None)
+    _refs.pop(key, None)
+    _release(key)
+
+
 def _on_collect(key):
-    with _lock:
-        _seen.pop(key, None)
-        _refs.pop(key, None)
-        _release(key)
+    # The owner is gone: its pages must be released NOW, before the allocator can hand the same
+    # addresses to a new array (a stale registration would DMA the old physical pages).  The
+    # unregister needs no lock (nobody else can touch a dead owner's entry); only the
+    # bookkeeping below may have to wait.
+    ent = _pinned.get(key)
+    if ent is not None and ent[0] is not None:
+        _pinned[key] = (None, ent[1], ent[2])
+        try:
+            _lib.load().tsds_host_unregister(None, ent[0])
+            stats["released"] += 1
+        except Exception:
+            pass
+    if _lock.acquire(blocking=False):
+        try:
+            _forget(key)
+        finally:
+            _lock.release()
+    else:  # this thread (or another) is inside the cache: handled at its next entry
+        _pending.append(key)
+
+
+def _drain_pending():
+    while _pending:
+        _forget(_pending.pop())
 
 
 def release_all():
     with _lock:
+        _drain_pending()
         for key in list(_pinned):
             _release(key)
         _seen.clear()
 
 
 def pinned_bytes():
-    return sum(e[1] for e in _pinned.values())
+    return sum(e[1] for e in list(_pinned.values()) if e[0] is not None)
 
 
 def note_host_input(a, device=None):
@@ -118,6 +150,7 @@ def note_host_input(a, device=None):
         return False
     key = id(o)
     with _lock:
+        _drain_pending()
         if key in _pinned:
             _pinned.move_to_end(key)
             stats["hits"] += 1
