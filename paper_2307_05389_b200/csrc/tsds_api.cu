@@ -364,7 +364,7 @@ int launch_scan_t(tsds_ctx* ctx, ScanArgs& A) {
   }
   if (A.atomic_mode) {
     cudaLaunchConfig_t fc = {};
-    fc.gridDim = dim3(1);
+    fc.gridDim = dim3((unsigned)std::min<int64_t>(32, (nbins + 1023) / 1024));
     fc.blockDim = dim3(1024);
     fc.stream = ctx->stream;
     cudaLaunchAttribute fa[1];

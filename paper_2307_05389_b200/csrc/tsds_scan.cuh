@@ -741,7 +741,11 @@ __global__ void __launch_bounds__(1024) atomic_finish_kernel(const ScanArgs A) {
   if (A.use_dyn_mode) B.mode = *(volatile int*)&F->mode;
   const bool aborted = A.check_flags && *(volatile int*)&F->status;
   const bool indep = A.independent || (A.check_flags && *(volatile int*)&F->nonmono);
-  for (int64_t g = A.g0 + threadIdx.x; g < A.g1; g += blockDim.x) {
+  // per-bin part over the whole grid (one bin per thread for <= 32K bins: a
+  // single CTA walking 10 bins per thread, each with dependent L2 / DRAM round
+  // trips, cost C4 ~30 us); the last CTA to finish runs the compaction
+  for (int64_t g = A.g0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < A.g1;
+       g += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long am = __ldcg(A.amin + (g - A.g0)), ax = __ldcg(A.amax + (g - A.g0));
     A.amin[g - A.g0] = ~0ull;
     A.amax[g - A.g0] = 0ull;
@@ -757,6 +761,17 @@ __global__ void __launch_bounds__(1024) atomic_finish_kernel(const ScanArgs A) {
     o[1] = hi;
   }
   __syncthreads();
+  if (gridDim.x > 1) {  // ticket (the scan skips its own epilogue in atomic mode, so its counter is free)
+    __shared__ int fin_last;
+    if (threadIdx.x == 0) {
+      fence_acq_rel_gpu();
+      const unsigned t = atomicAdd(&F->scan_blocks_done, 1u);
+      fin_last = (t == gridDim.x - 1);
+      if (fin_last) fence_acq_rel_gpu();
+    }
+    __syncthreads();
+    if (!fin_last) return;
+  }
   if (aborted) {
     if (threadIdx.x == 0) {
       if (A.epi == EPI_SLOTS_MINMAX || A.epi == EPI_SLOTS_M4) {
@@ -792,6 +807,7 @@ __global__ void __launch_bounds__(1024) atomic_finish_kernel(const ScanArgs A) {
       F->mode = 0;
     }
     F->work_ctr = 0ull;
+    F->scan_blocks_done = 0u;
   }
 }
 
