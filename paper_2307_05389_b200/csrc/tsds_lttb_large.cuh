@@ -961,6 +961,325 @@ __device__ __forceinline__ void lttb_plan_phase(const double* x, const void* y, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Few buckets (L <= a half / a quarter of the grid's warps): NWG = 2 or 4
+// adjacent warps of a CTA share a bucket -- each takes a contiguous share of
+// its sub-blocks, the partial results meet in shared memory (scratch: 64
+// bytes per warp and parity, double buffered) behind a named barrier of the
+// group.  Same results as the single-group phases except that the centroid's
+// summation tree gets one more level (the warps' partial sums, added in warp
+// order): a fixed function of the bucket and of NWG.
+struct LttbMwScratch {
+  double ty, tx;
+  float hi, lo;
+  unsigned key[LTTB_NC], pos[LTTB_NC];
+};
+
+template <int NWG>
+struct LttbMw {
+  int gi, r;          // group in the CTA, the warp's rank in the group
+  int64_t grp, ngrp;  // global group index / count
+  __device__ __forceinline__ LttbMw() {
+    const int wid = threadIdx.x >> 5;
+    gi = wid / NWG;
+    r = wid % NWG;
+    grp = (int64_t)blockIdx.x * ((blockDim.x >> 5) / NWG) + gi;
+    ngrp = (int64_t)gridDim.x * ((blockDim.x >> 5) / NWG);
+  }
+  __device__ __forceinline__ void sync() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + gi), "r"(NWG * 32) : "memory");
+  }
+  // the warp's share [ga, gb] of the bucket's sub-blocks [g0, g1]
+  __device__ __forceinline__ void share(int64_t g0, int64_t g1, int64_t& ga, int64_t& gb) const {
+    const int64_t chunk = (g1 - g0 + NWG) / NWG;
+    ga = g0 + r * chunk;
+    gb = ga + chunk - 1 < g1 ? ga + chunk - 1 : g1;
+  }
+};
+
+template <int YDT, int NWG>
+__device__ __forceinline__ void lttb_cent_phase_mw(const double* x, const void* y, const int64_t* off,
+                                                   const int32_t* nonempty, const int64_t* counts,
+                                                   const LttbSBArrays A, double2* cent, float2* yr,
+                                                   LttbMwScratch (*scr)[8]) {
+  constexpr int U = 4;
+  const LttbMw<NWG> M;
+  const int64_t SB = A.SB;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t L = counts[0];
+  int it = 0;
+  for (int64_t j = M.grp; j < L; j += M.ngrp, it++) {
+    const int64_t k = nonempty[j];
+    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+    const int64_t g0 = s / SB, g1 = (e - 1) / SB;
+    int64_t ga, gb_;
+    M.share(g0, g1, ga, gb_);
+    double sy = 0.0, sx = 0.0;
+    float hi = -INFINITY, lo = INFINITY;
+    for (int64_t gb = ga; gb <= gb_; gb += 32 * U) {
+      float2 m[U];
+      double vy[U], vx[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t g = gb + u * 32 + lane;
+        const bool full = g <= gb_ && g * SB >= s && (g + 1) * SB <= e;
+        m[u] = g <= gb_ ? A.mm[g] : make_float2(-INFINITY, INFINITY);
+        vy[u] = full ? A.sy[g] : 0.0;
+        vx[u] = (full && x) ? A.sx[g] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        hi = fmaxf(hi, m[u].x);
+        lo = fminf(lo, m[u].y);
+        sy = __dadd_rn(sy, vy[u]);
+        sx = __dadd_rn(sx, vx[u]);
+      }
+    }
+    auto partial = [&](int64_t a, int64_t b) {
+      for (int64_t i0 = a; i0 < b; i0 += 32 * U) {
+        double vy[U], vx[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const int64_t i = i0 + u * 32 + lane;
+          vy[u] = i < b ? yd<YDT>(y, i) : 0.0;
+          vx[u] = (i < b && x) ? __ldg(x + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          sy = __dadd_rn(sy, vy[u]);
+          sx = __dadd_rn(sx, vx[u]);
+        }
+      }
+    };
+    const int64_t h0e = (g0 + 1) * SB < e ? (g0 + 1) * SB : e;
+    if (M.r == 0 && (s % SB != 0 || h0e < (g0 + 1) * SB)) partial(s, h0e);           // head points: first warp
+    if (M.r == NWG - 1 && g1 > g0 && e % SB != 0) partial(g1 * SB, e);                // tail points: last warp
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      sy = __dadd_rn(sy, __shfl_xor_sync(0xffffffffu, sy, m));
+      sx = __dadd_rn(sx, __shfl_xor_sync(0xffffffffu, sx, m));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, m));
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, m));
+    }
+    LttbMwScratch* sc = scr[it & 1];
+    if (M.r > 0 && lane == 0) {
+      sc[wid].ty = sy;
+      sc[wid].tx = sx;
+      sc[wid].hi = hi;
+      sc[wid].lo = lo;
+    }
+    M.sync();
+    if (M.r == 0 && lane == 0) {
+      double py[NWG], px[NWG];
+      py[0] = sy;
+      px[0] = sx;
+#pragma unroll
+      for (int q = 1; q < NWG; q++) {
+        py[q] = sc[wid + q].ty;
+        px[q] = sc[wid + q].tx;
+        hi = fmaxf(hi, sc[wid + q].hi);
+        lo = fminf(lo, sc[wid + q].lo);
+      }
+      double ty, tx;
+      if constexpr (NWG == 2) {
+        ty = __dadd_rn(py[0], py[1]);
+        tx = __dadd_rn(px[0], px[1]);
+      } else {
+        ty = __dadd_rn(__dadd_rn(py[0], py[1]), __dadd_rn(py[2], py[3]));
+        tx = __dadd_rn(__dadd_rn(px[0], px[1]), __dadd_rn(px[2], px[3]));
+      }
+      const double cw = (double)(e - s);
+      if (!x) {
+        tx = (double)(s + e - 1) * cw < 9007199254740992.0 ? (double)((s + e - 1) * (e - s) / 2)
+                                                           : 0.5 * ((double)(s + e - 1) * cw);
+      }
+      cent[k] = make_double2(__ddiv_rn(tx, cw), __ddiv_rn(ty, cw));
+      yr[k] = make_float2(hi, lo);
+    }
+  }
+}
+
+template <int YDT, int NWG>
+__device__ __forceinline__ void lttb_cand_phase_mw(const double* x, const void* y, const int64_t* off, int64_t nb,
+                                                   int64_t n, const double2* cent, const float2* yr,
+                                                   const int32_t* nonempty, const int64_t* counts,
+                                                   const LttbSBArrays A, int64_t* ext, LttbMwScratch (*scr)[8]) {
+  constexpr int U = 4;
+  const LttbMw<NWG> M;
+  const int64_t SB = A.SB;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t L = counts[0];
+  int it = 0;
+  for (int64_t j = M.grp; j < L; j += M.ngrp, it++) {
+    const int64_t k = nonempty[j];
+    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+    const double2 sr = lttb_slope_range<YDT>(x, y, off, nb, n, cent, yr, nonempty, j, k);
+    float sl[LTTB_K];
+#pragma unroll
+    for (int t = 0; t < LTTB_K; t++) sl[t] = (float)(sr.x + (sr.y - sr.x) * ((double)t / (double)(LTTB_K - 1)));
+    const double xs = xd(x, s);
+    float bv[LTTB_NC];
+    unsigned bi[LTTB_NC];
+#pragma unroll
+    for (int c = 0; c < LTTB_NC; c++) { bv[c] = (c & 1) ? INFINITY : -INFINITY; bi[c] = 0xffffffffu; }
+    const int64_t g0 = s / SB, g1 = (e - 1) / SB;
+    int64_t ga, gb_;
+    M.share(g0, g1, ga, gb_);
+    for (int64_t gb = ga; gb <= gb_; gb += 32 * U) {
+      float2 m4[U];
+      unsigned am4[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t g = gb + u * 32 + lane;
+        m4[u] = g <= gb_ ? A.mm[g] : make_float2(-INFINITY, INFINITY);
+        am4[u] = g <= gb_ ? A.am[g] : 0xffffffffu;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t g = gb + u * 32 + lane;
+        const float2 m = m4[u];
+        const unsigned am = am4[u];
+        const int64_t px = g * SB + (am & 0xffff), pn = g * SB + (am >> 16);
+        const bool okx = (am & 0xffff) != 0xffff && px >= s && px < e;
+        const bool okn = (am >> 16) != 0xffff && pn >= s && pn < e;
+        const float dxx = okx ? (float)(xd(x, px) - xs) : 0.0f, dxn = okn ? (float)(xd(x, pn) - xs) : 0.0f;
+#pragma unroll
+        for (int t = 0; t < LTTB_K; t++) {
+          const float vx = fmaf(-sl[t], dxx, m.x), vn = fmaf(-sl[t], dxn, m.y);
+          if (okx && vx > bv[2 * t]) { bv[2 * t] = vx; bi[2 * t] = (unsigned)(px - s); }
+          if (okn && vn < bv[2 * t + 1]) { bv[2 * t + 1] = vn; bi[2 * t + 1] = (unsigned)(pn - s); }
+        }
+      }
+    }
+    // warp-wide winners; lane c keeps candidate c's (key, position)
+    unsigned mykey = 0, mypos = 0xffffffffu;
+#pragma unroll
+    for (int c = 0; c < LTTB_NC; c++) {
+      const bool mx = (c & 1) == 0;
+      const bool has = bi[c] != 0xffffffffu;
+      const unsigned key = has ? f32_key(bv[c]) : (mx ? 0u : 0xffffffffu);
+      const unsigned w = mx ? __reduce_max_sync(0xffffffffu, key) : __reduce_min_sync(0xffffffffu, key);
+      const unsigned rr = __reduce_min_sync(0xffffffffu, (has && key == w) ? bi[c] : 0xffffffffu);
+      if (lane == c) { mykey = w; mypos = rr; }
+    }
+    LttbMwScratch* sc = scr[it & 1];
+    if (M.r > 0 && lane < LTTB_NC) {
+      sc[wid].key[lane] = mykey;
+      sc[wid].pos[lane] = mypos;
+    }
+    M.sync();
+    if (M.r == 0) {
+      if (lane < LTTB_NC) {  // merge the group's warps: best key, then the lowest position
+        const bool mx = (lane & 1) == 0;
+#pragma unroll
+        for (int q = 1; q < NWG; q++) {
+          const unsigned kk = sc[wid + q].key[lane], pp = sc[wid + q].pos[lane];
+          if ((mx ? kk > mykey : kk < mykey) || (kk == mykey && pp < mypos)) { mykey = kk; mypos = pp; }
+        }
+      }
+      const unsigned myrel = mypos == 0xffffffffu ? 0u : mypos;
+      unsigned rel[LTTB_NC];
+#pragma unroll
+      for (int c = 0; c < LTTB_NC; c++) rel[c] = __shfl_sync(0xffffffffu, myrel, c);
+#pragma unroll
+      for (int rr = 0; rr < LTTB_NC; rr++) {
+#pragma unroll
+        for (int c = rr & 1; c + 1 < LTTB_NC; c += 2) {
+          const unsigned a0 = rel[c], a1 = rel[c + 1];
+          rel[c] = a0 < a1 ? a0 : a1;
+          rel[c + 1] = a0 < a1 ? a1 : a0;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < LTTB_NC; c++)
+        if (c == lane) ext[k * LTTB_NC + c] = s + (int64_t)rel[c];
+    }
+  }
+}
+
+template <int YDT, int NWG>
+__device__ __forceinline__ void lttb_plan_phase_mw(const double* x, const void* y, int64_t n, const int64_t* off,
+                                                   int64_t nb, const LttbSBArrays A, const double2* cent,
+                                                   const int32_t* nonempty, const int64_t* counts,
+                                                   const int64_t* ext, int64_t* picks, LttbRound1* r1,
+                                                   int32_t* arrive, int64_t* slots, int64_t* wl, int32_t* list,
+                                                   int32_t* ctr, int* scnt) {
+  constexpr int U = 4;
+  const LttbMw<NWG> M;
+  const int64_t SB = A.SB;
+  const int lane = threadIdx.x & 31;
+  const int64_t L = counts[0];
+  unsigned long long* nsb = (unsigned long long*)(ctr + 6);
+  for (int64_t j = M.grp; j < L; j += M.ngrp) {
+    const int64_t k = nonempty[j];
+    const int64_t s = __ldg(off + k), e = __ldg(off + k + 1);
+    LttbPlan P;
+    AreaCand cb;
+    double cx, cy;
+    int64_t kk = k, ss = s, ee = e;
+    lttb_plan_bucket<YDT>(x, y, n, off, nb, cent, nonempty, ext, picks, j, lane, kk, ss, ee, P, cb, cx, cy, true);
+    if (M.r == 0 && lane == 0) scnt[M.gi] = 0;
+    M.sync();
+    const int64_t g0 = s / SB, g1 = (e - 1) / SB;
+    const int64_t base = g0 + j;
+    int64_t ga, gb_;
+    M.share(g0, g1, ga, gb_);
+    for (int64_t gb = ga; gb <= gb_; gb += 32 * U) {
+      float2 m4[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t g = gb + u * 32 + lane;
+        m4[u] = g <= gb_ ? A.mm[g] : make_float2(-INFINITY, INFINITY);
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t g = gb + u * 32 + lane;
+        bool keep = false;
+        if (g <= gb_) {
+          if (x) keep = true;
+          else {
+            int64_t cs, ce;
+            lttb_sb_range(A.SB, g, s, e, cs, ce);
+            keep = !(lttb_sb_bound(m4[u], s, cs, ce, P) < cb.a);
+          }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (bal) {
+          const int before = __popc(bal & ((1u << lane) - 1u));
+          int64_t w0 = 0;
+          int c0 = 0;
+          if (lane == 0) {
+            w0 = (int64_t)atomicAdd(nsb, (unsigned long long)__popc(bal));
+            c0 = atomicAdd(&scnt[M.gi], __popc(bal));
+          }
+          w0 = __shfl_sync(0xffffffffu, w0, 0);
+          c0 = __shfl_sync(0xffffffffu, c0, 0);
+          if (keep) {
+            const int64_t pos = base + c0 + before;
+            TSDS_CHECK(pos >= g0 + j && pos <= g1 + j);
+            slots[pos] = (g << 24) | j;
+            wl[w0 + before] = pos;
+          }
+        }
+      }
+    }
+    M.sync();
+    if (M.r == 0 && lane == 0) {
+      const int64_t cnt = scnt[M.gi];
+      r1[j] = LttbRound1{P, cb, base, cnt};
+      arrive[j] = (int32_t)cnt;
+      if (cnt == 0) {
+        const int64_t p = cb.i == IDX_NONE ? s : cb.i;
+        if (p != __ldcg(picks + j)) {
+          __stcg(picks + j, p);
+          if (j + 1 < L) list[atomicAdd(ctr + 2, 1)] = (int32_t)(j + 1);
+        }
+      }
+    }
+    M.sync();  // scnt is reset for the next bucket only after it was read
+  }
+}
+
 // The guess and the round-1 plan in one cooperative launch (grid barriers
 // between the phases):
 //   count/list  non-empty bucket list (nonempty, rank, counts[0] = L)
@@ -995,6 +1314,8 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   __shared__ uint8_t segc[8][LTTB_SEG];
   __shared__ int s_red[32];
   __shared__ int s_base;
+  __shared__ LttbMwScratch mw_scr[2][8];
+  __shared__ int mw_cnt[4];
   const double* x = eff_x(xin, drop);
   unsigned long long* tsb = (unsigned long long*)(ctr + 16);  // phase timestamps (tsds_ctx_stat "lttb_tsN")
   auto stamp = [&](int i) {
@@ -1027,7 +1348,12 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   }
   stamp(1);
   const int G = lttb_pick_group(counts[0]);
-  if (G == 32) lttb_cent_phase<YDT, 32>(x, y, off, nonempty, counts, A, cent, yr);
+  // warps per bucket when the buckets are few (every bucket still in the first round)
+  const int64_t nw_grid = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int NWG = counts[0] * 4 <= nw_grid ? 4 : (counts[0] * 2 <= nw_grid ? 2 : 1);
+  if (NWG == 4) lttb_cent_phase_mw<YDT, 4>(x, y, off, nonempty, counts, A, cent, yr, mw_scr);
+  else if (NWG == 2) lttb_cent_phase_mw<YDT, 2>(x, y, off, nonempty, counts, A, cent, yr, mw_scr);
+  else if (G == 32) lttb_cent_phase<YDT, 32>(x, y, off, nonempty, counts, A, cent, yr);
   else if (G == 16) lttb_cent_phase<YDT, 16>(x, y, off, nonempty, counts, A, cent, yr);
   else lttb_cent_phase<YDT, 8>(x, y, off, nonempty, counts, A, cent, yr);
   grid.sync();
@@ -1036,7 +1362,9 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
     grid.sync();
   }
   stamp(2);
-  if (G == 32) lttb_cand_phase<YDT, 32>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext);
+  if (NWG == 4) lttb_cand_phase_mw<YDT, 4>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext, mw_scr);
+  else if (NWG == 2) lttb_cand_phase_mw<YDT, 2>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext, mw_scr);
+  else if (G == 32) lttb_cand_phase<YDT, 32>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext);
   else if (G == 16) lttb_cand_phase<YDT, 16>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext);
   else lttb_cand_phase<YDT, 8>(x, y, off, nb, n, cent, yr, nonempty, counts, A, ext);
   grid.sync();
@@ -1055,7 +1383,9 @@ lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, 
   grid.sync();
   stamp(4);
   // ---- round-1 plan
-  if (G == 32) lttb_plan_phase<YDT, 32>(x, y, n, off, nb, A, cent, nonempty, counts, ext, picks, r1, arrive, slots, wl, list, ctr);
+  if (NWG == 4) lttb_plan_phase_mw<YDT, 4>(x, y, n, off, nb, A, cent, nonempty, counts, ext, picks, r1, arrive, slots, wl, list, ctr, mw_cnt);
+  else if (NWG == 2) lttb_plan_phase_mw<YDT, 2>(x, y, n, off, nb, A, cent, nonempty, counts, ext, picks, r1, arrive, slots, wl, list, ctr, mw_cnt);
+  else if (G == 32) lttb_plan_phase<YDT, 32>(x, y, n, off, nb, A, cent, nonempty, counts, ext, picks, r1, arrive, slots, wl, list, ctr);
   else if (G == 16) lttb_plan_phase<YDT, 16>(x, y, n, off, nb, A, cent, nonempty, counts, ext, picks, r1, arrive, slots, wl, list, ctr);
   else lttb_plan_phase<YDT, 8>(x, y, n, off, nb, A, cent, nonempty, counts, ext, picks, r1, arrive, slots, wl, list, ctr);
   grid.sync();
