@@ -60,7 +60,7 @@ const char *tsds_last_error(void);
  * the scan handed out dynamically; default 0, env TSDS_DYN_PERCENT),
  * "cta_bins_max_bytes" (inputs up to this size with >= #SM bins use the
  * CTA-per-bin scan; default 128 MiB, env TSDS_CTA_BINS_MAX_BYTES),
- * "lane_bins" (batched MinMax with short bins: thread-per-bin kernel; 0 off,
+ * "lane_bins" (batched MinMax with short bins: lane-group-per-bin kernel; 0 off,
  * 1 auto, 2 whenever eligible; env TSDS_LANE_BINS), "atomic_bins" (scans of
  * <= 32-bit values with >= #SM bins merge bin segments with 64-bit atomics
  * and compact in a dependent one-CTA kernel; 0 off, 1 auto, 2 whenever
@@ -87,7 +87,7 @@ int64_t tsds_ctx_launches(tsds_ctx *ctx);
 int64_t tsds_ctx_stat(tsds_ctx *ctx, const char *name);
 /* measurement hooks: record CUDA events around every launch of the call's
  * streaming kernel (the one pass over y: the argmin/argmax scan, the
- * thread-per-bin batched kernel, or the LTTB summary pass); programmatic
+ * lane-group batched kernel, the TMA tile kernel, or the LTTB summary pass); programmatic
  * dependent launch is off for them while enabled.  _read synchronises,
  * returns their summed duration and count, and clears the record */
 int tsds_ctx_profile(tsds_ctx *ctx, int enable);

@@ -187,7 +187,7 @@ int dtype_ok(int dt) { return dt >= 0 && dt < DT_COUNT; }
 // tuning knobs: environment defaults, overridable with tsds_set_option
 int64_t g_dyn_percent = -1, g_cta_bins_max = -1, g_lane_bins = -1;
 
-// thread-per-bin batched kernel: 0 off, 1 auto (default), 2 whenever eligible
+// lane-group-per-bin batched kernel: 0 off, 1 auto (default), 2 whenever eligible
 int64_t lane_bins_mode() {
   if (g_lane_bins < 0) {
     const char* e = getenv("TSDS_LANE_BINS");
@@ -1576,14 +1576,15 @@ static int batched_enqueue(tsds_ctx* ctx, const void* dy, int ydt, int64_t S, in
   ScanArgs A = scan_args(dy, BinSpec{0, nullptr, L, nb, 0}, 0, S * nb, 0, S * L);
   A.epi = EPI_PAIR;
   A.out = nullptr;
-  // many short bins (4 .. 256 vectors each, enough of them to fill the GPU
-  // with one thread per bin): thread-per-bin kernel.  Measured on C5 (1024
-  // series, 4000-point bins): u8 749 -> 405 us, f16 887 -> 809 us; i16 stays
-  // on the warp scan (745 vs 806 us).  Option / env "lane_bins" (TSDS_LANE_BINS).
+  // many short bins (4 .. 1024 vectors each, enough of them to fill the GPU
+  // with eight lanes per bin): lane-group kernel (tsds_lanebins.cuh).
+  // Measured on C5 (4096 series, 4000-point bins) against the warp scan:
+  // u8 1.94 -> 1.50 ms, f16 3.62 -> 2.58 ms.
+  // Option / env "lane_bins" (TSDS_LANE_BINS).
   const int64_t es = dtype_size(ydt), bin_bytes = (L / nb) * es;
   const int64_t mode = lane_bins_mode();  // 0 off, 1 auto, 2 whenever eligible (tests)
   const bool eligible = !nan_mode && ((uintptr_t)dy % 16) == 0;
-  const int64_t max_bytes = ydt == DT_F16 ? 16384 : 4096;  // f16: the warp scan's ordinal keys cost more
+  const int64_t max_bytes = es <= 2 ? 16384 : 4096;  // packed 16x2 block folds pay for the 1- and 2-byte types
   const bool lane_ok = eligible && (mode == 2 || (mode == 1 && bin_bytes >= 64 && bin_bytes <= max_bytes &&
                                                   S * nb >= (int64_t)ctx->sms * 1024));
   if (lane_ok) RC_TRY(launch_lane_bins(ctx, ydt, A));

@@ -161,7 +161,7 @@ struct Packed16 {
     mn = min(half_lo(m), half_hi(m));
     mx = max(half_lo(M), half_hi(M));
   }
-  // packed block fold (thread-per-bin kernel): two 16-bit columns of running
+  // packed block fold (lane-group batched kernel): two 16-bit columns of running
   // extrema, folded over several vectors before one horizontal reduction
   __device__ static uint32_t pmin_init() { return SIGNED ? 0x7fff7fffu : 0xffffffffu; }
   __device__ static uint32_t pmax_init() { return SIGNED ? 0x80008000u : 0u; }

@@ -149,7 +149,7 @@ def test_batched_rows_equal_single(ts, oracle):
 
 
 def test_batched_thread_per_bin_kernel(ts, oracle):
-    """The thread-per-bin batched kernel (forced on for small inputs): every
+    """The lane-group batched kernel (8 lanes per bin; forced on for small inputs): every
     width, ties, f16 +-0/NaN ordering, f32 NaNs, and bins that do not start
     or end on a 16-byte boundary (head/tail elements)."""
     from paper_2307_05389_b200 import _lib

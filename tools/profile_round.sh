@@ -7,7 +7,7 @@ TAG=${1:-r02}; shift
 KEYS=${@:-C1 C2 C3_1000 C3_10000 C4 C5_i16 C5_u8 C5_f16}
 mkdir -p gpurun_out
 declare -A KREGEX=( [C1]=tile_bins_kernel [C2]=scan_kernel [C3_1000]=lttb_sb_kernel [C3_10000]=lttb_guess_kernel
-                    [C4]=scan_kernel [C5_i16]=scan_kernel [C5_u8]=lane_bins_kernel [C5_f16]=lane_bins_kernel )
+                    [C4]=scan_kernel [C5_i16]=lane_bins_kernel [C5_u8]=lane_bins_kernel [C5_f16]=lane_bins_kernel )
 for K in $KEYS; do
   python tools/step_profile.py $K --steps 5 --warmup 3 > gpurun_out/${TAG}_plain_$K.log 2>&1 || { echo "plain $K failed"; continue; }
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
