@@ -5,9 +5,16 @@ slots (csrc/tsds_staging.h), which costs host-DRAM bandwidth (read + write +
 DMA read) and tops out below the PCIe rate.  Downsampling is typically
 called again and again on the same array (interactive zooming, different
 n_out, the estimator classes), so the second time an array of at least
-``TSDS_PIN_MIN_BYTES`` (default 8 MiB, the staging ring's own threshold) is seen, its owner's buffer is
+``TSDS_PIN_MIN_BYTES`` (default 64 MiB) is seen, its owner's buffer is
 page-locked in place with ``tsds_host_register`` (cudaHostRegister,
 ~13 GB/s once) and later uploads are DMA'd directly from it at link speed.
+
+Why not smaller arrays: DMA from registered 4 KiB pages can be slow when the
+pages are scattered (measured on the pool's VMs: a 40 MB array moved at 17-55
+GB/s depending on where the allocator had placed it, against a steady 32-39
+GB/s through the staging ring, whose slots are driver-allocated); from 64 MiB
+up the registered path was at least on par with the ring (43-55 against
+41-47 GB/s) and at the link rate for multi-GB inputs (54.5 GB/s).
 
 Safety: the registration is tied, through a weak reference, to the array at
 the end of the ``.base`` chain -- the one that owns the memory or holds the
@@ -37,7 +44,7 @@ def _default_cap():
 
 
 _mode = os.environ.get("TSDS_PIN_CACHE", "reuse").lower()
-_min_bytes = int(os.environ.get("TSDS_PIN_MIN_BYTES", 8 << 20))
+_min_bytes = int(os.environ.get("TSDS_PIN_MIN_BYTES", 64 << 20))
 _max_bytes = int(os.environ.get("TSDS_PIN_MAX_BYTES", _default_cap()))
 _lock = threading.Lock()
 _seen = {}  # id(owner) -> sightings (negative: registration failed, do not retry)

@@ -55,5 +55,5 @@ def test_pin_on_second_call_and_release_on_collect():
         gc.collect()
         assert pinning.pinned_bytes() == 0 and pinning.stats["released"] == rel0 + 1
     finally:
-        pinning.configure(mode="reuse", min_bytes=8 << 20)
+        pinning.configure(mode="reuse", min_bytes=64 << 20)
         pinning.release_all()
