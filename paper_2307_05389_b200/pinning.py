@@ -9,12 +9,14 @@ n_out, the estimator classes), so the second time an array of at least
 page-locked in place with ``tsds_host_register`` (cudaHostRegister,
 ~13 GB/s once) and later uploads are DMA'd directly from it at link speed.
 
-Why not smaller arrays: DMA from registered 4 KiB pages can be slow when the
-pages are scattered (measured on the pool's VMs: a 40 MB array moved at 17-55
-GB/s depending on where the allocator had placed it, against a steady 32-39
-GB/s through the staging ring, whose slots are driver-allocated); from 64 MiB
-up the registered path was at least on par with the ring (43-55 against
-41-47 GB/s) and at the link rate for multi-GB inputs (54.5 GB/s).
+Why not smaller arrays: on the pool's VMs the DMA rate from a registered
+array depends on where the allocator placed it -- the same 40 MB series moved
+at 23 GB/s in one process and 54 GB/s in another (transparent huge pages in
+both, tools/thp_probe.py; the placement relative to the GPU's root complex is
+not visible to the guest) -- against a steady 32-39 GB/s through the staging
+ring, whose slots are driver-allocated.  From 64 MiB up the registered path
+was at least on par with the ring (43-55 against 41-47 GB/s) and at the link
+rate for multi-GB inputs (54.5 GB/s).
 
 Safety: the registration is tied, through a weak reference, to the array at
 the end of the ``.base`` chain -- the one that owns the memory or holds the
