@@ -407,6 +407,21 @@ def measure_config(key, runner, args, clk, cpu, peak, peak_kind):
     del t1
     ms_step = ms / args.steps
     kms, kper = runner.kernel_ms(step, args.steps, flush)
+    graph_ms = None
+    try:  # the same call replayed from a CUDA graph (tests/test_gpu_graph.py): no launch gaps
+        g = runner.torch.cuda.CUDAGraph()
+        with runner.torch.cuda.graph(g, stream=runner.stream):
+            step()
+        g.replay()
+        ms_g, _ = runner.time_steps(g.replay, args.steps, flush)
+        graph_ms = ms_g / args.steps
+        got_g, counts_g = result()
+        assert golden_ok(key, got_g, counts_g), f"{key}: graph replay differs from the reference's golden output"
+        del g
+    except AssertionError:
+        raise
+    except Exception as e:  # capture unavailable: report the direct call only
+        print(f"[bench] {key}: CUDA graph capture skipped ({type(e).__name__}: {e})", file=sys.stderr)
     gbs = nbytes / (ms_step * 1e-3) / 1e9
     achieved = nbytes / (kms * 1e-3) / 1e9
     entry = {
@@ -417,6 +432,9 @@ def measure_config(key, runner, args, clk, cpu, peak, peak_kind):
               f"inputs ({nbytes / 1e9:.2f} GB) larger than L2 (126 MB); no flush",
         "parity": "equal to the reference's output (tests/golden/configs.npz)",
         "gpu_launches": int(launches),
+        "graph_replay": None if graph_ms is None else {
+            "ms_per_step": round(graph_ms, 5), "value": round(nbytes / (graph_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "note": "the same asynchronous call captured once into a CUDA graph and replayed (same kernels, no launch gaps)"},
         "roofline": {"bound": "hbm", "kernel": {"minmax": "tile_bins_kernel<f32> (TMA bulk copies into a shared-memory ring)",
                                                 "m4": "scan_kernel<f64>", "lttb": "lttb_sb_kernel<f64>",
                                                 "minmaxlttb": "scan_kernel<f32> (MinMax preselection)",
