@@ -36,6 +36,9 @@
 
 namespace tsds {
 
+#ifndef LTTB_PHASE_U
+#define LTTB_PHASE_U 4  // sub-block summaries in flight per lane in the per-bucket phases
+#endif
 constexpr int LTTB_K = 7;            // steering slopes per bucket
 constexpr int LTTB_NC = 2 * LTTB_K;  // candidates per bucket (argmax + argmin per slope)
 constexpr int LTTB_SEG = 64;         // buckets per composed segment
@@ -333,7 +336,7 @@ __device__ __forceinline__ void lttb_cent_phase(const double* x, const void* y, 
                                                 const int32_t* nonempty, const int64_t* counts,
                                                 const LttbSBArrays A, double2* cent, float2* yr) {
   constexpr int VL = 32 / G;  // virtual lanes per physical lane
-  constexpr int U = 4;        // items in flight per lane (a multiple of VL)
+  constexpr int U = LTTB_PHASE_U;  // items in flight per lane (a multiple of VL)
   const int64_t SB = A.SB;
   const int lane = threadIdx.x & 31, l = lane & (G - 1);
   const unsigned gmask = lttb_gmask<G>(lane);
@@ -464,7 +467,7 @@ __device__ __forceinline__ void lttb_cand_phase(const double* x, const void* y, 
                                                 int64_t n, const double2* cent, const float2* yr,
                                                 const int32_t* nonempty, const int64_t* counts,
                                                 const LttbSBArrays A, int64_t* ext) {
-  constexpr int U = 4;
+  constexpr int U = LTTB_PHASE_U;
   const int64_t SB = A.SB;
   const int lane = threadIdx.x & 31, l = lane & (G - 1);
   const unsigned gmask = lttb_gmask<G>(lane);
@@ -873,7 +876,7 @@ __device__ __forceinline__ void lttb_plan_phase(const double* x, const void* y, 
                                                 const int32_t* nonempty, const int64_t* counts, const int64_t* ext,
                                                 int64_t* picks, LttbRound1* r1, int32_t* arrive, int64_t* slots,
                                                 int64_t* wl, int32_t* list, int32_t* ctr) {
-  constexpr int U = 4;
+  constexpr int U = LTTB_PHASE_U;
   const int64_t SB = A.SB;
   const int lane = threadIdx.x & 31, l = lane & (G - 1), gbase = lane & ~(G - 1);
   const unsigned gmask = lttb_gmask<G>(lane);
@@ -1002,7 +1005,7 @@ __device__ __forceinline__ void lttb_cent_phase_mw(const double* x, const void* 
                                                    const int32_t* nonempty, const int64_t* counts,
                                                    const LttbSBArrays A, double2* cent, float2* yr,
                                                    LttbMwScratch (*scr)[8]) {
-  constexpr int U = 4;
+  constexpr int U = LTTB_PHASE_U;
   const LttbMw<NWG> M;
   const int64_t SB = A.SB;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1104,7 +1107,7 @@ __device__ __forceinline__ void lttb_cand_phase_mw(const double* x, const void* 
                                                    int64_t n, const double2* cent, const float2* yr,
                                                    const int32_t* nonempty, const int64_t* counts,
                                                    const LttbSBArrays A, int64_t* ext, LttbMwScratch (*scr)[8]) {
-  constexpr int U = 4;
+  constexpr int U = LTTB_PHASE_U;
   const LttbMw<NWG> M;
   const int64_t SB = A.SB;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1204,7 +1207,7 @@ __device__ __forceinline__ void lttb_plan_phase_mw(const double* x, const void* 
                                                    const int64_t* ext, int64_t* picks, LttbRound1* r1,
                                                    int32_t* arrive, int64_t* slots, int64_t* wl, int32_t* list,
                                                    int32_t* ctr, int* scnt) {
-  constexpr int U = 4;
+  constexpr int U = LTTB_PHASE_U;
   const LttbMw<NWG> M;
   const int64_t SB = A.SB;
   const int lane = threadIdx.x & 31;
