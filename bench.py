@@ -438,7 +438,7 @@ def measure_config(key, runner, args, clk, cpu, peak, peak_kind):
         "roofline": {"bound": "hbm", "kernel": {"minmax": "tile_bins_kernel<f32> (TMA bulk copies into a shared-memory ring)",
                                                 "m4": "scan_kernel<f64>", "lttb": "lttb_sb_kernel<f64>",
                                                 "minmaxlttb": "scan_kernel<f32> (MinMax preselection)",
-                                                "minmax_batched": f"lane_bins_kernel<{s.get('tag')}> (8 lanes per bin)"}[s["algo"]],
+                                                "minmax_batched": f"lane_bins_kernel<{s.get('tag')}> ({4 if s.get('tag') == 'u8' else 8} lanes per bin)"}[s["algo"]],
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "frac_of_step": round(gbs / peak, 4),
                      "traffic": _traffic(key), "algorithmic_bytes_per_launch": nbytes,

@@ -404,9 +404,9 @@ int prof_mark(tsds_ctx* ctx, std::pair<cudaEvent_t, cudaEvent_t>& ev, bool end);
 
 // lane-group-per-bin argmin/argmax (tsds_lanebins.cuh) over the composite bins of
 // a batch; same res[] layout and epilogue as the scan
-template <int DT>
-int launch_lane_bins_t(tsds_ctx* ctx, ScanArgs& A) {
-  auto kern = lane_bins_kernel<DT>;
+template <int DT, int LG>
+int launch_lane_bins_g(tsds_ctx* ctx, ScanArgs& A) {
+  auto kern = lane_bins_kernel<DT, LG>;
   static int occ = 0;
   if (occ == 0) {
     int o = 0;
@@ -418,13 +418,21 @@ int launch_lane_bins_t(tsds_ctx* ctx, ScanArgs& A) {
   RC_TRY(ensure(ctx, ctx->res, (size_t)nbins * 2 * sizeof(int64_t)));
   A.res = (int64_t*)ctx->res.p;
   A.flags = &misc(ctx)->F;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * occ, (nbins * LB_LANES + 255) / 256));
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * occ, (nbins * LG + 255) / 256));
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
   RC_TRY(prof_mark(ctx, ev, false));
   kern<<<(unsigned)grid, SCAN_WARPS * 32, 0, ctx->stream>>>(A);
   LAUNCH_CHECK();
   RC_TRY(prof_mark(ctx, ev, true));
   return TSDS_OK;
+}
+
+// lanes per bin: about 64 vectors (1 KB) per lane and bin
+template <int DT>
+int launch_lane_bins_t(tsds_ctx* ctx, ScanArgs& A) {
+  const int64_t bin_bytes = (A.E1 - A.E0) / std::max<int64_t>(A.g1 - A.g0, 1) * dtype_size(DT);
+  if (bin_bytes <= 4096) return launch_lane_bins_g<DT, 4>(ctx, A);
+  return launch_lane_bins_g<DT, LB_LANES>(ctx, A);
 }
 
 int launch_lane_bins(tsds_ctx* ctx, int dt, ScanArgs& A) {

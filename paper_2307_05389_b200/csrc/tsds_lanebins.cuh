@@ -1,5 +1,5 @@
 // tsds_lanebins.cuh -- per-bin argmin/argmax for batches of SHORT bins: a
-// group of LB_LANES lanes per bin.
+// group of 4 or 8 lanes per bin.
 //
 // For many short, equal bins (batched MinMax, config 5: 4000-element bins)
 // the warp-per-segment scan pays two dependent round trips per bin (the
@@ -30,7 +30,7 @@ namespace tsds {
 #ifndef LB_MIN_BLOCKS_N
 #define LB_MIN_BLOCKS_N 2  // 3 resident CTAs (85 registers) spill ~220 bytes in the block rotation; measured slower
 #endif
-constexpr int LB_LANES = LB_LANES_N;  // lanes per bin (power of two <= 32)
+constexpr int LB_LANES = LB_LANES_N;  // lanes per bin for bins above 4 KB (4 below)
 constexpr int LB_V = 4;               // vectors per folded block
 
 // first element (in index order) of block c equal to r; c[u] is the lane's
@@ -53,14 +53,16 @@ __device__ __forceinline__ int lb_find(const uint4 (&c)[LB_V], typename Ops<DT>:
   return f;
 }
 
-template <int DT>
+// LG = lanes per bin (4 or 8): chosen at launch so that a lane gets about 64
+// vectors per bin (measured on C5: 4000-byte u8 bins 1.50 ms with 8 lanes,
+// 1.37 ms with 4; 8000-byte i16 bins 2.54 ms with 8, 2.71 ms with 4)
+template <int DT, int LG>
 __global__ void __launch_bounds__(SCAN_WARPS * 32, LB_MIN_BLOCKS_N)
 lane_bins_kernel(const ScanArgs A) {
   using O = Ops<DT>;
   using E = typename O::E;
   using R = typename O::R;
   constexpr int VEC = O::VEC;
-  constexpr int LG = LB_LANES;
   const E* y = static_cast<const E*>(A.y);
   const uint4* yv = reinterpret_cast<const uint4*>(y);  // host guarantees 16-byte alignment
   const BinSpec B = A.bins;
