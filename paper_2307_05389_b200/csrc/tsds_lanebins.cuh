@@ -31,7 +31,10 @@ namespace tsds {
 #define LB_MIN_BLOCKS_N 2  // 3 resident CTAs (85 registers) spill ~220 bytes in the block rotation; measured slower
 #endif
 constexpr int LB_LANES = LB_LANES_N;  // lanes per bin for bins above 4 KB (4 below)
-constexpr int LB_V = 4;               // vectors per folded block
+#ifndef LB_V_N
+#define LB_V_N 4
+#endif
+constexpr int LB_V = LB_V_N;          // vectors per folded block
 
 // first element (in index order) of block c equal to r; c[u] is the lane's
 // u-th vector of the block
