@@ -442,7 +442,9 @@ def measure_config(key, runner, args, clk, cpu, peak, peak_kind):
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "frac_of_step": round(gbs / peak, 4),
                      "traffic": _traffic(key), "algorithmic_bytes_per_launch": nbytes,
-                     "avg_launch_ms": round(kms, 5), "launches_per_step": kper},
+                     "avg_launch_ms": round(kms, 5), "launches_per_step": kper,
+                     "note": "peak is the measured COPY bandwidth (read + write streams); a read-only stream such as "
+                             "this scan can exceed it, so frac may be above 1"},
     }
     if s["algo"] == "lttb":
         # north star: LTTB picks may differ from the reference only at area ties within 1e-12
