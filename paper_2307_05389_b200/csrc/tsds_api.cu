@@ -816,13 +816,18 @@ int run_lttb_large(tsds_ctx* ctx, const double* xf, const int* drop, const void*
   RC_TRY(prof_mark(ctx, ev, true));
   // ---- 2. guess + round-1 plan (cooperative)
   const int64_t cap = 32768;
+  // few buckets: 2 fat CTAs per SM (no spills), as long as 2-warp groups still give every bucket its own
+  const bool fat = nb * 2 <= (int64_t)ctx->sms * 2 * 8;
+  auto launch_guess = [&](auto kg) -> int {
+    cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(cap + 16));
+    const unsigned gg = std::min<unsigned>(one_wave(ctx, kg, 256, (size_t)(cap + 16)), (unsigned)nbl);
+    return launch_coop(ctx, kg, gg, 256, (size_t)(cap + 16), xf, drop, y, n, (int64_t*)off, nb, A, cent, yr, bcnt, nonempty,
+                       rank, counts, ext, T, C, entry, picks, r1, arrive, slots, wl, list_a, ctr, exact, cap, fill_len,
+                       fill_add);
+  };
   YDT_SWITCH(ydt, ({
-               auto kg = lttb_guess_kernel<YD>;
-               cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(cap + 16));
-               const unsigned gg = std::min<unsigned>(one_wave(ctx, kg, 256, (size_t)(cap + 16)), (unsigned)nbl);
-               RC_TRY(launch_coop(ctx, kg, gg, 256, (size_t)(cap + 16), xf, drop, y, n, (int64_t*)off, nb, A, cent, yr,
-                                  bcnt, nonempty, rank, counts, ext, T, C, entry, picks, r1, arrive, slots, wl, list_a,
-                                  ctr, exact, cap, fill_len, fill_add));
+               if (fat) RC_TRY(launch_guess(lttb_guess_kernel<YD, 2>));
+               else RC_TRY(launch_guess(lttb_guess_kernel<YD, 3>));
              }));
   // ---- 3. round-1 evaluation, 4. correction chains, 5. output
   YDT_SWITCH(ydt, RC_TRY(launch_pdl(ctx, lttb_eval_kernel<YD>, one_wave(ctx, lttb_eval_kernel<YD>, 256), 256, 0, xf,

@@ -1300,8 +1300,12 @@ __device__ __forceinline__ void lttb_plan_phase_mw(const double* x, const void* 
 //               and appended to the work list wl; a bucket with none
 //               settles at once.
 // ctr: [2] |D|, [6..7] sub-blocks listed (int64).
-template <int YDT>
-__global__ void __launch_bounds__(256, 3)
+// MINB = resident CTAs per SM: 3 (85 registers, small spills) when the
+// buckets are many -- more warps, one bucket group each -- and 2 (128
+// registers, no spills) when they are few (measured on C3: n_out 1000 194 ->
+// 184 us with 2, n_out 10000 256 -> 278 us with 2)
+template <int YDT, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 lttb_guess_kernel(const double* xin, const int* drop, const void* y, int64_t n, int64_t* off_w, int64_t nb,
                   const LttbSBArrays A, double2* cent, float2* yr, int32_t* bcnt, int32_t* nonempty, int32_t* rank,
                   int64_t* counts, int64_t* ext, uint8_t* T, uint8_t* C, uint8_t* entry, int64_t* picks,
